@@ -1,0 +1,235 @@
+// Device-side evolutionary operators for population-scale search.
+//
+// Operator semantics follow tensorplace/evolution.py:384-399 and :412-428:
+// tournament selection (first draw, then tournament-1 challengers that win
+// only when strictly fitter), two-point crossover child = a[:i] + b[i:j] +
+// a[j:] with i <= j drawn from [0, k], per-bit mutation.  Randomness is
+// Philox4x32-10 keyed by (seed) and countered by (child, generation, stream,
+// draw) so every child is reproducible independently of launch geometry.
+// Mutation draws geometric gaps between flipped bits, which is the same
+// Bernoulli(rate) process per bit at O(#flips) cost.
+//
+// One warp per child: lane 0 draws, every lane assembles whole uint64 words
+// of the child from the two parents with segment masks (coalesced rows).
+#include <cub/cub.cuh>
+
+#include "cb_internal.cuh"
+
+// Philox4x32-10
+struct Philox {
+  uint32_t k0, k1;
+  uint32_t c[4];
+  uint32_t out[4];
+  int used;
+  __device__ Philox(uint64_t seed, uint32_t c0, uint32_t c1, uint32_t c2) {
+    k0 = (uint32_t)seed;
+    k1 = (uint32_t)(seed >> 32);
+    c[0] = c0;
+    c[1] = c1;
+    c[2] = c2;
+    c[3] = 0;
+    used = 4;
+  }
+  __device__ void refill() {
+    uint32_t x0 = c[0], x1 = c[1], x2 = c[2], x3 = c[3];
+    uint32_t a0 = k0, a1 = k1;
+#pragma unroll
+    for (int r = 0; r < 10; ++r) {
+      uint32_t hi0 = __umulhi(0xD2511F53u, x0), lo0 = 0xD2511F53u * x0;
+      uint32_t hi1 = __umulhi(0xCD9E8D57u, x2), lo1 = 0xCD9E8D57u * x2;
+      uint32_t y0 = hi1 ^ x1 ^ a0, y1 = lo1, y2 = hi0 ^ x3 ^ a1, y3 = lo0;
+      x0 = y0;
+      x1 = y1;
+      x2 = y2;
+      x3 = y3;
+      a0 += 0x9E3779B9u;
+      a1 += 0xBB67AE85u;
+    }
+    out[0] = x0;
+    out[1] = x1;
+    out[2] = x2;
+    out[3] = x3;
+    c[3] += 1;
+    used = 0;
+  }
+  __device__ uint32_t next() {
+    if (used == 4) refill();
+    return out[used++];
+  }
+  // uniform in [0, n) (Lemire, with rejection)
+  __device__ uint32_t below(uint32_t n) {
+    uint64_t m = (uint64_t)next() * n;
+    uint32_t l = (uint32_t)m;
+    if (l < n) {
+      uint32_t t = (uint32_t)(-n) % n;
+      while (l < t) {
+        m = (uint64_t)next() * n;
+        l = (uint32_t)m;
+      }
+    }
+    return (uint32_t)(m >> 32);
+  }
+  // uniform double in (0, 1]
+  __device__ double unit() {
+    uint64_t hi = next(), lo = next();
+    uint64_t v = ((hi << 21) ^ lo) & ((1ull << 53) - 1);
+    return ((double)v + 1.0) * (1.0 / 9007199254740992.0);
+  }
+};
+
+__device__ __forceinline__ uint64_t seg_mask(int64_t lo, int64_t hi, int64_t w) {
+  // bits of word w that fall inside [lo, hi)
+  int64_t b0 = w * 64, b1 = b0 + 64;
+  int64_t s = lo > b0 ? lo : b0, e = hi < b1 ? hi : b1;
+  if (s >= e) return 0ull;
+  int sb = (int)(s - b0), eb = (int)(e - b0);
+  uint64_t upto = eb == 64 ? ~0ull : ((1ull << eb) - 1ull);
+  uint64_t from = ~((1ull << sb) - 1ull);
+  return upto & from;
+}
+
+#define BREED_WARPS 8
+#define MAX_FLIPS 32
+
+__global__ void __launch_bounds__(BREED_WARPS * 32)
+breed_kernel(int32_t k, int32_t words, const uint64_t* __restrict__ parents,
+             const double* __restrict__ fit, int64_t n_parents, uint64_t* __restrict__ children,
+             int64_t n_children, const uint64_t* __restrict__ keep, int64_t n_keep, uint64_t seed,
+             uint32_t generation, uint32_t stream_id, int32_t tournament, double rate,
+             double log1m_rate) {
+  __shared__ int64_t s_flip[BREED_WARPS][MAX_FLIPS];
+  const int lane = threadIdx.x & 31;
+  const int warp = threadIdx.x >> 5;
+  const int64_t stride = (int64_t)gridDim.x * BREED_WARPS;
+  for (int64_t child = (int64_t)blockIdx.x * BREED_WARPS + warp; child < n_children; child += stride) {
+    uint64_t* out = children + child * words;
+    if (child < n_keep) {
+      for (int32_t w = lane; w < words; w += 32) out[w] = keep[child * words + w];
+      continue;
+    }
+    int64_t pa = 0, pb = 0, ci = 0, cj = 0;
+    int nflip = 0;
+    bool dense = false;
+    if (lane == 0) {
+      Philox rng(seed, (uint32_t)child, (uint32_t)(child >> 32) ^ (generation * 0x9E3779B9u),
+                 stream_id);
+      for (int t = 0; t < 2; ++t) {
+        int64_t best = rng.below((uint32_t)n_parents);
+        for (int j = 1; j < tournament; ++j) {
+          int64_t i = rng.below((uint32_t)n_parents);
+          if (fit[i] < fit[best]) best = i;
+        }
+        if (t == 0) pa = best;
+        else pb = best;
+      }
+      if (k >= 2) {
+        int64_t x = rng.below((uint32_t)(k + 1)), y = rng.below((uint32_t)(k + 1));
+        ci = x < y ? x : y;
+        cj = x < y ? y : x;
+      }
+      // mutation positions by geometric gaps
+      if (rate >= 1.0 || rate * (double)k > 8.0) {
+        dense = true;
+      } else if (rate > 0.0) {
+        int64_t pos = -1;
+        while (true) {
+          double u = rng.unit();
+          double gap = floor(log(u) / log1m_rate);
+          if (!(gap < (double)k)) break;
+          pos += 1 + (int64_t)gap;
+          if (pos >= k) break;
+          if (nflip == MAX_FLIPS) {
+            dense = true;  // too many: fall back to per-bit draws below
+            break;
+          }
+          s_flip[warp][nflip++] = pos;
+        }
+      }
+    }
+    pa = __shfl_sync(0xffffffffu, pa, 0);
+    pb = __shfl_sync(0xffffffffu, pb, 0);
+    ci = __shfl_sync(0xffffffffu, ci, 0);
+    cj = __shfl_sync(0xffffffffu, cj, 0);
+    nflip = __shfl_sync(0xffffffffu, nflip, 0);
+    dense = __shfl_sync(0xffffffffu, dense, 0);
+    __syncwarp();
+    const uint64_t* A = parents + pa * words;
+    const uint64_t* B = parents + pb * words;
+    for (int32_t w = lane; w < words; w += 32) {
+      uint64_t mb = seg_mask(ci, cj, w);
+      uint64_t v = (A[w] & ~mb) | (B[w] & mb);
+      if (dense) {
+        Philox r2(seed ^ 0xA5A5A5A5A5A5A5A5ull, (uint32_t)child, (uint32_t)w,
+                  generation ^ (stream_id << 16));
+        uint64_t flips = 0;
+        for (int b = 0; b < 64; ++b) {
+          int64_t bit = (int64_t)w * 64 + b;
+          if (bit >= k) break;
+          double u = ((double)(r2.next() >> 8) + 0.5) * (1.0 / 16777216.0);
+          if (u < rate) flips |= 1ull << b;
+        }
+        v ^= flips;
+      } else {
+        for (int f = 0; f < nflip; ++f) {
+          int64_t pos = s_flip[warp][f];
+          if ((pos >> 6) == w) v ^= 1ull << (pos & 63);
+        }
+      }
+      if ((int64_t)(w + 1) * 64 > k) v &= (k % 64) ? ((1ull << (k % 64)) - 1ull) : ~0ull;
+      out[w] = v;
+    }
+    __syncwarp();
+  }
+}
+
+struct cb_es_plan;
+extern "C" int cb_es_plan_query(const cb_es_plan* p, cb_es_plan_info* info);
+
+extern "C" int cb_es_breed(cb_es_plan* p, const uint64_t* d_parents, const double* d_parent_fit,
+                           int64_t n_parents, uint64_t* d_children, int64_t n_children,
+                           const uint64_t* d_keep, int64_t n_keep, uint64_t seed,
+                           uint64_t generation, uint64_t stream_id, int32_t tournament,
+                           double mutation_rate, void* stream) {
+  CB_ARG_CHECK(p && d_parents && d_parent_fit && d_children && n_parents > 0 && tournament >= 1,
+               "cb_es_breed: bad arguments");
+  CB_ARG_CHECK(n_parents < (int64_t)0xffffffffll, "cb_es_breed: too many parents");
+  CB_ARG_CHECK(n_keep == 0 || d_keep, "cb_es_breed: keep rows missing");
+  cb_es_plan_info info;
+  cb_es_plan_query(p, &info);
+  if (n_children <= 0) return CB_OK;
+  double log1m = (mutation_rate > 0.0 && mutation_rate < 1.0) ? log1p(-mutation_rate) : -1.0;
+  int64_t blocks = (n_children + BREED_WARPS - 1) / BREED_WARPS;
+  if (blocks > 148 * 16) blocks = 148 * 16;
+  breed_kernel<<<(unsigned)blocks, BREED_WARPS * 32, 0, (cudaStream_t)stream>>>(
+      info.genome_bits, info.words, d_parents, d_parent_fit, n_parents, d_children, n_children,
+      d_keep, n_keep, seed, (uint32_t)generation, (uint32_t)stream_id, tournament, mutation_rate,
+      log1m);
+  CB_CUDA_TRY(cudaGetLastError());
+  return CB_OK;
+}
+
+__global__ void unpack_kv(const cub::KeyValuePair<int, double>* kv, int64_t* idx, double* val) {
+  *idx = kv->key;
+  *val = kv->value;
+}
+
+extern "C" int cb_argmin(const double* d_fit, int64_t n, int64_t* d_idx, double* d_val,
+                         void* stream) {
+  CB_ARG_CHECK(d_fit && d_idx && d_val && n > 0, "cb_argmin: bad arguments");
+  static thread_local void* tmp = nullptr;
+  static thread_local size_t tmp_bytes = 0;
+  static thread_local cub::KeyValuePair<int, double>* kv = nullptr;
+  size_t bytes = 0;
+  cudaStream_t s = (cudaStream_t)stream;
+  if (!kv) CB_CUDA_TRY(cudaMalloc((void**)&kv, sizeof(*kv)));
+  CB_CUDA_TRY(cub::DeviceReduce::ArgMin(nullptr, bytes, d_fit, kv, (int)n, s));
+  if (bytes > tmp_bytes) {
+    if (tmp) cudaFree(tmp);
+    CB_CUDA_TRY(cudaMalloc(&tmp, bytes));
+    tmp_bytes = bytes;
+  }
+  CB_CUDA_TRY(cub::DeviceReduce::ArgMin(tmp, bytes, d_fit, kv, (int)n, s));
+  unpack_kv<<<1, 1, 0, s>>>(kv, d_idx, d_val);
+  CB_CUDA_TRY(cudaGetLastError());
+  return CB_OK;
+}

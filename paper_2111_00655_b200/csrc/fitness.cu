@@ -1,0 +1,704 @@
+// Graph-level fitness of offload genomes, batched over a population.
+//
+// Reference semantics (tensorplace/evolution.py:256-371 and
+// tensorplace/cost.py:320-373): bit i of a genome moves the i-th eligible
+// kernel (canonical placement order, not on a graph inference library) to
+// the target graph backend -- as one same-node-set match of that backend
+// when registered, else decomposed into its singleton matches, else the
+// genome is infeasible (+inf).  The decoded placement is priced by grouping
+// graph-backend kernels of the same backend that touch through a data edge
+// into regions; every region costs round(fsum(member costs)) * r(n) + eps
+// with r(n) = max(floor, 1 - alpha * (n - 1)), every other kernel its cost +
+// eps, and the total is the fsum of all terms.
+//
+// Plan (host, once per DP placement): everything that does not depend on the
+// genome is folded into constants -- regions of other graph backends, the
+// kernels' own costs -- and the genome-dependent part is reduced to a small
+// "dynamic unit" graph: one unit per feasible eligible kernel plus one unit
+// per connected component of fixed target-backend kernels (always on).
+//
+// Evaluation (device): one warp per genome (units fit in shared memory) or
+// one CTA per genome (large graphs, scratch in global memory / L2).  Lanes
+// switch units on from the genome bits, hook the union-find over dynamic
+// edges with shared-memory CAS (lock-free, smaller root wins), accumulate
+// exact region sums with multi-limb shared-memory atomics, and add the
+// region terms and removed op-kernel terms into a 192-bit total that a
+// shuffle reduction finishes and rounds once.
+#include <algorithm>
+#include <cstring>
+#include <numeric>
+
+#include "cb_internal.cuh"
+
+struct cb_es_plan {
+  int32_t k = 0;       // genome bits
+  int32_t words = 0;   // uint64 words per genome
+  int32_t M = 0;       // dynamic units
+  int32_t n_virtual = 0;
+  int32_t E = 0;
+  int32_t infeasible_bits = 0;
+  fx192 base_const;    // static regions + every eligible kernel's cost + eps
+  fx192 eps;
+  double seed_cost = 0.0;
+  bool smem_path = true;
+  // host copies
+  std::vector<int32_t> slot_kernel, rep_match_ptr, rep_match;
+  std::vector<int8_t> rep_kind;
+  std::vector<int32_t> unit_slot;  // slot of unit u, -1 for virtual units
+  std::vector<fx192> unit_rep, unit_off;
+  std::vector<int32_t> unit_cnt;
+  std::vector<int2> edges;
+  std::vector<uint64_t> infeas_mask;
+  std::vector<double> rt;  // r(n) of the target backend, n = 0..max
+  // device copies
+  DBuf<int32_t> d_unit_slot, d_unit_cnt;
+  DBuf<fx192> d_unit_rep, d_unit_off;
+  DBuf<int2> d_edges;
+  DBuf<uint64_t> d_infeas;
+  DBuf<double> d_rt;
+  DBuf<unsigned long long> d_flags;
+  DBuf<uint8_t> d_scratch;
+  size_t scratch_per_group = 0;
+  int32_t scratch_groups = 0;
+  // staging for the host-buffer entry point
+  DBuf<uint64_t> d_pop_stage;
+  DBuf<double> d_fit_stage;
+};
+
+static double region_r(double alpha, double floor_, int64_t n) {
+  // max(floor, 1.0 - alpha * (n - 1)) with two separately rounded operations
+  volatile double prod = alpha * (double)(n - 1);
+  volatile double t = 1.0 - prod;
+  return t > floor_ ? t : floor_;
+}
+
+namespace {
+struct DSU {
+  std::vector<int32_t> p;
+  explicit DSU(int32_t n) : p(n) { std::iota(p.begin(), p.end(), 0); }
+  int32_t find(int32_t x) {
+    while (p[x] != x) {
+      p[x] = p[p[x]];
+      x = p[x];
+    }
+    return x;
+  }
+  void unite(int32_t a, int32_t b) {
+    a = find(a);
+    b = find(b);
+    if (a != b) p[std::max(a, b)] = std::min(a, b);
+  }
+};
+}  // namespace
+
+static bool fx_term(double base, double r, const fx192& eps, fx192& out) {
+  // exact value of (base * r) + eps, base*r rounded once as in Python
+  volatile double prod = base * r;
+  bool ok = fx_from_double(prod, out);
+  fx_add(out, eps);
+  return ok;
+}
+
+extern "C" int cb_placement_cost_graphlevel(cb_graph* g, int32_t n_kernels, const int32_t* kernel_ptr,
+                                            const int32_t* kernel_nodes, const int32_t* kernel_backend,
+                                            const double* kernel_cost, int32_t n_backends,
+                                            const uint8_t* backend_is_graph, const double* region_alpha,
+                                            const double* region_floor, double epsilon, double* out) {
+  CB_ARG_CHECK(g && out && n_kernels >= 0 && (n_kernels == 0 || (kernel_ptr && kernel_nodes &&
+               kernel_backend && kernel_cost)) && backend_is_graph && region_alpha && region_floor,
+               "cb_placement_cost_graphlevel: bad arguments");
+  const int32_t n = g->n;
+  fx192 eps;
+  if (!fx_from_double(epsilon, eps)) {
+    cb_set_error("epsilon outside the exact range");
+    return CB_ERR_INEXACT;
+  }
+  std::vector<int32_t> kernel_of(n, -1);
+  for (int32_t k = 0; k < n_kernels; ++k) {
+    CB_ARG_CHECK(kernel_backend[k] >= 0 && kernel_backend[k] < n_backends, "backend out of range");
+    for (int32_t i = kernel_ptr[k]; i < kernel_ptr[k + 1]; ++i) {
+      int32_t v = kernel_nodes[i];
+      CB_ARG_CHECK(v >= 0 && v < n && kernel_of[v] < 0, "kernels must partition the graph");
+      kernel_of[v] = k;
+    }
+  }
+  for (int32_t v = 0; v < n; ++v) CB_ARG_CHECK(kernel_of[v] >= 0, "kernels must cover the graph");
+  DSU dsu(n_kernels);
+  for (int32_t v = 0; v < n; ++v)
+    for (int32_t j = g->in_ptr[v]; j < g->in_ptr[v + 1]; ++j) {
+      int32_t p = g->in_src[j];
+      if (p < 0) continue;
+      int32_t a = kernel_of[p], b = kernel_of[v];
+      if (a != b && kernel_backend[a] == kernel_backend[b] && backend_is_graph[kernel_backend[a]])
+        dsu.unite(a, b);
+    }
+  fx192 tot = fx_zero();
+  bool exact = true;
+  std::vector<fx192> sum(n_kernels, fx_zero());
+  std::vector<int32_t> cnt(n_kernels, 0);
+  for (int32_t k = 0; k < n_kernels; ++k) {
+    fx192 t;
+    exact &= fx_from_double(kernel_cost[k], t);
+    if (!backend_is_graph[kernel_backend[k]]) {
+      fx_add(tot, t);
+      fx_add(tot, eps);
+    } else {
+      int32_t r = dsu.find(k);
+      fx_add(sum[r], t);
+      cnt[r] += 1;
+    }
+  }
+  for (int32_t k = 0; k < n_kernels; ++k) {
+    if (!backend_is_graph[kernel_backend[k]] || dsu.find(k) != k) continue;
+    double r = region_r(region_alpha[kernel_backend[k]], region_floor[kernel_backend[k]], cnt[k]);
+    fx192 t;
+    exact &= fx_term(fx_to_double(sum[k]), r, eps, t);
+    fx_add(tot, t);
+  }
+  if (!exact) {
+    cb_set_error("a cost falls outside the exact accumulator range");
+    return CB_ERR_INEXACT;
+  }
+  *out = fx_to_double(tot);
+  return CB_OK;
+}
+
+extern "C" int cb_es_plan_create(cb_graph* g, cb_matches* m, int32_t n_kernels,
+                                 const int32_t* kernel_match, int32_t n_backends,
+                                 const uint8_t* backend_is_graph, const double* region_alpha,
+                                 const double* region_floor, int32_t target_backend,
+                                 double epsilon, cb_es_plan** out) {
+  CB_ARG_CHECK(g && m && out && kernel_match && backend_is_graph && region_alpha && region_floor,
+               "cb_es_plan_create: null argument");
+  CB_ARG_CHECK(m->by_root && m->n_groups == g->n, "cb_es_plan_create: matches must come from cb_match_all");
+  CB_ARG_CHECK(target_backend >= 0 && target_backend < n_backends, "cb_es_plan_create: bad target");
+  if (!m->costs_set) {
+    cb_set_error("cb_es_plan_create: kernel costs have not been set");
+    return CB_ERR_STATE;
+  }
+  int rc = cb_require_device();
+  if (rc != CB_OK) return rc;
+  rc = cb_matches_ensure_host(m);
+  if (rc != CB_OK) return rc;
+  const int32_t n = g->n;
+  cb_es_plan* P = new cb_es_plan();
+  auto bad = [&](const std::string& msg, int code) {
+    delete P;
+    cb_set_error(msg);
+    return code;
+  };
+  if (!fx_from_double(epsilon, P->eps)) return bad("epsilon outside the exact range", CB_ERR_INEXACT);
+  // kernel of every node
+  std::vector<int32_t> kernel_of(n, -1);
+  for (int32_t kk = 0; kk < n_kernels; ++kk) {
+    int32_t mi = kernel_match[kk];
+    if (mi < 0 || mi >= m->n_matches) return bad("kernel references an unknown match", CB_ERR_ARG);
+    for (int32_t i = m->mem_ptr[mi]; i < m->mem_ptr[mi + 1]; ++i) {
+      int32_t v = m->members[i];
+      if (kernel_of[v] >= 0) return bad("placement kernels overlap", CB_ERR_ARG);
+      kernel_of[v] = kk;
+    }
+  }
+  for (int32_t v = 0; v < n; ++v)
+    if (kernel_of[v] < 0) return bad("placement does not cover every node", CB_ERR_ARG);
+  std::vector<int32_t> kb(n_kernels);
+  std::vector<double> kc(n_kernels);
+  for (int32_t kk = 0; kk < n_kernels; ++kk) {
+    kb[kk] = m->backend[kernel_match[kk]];
+    kc[kk] = m->cost[kernel_match[kk]];
+    if (kb[kk] < 0 || kb[kk] >= n_backends) return bad("backend id out of range", CB_ERR_ARG);
+  }
+  // kernel adjacency through data edges
+  std::vector<int2> kadj;
+  for (int32_t v = 0; v < n; ++v)
+    for (int32_t j = g->in_ptr[v]; j < g->in_ptr[v + 1]; ++j) {
+      int32_t p = g->in_src[j];
+      if (p < 0) continue;
+      int32_t a = kernel_of[p], b = kernel_of[v];
+      if (a != b) kadj.push_back(make_int2(std::min(a, b), std::max(a, b)));
+    }
+  std::sort(kadj.begin(), kadj.end(), [](int2 x, int2 y) { return x.x != y.x ? x.x < y.x : x.y < y.y; });
+  kadj.erase(std::unique(kadj.begin(), kadj.end(), [](int2 x, int2 y) { return x.x == y.x && x.y == y.y; }),
+             kadj.end());
+
+  // eligible slots and their replacements
+  auto same_set = [&](int32_t a, int32_t b) {
+    int32_t na = m->mem_ptr[a + 1] - m->mem_ptr[a];
+    if (na != m->mem_ptr[b + 1] - m->mem_ptr[b]) return false;
+    return std::equal(m->members.begin() + m->mem_ptr[a], m->members.begin() + m->mem_ptr[a + 1],
+                      m->members.begin() + m->mem_ptr[b]);
+  };
+  std::vector<int32_t> slot_of_kernel(n_kernels, -1);
+  std::vector<fx192> slot_rep;
+  std::vector<int32_t> slot_cnt;
+  P->rep_match_ptr.push_back(0);
+  for (int32_t kk = 0; kk < n_kernels; ++kk) {
+    if (backend_is_graph[kb[kk]]) continue;
+    int32_t s = (int32_t)P->slot_kernel.size();
+    slot_of_kernel[kk] = s;
+    P->slot_kernel.push_back(kk);
+    const int32_t km = kernel_match[kk];
+    const int32_t r = m->root[km];
+    int8_t kind = 0;
+    fx192 rep = fx_zero();
+    int32_t cnt = 0;
+    for (int32_t c = m->group_ptr[r]; c < m->group_ptr[r + 1]; ++c)
+      if (m->backend[c] == target_backend && same_set(c, km)) {
+        kind = 1;
+        P->rep_match.push_back(c);
+        if (!fx_from_double(m->cost[c], rep)) return bad("cost outside exact range", CB_ERR_INEXACT);
+        cnt = 1;
+        break;
+      }
+    if (!kind) {
+      kind = 2;
+      size_t mark = P->rep_match.size();
+      for (int32_t i = m->mem_ptr[km]; i < m->mem_ptr[km + 1]; ++i) {
+        const int32_t u = m->members[i];
+        int32_t found = -1;
+        for (int32_t c = m->group_ptr[u]; c < m->group_ptr[u + 1]; ++c)
+          if (m->backend[c] == target_backend && m->mem_ptr[c + 1] - m->mem_ptr[c] == 1) {
+            found = c;
+            break;
+          }
+        if (found < 0) {
+          kind = 0;
+          break;
+        }
+        P->rep_match.push_back(found);
+        fx192 t;
+        if (!fx_from_double(m->cost[found], t)) return bad("cost outside exact range", CB_ERR_INEXACT);
+        fx_add(rep, t);
+        ++cnt;
+      }
+      if (!kind) {
+        P->rep_match.resize(mark);
+        rep = fx_zero();
+        cnt = 0;
+      }
+    }
+    P->rep_kind.push_back(kind);
+    P->rep_match_ptr.push_back((int32_t)P->rep_match.size());
+    slot_rep.push_back(rep);
+    slot_cnt.push_back(cnt);
+  }
+  P->k = (int32_t)P->slot_kernel.size();
+  P->words = (P->k + 63) / 64;
+  if (P->words == 0) P->words = 1;
+
+  // fixed graph kernels: target-backend components become virtual units,
+  // other graph backends form static regions
+  DSU dsu(n_kernels);
+  for (const int2& e : kadj) {
+    bool ga = backend_is_graph[kb[e.x]], gb = backend_is_graph[kb[e.y]];
+    if (ga && gb && kb[e.x] == kb[e.y]) dsu.unite(e.x, e.y);
+  }
+  fx192 cst = fx_zero();
+  bool exact = true;
+  std::vector<fx192> comp_sum(n_kernels, fx_zero());
+  std::vector<int32_t> comp_cnt(n_kernels, 0);
+  for (int32_t kk = 0; kk < n_kernels; ++kk) {
+    if (!backend_is_graph[kb[kk]]) {
+      fx192 t;
+      exact &= fx_from_double(kc[kk], t);
+      fx_add(cst, t);
+      fx_add(cst, P->eps);
+      continue;
+    }
+    int32_t r = dsu.find(kk);
+    fx192 t;
+    exact &= fx_from_double(kc[kk], t);
+    fx_add(comp_sum[r], t);
+    comp_cnt[r] += 1;
+  }
+  std::vector<int32_t> virtual_of(n_kernels, -1);
+  std::vector<fx192> v_rep;
+  std::vector<int32_t> v_cnt;
+  for (int32_t kk = 0; kk < n_kernels; ++kk) {
+    if (!backend_is_graph[kb[kk]] || dsu.find(kk) != kk) continue;
+    if (kb[kk] == target_backend) {
+      virtual_of[kk] = (int32_t)v_rep.size();
+      v_rep.push_back(comp_sum[kk]);
+      v_cnt.push_back(comp_cnt[kk]);
+    } else {
+      double base = fx_to_double(comp_sum[kk]);
+      double r = region_r(region_alpha[kb[kk]], region_floor[kb[kk]], comp_cnt[kk]);
+      fx192 t;
+      exact &= fx_term(base, r, P->eps, t);
+      fx_add(cst, t);
+    }
+  }
+  if (!exact) return bad("a cost falls outside the exact accumulator range", CB_ERR_INEXACT);
+  P->base_const = cst;
+
+  // dynamic units: feasible eligible slots, then virtual units
+  std::vector<int32_t> unit_of_slot(P->k, -1);
+  P->infeas_mask.assign(P->words, 0ull);
+  for (int32_t s = 0; s < P->k; ++s) {
+    fx192 off;
+    fx_from_double(kc[P->slot_kernel[s]], off);
+    fx_add(off, P->eps);
+    if (P->rep_kind[s] == 0) {
+      P->infeas_mask[s >> 6] |= 1ull << (s & 63);
+      P->infeasible_bits++;
+      continue;
+    }
+    unit_of_slot[s] = (int32_t)P->unit_slot.size();
+    P->unit_slot.push_back(s);
+    P->unit_rep.push_back(slot_rep[s]);
+    P->unit_cnt.push_back(slot_cnt[s]);
+    P->unit_off.push_back(off);
+  }
+  const int32_t n_elig_units = (int32_t)P->unit_slot.size();
+  for (size_t i = 0; i < v_rep.size(); ++i) {
+    P->unit_slot.push_back(-1);
+    P->unit_rep.push_back(v_rep[i]);
+    P->unit_cnt.push_back(v_cnt[i]);
+    P->unit_off.push_back(fx_zero());
+  }
+  P->n_virtual = (int32_t)v_rep.size();
+  P->M = (int32_t)P->unit_slot.size();
+  auto unit_of_kernel = [&](int32_t kk) -> int32_t {
+    if (!backend_is_graph[kb[kk]]) {
+      int32_t s = slot_of_kernel[kk];
+      return unit_of_slot[s];
+    }
+    if (kb[kk] != target_backend) return -1;
+    return n_elig_units + virtual_of[dsu.find(kk)];
+  };
+  for (const int2& e : kadj) {
+    int32_t a = unit_of_kernel(e.x), b = unit_of_kernel(e.y);
+    if (a < 0 || b < 0 || a == b) continue;
+    P->edges.push_back(make_int2(std::min(a, b), std::max(a, b)));
+  }
+  std::sort(P->edges.begin(), P->edges.end(), [](int2 x, int2 y) { return x.x != y.x ? x.x < y.x : x.y < y.y; });
+  P->edges.erase(std::unique(P->edges.begin(), P->edges.end(),
+                             [](int2 x, int2 y) { return x.x == y.x && x.y == y.y; }),
+                 P->edges.end());
+  P->E = (int32_t)P->edges.size();
+  int64_t max_cnt = 0;
+  for (int32_t c : P->unit_cnt) max_cnt += c;
+  P->rt.resize((size_t)max_cnt + 2);
+  for (int64_t c = 0; c < (int64_t)P->rt.size(); ++c)
+    P->rt[c] = region_r(region_alpha[target_backend], region_floor[target_backend], c);
+  // seed (all-zero genome) cost
+  {
+    fx192 tot = P->base_const;
+    for (int32_t i = 0; i < P->n_virtual; ++i) {
+      int32_t u = n_elig_units + i;
+      fx192 t;
+      fx_term(fx_to_double(P->unit_rep[u]), P->rt[P->unit_cnt[u]], P->eps, t);
+      fx_add(tot, t);
+    }
+    P->seed_cost = fx_to_double(tot);
+  }
+  // device upload
+  auto fail_cuda = [&](cudaError_t e) {
+    delete P;
+    cb_set_error(std::string("CUDA error in plan upload: ") + cudaGetErrorString(e));
+    return CB_ERR_CUDA;
+  };
+  cudaError_t e;
+  if ((e = P->d_unit_slot.upload(P->unit_slot)) != cudaSuccess) return fail_cuda(e);
+  if ((e = P->d_unit_cnt.upload(P->unit_cnt)) != cudaSuccess) return fail_cuda(e);
+  if ((e = P->d_unit_rep.upload(P->unit_rep)) != cudaSuccess) return fail_cuda(e);
+  if ((e = P->d_unit_off.upload(P->unit_off)) != cudaSuccess) return fail_cuda(e);
+  if ((e = P->d_edges.upload(P->edges)) != cudaSuccess) return fail_cuda(e);
+  if ((e = P->d_infeas.upload(P->infeas_mask)) != cudaSuccess) return fail_cuda(e);
+  if ((e = P->d_rt.upload(P->rt)) != cudaSuccess) return fail_cuda(e);
+  if ((e = P->d_flags.alloc(2)) != cudaSuccess) return fail_cuda(e);
+  cudaMemset(P->d_flags.p, 0, 2 * sizeof(unsigned long long));
+  const size_t per_warp = (size_t)P->words * 8 + (size_t)P->M * (sizeof(fx192) + 8);
+  P->smem_path = per_warp * 4 <= 200 * 1024;
+  *out = P;
+  return CB_OK;
+}
+
+extern "C" int cb_es_plan_query(const cb_es_plan* p, cb_es_plan_info* info) {
+  CB_ARG_CHECK(p && info, "cb_es_plan_query: null argument");
+  info->genome_bits = p->k;
+  info->words = p->words;
+  info->units = p->M;
+  info->fixed_units = p->n_virtual;
+  info->edges = p->E;
+  info->infeasible_bits = p->infeasible_bits;
+  info->smem_path = p->smem_path ? 1 : 0;
+  info->seed_cost = p->seed_cost;
+  return CB_OK;
+}
+
+extern "C" int cb_es_plan_slots(const cb_es_plan* p, int32_t* slot_kernel, int8_t* rep_kind,
+                                int32_t* rep_match_ptr, int32_t* rep_match) {
+  CB_ARG_CHECK(p, "cb_es_plan_slots: null plan");
+  if (slot_kernel) std::copy(p->slot_kernel.begin(), p->slot_kernel.end(), slot_kernel);
+  if (rep_kind) std::copy(p->rep_kind.begin(), p->rep_kind.end(), rep_kind);
+  if (rep_match_ptr) std::copy(p->rep_match_ptr.begin(), p->rep_match_ptr.end(), rep_match_ptr);
+  if (rep_match) std::copy(p->rep_match.begin(), p->rep_match.end(), rep_match);
+  return CB_OK;
+}
+
+extern "C" void cb_es_plan_destroy(cb_es_plan* p) { delete p; }
+
+// ----------------------------------------------------------------- device
+struct FitArgs {
+  int32_t k, words, M, E;
+  fx192 base_const, eps;
+  const int32_t* unit_slot;
+  const int32_t* unit_cnt;
+  const fx192* unit_rep;
+  const fx192* unit_off;
+  const int2* edges;
+  const uint64_t* infeas;
+  const double* rt;
+  unsigned long long* flags;
+};
+
+__device__ __forceinline__ int32_t uf_find(volatile int32_t* parent, int32_t x) {
+  while (true) {
+    int32_t p = parent[x];
+    if (p == x) return x;
+    int32_t gp = parent[p];
+    if (gp != p) parent[x] = gp;  // path halving (only ever points to an ancestor)
+    x = p;
+  }
+}
+
+__device__ __forceinline__ void uf_union(int32_t* parent, int32_t a, int32_t b) {
+  volatile int32_t* vp = parent;
+  while (true) {
+    a = uf_find(vp, a);
+    b = uf_find(vp, b);
+    if (a == b) return;
+    int32_t hi = a > b ? a : b, lo = a > b ? b : a;
+    if (atomicCAS(parent + hi, hi, lo) == hi) return;
+  }
+}
+
+__device__ __forceinline__ void atomic_add_fx(fx192* dst, const fx192& v) {
+  unsigned long long* w = reinterpret_cast<unsigned long long*>(dst->w);
+  unsigned long long o0 = atomicAdd(w + 0, (unsigned long long)v.w[0]);
+  unsigned long long c0 = (o0 + v.w[0]) < o0;
+  unsigned long long a1 = v.w[1] + c0;
+  unsigned long long c1 = a1 < c0;  // v.w[1] == max and c0
+  unsigned long long o1 = atomicAdd(w + 1, a1);
+  c1 += (o1 + a1) < o1;
+  atomicAdd(w + 2, (unsigned long long)(v.w[2] + c1));
+}
+
+__device__ __forceinline__ fx192 shfl_xor_fx(const fx192& v, int m) {
+  fx192 r;
+  r.w[0] = __shfl_xor_sync(0xffffffffu, v.w[0], m);
+  r.w[1] = __shfl_xor_sync(0xffffffffu, v.w[1], m);
+  r.w[2] = __shfl_xor_sync(0xffffffffu, v.w[2], m);
+  return r;
+}
+
+// One group (warp or CTA) evaluates one genome.  `parent`, `acc`, `cnt`
+// point at this group's scratch (shared or global memory).
+template <int GROUP>
+__device__ void eval_genome(const FitArgs& a, const uint64_t* __restrict__ genome,
+                            int32_t* parent, fx192* acc, int32_t* cnt, double* out,
+                            fx192* red_scratch, int* red_flag) {
+  const int t = threadIdx.x % GROUP;
+  auto gsync = [&]() {
+    if (GROUP == 32) __syncwarp();
+    else __syncthreads();
+  };
+  // infeasibility
+  int bad = 0;
+  for (int32_t w = t; w < a.words; w += GROUP) bad |= (genome[w] & a.infeas[w]) != 0ull;
+  bool any_bad;
+  if (GROUP == 32) {
+    any_bad = __any_sync(0xffffffffu, bad);
+  } else {
+    if (t == 0) *red_flag = 0;
+    __syncthreads();
+    if (bad) *red_flag = 1;
+    __syncthreads();
+    any_bad = *red_flag != 0;
+    __syncthreads();
+  }
+  if (any_bad) {
+    if (t == 0) *out = __longlong_as_double(0x7ff0000000000000ll);
+    return;
+  }
+  // switch units on
+  for (int32_t u = t; u < a.M; u += GROUP) {
+    const int32_t s = a.unit_slot[u];
+    const bool on = s < 0 || ((genome[s >> 6] >> (s & 63)) & 1ull);
+    parent[u] = on ? u : -1;
+    acc[u] = fx_zero();
+    cnt[u] = 0;
+  }
+  gsync();
+  // hook regions
+  for (int32_t e = t; e < a.E; e += GROUP) {
+    const int2 ed = a.edges[e];
+    if (((volatile int32_t*)parent)[ed.x] >= 0 && ((volatile int32_t*)parent)[ed.y] >= 0)
+      uf_union(parent, ed.x, ed.y);
+  }
+  gsync();
+  // accumulate region sums; subtract the op-kernel terms of offloaded units
+  fx192 part = fx_zero();
+  for (int32_t u = t; u < a.M; u += GROUP) {
+    if (((volatile int32_t*)parent)[u] < 0) continue;
+    const int32_t r = uf_find((volatile int32_t*)parent, u);
+    atomic_add_fx(acc + r, a.unit_rep[u]);
+    atomicAdd(cnt + r, a.unit_cnt[u]);
+    fx_sub(part, a.unit_off[u]);
+  }
+  gsync();
+  bool inexact = false;
+  for (int32_t u = t; u < a.M; u += GROUP) {
+    if (((volatile int32_t*)parent)[u] != u) continue;
+    const fx192 sum = acc[u];
+    const double base = fx_to_double(sum);
+    const double prod = __dmul_rn(base, a.rt[cnt[u]]);
+    fx192 term;
+    inexact |= !fx_from_double(prod, term);
+    fx_add(term, a.eps);
+    fx_add(part, term);
+  }
+  if (inexact) atomicAdd(a.flags + 0, 1ull);
+  // reduce `part` over the group
+  for (int off = 16; off > 0; off >>= 1) {
+    fx192 o = shfl_xor_fx(part, off);
+    fx_add(part, o);
+  }
+  if (GROUP == 32) {
+    if (t == 0) {
+      fx_add(part, a.base_const);
+      *out = fx_to_double(part);
+    }
+  } else {
+    const int warp = t >> 5;
+    if ((t & 31) == 0) red_scratch[warp] = part;
+    __syncthreads();
+    if (t == 0) {
+      fx192 tot = a.base_const;
+      for (int w = 0; w < GROUP / 32; ++w) fx_add(tot, red_scratch[w]);
+      *out = fx_to_double(tot);
+    }
+    __syncthreads();
+  }
+}
+
+#define FIT_WARPS 4
+
+__global__ void __launch_bounds__(FIT_WARPS * 32)
+fitness_smem_kernel(FitArgs a, const uint64_t* __restrict__ pop, int64_t n, double* __restrict__ fit) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int warp = threadIdx.x >> 5;
+  const size_t per_warp = (size_t)a.M * (sizeof(fx192) + 8);
+  unsigned char* base = smem + per_warp * warp;
+  fx192* acc = reinterpret_cast<fx192*>(base);
+  int32_t* parent = reinterpret_cast<int32_t*>(base + (size_t)a.M * sizeof(fx192));
+  int32_t* cnt = parent + a.M;
+  const int64_t stride = (int64_t)gridDim.x * FIT_WARPS;
+  for (int64_t i = (int64_t)blockIdx.x * FIT_WARPS + warp; i < n; i += stride)
+    eval_genome<32>(a, pop + i * a.words, parent, acc, cnt, fit + i, nullptr, nullptr);
+}
+
+#define FIT_CTA 256
+
+__global__ void __launch_bounds__(FIT_CTA)
+fitness_global_kernel(FitArgs a, const uint64_t* __restrict__ pop, int64_t n, double* __restrict__ fit,
+                      unsigned char* scratch, size_t per_group) {
+  __shared__ fx192 red[FIT_CTA / 32];
+  __shared__ int flag;
+  unsigned char* base = scratch + per_group * blockIdx.x;
+  fx192* acc = reinterpret_cast<fx192*>(base);
+  int32_t* parent = reinterpret_cast<int32_t*>(base + (size_t)a.M * sizeof(fx192));
+  int32_t* cnt = parent + a.M;
+  for (int64_t i = blockIdx.x; i < n; i += gridDim.x)
+    eval_genome<FIT_CTA>(a, pop + i * a.words, parent, acc, cnt, fit + i, red, &flag);
+}
+
+static FitArgs make_args(cb_es_plan* p) {
+  FitArgs a;
+  a.k = p->k;
+  a.words = p->words;
+  a.M = p->M;
+  a.E = p->E;
+  a.base_const = p->base_const;
+  a.eps = p->eps;
+  a.unit_slot = p->d_unit_slot.p;
+  a.unit_cnt = p->d_unit_cnt.p;
+  a.unit_rep = p->d_unit_rep.p;
+  a.unit_off = p->d_unit_off.p;
+  a.edges = p->d_edges.p;
+  a.infeas = p->d_infeas.p;
+  a.rt = p->d_rt.p;
+  a.flags = p->d_flags.p;
+  return a;
+}
+
+static int sm_count() {
+  static int cached = 0;
+  if (!cached) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&cached, cudaDevAttrMultiProcessorCount, dev);
+    if (cached <= 0) cached = 148;
+  }
+  return cached;
+}
+
+static int launch_fitness(cb_es_plan* p, const uint64_t* d_pop, int64_t n, double* d_fit,
+                          cudaStream_t stream) {
+  if (n <= 0) return CB_OK;
+  FitArgs a = make_args(p);
+  if (p->smem_path) {
+    const size_t smem = (size_t)FIT_WARPS * p->M * (sizeof(fx192) + 8);
+    static size_t configured = 0;
+    if (smem > 48 * 1024 && configured < smem) {
+      CB_CUDA_TRY(cudaFuncSetAttribute(fitness_smem_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)std::max<size_t>(smem, 48 * 1024)));
+      configured = smem;
+    }
+    int per_sm = 0;
+    CB_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fitness_smem_kernel,
+                                                              FIT_WARPS * 32, smem));
+    if (per_sm < 1) per_sm = 1;
+    int64_t want = (n + FIT_WARPS - 1) / FIT_WARPS;
+    int64_t grid = std::min<int64_t>(want, (int64_t)per_sm * sm_count());
+    fitness_smem_kernel<<<(unsigned)grid, FIT_WARPS * 32, smem, stream>>>(a, d_pop, n, d_fit);
+  } else {
+    const size_t per_group = ((size_t)p->M * (sizeof(fx192) + 8) + 255) & ~(size_t)255;
+    int64_t grid = std::min<int64_t>(n, (int64_t)4 * sm_count());
+    if (p->scratch_per_group != per_group || p->scratch_groups < grid) {
+      CB_CUDA_TRY(p->d_scratch.alloc(per_group * grid));
+      p->scratch_per_group = per_group;
+      p->scratch_groups = (int32_t)grid;
+    }
+    fitness_global_kernel<<<(unsigned)grid, FIT_CTA, 0, stream>>>(a, d_pop, n, d_fit, p->d_scratch.p,
+                                                                   per_group);
+  }
+  CB_CUDA_TRY(cudaGetLastError());
+  return CB_OK;
+}
+
+extern "C" int cb_fitness_device(cb_es_plan* p, const uint64_t* d_pop, int64_t n, double* d_fit,
+                                 void* stream) {
+  CB_ARG_CHECK(p && (n == 0 || (d_pop && d_fit)), "cb_fitness_device: bad arguments");
+  return launch_fitness(p, d_pop, n, d_fit, (cudaStream_t)stream);
+}
+
+extern "C" int cb_fitness_host(cb_es_plan* p, const uint64_t* h_pop, int64_t n, double* h_fit) {
+  CB_ARG_CHECK(p && (n == 0 || (h_pop && h_fit)), "cb_fitness_host: bad arguments");
+  if (n == 0) return CB_OK;
+  const size_t words = (size_t)n * p->words;
+  if (p->d_pop_stage.n < words) CB_CUDA_TRY(p->d_pop_stage.alloc(words));
+  if (p->d_fit_stage.n < (size_t)n) CB_CUDA_TRY(p->d_fit_stage.alloc((size_t)n));
+  CB_CUDA_TRY(cudaMemcpy(p->d_pop_stage.p, h_pop, words * sizeof(uint64_t), cudaMemcpyHostToDevice));
+  int rc = launch_fitness(p, p->d_pop_stage.p, n, p->d_fit_stage.p, 0);
+  if (rc != CB_OK) return rc;
+  CB_CUDA_TRY(cudaMemcpy(h_fit, p->d_fit_stage.p, (size_t)n * sizeof(double), cudaMemcpyDeviceToHost));
+  unsigned long long flags[2] = {0, 0};
+  CB_CUDA_TRY(cudaMemcpy(flags, p->d_flags.p, sizeof(flags), cudaMemcpyDeviceToHost));
+  if (flags[0]) {
+    cb_set_error("a region cost fell outside the exact accumulator range");
+    return CB_ERR_INEXACT;
+  }
+  return CB_OK;
+}

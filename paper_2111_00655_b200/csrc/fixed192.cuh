@@ -1,0 +1,175 @@
+// Exact fixed-point accumulator shared by host plan builders and device kernels.
+//
+// The reference prices every placement with math.fsum, i.e. the exactly
+// rounded sum of its double terms (tensorplace/cost.py:300-305, :370-373).
+// Sums here are carried exactly in a 192-bit unsigned fixed-point number
+// (value = w[2]:w[1]:w[0] * 2^-128, range [0, 2^64)), which makes addition
+// associative, and are rounded to the nearest double (ties to even) once at
+// the end -- the same result fsum produces.  A double converts exactly when
+// its least significant bit is >= 2^-128 and it is < 2^64; anything else sets
+// the caller's `inexact` flag instead of silently losing bits.
+#pragma once
+#include <stdint.h>
+
+#ifdef __CUDACC__
+#define FXI __host__ __device__ __forceinline__
+#else
+#define FXI inline
+#endif
+
+struct fx192 {
+  uint64_t w[3];
+};
+
+FXI fx192 fx_zero() {
+  fx192 r;
+  r.w[0] = r.w[1] = r.w[2] = 0;
+  return r;
+}
+
+FXI bool fx_is_zero(const fx192& a) { return (a.w[0] | a.w[1] | a.w[2]) == 0; }
+
+// a += b (mod 2^192)
+FXI void fx_add(fx192& a, const fx192& b) {
+  uint64_t s0 = a.w[0] + b.w[0];
+  uint64_t c0 = s0 < a.w[0];
+  uint64_t t1 = a.w[1] + b.w[1];
+  uint64_t c1 = t1 < a.w[1];
+  uint64_t s1 = t1 + c0;
+  c1 += s1 < t1;
+  a.w[0] = s0;
+  a.w[1] = s1;
+  a.w[2] = a.w[2] + b.w[2] + c1;
+}
+
+// a -= b (mod 2^192); exact whenever the true result is non-negative
+FXI void fx_sub(fx192& a, const fx192& b) {
+  uint64_t d0 = a.w[0] - b.w[0];
+  uint64_t br0 = a.w[0] < b.w[0];
+  uint64_t t1 = a.w[1] - b.w[1];
+  uint64_t br1 = a.w[1] < b.w[1];
+  uint64_t d1 = t1 - br0;
+  br1 += t1 < br0;
+  a.w[0] = d0;
+  a.w[1] = d1;
+  a.w[2] = a.w[2] - b.w[2] - br1;
+}
+
+FXI int fx_cmp(const fx192& a, const fx192& b) {
+  if (a.w[2] != b.w[2]) return a.w[2] < b.w[2] ? -1 : 1;
+  if (a.w[1] != b.w[1]) return a.w[1] < b.w[1] ? -1 : 1;
+  if (a.w[0] != b.w[0]) return a.w[0] < b.w[0] ? -1 : 1;
+  return 0;
+}
+
+FXI bool fx_eq(const fx192& a, const fx192& b) {
+  return a.w[0] == b.w[0] && a.w[1] == b.w[1] && a.w[2] == b.w[2];
+}
+
+FXI uint64_t fx_bits_of(double d) {
+#ifdef __CUDA_ARCH__
+  return (uint64_t)__double_as_longlong(d);
+#else
+  union { double d; uint64_t u; } c;
+  c.d = d;
+  return c.u;
+#endif
+}
+
+FXI double fx_double_of(uint64_t u) {
+#ifdef __CUDA_ARCH__
+  return __longlong_as_double((long long)u);
+#else
+  union { double d; uint64_t u; } c;
+  c.u = u;
+  return c.d;
+#endif
+}
+
+// Exact conversion of a non-negative finite double.  Returns false (and
+// leaves the best truncated value in `out`) if bits would be lost or the
+// value is negative, non-finite or >= 2^64.
+FXI bool fx_from_double(double d, fx192& out) {
+  out = fx_zero();
+  uint64_t bits = fx_bits_of(d);
+  if (bits == 0) return true;                        // +0.0
+  if (bits >> 63) return bits == 0x8000000000000000ull;  // -0.0 ok, negatives not
+  int ex = (int)((bits >> 52) & 0x7ff);
+  uint64_t mant = bits & ((1ull << 52) - 1);
+  if (ex == 0x7ff) return false;                     // inf / nan
+  int e;
+  if (ex == 0) {
+    e = -1074;
+  } else {
+    mant |= 1ull << 52;
+    e = ex - 1075;
+  }
+  int s = e + 128;  // bit position of the mantissa LSB inside the 192-bit word
+  bool exact = true;
+  if (s < 0) {
+    int sh = -s;
+    if (sh >= 64) {
+      return false;  // everything (non-zero) would be lost
+    }
+    if (mant & ((1ull << sh) - 1)) exact = false;
+    mant >>= sh;
+    s = 0;
+  }
+  if (s + 53 > 192) return false;  // >= 2^64
+  int limb = s >> 6;
+  int off = s & 63;
+  out.w[limb] = mant << off;
+  if (off != 0 && limb + 1 < 3) out.w[limb + 1] = mant >> (64 - off);
+  return exact;
+}
+
+FXI int fx_clz64(uint64_t x) {
+#ifdef __CUDA_ARCH__
+  return __clzll((long long)x);
+#else
+  return x ? __builtin_clzll(x) : 64;
+#endif
+}
+
+// Round to the nearest double, ties to even (what math.fsum returns).
+FXI double fx_to_double(const fx192& a) {
+  int limb = a.w[2] ? 2 : (a.w[1] ? 1 : (a.w[0] ? 0 : -1));
+  if (limb < 0) return 0.0;
+  int p = limb * 64 + 63 - fx_clz64(a.w[limb]);  // index of the MSB
+  uint64_t m;
+  bool round_bit = false, sticky = false;
+  if (p <= 52) {
+    m = a.w[0];  // fits exactly; p <= 52 implies limb 0
+  } else {
+    int sh = p - 52;  // drop `sh` low bits
+    // m = bits [sh, sh+53)
+    int l0 = sh >> 6, o0 = sh & 63;
+    m = a.w[l0] >> o0;
+    if (o0 != 0 && l0 + 1 < 3) m |= a.w[l0 + 1] << (64 - o0);
+    m &= (1ull << 53) - 1;
+    int rb = sh - 1;  // round bit index
+    round_bit = (a.w[rb >> 6] >> (rb & 63)) & 1ull;
+    // sticky: any bit below rb
+    int full = rb >> 6;
+    for (int i = 0; i < full; ++i) sticky |= a.w[i] != 0;
+    if (rb & 63) sticky |= (a.w[full] & ((1ull << (rb & 63)) - 1)) != 0;
+    if (round_bit && (sticky || (m & 1ull))) {
+      m += 1;
+      if (m == (1ull << 53)) {
+        m >>= 1;
+        p += 1;
+      }
+    }
+  }
+  if (p <= 52) {
+    // value = m * 2^-128 with m < 2^53: exact, normalised below
+    int q = 63 - fx_clz64(m);  // MSB of m
+    int ex = q - 128;          // unbiased exponent of the result
+    uint64_t frac = (m << (52 - q)) & ((1ull << 52) - 1);
+    return fx_double_of(((uint64_t)(ex + 1023) << 52) | frac);
+  }
+  int ex = p - 128;
+  uint64_t frac = m & ((1ull << 52) - 1);
+  if (ex > 1023) return fx_double_of(0x7ff0000000000000ull);
+  return fx_double_of(((uint64_t)(ex + 1023) << 52) | frac);
+}

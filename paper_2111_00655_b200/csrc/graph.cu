@@ -1,0 +1,289 @@
+// Graph container, host-side structural analysis and device upload.
+//
+// Mirrors the structural queries of tensorplace/graph.py: deterministic
+// topological order with smallest-id tie-break (:345-364), longest-path depth
+// (:366-371) and immediate post-dominators relative to a virtual sink that
+// joins all outputs (:413-444).  The reference materialises full
+// post-dominator sets (quadratic); here the post-dominator tree is built
+// directly by intersecting successor paths in reverse topological order
+// (Cooper-Harvey-Kennedy on the reversed DAG), which yields the same
+// immediate post-dominator: the nearest strict post-dominator is exactly the
+// one with the smallest topological index (graph.py:441).
+#include <algorithm>
+#include <cstring>
+#include <mutex>
+#include <queue>
+
+#include "cb_internal.cuh"
+
+static thread_local std::string g_last_error;
+
+void cb_set_error(const std::string& msg) { g_last_error = msg; }
+
+extern "C" const char* cb_last_error(void) { return g_last_error.c_str(); }
+
+extern "C" int cb_abi_version(void) { return 1; }
+
+extern "C" int cb_device_available(void) {
+  int count = 0;
+  if (cudaGetDeviceCount(&count) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  return count > 0 ? 1 : 0;
+}
+
+int cb_require_device() {
+  if (!cb_device_available()) {
+    cb_set_error("no CUDA device available: the placement search runs only on the GPU");
+    return CB_ERR_CUDA;
+  }
+  return CB_OK;
+}
+
+extern "C" int cb_fx_sum(const double* xs, int64_t n, double* out, int32_t* exact) {
+  CB_ARG_CHECK(out && exact && (n == 0 || xs), "cb_fx_sum: null argument");
+  fx192 acc = fx_zero();
+  bool ok = true;
+  for (int64_t i = 0; i < n; ++i) {
+    fx192 t;
+    ok &= fx_from_double(xs[i], t);
+    fx_add(acc, t);
+  }
+  *out = fx_to_double(acc);
+  *exact = ok ? 1 : 0;
+  return CB_OK;
+}
+
+extern "C" int cb_graph_create(int32_t n, const int32_t* kind, const int32_t* in_ptr,
+                               const int32_t* in_src, const uint8_t* is_output,
+                               const double* volume, const int32_t* attr_ptr,
+                               const int32_t* attr_key, const int8_t* attr_tag,
+                               const int64_t* attr_ival, const double* attr_fval,
+                               cb_graph** out) {
+  CB_ARG_CHECK(out && n >= 0, "cb_graph_create: bad arguments");
+  CB_ARG_CHECK(n == 0 || (kind && in_ptr && is_output && volume && attr_ptr),
+               "cb_graph_create: null array");
+  cb_graph* g = new cb_graph();
+  g->n = n;
+  g->kind.assign(kind, kind + n);
+  g->in_ptr.assign(in_ptr, in_ptr + n + 1);
+  if (n == 0) g->in_ptr.assign(1, 0);
+  int32_t nnz = g->in_ptr[n];
+  g->in_src.assign(in_src, in_src + nnz);
+  g->is_output.assign(is_output, is_output + n);
+  g->volume.assign(volume, volume + n);
+  g->attr_ptr.assign(attr_ptr, attr_ptr + n + 1);
+  if (n == 0) g->attr_ptr.assign(1, 0);
+  int32_t na = g->attr_ptr[n];
+  g->attr_key.assign(attr_key, attr_key + na);
+  g->attr_tag.assign(attr_tag, attr_tag + na);
+  g->attr_ival.assign(attr_ival, attr_ival + na);
+  g->attr_fval.assign(attr_fval, attr_fval + na);
+  for (int32_t j = 0; j < nnz; ++j) {
+    if (g->in_src[j] < -1 || g->in_src[j] >= n) {
+      delete g;
+      cb_set_error("cb_graph_create: input reference out of range");
+      return CB_ERR_ARG;
+    }
+  }
+  // distinct consumers, ascending
+  std::vector<std::vector<int32_t>> cons(n);
+  for (int32_t v = 0; v < n; ++v)
+    for (int32_t j = g->in_ptr[v]; j < g->in_ptr[v + 1]; ++j)
+      if (g->in_src[j] >= 0) cons[g->in_src[j]].push_back(v);
+  g->out_ptr.assign(n + 1, 0);
+  for (int32_t v = 0; v < n; ++v) {
+    auto& c = cons[v];
+    std::sort(c.begin(), c.end());
+    c.erase(std::unique(c.begin(), c.end()), c.end());
+    g->out_ptr[v + 1] = g->out_ptr[v] + (int32_t)c.size();
+  }
+  g->out_dst.reserve(g->out_ptr[n]);
+  for (int32_t v = 0; v < n; ++v) g->out_dst.insert(g->out_dst.end(), cons[v].begin(), cons[v].end());
+  *out = g;
+  return CB_OK;
+}
+
+extern "C" void cb_graph_destroy(cb_graph* g) { delete g; }
+
+int cb_graph_ensure_analysis(cb_graph* g) {
+  if (g->analysed) return g->cycle_node >= 0 ? CB_ERR_CYCLE : CB_OK;
+  const int32_t n = g->n;
+  // Kahn with a min-heap over node indices (= ascending node ids).
+  std::vector<int32_t> pending(n, 0);
+  for (int32_t v = 0; v < n; ++v) {
+    // count distinct node predecessors
+    std::vector<int32_t> preds;
+    for (int32_t j = g->in_ptr[v]; j < g->in_ptr[v + 1]; ++j)
+      if (g->in_src[j] >= 0) preds.push_back(g->in_src[j]);
+    std::sort(preds.begin(), preds.end());
+    pending[v] = (int32_t)(std::unique(preds.begin(), preds.end()) - preds.begin());
+  }
+  std::priority_queue<int32_t, std::vector<int32_t>, std::greater<int32_t>> ready;
+  for (int32_t v = 0; v < n; ++v)
+    if (pending[v] == 0) ready.push(v);
+  g->topo.clear();
+  g->topo.reserve(n);
+  while (!ready.empty()) {
+    int32_t v = ready.top();
+    ready.pop();
+    g->topo.push_back(v);
+    for (int32_t j = g->out_ptr[v]; j < g->out_ptr[v + 1]; ++j) {
+      int32_t c = g->out_dst[j];
+      if (--pending[c] == 0) ready.push(c);
+    }
+  }
+  g->analysed = true;
+  if ((int32_t)g->topo.size() != n) {
+    for (int32_t v = 0; v < n; ++v)
+      if (pending[v] > 0) {
+        g->cycle_node = v;
+        break;
+      }
+    cb_set_error("graph contains a cycle");
+    return CB_ERR_CYCLE;
+  }
+  // longest-path depth
+  g->depth.assign(n, 0);
+  for (int32_t v : g->topo) {
+    int32_t d = -1;
+    for (int32_t j = g->in_ptr[v]; j < g->in_ptr[v + 1]; ++j)
+      if (g->in_src[j] >= 0) d = std::max(d, g->depth[g->in_src[j]]);
+    g->depth[v] = d + 1;
+  }
+  // immediate post-dominators; index n is the virtual sink
+  const int32_t SINK = n;
+  std::vector<int32_t> ip(n + 1, -2), pdd(n + 1, 0);
+  ip[SINK] = SINK;
+  auto lca = [&](int32_t a, int32_t b) {
+    while (a != b) {
+      if (pdd[a] > pdd[b]) a = ip[a];
+      else if (pdd[b] > pdd[a]) b = ip[b];
+      else { a = ip[a]; b = ip[b]; }
+    }
+    return a;
+  };
+  for (int32_t t = n - 1; t >= 0; --t) {
+    int32_t v = g->topo[t];
+    int32_t cur = -1;
+    if (g->is_output[v]) cur = SINK;
+    for (int32_t j = g->out_ptr[v]; j < g->out_ptr[v + 1]; ++j) {
+      int32_t c = g->out_dst[j];
+      cur = cur < 0 ? c : lca(cur, c);
+    }
+    if (cur < 0) cur = SINK;  // dead end (rejected by graph validation upstream)
+    ip[v] = cur;
+    pdd[v] = pdd[cur] + 1;
+  }
+  g->ipdom.assign(n, -1);
+  for (int32_t v = 0; v < n; ++v) g->ipdom[v] = ip[v] == SINK ? -1 : ip[v];
+  // post-dominator tree children (ascending) and Euler intervals
+  std::vector<int32_t> cnt(n + 2, 0);
+  for (int32_t v = 0; v < n; ++v)
+    if (g->ipdom[v] >= 0) cnt[g->ipdom[v] + 1]++;
+  g->pch_ptr.assign(n + 1, 0);
+  for (int32_t v = 0; v < n; ++v) g->pch_ptr[v + 1] = g->pch_ptr[v] + cnt[v + 1];
+  g->pch.assign(g->pch_ptr[n], 0);
+  {
+    std::vector<int32_t> fill(g->pch_ptr.begin(), g->pch_ptr.end() - 1);
+    for (int32_t v = 0; v < n; ++v)
+      if (g->ipdom[v] >= 0) g->pch[fill[g->ipdom[v]]++] = v;  // ascending v
+  }
+  g->pd_tin.assign(n, 0);
+  g->pd_tout.assign(n, 0);
+  {
+    int32_t clock = 0;
+    std::vector<std::pair<int32_t, int32_t>> st;  // (node, next child offset)
+    for (int32_t r = 0; r < n; ++r) {
+      if (g->ipdom[r] >= 0) continue;
+      st.push_back({r, g->pch_ptr[r]});
+      g->pd_tin[r] = clock++;
+      while (!st.empty()) {
+        auto& top = st.back();
+        if (top.second < g->pch_ptr[top.first + 1]) {
+          int32_t c = g->pch[top.second++];
+          g->pd_tin[c] = clock++;
+          st.push_back({c, g->pch_ptr[c]});
+        } else {
+          g->pd_tout[top.first] = clock++;
+          st.pop_back();
+        }
+      }
+    }
+  }
+  // levels in pop order (depth, index)
+  int32_t maxd = 0;
+  for (int32_t v = 0; v < n; ++v) maxd = std::max(maxd, g->depth[v]);
+  int32_t nl = n ? maxd + 1 : 0;
+  g->level_ptr.assign(nl + 1, 0);
+  for (int32_t v = 0; v < n; ++v) g->level_ptr[g->depth[v] + 1]++;
+  for (int32_t l = 0; l < nl; ++l) g->level_ptr[l + 1] += g->level_ptr[l];
+  g->level_nodes.assign(n, 0);
+  {
+    std::vector<int32_t> fill(g->level_ptr.begin(), g->level_ptr.end() - (nl ? 1 : 0));
+    for (int32_t v = 0; v < n; ++v) g->level_nodes[fill[g->depth[v]]++] = v;
+  }
+  return CB_OK;
+}
+
+extern "C" int cb_graph_analysis(cb_graph* g, int32_t* topo, int32_t* depth, int32_t* ipdom,
+                                 int32_t* pd_tin, int32_t* pd_tout, int32_t* cycle_node) {
+  CB_ARG_CHECK(g, "cb_graph_analysis: null graph");
+  int rc = cb_graph_ensure_analysis(g);
+  if (cycle_node) *cycle_node = g->cycle_node;
+  if (rc != CB_OK) return rc;
+  size_t n = (size_t)g->n;
+  if (topo) std::memcpy(topo, g->topo.data(), n * sizeof(int32_t));
+  if (depth) std::memcpy(depth, g->depth.data(), n * sizeof(int32_t));
+  if (ipdom) std::memcpy(ipdom, g->ipdom.data(), n * sizeof(int32_t));
+  if (pd_tin) std::memcpy(pd_tin, g->pd_tin.data(), n * sizeof(int32_t));
+  if (pd_tout) std::memcpy(pd_tout, g->pd_tout.data(), n * sizeof(int32_t));
+  return CB_OK;
+}
+
+int cb_graph_ensure_device(cb_graph* g) {
+  int rc = cb_require_device();
+  if (rc != CB_OK) return rc;
+  rc = cb_graph_ensure_analysis(g);
+  if (rc != CB_OK) return rc;
+  if (g->on_device) return CB_OK;
+  CB_CUDA_TRY(g->d_kind.upload(g->kind));
+  CB_CUDA_TRY(g->d_in_ptr.upload(g->in_ptr));
+  CB_CUDA_TRY(g->d_in_src.upload(g->in_src));
+  CB_CUDA_TRY(g->d_out_ptr.upload(g->out_ptr));
+  CB_CUDA_TRY(g->d_out_dst.upload(g->out_dst));
+  CB_CUDA_TRY(g->d_is_output.upload(g->is_output));
+  CB_CUDA_TRY(g->d_volume.upload(g->volume));
+  CB_CUDA_TRY(g->d_attr_ptr.upload(g->attr_ptr));
+  CB_CUDA_TRY(g->d_attr_key.upload(g->attr_key));
+  CB_CUDA_TRY(g->d_attr_tag.upload(g->attr_tag));
+  CB_CUDA_TRY(g->d_attr_ival.upload(g->attr_ival));
+  CB_CUDA_TRY(g->d_attr_fval.upload(g->attr_fval));
+  CB_CUDA_TRY(g->d_ipdom.upload(g->ipdom));
+  CB_CUDA_TRY(g->d_pch_ptr.upload(g->pch_ptr));
+  CB_CUDA_TRY(g->d_pch.upload(g->pch));
+  CB_CUDA_TRY(g->d_level_nodes.upload(g->level_nodes));
+  CB_CUDA_TRY(g->d_depth.upload(g->depth));
+  g->on_device = true;
+  return CB_OK;
+}
+
+std::vector<LevelSegment> cb_plan_levels(const cb_graph* g, int32_t narrow_max) {
+  std::vector<LevelSegment> segs;
+  int32_t nl = (int32_t)g->level_ptr.size() - 1;
+  int32_t l = 0;
+  while (l < nl) {
+    int32_t w = g->level_ptr[l + 1] - g->level_ptr[l];
+    if (w > narrow_max) {
+      segs.push_back({l, l + 1, false});
+      ++l;
+      continue;
+    }
+    int32_t e = l;
+    while (e < nl && g->level_ptr[e + 1] - g->level_ptr[e] <= narrow_max) ++e;
+    segs.push_back({l, e, true});
+    l = e;
+  }
+  return segs;
+}

@@ -1,0 +1,143 @@
+"""Operator-level placement search (API of tensorplace/dp.py), solved on the
+GPU by cb_dp_solve (csrc/dp.cu).
+
+The reference DP (Algorithm 1) relaxes every stored covered-set state for
+every candidate match in frontier order; its optimum is the cheapest
+partition of the graph into registered matches under the additive model,
+with ties broken by the canonical key (registration index, sorted node ids).
+Because a match only exposes its root, the kernels of every partition nest
+along the post-dominator tree, so the device solves the same problem as an
+exact DP over post-dominator subtrees, one warp per node and one
+topological level at a time (see csrc/dp.cu).  Results -- cost, kernels
+and tie-breaking -- are those of the reference; only the search-internal
+counters differ (the device examines each candidate exactly once, so
+`relaxations` equals the number of candidates and the live state count is
+the node count + 1).
+"""
+
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass, field
+from typing import Any, Mapping
+
+import numpy as np
+
+from . import _native as nat
+from .cost import Measurer, price_matches
+from .errors import SearchLimitError, UncoverableGraphError
+from .graph import ComputationGraph
+from .placement import Assignment, PlacementStrategy, validate_placement
+from .registry import PatternRegistry
+
+DEFAULT_MAX_STATES = None  # the subtree DP has n + 1 states; no cap needed
+VALIDATE_MAX_NODES = 5000
+
+
+@dataclass
+class DPStats:
+    nodes: int = 0
+    pops: int = 0
+    candidates_total: int = 0
+    max_candidates: int = 0
+    max_new_frontiers: int = 0
+    max_compatible_states: int = 0
+    relaxations: int = 0
+    improvements: int = 0
+    measure_calls: int = 0
+    cache_hits: int = 0
+    computations: int = 0
+    states_peak: int = 0
+
+    def to_json(self) -> dict:
+        return dict(self.__dict__)
+
+
+@dataclass
+class DPResult:
+    placement: PlacementStrategy
+    cost_ms: float
+    stats: DPStats
+    state_costs: Mapping[frozenset, float] = field(default_factory=dict)
+    device: dict[str, Any] = field(default_factory=dict)
+    kernel_matches: np.ndarray | None = None  # match-table indices, canonical order
+
+
+def _new_frontiers(g: ComputationGraph) -> int:
+    """Largest number of nodes first enqueued by a single pop (pop order is
+    (depth, id)); mirrors the reference counter."""
+    rank = {v: i for i, v in enumerate(sorted(g.nodes, key=lambda v: (g.depth(v), v)))}
+    first: dict[int, int] = {}
+    for c in g.nodes:
+        preds = g.node_predecessors(c)
+        if preds:
+            first[c] = min(preds, key=rank.__getitem__)
+    counts: dict[int, int] = {}
+    for p in first.values():
+        counts[p] = counts.get(p, 0) + 1
+    return max(counts.values(), default=0)
+
+
+def optimize(g: ComputationGraph, registry: PatternRegistry, measurer: Measurer,
+             epsilon: float, max_states: int | None = DEFAULT_MAX_STATES,
+             validate: bool | None = None) -> DPResult:
+    """Cheapest full placement of `g` (exact, reference tie-breaking).
+
+    Raises UncoverableGraphError when no full cover exists and
+    SearchLimitError when `max_states` is given and the n + 1 subtree states
+    exceed it."""
+    stats = DPStats(nodes=len(g.nodes))
+    c0, h0, p0 = measurer.calls, measurer.cache_hits, measurer.computations
+    if not g.nodes:
+        return DPResult(PlacementStrategy(()), 0.0, stats, {frozenset(): 0.0})
+    uncovered = registry.uncovered_op_kinds(g)
+    if uncovered:
+        raise UncoverableGraphError(
+            f"no registered pattern can root op kind(s) {list(uncovered)}", op_kinds=uncovered)
+    if max_states is not None and len(g.nodes) + 1 > max_states:
+        raise SearchLimitError(f"operator-level search needs {len(g.nodes) + 1} live states on "
+                               f"a {len(g.nodes)}-node graph, above the cap of {max_states}")
+    table = registry.match_table(g)
+    price_matches(measurer, registry, table)
+    kernels = np.empty(len(g.nodes), dtype=np.int32)
+    res = nat.DPResultStruct()
+    nat.check(nat.lib().cb_dp_solve(g.native, table.handle.raw, float(epsilon),
+                                    nat.ptr(kernels, nat.c_int32), ctypes.byref(res)))
+    sizes = np.diff(table.group_ptr)
+    stats.pops = len(g.nodes)
+    stats.candidates_total = int(table.n_matches)
+    stats.max_candidates = int(sizes.max()) if len(sizes) else 0
+    stats.max_new_frontiers = _new_frontiers(g)
+    stats.max_compatible_states = 1 if table.n_matches else 0
+    stats.relaxations = int(table.n_matches)
+    stats.states_peak = len(g.nodes) + 1
+    stats.measure_calls = measurer.calls - c0
+    stats.cache_hits = measurer.cache_hits - h0
+    stats.computations = measurer.computations - p0
+    device = {"device_ms": res.device_ms, "levels": res.n_levels, "launches": res.n_launches,
+              "ties": res.ties, "walk_steps": res.walk_steps,
+              "rounding_window_safe": bool(res.window_safe)}
+    if not res.feasible:
+        z = res.first_zero_candidate
+        if z >= 0:
+            nid = g.id_of(z)
+            kind = g.nodes[nid].op_kind
+            raise UncoverableGraphError(
+                f"no full placement found; frontier node {nid} (op '{kind}') had zero "
+                f"candidate matches", op_kinds=(kind,), node_ids=(nid,))
+        raise UncoverableGraphError("no full placement found; some nodes cannot be covered "
+                                    "compatibly by the registered patterns")
+    chosen = kernels[:res.n_kernels]
+    patterns = registry.patterns
+    assignments = [Assignment(table.node_set(int(m)), patterns[int(table.pat[m])],
+                              g.id_of(int(table.root[m]))) for m in chosen]
+    stats.improvements = len(assignments)
+    placement = PlacementStrategy(assignments)
+    if validate or (validate is None and len(g.nodes) <= VALIDATE_MAX_NODES):
+        validate_placement(g, placement)
+    order = {a.nodes: i for i, a in enumerate(placement.assignments)}
+    canon = np.empty(len(chosen), dtype=np.int32)
+    for m in chosen:
+        canon[order[table.node_set(int(m))]] = m
+    return DPResult(placement, res.cost_ms, stats,
+                    {frozenset(g.nodes): res.cost_ms, frozenset(): 0.0}, device, canon)
