@@ -138,6 +138,8 @@ def ref_registry(case: dict):
         reg.add_backend(ref.BackendDescriptor(bid, ref.BackendKind(kind)))
     for bid, text, source in case["patterns"]:
         reg.add_pattern(bid, text, ref.PatternSource(source))
+    # keep exactly what was registered (duplicates are refused by the registry)
+    case["patterns"] = [[bp.backend, bp.text(), bp.source.value] for bp in reg.patterns]
     measurer = ref.SimMeasurer({bid: ref_profile_from_json(doc)
                                 for bid, doc in case["profiles"].items()})
     return reg, measurer
