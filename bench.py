@@ -1,0 +1,381 @@
+"""Benchmark of the placement-search hot path (BASELINE.json metric:
+placement-search wall time and fitness evals/sec).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl mine|reference]
+    python -m torch.distributed.run --nproc-per-node N ... bench.py --gpus N
+
+Workload (N=1, BASELINE.json configs[1]): BERT-base (seq 128) inference
+graph, paper backend set (cuDNN / cuBLAS / TVM with rule-generated patterns
+/ TensorRT as the graph inference library), op-level DP then evolutionary
+search.  A step is one ES generation of the rank's population shard on the
+GPU: tournament selection + two-point crossover + mutation (cb_es_breed)
+and batched graph-level fitness of every genome (cb_fitness_device), plus
+for N>1 the NCCL all-gather of the per-rank elites.  `value` is genomes
+evaluated per second over all ranks (weak scaling: the shard per GPU is
+fixed).  The shard is sized so the population exceeds L2 (inputs larger
+than L2; no flush).  `e2e` prices a host-resident population through the
+public API (FitnessPlan.evaluate_packed -> cb_fitness_host: pinned H2D,
+fitness, D2H).  `search` reports the wall time of one full placement search
+(match + price + DP + plan + ES generations).
+
+--impl reference times the reference algorithm (the CPU oracle restating
+tensorplace, oracle/oracle.c) on the host cores for the same workload.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+L2_BYTES = 126 * 1024 * 1024
+
+
+def _peaks() -> tuple[float, str]:
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            return float(json.load(fh)["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled while the timed region runs."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.samples: list[list[str]] = []
+        self._stop = threading.Event()
+        self._thread = threading.Thread(target=self._run, daemon=True)
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                                      "--format=csv,noheader,nounits"], capture_output=True,
+                                     text=True, timeout=5).stdout.strip()
+                if out:
+                    self.samples.append([x.strip() for x in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._thread.start()
+        return self
+
+    def __exit__(self, *exc):
+        self._stop.set()
+        self._thread.join(timeout=10)
+
+    def summary(self) -> dict:
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+        reasons = sorted({names[i] for s in self.samples for i in range(4)
+                          if len(s) > i + 2 and s[i + 2].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.samples)}
+
+
+def build_workload(name: str):
+    import paper_2111_00655_b200 as tp
+    from paper_2111_00655_b200 import workloads
+    g = workloads.CONFIGS[name]()
+    from paper_2111_00655_b200 import _native
+    bs = workloads.paper_backends(g, verify=_native.device_available()) if name != "random100k" else \
+        workloads.random_backends(g, n_backends=8, n_graph=1, seed=0)
+    return tp, g, bs
+
+
+def shard_size(words: int, requested: int | None) -> int:
+    if requested:
+        return requested
+    p = 1 << 20
+    while p * words * 8 < 2 * L2_BYTES:
+        p <<= 1
+    return p
+
+
+def run_mine(args) -> None:
+    import numpy as np
+    import torch
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    group = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=dev)
+        group = dist.group.WORLD
+
+    def barrier():
+        if world > 1:
+            import torch.distributed as dist
+            dist.barrier()
+        torch.cuda.synchronize(dev)
+
+    from paper_2111_00655_b200.es_device import DeviceEvolution
+
+    tp, g, bs = build_workload(args.workload)
+
+    def search(P: int, gens: int, timed: bool):
+        t = {}
+        t0 = time.perf_counter()
+        res = tp.optimize(g, bs.registry, bs.measurer, 0.01)
+        t["dp_s"] = time.perf_counter() - t0
+        plan = tp.FitnessPlan(g, bs.registry, bs.measurer, res.placement, 0.01, bs.graph_backend,
+                              res.kernel_matches)
+        es = DeviceEvolution(plan, P, seed=args.seed, device=dev, process_group=group)
+        es.initialize()
+        for _ in range(gens):
+            es.step()
+        torch.cuda.synchronize(dev)
+        t["total_s"] = time.perf_counter() - t0
+        t["es_s"] = t["total_s"] - t["dp_s"]
+        return res, plan, es, t
+
+    # warm search (module load, first launches), then the timed one on fresh objects
+    bs.registry._tables.clear()
+    search(4096, 2, False)
+    bs.registry._tables.clear()
+    res, plan, es0, search_t = search(args.search_population, args.search_generations, True)
+    P = shard_size(plan.words, args.population)
+    es = DeviceEvolution(plan, P, seed=args.seed, device=dev, process_group=group)
+    es.initialize()
+    for _ in range(args.warmup):
+        es.step()
+    barrier()
+    es.enable_kernel_timing(True)
+    t_start = torch.cuda.Event(enable_timing=True)
+    t_end = torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clocks:
+        barrier()
+        t_start.record()
+        for _ in range(args.steps):
+            es.step()
+        t_end.record()
+        barrier()
+    ms = t_start.elapsed_time(t_end)
+    kt = es.kernel_times_ms()
+    fit_ms = sum(kt["fitness"]) / len(kt["fitness"])
+    breed_ms = sum(kt["breed"]) / len(kt["breed"])
+    best_cost, _ = es.best()
+
+    # e2e through the public API with host buffers (pinned)
+    rng = np.random.default_rng(rank)
+    host = torch.empty((P, plan.words), dtype=torch.int64, pin_memory=True)
+    host.copy_(torch.from_numpy(rng.integers(-(1 << 62), 1 << 62, size=(P, plan.words))))
+    host_np = host.numpy().view(np.uint64)
+    plan.evaluate_packed(host_np)  # warm
+    barrier()
+    t0 = time.perf_counter()
+    for _ in range(args.e2e_steps):
+        fit = plan.evaluate_packed(host_np)
+    e2e_s = time.perf_counter() - t0
+    barrier()
+
+    vals = torch.tensor([ms, e2e_s, fit_ms, breed_ms, search_t["total_s"]], dtype=torch.float64,
+                        device=dev)
+    if world > 1:
+        import torch.distributed as dist
+        dist.all_reduce(vals, op=dist.ReduceOp.MAX)
+    ms, e2e_s, fit_ms, breed_ms, search_s = vals.tolist()
+    if rank != 0:
+        if world > 1:
+            import torch.distributed as dist
+            dist.destroy_process_group()
+        return
+    step_ms = ms / args.steps
+    evals_per_s = world * P * args.steps / (ms / 1e3)
+    bytes_per_launch = P * (plan.words * 8 + 8)
+    peak, peak_src = _peaks()
+    achieved = bytes_per_launch / (fit_ms / 1e3) / 1e9
+    traffic = None
+    prof = os.path.join(ROOT, "profiles", "fitness_ncu_summary.json")
+    if os.path.exists(prof):
+        try:
+            with open(prof) as fh:
+                d = json.load(fh)
+            if d.get("workload") == args.workload:
+                traffic = d.get("dram_bytes_per_launch_per_genome", 0) * P or None
+        except Exception:
+            traffic = None
+    cpu = None
+    if world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_baseline(g, bs, res, plan, args)
+    line = {
+        "metric": "fitness_evals_per_sec",
+        "value": evals_per_s,
+        "unit": "genomes/s",
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": step_ms,
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "u64 bit-genomes, exact 192-bit fixed-point costs",
+        "data": "synthetic (BERT-base graph built op by op; simulated backend cost tables)",
+        "config": {"workload": f"{args.workload}: op-level DP + evolutionary search",
+                   "nodes": len(g.nodes), "dp_kernels": len(res.placement),
+                   "genome_bits": plan.k, "genome_words": plan.words,
+                   "population_per_gpu": P, "global_population": P * world,
+                   "parallelism": f"population sharded over {world} GPU(s), NCCL all-gather of elites",
+                   "l2": "population > L2 (no flush)"},
+        "search": {"wall_s": search_s, "dp_s": search_t["dp_s"], "es_s": search_t["es_s"],
+                   "es_population_per_gpu": args.search_population,
+                   "es_generations": args.search_generations, "dp_cost_ms": res.cost_ms,
+                   "best_cost_ms_after_timed_steps": best_cost},
+        "kernels_ms": {"fitness": fit_ms, "breed": breed_ms},
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak, "traffic": traffic, "kernel": "fitness_smem_kernel",
+                     "peak_source": peak_src,
+                     "algorithmic_bytes_per_launch": bytes_per_launch},
+        "e2e": {"value": world * P * args.e2e_steps / e2e_s, "unit": "genomes/s",
+                "h2d_bytes_per_step": P * plan.words * 8, "d2h_bytes_per_step": P * 8},
+        "gpu_launches": args.steps * (es.launches_per_generation + 1),
+        "clocks": clocks.summary(),
+    }
+    if cpu is not None:
+        line["cpu_baseline"] = cpu
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+def _oracle_case(g, bs):
+    from paper_2111_00655_b200.cost import profile_to_json
+    from paper_2111_00655_b200.graph import graph_to_json
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    from oracle import OracleCase  # checker / baseline only
+    case = {"graph": graph_to_json(g),
+            "backends": [[b.id, b.kind.value] for b in bs.registry.backends.values()],
+            "patterns": [[bp.backend, bp.text(), bp.source.value] for bp in bs.registry.patterns],
+            "profiles": {b: profile_to_json(p) for b, p in bs.measurer.profiles.items()},
+            "epsilon": 0.01}
+    return OracleCase(json.loads(json.dumps(case)))
+
+
+def cpu_baseline(g, bs, res, plan, args) -> dict:
+    """The reference algorithm restated in C (oracle) on the host cores,
+    bounded sample: fitness of `sample` random genomes."""
+    import numpy as np
+    oc = _oracle_case(g, bs)
+    oc.price()
+    kernels = [[a.backend_pattern.order, a.root, sorted(a.nodes)] for a in res.placement.assignments]
+    threads = os.cpu_count() or 1
+    rng = np.random.default_rng(1)
+    sample = args.cpu_sample
+    pop = rng.integers(0, 2, size=(sample, plan.k), dtype=np.uint8)
+    oc.fitness(kernels, bs.graph_backend, pop[:64], threads=threads)
+    t0 = time.perf_counter()
+    oc.fitness(kernels, bs.graph_backend, pop, threads=threads)
+    dt = time.perf_counter() - t0
+    return {"value": sample / dt, "unit": "genomes/s", "cores": threads, "kind": "port",
+            "sample": f"{sample} random genomes of the {args.workload} DP placement "
+                      f"({plan.k} bits), oracle/oracle.c or_fitness with {threads} OpenMP threads"}
+
+
+def run_reference(args) -> None:
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    import numpy as np
+    tp, g, bs = build_workload(args.workload)
+    oc = _oracle_case(g, bs)
+    t0 = time.perf_counter()
+    oc.price()
+    status, cost, kernels = oc.dp(max_states=2_000_000)
+    dp_s = time.perf_counter() - t0
+    threads = os.cpu_count() or 1
+    from paper_2111_00655_b200.evolution import pack_genomes  # noqa: F401  (layout only)
+    k = sum(1 for _, _, _ in kernels) if kernels else 0
+    # genome length: kernels not on graph backends
+    gb = {b for b, kind in [[b.id, b.kind.value] for b in bs.registry.backends.values()]
+          if kind == "graph_inference_library"}
+    order_backend = [bp.backend for bp in bs.registry.patterns]
+    k = sum(1 for o, _, _ in kernels if order_backend[o] not in gb)
+    rng = np.random.default_rng(2)
+    sample = args.cpu_sample
+    for _ in range(args.warmup):
+        oc.fitness(kernels, bs.graph_backend, rng.integers(0, 2, size=(256, k), dtype=np.uint8),
+                   threads=threads)
+    times = []
+    for _ in range(args.steps):
+        pop = rng.integers(0, 2, size=(sample, k), dtype=np.uint8)
+        t0 = time.perf_counter()
+        oc.fitness(kernels, bs.graph_backend, pop, threads=threads)
+        times.append(time.perf_counter() - t0)
+    value = sample * len(times) / sum(times)
+    line = {
+        "impl": "reference",
+        "metric": "fitness_evals_per_sec",
+        "value": value,
+        "unit": "genomes/s",
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": 1e3 * sum(times) / len(times),
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "f64 (fsum-exact), CPU",
+        "data": "synthetic (BERT-base graph; simulated backend cost tables)",
+        "config": {"workload": f"{args.workload}: op-level DP + evolutionary search",
+                   "nodes": len(g.nodes), "genome_bits": k, "dp_status": status,
+                   "dp_cost_ms": cost, "dp_s": dp_s},
+        "cpu_baseline": {"value": value, "unit": "genomes/s", "cores": threads, "kind": "port",
+                         "sample": f"{sample} random genomes per step, oracle/oracle.c "
+                                   f"(reference algorithm restated in C), {threads} threads"},
+        "e2e": {"value": value, "unit": "genomes/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main() -> None:
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=("mine", "reference"), default="mine")
+    ap.add_argument("--workload", default="bert_base")
+    ap.add_argument("--population", type=int, default=None, help="genomes per GPU")
+    ap.add_argument("--search-population", type=int, default=65536)
+    ap.add_argument("--search-generations", type=int, default=50)
+    ap.add_argument("--e2e-steps", type=int, default=5)
+    ap.add_argument("--cpu-sample", type=int, default=200_000)
+    ap.add_argument("--seed", type=int, default=0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_mine(args)
+
+
+if __name__ == "__main__":
+    main()

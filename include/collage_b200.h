@@ -199,10 +199,14 @@ typedef struct {
   int32_t fixed_units;   /* contracted fixed target-backend components */
   int32_t edges;         /* dynamic adjacency edges */
   int32_t infeasible_bits;
-  int32_t smem_path;     /* 1 warp/individual in shared memory */
+  int32_t smem_path;     /* union-find path: 1 warp/genome in shared memory */
+  int32_t frontier_slots;/* thread/genome frontier program width (0 = none) */
   double seed_cost;      /* graph-level cost of the all-zero genome */
 } cb_es_plan_info;
 int cb_es_plan_query(const cb_es_plan* p, cb_es_plan_info* info);
+/* Evaluation path: -1 automatic (frontier program when available), 0 the
+ * union-find kernels, 1 the frontier program.  For tests and profiling. */
+int cb_es_plan_set_path(cb_es_plan* p, int32_t path);
 /* slot_kernel (host, genome_bits): canonical kernel index of each bit;
  * rep_kind (host, genome_bits): 0 infeasible, 1 same-set pattern,
  * 2 decomposed into singletons; rep_match_ptr/rep_match: replacement

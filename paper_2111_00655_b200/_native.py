@@ -67,6 +67,7 @@ class ESPlanInfo(ctypes.Structure):
         ("edges", c_int32),
         ("infeasible_bits", c_int32),
         ("smem_path", c_int32),
+        ("frontier_slots", c_int32),
         ("seed_cost", c_double),
     ]
 
@@ -109,6 +110,7 @@ _SIGNATURES = {
                                   _P_F64, c_int32, c_double, POINTER(c_void_p)]),
     "cb_es_plan_query": (c_int, [c_void_p, POINTER(ESPlanInfo)]),
     "cb_es_plan_slots": (c_int, [c_void_p, _P_I32, _P_I8, _P_I32, _P_I32]),
+    "cb_es_plan_set_path": (c_int, [c_void_p, c_int32]),
     "cb_es_plan_destroy": (None, [c_void_p]),
     "cb_fitness_device": (c_int, [c_void_p, c_void_p, c_int64, c_void_p, c_void_p]),
     "cb_fitness_host": (c_int, [c_void_p, _P_U64, c_int64, _P_F64]),

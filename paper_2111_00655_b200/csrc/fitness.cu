@@ -30,6 +30,21 @@
 
 #include "cb_internal.cuh"
 
+// One record per dynamic unit of the frontier program (thread-per-genome
+// evaluation): the unit's costs, its genome bit, the frontier slot it
+// occupies while it still has unvisited neighbours, and the slots of its
+// earlier neighbours / of the units whose last neighbour it is.
+struct __align__(16) UnitRec {
+  fx192 rep;    // exact sum of its replacement kernels (region member value)
+  fx192 off;    // its own kernel cost + eps (removed when offloaded)
+  fx192 term1;  // round(rep) * r(cnt) + eps: its term as a region of one
+  int32_t bit;  // genome bit, -1 for always-on fixed units
+  int32_t cnt;  // kernels it contributes to a region
+  int32_t back_off, end_off;
+  uint8_t slot, nback, nend, pad;
+  uint8_t pad2[4];
+};
+
 struct cb_es_plan {
   int32_t k = 0;       // genome bits
   int32_t words = 0;   // uint64 words per genome
@@ -63,7 +78,98 @@ struct cb_es_plan {
   // staging for the host-buffer entry point
   DBuf<uint64_t> d_pop_stage;
   DBuf<double> d_fit_stage;
+  // frontier program (0 slots = not built / too wide)
+  int32_t F = 0;
+  std::vector<UnitRec> prog;
+  std::vector<uint8_t> prog_slots;
+  DBuf<UnitRec> d_prog;
+  DBuf<uint8_t> d_prog_slots;
+  int32_t force_path = -1;  // testing: 0 union-find, 1 frontier
 };
+
+#define FRONTIER_MAX 32
+
+static bool fx_term(double base, double r, const fx192& eps, fx192& out);
+
+// Order the dynamic units (eligible ones in genome order, each fixed unit
+// just before its first eligible neighbour), give every unit a frontier
+// slot for the span between its position and its last neighbour's, and
+// record the back / end slot lists.  F = number of slots = the largest
+// number of units simultaneously waiting for a later neighbour.
+static void build_frontier_program(cb_es_plan* P, int32_t n_elig_units) {
+  const int32_t M = P->M;
+  std::vector<std::vector<int32_t>> nbr(M);
+  for (const int2& e : P->edges) {
+    nbr[e.x].push_back(e.y);
+    nbr[e.y].push_back(e.x);
+  }
+  std::vector<int32_t> key(M, M);
+  for (int32_t v = n_elig_units; v < M; ++v)
+    for (int32_t q : nbr[v])
+      if (q < n_elig_units) key[v] = std::min(key[v], q);
+  std::vector<std::vector<int32_t>> before(n_elig_units + 1);
+  for (int32_t v = n_elig_units; v < M; ++v) before[std::min(key[v], n_elig_units)].push_back(v);
+  std::vector<int32_t> order;
+  order.reserve(M);
+  for (int32_t e = 0; e <= n_elig_units; ++e) {
+    for (int32_t v : before[e]) order.push_back(v);
+    if (e < n_elig_units) order.push_back(e);
+  }
+  std::vector<int32_t> pos(M);
+  for (int32_t p = 0; p < M; ++p) pos[order[p]] = p;
+  std::vector<int32_t> last(M);
+  std::vector<std::vector<int32_t>> ends_at(M);
+  for (int32_t p = 0; p < M; ++p) {
+    int32_t u = order[p], l = p;
+    for (int32_t q : nbr[u]) l = std::max(l, pos[q]);
+    last[p] = l;
+    ends_at[l].push_back(p);
+  }
+  std::vector<int32_t> slot(M, -1);
+  std::vector<int32_t> free_slots;  // kept sorted descending; back() = smallest
+  int32_t used = 0;
+  for (int32_t p = 0; p < M; ++p) {
+    int32_t s;
+    if (free_slots.empty()) {
+      s = used++;
+    } else {
+      s = free_slots.back();
+      free_slots.pop_back();
+    }
+    slot[p] = s;
+    for (int32_t q : ends_at[p]) {
+      free_slots.push_back(slot[q]);
+    }
+    std::sort(free_slots.begin(), free_slots.end(), std::greater<int32_t>());
+    if (used > FRONTIER_MAX) {
+      P->F = 0;
+      return;
+    }
+  }
+  P->F = used;
+  P->prog.resize(M);
+  P->prog_slots.clear();
+  for (int32_t p = 0; p < M; ++p) {
+    const int32_t u = order[p];
+    UnitRec r;
+    std::memset(&r, 0, sizeof(r));
+    r.rep = P->unit_rep[u];
+    r.off = P->unit_off[u];
+    fx_term(fx_to_double(r.rep), P->rt[P->unit_cnt[u]], P->eps, r.term1);
+    r.bit = P->unit_slot[u];
+    r.cnt = P->unit_cnt[u];
+    r.slot = (uint8_t)slot[p];
+    r.back_off = (int32_t)P->prog_slots.size();
+    for (int32_t q : nbr[u])
+      if (pos[q] < p) P->prog_slots.push_back((uint8_t)slot[pos[q]]);
+    r.nback = (uint8_t)(P->prog_slots.size() - r.back_off);
+    r.end_off = (int32_t)P->prog_slots.size();
+    for (int32_t q : ends_at[p]) P->prog_slots.push_back((uint8_t)slot[q]);
+    r.nend = (uint8_t)(P->prog_slots.size() - r.end_off);
+    P->prog[p] = r;
+  }
+  if (P->prog_slots.empty()) P->prog_slots.push_back(0);
+}
 
 static double region_r(double alpha, double floor_, int64_t n) {
   // max(floor, 1.0 - alpha * (n - 1)) with two separately rounded operations
@@ -381,6 +487,7 @@ extern "C" int cb_es_plan_create(cb_graph* g, cb_matches* m, int32_t n_kernels,
   P->rt.resize((size_t)max_cnt + 2);
   for (int64_t c = 0; c < (int64_t)P->rt.size(); ++c)
     P->rt[c] = region_r(region_alpha[target_backend], region_floor[target_backend], c);
+  build_frontier_program(P, n_elig_units);
   // seed (all-zero genome) cost
   {
     fx192 tot = P->base_const;
@@ -406,6 +513,10 @@ extern "C" int cb_es_plan_create(cb_graph* g, cb_matches* m, int32_t n_kernels,
   if ((e = P->d_edges.upload(P->edges)) != cudaSuccess) return fail_cuda(e);
   if ((e = P->d_infeas.upload(P->infeas_mask)) != cudaSuccess) return fail_cuda(e);
   if ((e = P->d_rt.upload(P->rt)) != cudaSuccess) return fail_cuda(e);
+  if (P->F > 0) {
+    if ((e = P->d_prog.upload(P->prog)) != cudaSuccess) return fail_cuda(e);
+    if ((e = P->d_prog_slots.upload(P->prog_slots)) != cudaSuccess) return fail_cuda(e);
+  }
   if ((e = P->d_flags.alloc(2)) != cudaSuccess) return fail_cuda(e);
   cudaMemset(P->d_flags.p, 0, 2 * sizeof(unsigned long long));
   const size_t per_warp = (size_t)P->words * 8 + (size_t)P->M * (sizeof(fx192) + 8);
@@ -423,7 +534,15 @@ extern "C" int cb_es_plan_query(const cb_es_plan* p, cb_es_plan_info* info) {
   info->edges = p->E;
   info->infeasible_bits = p->infeasible_bits;
   info->smem_path = p->smem_path ? 1 : 0;
+  info->frontier_slots = p->F;
   info->seed_cost = p->seed_cost;
+  return CB_OK;
+}
+
+extern "C" int cb_es_plan_set_path(cb_es_plan* p, int32_t path) {
+  CB_ARG_CHECK(p && path >= -1 && path <= 1, "cb_es_plan_set_path: bad arguments");
+  CB_ARG_CHECK(path != 1 || p->F > 0, "cb_es_plan_set_path: no frontier program for this plan");
+  p->force_path = path;
   return CB_OK;
 }
 
@@ -614,6 +733,208 @@ fitness_global_kernel(FitArgs a, const uint64_t* __restrict__ pop, int64_t n, do
     eval_genome<FIT_CTA>(a, pop + i * a.words, parent, acc, cnt, fit + i, red, &flag);
 }
 
+// ------------------------------------------------- frontier program kernel
+// One thread per genome.  Units are visited in program order; an on unit
+// opens a component in its slot and merges the components of its on earlier
+// neighbours; when a slot's unit has seen its last neighbour the slot is
+// released, and a component whose last member leaves is emitted as a
+// region.  Component data (exact sum, kernel count, single-unit id) lives
+// at its label slot, which is always an occupied slot.  Slot state is kept
+// in shared memory, [field][slot][thread], so lanes never conflict.
+#define FR_THREADS 128
+
+template <int F>
+struct FrontierSmem {
+  uint64_t sum0[F][FR_THREADS];
+  uint64_t sum1[F][FR_THREADS];
+  uint64_t sum2[F][FR_THREADS];
+  int32_t cnt[F][FR_THREADS];
+  int32_t single[F][FR_THREADS];
+  uint8_t label[F][FR_THREADS];
+  uint8_t active[F][FR_THREADS];
+};
+
+template <int F>
+__device__ __forceinline__ void fr_emit(FrontierSmem<F>& s, int L, int t, const UnitRec* __restrict__ prog,
+                                        const double* __restrict__ rt, const fx192& eps, fx192& total,
+                                        bool& inexact) {
+  const int32_t one = s.single[L][t];
+  if (one >= 0) {
+    fx192 v;
+    v.w[0] = __ldg(&prog[one].term1.w[0]);
+    v.w[1] = __ldg(&prog[one].term1.w[1]);
+    v.w[2] = __ldg(&prog[one].term1.w[2]);
+    fx_add(total, v);
+    return;
+  }
+  fx192 sum;
+  sum.w[0] = s.sum0[L][t];
+  sum.w[1] = s.sum1[L][t];
+  sum.w[2] = s.sum2[L][t];
+  const double prod = __dmul_rn(fx_to_double(sum), __ldg(rt + s.cnt[L][t]));
+  fx192 term;
+  inexact |= !fx_from_double(prod, term);
+  fx_add(total, term);
+  fx_add(total, eps);
+}
+
+template <int F>
+__global__ void __launch_bounds__(FR_THREADS)
+fitness_frontier_kernel(int32_t M, int32_t words, fx192 base_const, fx192 eps,
+                        const UnitRec* __restrict__ prog, const uint8_t* __restrict__ slots,
+                        const uint64_t* __restrict__ infeas, const double* __restrict__ rt,
+                        const uint64_t* __restrict__ pop, int64_t n, double* __restrict__ fit,
+                        unsigned long long* flags) {
+  extern __shared__ __align__(16) unsigned char fr_smem[];
+  FrontierSmem<F>& s = *reinterpret_cast<FrontierSmem<F>*>(fr_smem);
+  const int t = threadIdx.x;
+  bool inexact = false;
+  // Lanes of a warp walk the program in lockstep: the genome loop is warp
+  // uniform, infeasible / out-of-range lanes run with every unit off, and
+  // multi-unit region terms (the expensive rounding) are deferred through a
+  // one-entry queue that the warp drains together when any lane collides.
+  const int64_t stride = (int64_t)gridDim.x * FR_THREADS;
+  for (int64_t base = (int64_t)blockIdx.x * FR_THREADS + (t & ~31); base < n; base += stride) {
+    const int64_t i = base + (t & 31);
+    const bool in_range = i < n;
+    const uint64_t* gen = pop + (in_range ? i : 0) * words;
+    bool dead = !in_range;
+    if (in_range)
+      for (int32_t w = 0; w < words; ++w) dead |= (__ldg(gen + w) & __ldg(infeas + w)) != 0ull;
+#pragma unroll
+    for (int q = 0; q < F; ++q) s.active[q][t] = 0;
+    fx192 total = base_const;
+    fx192 pend = fx_zero();
+    int32_t pend_cnt = 0;
+    bool pend_valid = false;
+    int32_t cached_word = -1;
+    uint64_t word = 0;
+    for (int32_t p = 0; p < M; ++p) {
+      const UnitRec* r = prog + p;
+      const int32_t bit = __ldg(&r->bit);
+      bool on = !dead;
+      if (bit >= 0) {
+        const int32_t wi = bit >> 6;
+        if (wi != cached_word) {
+          word = dead ? 0ull : __ldg(gen + wi);
+          cached_word = wi;
+        }
+        on = (word >> (bit & 63)) & 1ull;
+      }
+      const uint4 meta = __ldg(reinterpret_cast<const uint4*>(&r->back_off));
+      // meta.x = back_off, meta.y = end_off, meta.z = slot|nback|nend|pad
+      const int S = meta.z & 0xff;
+      const int nback = (meta.z >> 8) & 0xff;
+      const int nend = (meta.z >> 16) & 0xff;
+      if (on) {
+        if (bit >= 0) {
+          fx192 off;
+          off.w[0] = __ldg(&r->off.w[0]);
+          off.w[1] = __ldg(&r->off.w[1]);
+          off.w[2] = __ldg(&r->off.w[2]);
+          fx_sub(total, off);
+        }
+        s.sum0[S][t] = __ldg(&r->rep.w[0]);
+        s.sum1[S][t] = __ldg(&r->rep.w[1]);
+        s.sum2[S][t] = __ldg(&r->rep.w[2]);
+        s.cnt[S][t] = __ldg(&r->cnt);
+        s.single[S][t] = p;
+        s.label[S][t] = (uint8_t)S;
+        s.active[S][t] = 1;
+        for (int j = 0; j < nback; ++j) {
+          const int b = __ldg(slots + meta.x + j);
+          if (!s.active[b][t]) continue;
+          const int A = s.label[S][t], B = s.label[b][t];
+          if (A == B) continue;
+          fx192 x, y;
+          x.w[0] = s.sum0[A][t]; x.w[1] = s.sum1[A][t]; x.w[2] = s.sum2[A][t];
+          y.w[0] = s.sum0[B][t]; y.w[1] = s.sum1[B][t]; y.w[2] = s.sum2[B][t];
+          fx_add(x, y);
+          s.sum0[A][t] = x.w[0]; s.sum1[A][t] = x.w[1]; s.sum2[A][t] = x.w[2];
+          s.cnt[A][t] += s.cnt[B][t];
+          s.single[A][t] = -1;
+#pragma unroll
+          for (int q = 0; q < F; ++q)
+            if (s.active[q][t] && s.label[q][t] == B) s.label[q][t] = (uint8_t)A;
+        }
+      }
+      for (int j = 0; j < nend; ++j) {
+        const int e = __ldg(slots + meta.y + j);
+        int emit_slot = -1;  // slot holding a multi-unit region to price now
+        if (s.active[e][t]) {
+          const int L = s.label[e][t];
+          s.active[e][t] = 0;
+          int other = -1;
+#pragma unroll
+          for (int q = 0; q < F; ++q)
+            if (other < 0 && s.active[q][t] && s.label[q][t] == L) other = q;
+          if (other < 0) {
+            const int32_t one = s.single[L][t];
+            if (one >= 0) {  // region of one unit: precomputed term
+              fx192 v;
+              v.w[0] = __ldg(&prog[one].term1.w[0]);
+              v.w[1] = __ldg(&prog[one].term1.w[1]);
+              v.w[2] = __ldg(&prog[one].term1.w[2]);
+              fx_add(total, v);
+            } else {
+              const fx192 cur = {{s.sum0[L][t], s.sum1[L][t], s.sum2[L][t]}};
+              const int32_t ccnt = s.cnt[L][t];
+              if (!pend_valid) {
+                pend = cur;
+                pend_cnt = ccnt;
+                pend_valid = true;
+              } else {  // queue full: keep the new region, price the old one now
+                s.sum0[L][t] = pend.w[0];  // slot L is free until the next unit
+                s.sum1[L][t] = pend.w[1];
+                s.sum2[L][t] = pend.w[2];
+                s.cnt[L][t] = pend_cnt;
+                pend = cur;
+                pend_cnt = ccnt;
+                emit_slot = L;
+              }
+            }
+          } else if (L == e) {  // move the component to a slot that stays
+            s.sum0[other][t] = s.sum0[e][t];
+            s.sum1[other][t] = s.sum1[e][t];
+            s.sum2[other][t] = s.sum2[e][t];
+            s.cnt[other][t] = s.cnt[e][t];
+            s.single[other][t] = s.single[e][t];
+#pragma unroll
+            for (int q = 0; q < F; ++q)
+              if (s.active[q][t] && s.label[q][t] == e) s.label[q][t] = (uint8_t)other;
+          }
+        }
+        if (__any_sync(0xffffffffu, emit_slot >= 0)) {
+          if (emit_slot >= 0) {
+            const int L = emit_slot;
+            fx192 sum = {{s.sum0[L][t], s.sum1[L][t], s.sum2[L][t]}};
+            const double prod = __dmul_rn(fx_to_double(sum), __ldg(rt + s.cnt[L][t]));
+            fx192 term;
+            inexact |= !fx_from_double(prod, term);
+            fx_add(total, term);
+            fx_add(total, eps);
+          }
+        }
+      }
+    }
+    if (__any_sync(0xffffffffu, pend_valid)) {
+      if (pend_valid) {
+        const double prod = __dmul_rn(fx_to_double(pend), __ldg(rt + pend_cnt));
+        fx192 term;
+        inexact |= !fx_from_double(prod, term);
+        fx_add(total, term);
+        fx_add(total, eps);
+      }
+    }
+    if (in_range) fit[i] = dead ? __longlong_as_double(0x7ff0000000000000ll) : fx_to_double(total);
+  }
+  if (inexact) atomicAdd(flags, 1ull);
+}
+
+template <int F>
+static int launch_frontier_t(cb_es_plan* p, const uint64_t* d_pop, int64_t n, double* d_fit,
+                             cudaStream_t stream);
+
 static FitArgs make_args(cb_es_plan* p) {
   FitArgs a;
   a.k = p->k;
@@ -644,9 +965,39 @@ static int sm_count() {
   return cached;
 }
 
+template <int F>
+static int launch_frontier_t(cb_es_plan* p, const uint64_t* d_pop, int64_t n, double* d_fit,
+                             cudaStream_t stream) {
+  const size_t smem = sizeof(FrontierSmem<F>);
+  static bool configured = false;
+  if (!configured) {
+    CB_CUDA_TRY(cudaFuncSetAttribute(fitness_frontier_kernel<F>,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    configured = true;
+  }
+  int per_sm = 0;
+  CB_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fitness_frontier_kernel<F>,
+                                                            FR_THREADS, smem));
+  if (per_sm < 1) per_sm = 1;
+  const int64_t want = (n + FR_THREADS - 1) / FR_THREADS;
+  const int64_t grid = std::min<int64_t>(want, (int64_t)per_sm * sm_count());
+  fitness_frontier_kernel<F><<<(unsigned)grid, FR_THREADS, smem, stream>>>(
+      p->M, p->words, p->base_const, p->eps, p->d_prog.p, p->d_prog_slots.p, p->d_infeas.p,
+      p->d_rt.p, d_pop, n, d_fit, p->d_flags.p);
+  CB_CUDA_TRY(cudaGetLastError());
+  return CB_OK;
+}
+
 static int launch_fitness(cb_es_plan* p, const uint64_t* d_pop, int64_t n, double* d_fit,
                           cudaStream_t stream) {
   if (n <= 0) return CB_OK;
+  const bool frontier = p->F > 0 && p->force_path != 0;
+  if (frontier) {
+    if (p->F <= 4) return launch_frontier_t<4>(p, d_pop, n, d_fit, stream);
+    if (p->F <= 8) return launch_frontier_t<8>(p, d_pop, n, d_fit, stream);
+    if (p->F <= 16) return launch_frontier_t<16>(p, d_pop, n, d_fit, stream);
+    return launch_frontier_t<32>(p, d_pop, n, d_fit, stream);
+  }
   FitArgs a = make_args(p);
   if (p->smem_path) {
     const size_t smem = (size_t)FIT_WARPS * p->M * (sizeof(fx192) + 8);

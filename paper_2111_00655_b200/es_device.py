@@ -1,0 +1,163 @@
+"""Population-scale graph-level search that stays on the GPU, optionally
+sharded over the GPUs of one node.
+
+Each rank owns a population shard of packed genomes (uint64 rows, same bit
+layout as the reference's genome).  A generation is: the rank's best row
+(device argmin) -> all-gather of every rank's best fitness and genome over
+NCCL (NVLink) -> the global best becomes row 0 of every rank's next shard
+(elitism, as in tensorplace/evolution.py:416-418) -> tournament selection,
+two-point crossover and mutation of the remaining rows from the rank's own
+shard (cb_es_breed) -> batched fitness of the new shard (cb_fitness_device).
+No host synchronisation happens inside a generation; the per-generation best
+cost is recorded in a device tensor.
+
+Selection uses a counter-based generator (Philox) instead of Python's
+Mersenne Twister, so runs are reproducible per (seed, rank) but do not
+replay `evolution.evolve` draw for draw -- use `evolve` for that.
+"""
+
+from __future__ import annotations
+
+import ctypes
+
+import numpy as np
+
+from . import _native as nat
+from .evolution import FitnessPlan
+
+
+def _torch():
+    import torch
+    return torch
+
+
+class DeviceEvolution:
+    def __init__(self, plan: FitnessPlan, population: int, seed: int = 0, tournament: int = 4,
+                 mutation_rate: float | None = None, device=None, process_group=None,
+                 history_capacity: int = 4096):
+        torch = _torch()
+        if population < 2:
+            raise ValueError("population must be at least 2")
+        self.plan = plan
+        self.P = int(population)
+        self.W = plan.words
+        self.k = plan.k
+        self.seed = int(seed)
+        self.tournament = int(tournament)
+        self.rate = mutation_rate if mutation_rate is not None else (1.0 / self.k if self.k else 0.0)
+        self.device = torch.device(device or "cuda")
+        self.group = process_group
+        if process_group is not None:
+            import torch.distributed as dist
+            self.rank = dist.get_rank(process_group)
+            self.world = dist.get_world_size(process_group)
+        else:
+            self.rank, self.world = 0, 1
+        opts = dict(dtype=torch.int64, device=self.device)
+        self.pop = [torch.zeros((self.P, self.W), **opts), torch.zeros((self.P, self.W), **opts)]
+        self.fit = [torch.empty(self.P, dtype=torch.float64, device=self.device) for _ in range(2)]
+        self.cur = 0
+        self.best_idx = torch.zeros(1, dtype=torch.int64, device=self.device)
+        self.best_val = torch.zeros(1, dtype=torch.float64, device=self.device)
+        self.elite = torch.zeros((1, self.W), **opts)
+        self.gather_fit = torch.empty(self.world, dtype=torch.float64, device=self.device)
+        self.gather_rows = torch.empty((self.world, self.W), **opts)
+        self.history = torch.full((history_capacity,), float("inf"), dtype=torch.float64,
+                                  device=self.device)
+        self.generation = 0
+        self.launches_per_generation = 4  # argmin (2 CUB kernels + unpack) + breed + fitness
+
+    # -- helpers -----------------------------------------------------------------------
+    def _stream(self) -> int:
+        return _torch().cuda.current_stream(self.device).cuda_stream
+
+    @staticmethod
+    def _ptr(t) -> ctypes.c_void_p:
+        return ctypes.c_void_p(t.data_ptr())
+
+    def initialize(self) -> None:
+        """Row 0 of rank 0 is the all-zero genome (the DP placement itself);
+        every other row is uniformly random."""
+        torch = _torch()
+        gen = torch.Generator(device=self.device)
+        gen.manual_seed(self.seed * 1_000_003 + self.rank)
+        words = torch.randint(-(1 << 62), 1 << 62, (self.P, self.W), generator=gen,
+                              dtype=torch.int64, device=self.device)
+        words ^= torch.randint(0, 4, (self.P, self.W), generator=gen, dtype=torch.int64,
+                               device=self.device) << 62
+        self.pop[self.cur].copy_(words)
+        if self.rank == 0:
+            self.pop[self.cur][0].zero_()
+        self._evaluate(self.cur)
+        self._record_best()
+
+    def _evaluate(self, which: int) -> None:
+        self.plan.evaluate_device(self.pop[which].data_ptr(), self.P, self.fit[which].data_ptr(),
+                                  self._stream())
+
+    def _record_best(self) -> None:
+        nat.check(nat.lib().cb_argmin(self._ptr(self.fit[self.cur]), self.P,
+                                      self._ptr(self.best_idx), self._ptr(self.best_val),
+                                      ctypes.c_void_p(self._stream())))
+        row = self.pop[self.cur].index_select(0, self.best_idx)
+        if self.world > 1:
+            import torch.distributed as dist
+            dist.all_gather_into_tensor(self.gather_fit, self.best_val, group=self.group)
+            dist.all_gather_into_tensor(self.gather_rows, row, group=self.group)
+            who = _torch().argmin(self.gather_fit).view(1)
+            self.elite.copy_(self.gather_rows.index_select(0, who))
+            best = self.gather_fit.index_select(0, who)
+        else:
+            self.elite.copy_(row)
+            best = self.best_val
+        if self.generation < self.history.numel():
+            self.history[self.generation:self.generation + 1].copy_(best)
+
+    def enable_kernel_timing(self, on: bool = True) -> None:
+        """Record CUDA events around the breed and fitness launches of every
+        step (on the launching stream) for per-kernel durations."""
+        self.timing = on
+        self.kernel_events: list[tuple] = []
+
+    def kernel_times_ms(self) -> dict[str, list[float]]:
+        torch = _torch()
+        torch.cuda.synchronize(self.device)
+        out = {"breed": [], "fitness": []}
+        for e0, e1, e2 in self.kernel_events:
+            out["breed"].append(e0.elapsed_time(e1))
+            out["fitness"].append(e1.elapsed_time(e2))
+        return out
+
+    def step(self) -> None:
+        """One generation (no host synchronisation)."""
+        self.generation += 1
+        nxt = 1 - self.cur
+        timing = getattr(self, "timing", False)
+        if timing:
+            torch = _torch()
+            ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+            ev[0].record()
+        nat.check(nat.lib().cb_es_breed(
+            self.plan.handle.raw, self._ptr(self.pop[self.cur]), self._ptr(self.fit[self.cur]),
+            self.P, self._ptr(self.pop[nxt]), self.P, self._ptr(self.elite), 1,
+            ctypes.c_uint64(self.seed), ctypes.c_uint64(self.generation),
+            ctypes.c_uint64(self.rank), self.tournament, float(self.rate),
+            ctypes.c_void_p(self._stream())))
+        if timing:
+            ev[1].record()
+        self.cur = nxt
+        self._evaluate(self.cur)
+        if timing:
+            ev[2].record()
+            self.kernel_events.append(tuple(ev))
+        self._record_best()
+
+    def best(self) -> tuple[float, np.ndarray]:
+        """(cost, genome bits) of the global best; synchronises."""
+        bits = self.elite[0].cpu().numpy().view(np.uint8)
+        unpacked = np.unpackbits(bits, bitorder="little")[:self.k]
+        vals = self.history[:min(self.generation + 1, self.history.numel())].cpu().numpy()
+        return float(vals.min()), unpacked
+
+    def history_values(self) -> np.ndarray:
+        return self.history[:min(self.generation + 1, self.history.numel())].cpu().numpy()

@@ -204,6 +204,13 @@ class FitnessPlan:
             out[i] = hit
         return out
 
+    def set_path(self, path: str) -> None:
+        """'auto' | 'frontier' (thread per genome) | 'unionfind' (warp/CTA
+        per genome); both give identical results, `auto` picks the frontier
+        program whenever the plan has one."""
+        code = {"auto": -1, "unionfind": 0, "frontier": 1}[path]
+        nat.check(nat.lib().cb_es_plan_set_path(self.handle.raw, code))
+
     def evaluate(self, genomes: Sequence[Sequence[int]]) -> np.ndarray:
         """Fitness of each genome (host buffers in, host results out)."""
         pop = pack_genomes(genomes, self.k, self.words)

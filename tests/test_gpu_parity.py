@@ -128,3 +128,33 @@ def test_decode_and_validate_on_device(gpu):
     assert tp.decode_genome(g, reg, res.placement, (1, 0, 0, 0, 0, 0), "simgraph") is None
     cost = tp.placement_cost_graphlevel(meas, g, dec, 0.01, reg.graph_backend_ids())
     assert cost == 5.794
+
+
+def _plan_and_oracle(case):
+    g, reg, meas = build_case(case)
+    res = tp.optimize(g, reg, meas, case["epsilon"])
+    target = case.get("es", {}).get("graph_backend") or reg.graph_backend_ids()[-1]
+    plan = tp.FitnessPlan(g, reg, meas, res.placement, case["epsilon"], target,
+                          res.kernel_matches)
+    oc = OracleCase(case)
+    oc.price()
+    return res, plan, oc, target
+
+
+@pytest.mark.parametrize("case", list(_cases(["models", "es_random"], "es"))[:30])
+def test_fitness_paths_agree_with_oracle(gpu, case):
+    res, plan, oc, target = _plan_and_oracle(case)
+    rng = np.random.default_rng(7)
+    genomes = rng.integers(0, 2, size=(3000, plan.k), dtype=np.uint8)
+    # bias some rows towards long offloaded runs (large regions)
+    genomes[:1000] |= rng.integers(0, 2, size=(1000, plan.k), dtype=np.uint8)
+    genomes[1000:1500] = 1
+    want = oc.fitness(kernels_of(res.placement), target, genomes)
+    got_auto = plan.evaluate(genomes)
+    assert np.array_equal(got_auto, want)
+    plan.set_path("unionfind")
+    assert np.array_equal(plan.evaluate(genomes), want)
+    if plan.info.frontier_slots:
+        plan.set_path("frontier")
+        assert np.array_equal(plan.evaluate(genomes), want)
+    plan.set_path("auto")

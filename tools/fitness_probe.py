@@ -1,0 +1,42 @@
+"""Time the fitness kernels (both paths) on a workload's DP placement."""
+import sys
+sys.path.insert(0, '.')
+import numpy as np, torch
+import paper_2111_00655_b200 as tp
+from paper_2111_00655_b200 import workloads
+name = sys.argv[1] if len(sys.argv) > 1 else 'bert_base'
+P = int(sys.argv[2]) if len(sys.argv) > 2 else 1 << 22
+g = workloads.CONFIGS[name]()
+bs = workloads.paper_backends(g) if name != 'random100k' else workloads.random_backends(g, 8, 1, 0)
+res = tp.optimize(g, bs.registry, bs.measurer, 0.01)
+plan = tp.FitnessPlan(g, bs.registry, bs.measurer, res.placement, 0.01, bs.graph_backend, res.kernel_matches)
+i = plan.info
+print(name, 'k', plan.k, 'units', i.units, 'edges', i.edges, 'frontier', i.frontier_slots, 'dp', res.device)
+for label, fill in (('random', None), ('ones', 1), ('sparse', 0.1)):
+    if fill is None:
+        pop = torch.randint(-(1 << 62), 1 << 62, (P, plan.words), dtype=torch.int64, device='cuda')
+    elif fill == 1:
+        pop = torch.full((P, plan.words), -1, dtype=torch.int64, device='cuda')
+    else:
+        bits = (torch.rand((P, plan.words, 64), device='cuda') < fill).to(torch.int64)
+        pop = (bits << torch.arange(64, device='cuda')).sum(-1)
+    fit = torch.empty(P, dtype=torch.float64, device='cuda')
+    out = {}
+    for path in ('frontier', 'unionfind'):
+        if path == 'frontier' and not i.frontier_slots:
+            continue
+        plan.set_path(path)
+        for _ in range(2):
+            plan.evaluate_device(pop.data_ptr(), P, fit.data_ptr())
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(3):
+            plan.evaluate_device(pop.data_ptr(), P, fit.data_ptr())
+        e1.record(); torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1) / 3
+        out[path] = (ms, fit.clone())
+        print(f'  {label:7s} {path:9s} {ms:8.2f} ms  {P/ms/1e6:8.3f} Ggenomes/s')
+    if len(out) == 2:
+        assert torch.equal(out['frontier'][1], out['unionfind'][1]), 'paths disagree'
+    plan.set_path('auto')
