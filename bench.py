@@ -103,6 +103,10 @@ def build_workload(name: str):
     return tp, g, bs
 
 
+def _slots(f: int) -> int:
+    return 4 if f <= 4 else 8 if f <= 8 else 16 if f <= 16 else 32
+
+
 def shard_size(words: int, requested: int | None) -> int:
     if requested:
         return requested
@@ -219,6 +223,9 @@ def run_mine(args) -> None:
                 traffic = d.get("dram_bytes_per_launch_per_genome", 0) * P or None
         except Exception:
             traffic = None
+    kernel_name = (f"fitness_frontier_kernel<{_slots(plan.info.frontier_slots)}>"
+                   if plan.info.frontier_slots else
+                   ("fitness_smem_kernel" if plan.info.smem_path else "fitness_global_kernel"))
     cpu = None
     if world == 1 and not args.no_cpu_baseline:
         cpu = cpu_baseline(g, bs, res, plan, args)
@@ -247,7 +254,7 @@ def run_mine(args) -> None:
                    "best_cost_ms_after_timed_steps": best_cost},
         "kernels_ms": {"fitness": fit_ms, "breed": breed_ms},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                     "frac": achieved / peak, "traffic": traffic, "kernel": "fitness_smem_kernel",
+                     "frac": achieved / peak, "traffic": traffic, "kernel": kernel_name,
                      "peak_source": peak_src,
                      "algorithmic_bytes_per_launch": bytes_per_launch},
         "e2e": {"value": world * P * args.e2e_steps / e2e_s, "unit": "genomes/s",

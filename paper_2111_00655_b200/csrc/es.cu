@@ -182,8 +182,94 @@ breed_kernel(int32_t k, int32_t words, const uint64_t* __restrict__ parents,
   }
 }
 
+// Narrow genomes (W <= 8 words): one thread per child, the child row in
+// registers.  Same draws and semantics as breed_kernel.
+template <int W>
+__global__ void __launch_bounds__(256)
+breed_thread_kernel(int32_t k, const uint64_t* __restrict__ parents, const double* __restrict__ fit,
+                    int64_t n_parents, uint64_t* __restrict__ children, int64_t n_children,
+                    const uint64_t* __restrict__ keep, int64_t n_keep, uint64_t seed,
+                    uint32_t generation, uint32_t stream_id, int32_t tournament, double rate,
+                    double log1m_rate) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t child = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; child < n_children;
+       child += stride) {
+    uint64_t v[W];
+    if (child < n_keep) {
+#pragma unroll
+      for (int w = 0; w < W; ++w) v[w] = keep[child * W + w];
+    } else {
+      Philox rng(seed, (uint32_t)child, (uint32_t)(child >> 32) ^ (generation * 0x9E3779B9u),
+                 stream_id);
+      int64_t pa = 0, pb = 0;
+      for (int t = 0; t < 2; ++t) {
+        int64_t best = rng.below((uint32_t)n_parents);
+        double bf = __ldg(fit + best);
+        for (int j = 1; j < tournament; ++j) {
+          const int64_t i = rng.below((uint32_t)n_parents);
+          const double f = __ldg(fit + i);
+          if (f < bf) {
+            best = i;
+            bf = f;
+          }
+        }
+        if (t == 0) pa = best;
+        else pb = best;
+      }
+      int64_t ci = 0, cj = 0;
+      if (k >= 2) {
+        const int64_t x = rng.below((uint32_t)(k + 1)), y = rng.below((uint32_t)(k + 1));
+        ci = x < y ? x : y;
+        cj = x < y ? y : x;
+      }
+#pragma unroll
+      for (int w = 0; w < W; ++w) {
+        const uint64_t mb = seg_mask(ci, cj, w);
+        v[w] = (__ldg(parents + pa * W + w) & ~mb) | (__ldg(parents + pb * W + w) & mb);
+      }
+      if (rate >= 1.0 || rate * (double)k > 8.0) {
+        for (int64_t bit = 0; bit < k; ++bit) {
+          const double u = ((double)(rng.next() >> 8) + 0.5) * (1.0 / 16777216.0);
+          if (u < rate) {
+#pragma unroll
+            for (int w = 0; w < W; ++w)
+              if (w == (bit >> 6)) v[w] ^= 1ull << (bit & 63);
+          }
+        }
+      } else if (rate > 0.0) {
+        int64_t pos = -1;
+        while (true) {
+          const double gap = floor(log(rng.unit()) / log1m_rate);
+          if (!(gap < (double)k)) break;
+          pos += 1 + (int64_t)gap;
+          if (pos >= k) break;
+#pragma unroll
+          for (int w = 0; w < W; ++w)
+            if (w == (pos >> 6)) v[w] ^= 1ull << (pos & 63);
+        }
+      }
+      if (k % 64) v[(k - 1) >> 6] &= (1ull << (k % 64)) - 1ull;
+    }
+#pragma unroll
+    for (int w = 0; w < W; ++w) children[child * W + w] = v[w];
+  }
+}
+
 struct cb_es_plan;
 extern "C" int cb_es_plan_query(const cb_es_plan* p, cb_es_plan_info* info);
+
+template <int W>
+static void launch_breed_thread(int32_t k, const uint64_t* parents, const double* fit,
+                                int64_t n_parents, uint64_t* children, int64_t n_children,
+                                const uint64_t* keep, int64_t n_keep, uint64_t seed, uint32_t gen,
+                                uint32_t sid, int32_t tournament, double rate, double log1m,
+                                cudaStream_t s) {
+  int64_t blocks = (n_children + 255) / 256;
+  if (blocks > 148 * 8) blocks = 148 * 8;
+  breed_thread_kernel<W><<<(unsigned)blocks, 256, 0, s>>>(k, parents, fit, n_parents, children,
+                                                           n_children, keep, n_keep, seed, gen,
+                                                           sid, tournament, rate, log1m);
+}
 
 extern "C" int cb_es_breed(cb_es_plan* p, const uint64_t* d_parents, const double* d_parent_fit,
                            int64_t n_parents, uint64_t* d_children, int64_t n_children,
@@ -198,6 +284,28 @@ extern "C" int cb_es_breed(cb_es_plan* p, const uint64_t* d_parents, const doubl
   cb_es_plan_query(p, &info);
   if (n_children <= 0) return CB_OK;
   double log1m = (mutation_rate > 0.0 && mutation_rate < 1.0) ? log1p(-mutation_rate) : -1.0;
+  cudaStream_t s = (cudaStream_t)stream;
+  const uint32_t gen = (uint32_t)generation, sid = (uint32_t)stream_id;
+  switch (info.words) {
+#define CB_BREED_CASE(Wn)                                                                   \
+  case Wn:                                                                                  \
+    launch_breed_thread<Wn>(info.genome_bits, d_parents, d_parent_fit, n_parents, d_children, \
+                            n_children, d_keep, n_keep, seed, gen, sid, tournament,          \
+                            mutation_rate, log1m, s);                                        \
+    CB_CUDA_TRY(cudaGetLastError());                                                         \
+    return CB_OK;
+    CB_BREED_CASE(1)
+    CB_BREED_CASE(2)
+    CB_BREED_CASE(3)
+    CB_BREED_CASE(4)
+    CB_BREED_CASE(5)
+    CB_BREED_CASE(6)
+    CB_BREED_CASE(7)
+    CB_BREED_CASE(8)
+#undef CB_BREED_CASE
+    default:
+      break;
+  }
   int64_t blocks = (n_children + BREED_WARPS - 1) / BREED_WARPS;
   if (blocks > 148 * 16) blocks = 148 * 16;
   breed_kernel<<<(unsigned)blocks, BREED_WARPS * 32, 0, (cudaStream_t)stream>>>(

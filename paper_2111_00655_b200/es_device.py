@@ -31,6 +31,25 @@ def _torch():
     return torch
 
 
+def exchange_elites(best_val, best_row, group, out_fit, out_rows):
+    """All-gather every rank's best (fitness, genome row) and return the
+    global best row and value as device tensors (ties: lowest rank).
+
+    `best_val` (1,), `best_row` (1, W); `out_fit` (world,), `out_rows`
+    (world, W) are caller-owned buffers.  NCCL uses the in-place tensor
+    collective; other backends (gloo in the CPU tests) the list form."""
+    torch = _torch()
+    import torch.distributed as dist
+    if dist.get_backend(group) == "nccl":
+        dist.all_gather_into_tensor(out_fit, best_val, group=group)
+        dist.all_gather_into_tensor(out_rows, best_row, group=group)
+    else:
+        dist.all_gather(list(out_fit.view(-1, 1).unbind(0)), best_val, group=group)
+        dist.all_gather(list(out_rows.unbind(0)), best_row.view(-1), group=group)
+    who = torch.argmin(out_fit).view(1)
+    return out_rows.index_select(0, who), out_fit.index_select(0, who)
+
+
 class DeviceEvolution:
     def __init__(self, plan: FitnessPlan, population: int, seed: int = 0, tournament: int = 4,
                  mutation_rate: float | None = None, device=None, process_group=None,
@@ -85,6 +104,10 @@ class DeviceEvolution:
                               dtype=torch.int64, device=self.device)
         words ^= torch.randint(0, 4, (self.P, self.W), generator=gen, dtype=torch.int64,
                                device=self.device) << 62
+        if self.k % 64:  # bits past the genome length stay clear
+            words[:, -1] &= (1 << (self.k % 64)) - 1
+        elif self.k == 0:
+            words.zero_()
         self.pop[self.cur].copy_(words)
         if self.rank == 0:
             self.pop[self.cur][0].zero_()
@@ -101,12 +124,9 @@ class DeviceEvolution:
                                       ctypes.c_void_p(self._stream())))
         row = self.pop[self.cur].index_select(0, self.best_idx)
         if self.world > 1:
-            import torch.distributed as dist
-            dist.all_gather_into_tensor(self.gather_fit, self.best_val, group=self.group)
-            dist.all_gather_into_tensor(self.gather_rows, row, group=self.group)
-            who = _torch().argmin(self.gather_fit).view(1)
-            self.elite.copy_(self.gather_rows.index_select(0, who))
-            best = self.gather_fit.index_select(0, who)
+            elite, best = exchange_elites(self.best_val, row, self.group, self.gather_fit,
+                                          self.gather_rows)
+            self.elite.copy_(elite)
         else:
             self.elite.copy_(row)
             best = self.best_val

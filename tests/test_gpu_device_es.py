@@ -1,0 +1,59 @@
+"""Device-resident evolutionary loop (es_device.DeviceEvolution)."""
+
+import numpy as np
+import pytest
+import torch
+
+import paper_2111_00655_b200 as tp
+from conftest import build_case, golden, kernels_of
+from oracle import OracleCase
+from paper_2111_00655_b200.es_device import DeviceEvolution
+
+pytestmark = pytest.mark.gpu
+
+
+def _setup(name="bert_base"):
+    case = [c for c in golden("models") if c["name"] == name][0]
+    g, reg, meas = build_case(case)
+    res = tp.optimize(g, reg, meas, case["epsilon"])
+    plan = tp.FitnessPlan(g, reg, meas, res.placement, case["epsilon"],
+                          case["es"]["graph_backend"], res.kernel_matches)
+    return case, res, plan
+
+
+@pytest.mark.parametrize("name", ["resnet50", "bert_base"])
+def test_device_es_elitism_and_exact_fitness(gpu, name):
+    case, res, plan = _setup(name)
+    es = DeviceEvolution(plan, 4096, seed=3)
+    es.initialize()
+    for _ in range(15):
+        es.step()
+    hist = es.history_values()
+    assert len(hist) == 16
+    assert np.all(np.diff(hist) <= 0), "best cost must never increase (elitism)"
+    assert hist[0] <= plan.seed_cost  # the DP seed is row 0 of generation 0
+    # every stored fitness equals the oracle's graph-level cost of its genome
+    pop = es.pop[es.cur].cpu().numpy().view(np.uint64)
+    fit = es.fit[es.cur].cpu().numpy()
+    oc = OracleCase(case)
+    oc.price()
+    want = oc.fitness(kernels_of(res.placement), case["es"]["graph_backend"], pop[:1024])
+    assert np.array_equal(fit[:1024], want)
+    best, bits = es.best()
+    assert best == hist[-1]
+    assert plan.evaluate([bits.tolist()])[0] == best
+    # padding bits past the genome length stay clear
+    if plan.k % 64:
+        assert not np.any(pop[:, -1] >> np.uint64(plan.k % 64))
+
+
+def test_breed_identity_without_mutation(gpu):
+    _, _, plan = _setup("resnet50")
+    es = DeviceEvolution(plan, 512, seed=1, mutation_rate=0.0)
+    es.initialize()
+    row = es.pop[es.cur][5].clone()
+    es.pop[es.cur].copy_(row.expand_as(es.pop[es.cur]))
+    es.fit[es.cur].fill_(1.0)
+    es.elite.copy_(row.view(1, -1))
+    es.step()
+    assert torch.equal(es.pop[es.cur], row.expand_as(es.pop[es.cur]))
