@@ -205,7 +205,9 @@ typedef struct {
 } cb_es_plan_info;
 int cb_es_plan_query(const cb_es_plan* p, cb_es_plan_info* info);
 /* Evaluation path: -1 automatic (frontier program when available), 0 the
- * union-find kernels, 1 the frontier program.  For tests and profiling. */
+ * union-find kernels, 1 the frontier program (packed-label form when it has
+ * <= 16 slots), 2 the frontier program in its shared-memory-label form.
+ * For tests and profiling; all paths return identical results. */
 int cb_es_plan_set_path(cb_es_plan* p, int32_t path);
 /* slot_kernel (host, genome_bits): canonical kernel index of each bit;
  * rep_kind (host, genome_bits): 0 infeasible, 1 same-set pattern,

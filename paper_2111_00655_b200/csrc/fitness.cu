@@ -540,8 +540,8 @@ extern "C" int cb_es_plan_query(const cb_es_plan* p, cb_es_plan_info* info) {
 }
 
 extern "C" int cb_es_plan_set_path(cb_es_plan* p, int32_t path) {
-  CB_ARG_CHECK(p && path >= -1 && path <= 1, "cb_es_plan_set_path: bad arguments");
-  CB_ARG_CHECK(path != 1 || p->F > 0, "cb_es_plan_set_path: no frontier program for this plan");
+  CB_ARG_CHECK(p && path >= -1 && path <= 2, "cb_es_plan_set_path: bad arguments");
+  CB_ARG_CHECK(path < 1 || p->F > 0, "cb_es_plan_set_path: no frontier program for this plan");
   p->force_path = path;
   return CB_OK;
 }
@@ -931,9 +931,196 @@ fitness_frontier_kernel(int32_t M, int32_t words, fx192 base_const, fx192 eps,
   if (inexact) atomicAdd(flags, 1ull);
 }
 
-template <int F>
-static int launch_frontier_t(cb_es_plan* p, const uint64_t* d_pop, int64_t n, double* d_fit,
-                             cudaStream_t stream);
+// ------------------------------------- frontier program, packed-label form
+// Same walk for programs with at most 16 slots, but the component labels of
+// all slots live in one register (4 bits per slot) together with a nibble
+// mask of the occupied slots, so relabelling, "does the component have
+// another member" and slot (de)activation are a handful of branch-free ALU
+// operations (SWAR zero-nibble tests) instead of loops over shared memory.
+// Only the exact sums and the (count, single-unit) words sit in shared
+// memory, indexed by slot.  Every step is predicated so the 32 genomes of a
+// warp stay converged.
+template <typename LT>
+struct Nib;
+template <>
+struct Nib<uint32_t> {
+  static constexpr uint32_t ONE = 0x11111111u, LOW3 = 0x77777777u;
+};
+template <>
+struct Nib<uint64_t> {
+  static constexpr uint64_t ONE = 0x1111111111111111ull, LOW3 = 0x7777777777777777ull;
+};
+
+template <typename LT>
+__device__ __forceinline__ LT nib_eq(LT x, uint32_t v) {
+  // nibble mask (0xF) of the nibbles of x equal to v
+  const LT y = x ^ ((LT)v * Nib<LT>::ONE);
+  const LT z = ~(((y & Nib<LT>::LOW3) + Nib<LT>::LOW3) | y | Nib<LT>::LOW3);
+  return (z >> 3) * (LT)0xF;
+}
+
+template <typename LT>
+__device__ __forceinline__ int nib_first(LT m) {
+  if (sizeof(LT) == 8) return __ffsll((long long)m) - 1 >> 2;
+  return __ffs((int)m) - 1 >> 2;
+}
+
+template <typename LT, int F>
+__global__ void __launch_bounds__(FR_THREADS)
+fitness_frontier2_kernel(int32_t M, int32_t words, fx192 base_const, fx192 eps,
+                         const UnitRec* __restrict__ prog, const uint8_t* __restrict__ slots,
+                         const uint64_t* __restrict__ infeas, const double* __restrict__ rt,
+                         const uint64_t* __restrict__ pop, int64_t n, double* __restrict__ fit,
+                         unsigned long long* flags) {
+  extern __shared__ __align__(16) unsigned char fr_smem[];
+  uint64_t (*s0)[FR_THREADS] = reinterpret_cast<uint64_t (*)[FR_THREADS]>(fr_smem);
+  uint64_t (*s1)[FR_THREADS] = s0 + F;
+  uint64_t (*s2)[FR_THREADS] = s1 + F;
+  uint64_t (*cs)[FR_THREADS] = s2 + F;  // low 32: kernel count, high 32: single unit or -1
+  const int t = threadIdx.x;
+  bool inexact = false;
+  const int64_t stride = (int64_t)gridDim.x * FR_THREADS;
+  for (int64_t base = (int64_t)blockIdx.x * FR_THREADS + (t & ~31); base < n; base += stride) {
+    const int64_t i = base + (t & 31);
+    const bool in_range = i < n;
+    const uint64_t* gen = pop + (in_range ? i : 0) * words;
+    bool dead = !in_range;
+    if (in_range)
+      for (int32_t w = 0; w < words; ++w) dead |= (__ldg(gen + w) & __ldg(infeas + w)) != 0ull;
+    LT lab = 0;  // nibble s: label of slot s
+    LT act = 0;  // 0xF in nibble s while slot s is occupied
+    fx192 total = base_const;
+    fx192 pend = fx_zero();
+    int32_t pend_cnt = 0;
+    bool pend_valid = false;
+    int32_t cached_word = -1;
+    uint64_t word = 0;
+    for (int32_t p = 0; p < M; ++p) {
+      const uint4* rp = reinterpret_cast<const uint4*>(prog + p);
+      const uint4 meta = __ldg(rp + 5);  // back_off, end_off, slot|nback|nend, -
+      const uint4 q4 = __ldg(rp + 4);    // term1.w2 (x,y), bit (z), cnt (w)
+      const int32_t bit = (int32_t)q4.z;
+      bool on = !dead;
+      if (bit >= 0) {
+        const int32_t wi = bit >> 6;
+        if (wi != cached_word) {
+          word = dead ? 0ull : __ldg(gen + wi);
+          cached_word = wi;
+        }
+        on = (word >> (bit & 63)) & 1ull;
+      }
+      const int S = meta.z & 0xff;
+      const int nback = (meta.z >> 8) & 0xff;
+      const int nend = (meta.z >> 16) & 0xff;
+      const LT nibS = (LT)0xF << (4 * S);
+      if (on) {
+        const uint4 r0 = __ldg(rp + 0);
+        const uint4 r1 = __ldg(rp + 1);
+        if (bit >= 0) {
+          const uint4 r2 = __ldg(rp + 2);
+          fx192 off;
+          off.w[0] = ((uint64_t)r1.w << 32) | r1.z;
+          off.w[1] = ((uint64_t)r2.y << 32) | r2.x;
+          off.w[2] = ((uint64_t)r2.w << 32) | r2.z;
+          fx_sub(total, off);
+        }
+        s0[S][t] = ((uint64_t)r0.y << 32) | r0.x;
+        s1[S][t] = ((uint64_t)r0.w << 32) | r0.z;
+        s2[S][t] = ((uint64_t)r1.y << 32) | r1.x;
+        cs[S][t] = ((uint64_t)(uint32_t)p << 32) | q4.w;
+        act |= nibS;
+        lab = (lab & ~nibS) | ((LT)S << (4 * S));
+      }
+      for (int j = 0; j < nback; ++j) {
+        const int b = __ldg(slots + meta.x + j);
+        const uint32_t B = (uint32_t)(lab >> (4 * b)) & 0xF;
+        const bool merge = on && ((act >> (4 * b)) & 1) && B != (uint32_t)S;
+        if (merge) {
+          fx192 x = {{s0[S][t], s1[S][t], s2[S][t]}};
+          const fx192 y = {{s0[B][t], s1[B][t], s2[B][t]}};
+          fx_add(x, y);
+          s0[S][t] = x.w[0];
+          s1[S][t] = x.w[1];
+          s2[S][t] = x.w[2];
+          const uint32_t c = (uint32_t)cs[S][t] + (uint32_t)cs[B][t];
+          cs[S][t] = 0xffffffff00000000ull | c;
+          const LT m = nib_eq<LT>(lab, B) & act;
+          lab = (lab & ~m) | (((LT)S * Nib<LT>::ONE) & m);
+        }
+      }
+      for (int j = 0; j < nend; ++j) {
+        const int e = __ldg(slots + meta.y + j);
+        const LT nibE = (LT)0xF << (4 * e);
+        int emit_slot = -1;
+        if (act & nibE) {
+          const uint32_t X = (uint32_t)(lab >> (4 * e)) & 0xF;
+          act &= ~nibE;
+          const LT others = nib_eq<LT>(lab, X) & act;
+          if (others == 0) {  // last member leaves: the region is complete
+            const uint64_t cw = cs[e][t];
+            const int32_t one = (int32_t)(cw >> 32);
+            if (one >= 0) {
+              const uint4* tp = reinterpret_cast<const uint4*>(prog + one);
+              const uint4 a = __ldg(tp + 3), b2 = __ldg(tp + 4);
+              const fx192 v = {{((uint64_t)a.y << 32) | a.x, ((uint64_t)a.w << 32) | a.z,
+                                ((uint64_t)b2.y << 32) | b2.x}};
+              fx_add(total, v);
+            } else {
+              const fx192 cur = {{s0[e][t], s1[e][t], s2[e][t]}};
+              const int32_t ccnt = (int32_t)(uint32_t)cw;
+              if (!pend_valid) {
+                pend = cur;
+                pend_cnt = ccnt;
+                pend_valid = true;
+              } else {  // price the older region now, keep the new one queued
+                s0[e][t] = pend.w[0];
+                s1[e][t] = pend.w[1];
+                s2[e][t] = pend.w[2];
+                cs[e][t] = 0xffffffff00000000ull | (uint32_t)pend_cnt;
+                pend = cur;
+                pend_cnt = ccnt;
+                emit_slot = e;
+              }
+            }
+          } else if (X == (uint32_t)e) {  // data moves to a member that stays
+            const int tgt = nib_first<LT>(others);
+            s0[tgt][t] = s0[e][t];
+            s1[tgt][t] = s1[e][t];
+            s2[tgt][t] = s2[e][t];
+            cs[tgt][t] = cs[e][t];
+            lab = (lab & ~others) | (((LT)tgt * Nib<LT>::ONE) & others);
+          }
+        }
+        if (__any_sync(0xffffffffu, emit_slot >= 0)) {
+          if (emit_slot >= 0) {
+            const fx192 sum = {{s0[emit_slot][t], s1[emit_slot][t], s2[emit_slot][t]}};
+            const double prod =
+                __dmul_rn(fx_to_double(sum), __ldg(rt + (uint32_t)cs[emit_slot][t]));
+            fx192 term;
+            inexact |= !fx_from_double(prod, term);
+            fx_add(total, term);
+            fx_add(total, eps);
+          }
+        }
+      }
+    }
+    if (__any_sync(0xffffffffu, pend_valid)) {
+      if (pend_valid) {
+        const double prod = __dmul_rn(fx_to_double(pend), __ldg(rt + pend_cnt));
+        fx192 term;
+        inexact |= !fx_from_double(prod, term);
+        fx_add(total, term);
+        fx_add(total, eps);
+      }
+    }
+    if (in_range) fit[i] = dead ? __longlong_as_double(0x7ff0000000000000ll) : fx_to_double(total);
+  }
+  if (inexact) atomicAdd(flags, 1ull);
+}
+
+template <typename LT, int F>
+static int launch_frontier2_t(cb_es_plan* p, const uint64_t* d_pop, int64_t n, double* d_fit,
+                              cudaStream_t stream);
 
 static FitArgs make_args(cb_es_plan* p) {
   FitArgs a;
@@ -988,12 +1175,38 @@ static int launch_frontier_t(cb_es_plan* p, const uint64_t* d_pop, int64_t n, do
   return CB_OK;
 }
 
+template <typename LT, int F>
+static int launch_frontier2_t(cb_es_plan* p, const uint64_t* d_pop, int64_t n, double* d_fit,
+                              cudaStream_t stream) {
+  const size_t smem = (size_t)4 * F * FR_THREADS * sizeof(uint64_t);
+  static bool configured = false;
+  if (!configured) {
+    CB_CUDA_TRY(cudaFuncSetAttribute(fitness_frontier2_kernel<LT, F>,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    configured = true;
+  }
+  int per_sm = 0;
+  CB_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fitness_frontier2_kernel<LT, F>,
+                                                            FR_THREADS, smem));
+  if (per_sm < 1) per_sm = 1;
+  const int64_t want = (n + FR_THREADS - 1) / FR_THREADS;
+  const int64_t grid = std::min<int64_t>(want, (int64_t)per_sm * sm_count());
+  fitness_frontier2_kernel<LT, F><<<(unsigned)grid, FR_THREADS, smem, stream>>>(
+      p->M, p->words, p->base_const, p->eps, p->d_prog.p, p->d_prog_slots.p, p->d_infeas.p,
+      p->d_rt.p, d_pop, n, d_fit, p->d_flags.p);
+  CB_CUDA_TRY(cudaGetLastError());
+  return CB_OK;
+}
+
 static int launch_fitness(cb_es_plan* p, const uint64_t* d_pop, int64_t n, double* d_fit,
                           cudaStream_t stream) {
   if (n <= 0) return CB_OK;
   const bool frontier = p->F > 0 && p->force_path != 0;
   if (frontier) {
-    if (p->F <= 4) return launch_frontier_t<4>(p, d_pop, n, d_fit, stream);
+    if (p->force_path != 2) {
+      if (p->F <= 8) return launch_frontier2_t<uint32_t, 8>(p, d_pop, n, d_fit, stream);
+      if (p->F <= 16) return launch_frontier2_t<uint64_t, 16>(p, d_pop, n, d_fit, stream);
+    }
     if (p->F <= 8) return launch_frontier_t<8>(p, d_pop, n, d_fit, stream);
     if (p->F <= 16) return launch_frontier_t<16>(p, d_pop, n, d_fit, stream);
     return launch_frontier_t<32>(p, d_pop, n, d_fit, stream);

@@ -208,7 +208,7 @@ class FitnessPlan:
         """'auto' | 'frontier' (thread per genome) | 'unionfind' (warp/CTA
         per genome); both give identical results, `auto` picks the frontier
         program whenever the plan has one."""
-        code = {"auto": -1, "unionfind": 0, "frontier": 1}[path]
+        code = {"auto": -1, "unionfind": 0, "frontier": 1, "frontier_smem": 2}[path]
         nat.check(nat.lib().cb_es_plan_set_path(self.handle.raw, code))
 
     def evaluate(self, genomes: Sequence[Sequence[int]]) -> np.ndarray:

@@ -155,6 +155,7 @@ def test_fitness_paths_agree_with_oracle(gpu, case):
     plan.set_path("unionfind")
     assert np.array_equal(plan.evaluate(genomes), want)
     if plan.info.frontier_slots:
-        plan.set_path("frontier")
-        assert np.array_equal(plan.evaluate(genomes), want)
+        for path in ("frontier", "frontier_smem"):
+            plan.set_path(path)
+            assert np.array_equal(plan.evaluate(genomes), want), path
     plan.set_path("auto")

@@ -12,18 +12,21 @@ res = tp.optimize(g, bs.registry, bs.measurer, 0.01)
 plan = tp.FitnessPlan(g, bs.registry, bs.measurer, res.placement, 0.01, bs.graph_backend, res.kernel_matches)
 i = plan.info
 print(name, 'k', plan.k, 'units', i.units, 'edges', i.edges, 'frontier', i.frontier_slots, 'dp', res.device)
-for label, fill in (('random', None), ('ones', 1), ('sparse', 0.1)):
+for label, fill in (('random', None), ('sparse', 0.1), ('dense', 0.9)):
     if fill is None:
         pop = torch.randint(-(1 << 62), 1 << 62, (P, plan.words), dtype=torch.int64, device='cuda')
-    elif fill == 1:
-        pop = torch.full((P, plan.words), -1, dtype=torch.int64, device='cuda')
     else:
         bits = (torch.rand((P, plan.words, 64), device='cuda') < fill).to(torch.int64)
         pop = (bits << torch.arange(64, device='cuda')).sum(-1)
+    feas = np.zeros(plan.words, np.uint64)  # keep genomes feasible, as an ES population is
+    for s_ in range(plan.k):
+        if plan.rep_kind[s_] != 0:
+            feas[s_ // 64] |= np.uint64(1) << np.uint64(s_ % 64)
+    pop &= torch.from_numpy(feas.view(np.int64)).cuda()
     fit = torch.empty(P, dtype=torch.float64, device='cuda')
     out = {}
-    for path in ('frontier', 'unionfind'):
-        if path == 'frontier' and not i.frontier_slots:
+    for path in ('frontier', 'frontier_smem', 'unionfind'):
+        if path.startswith('frontier') and not i.frontier_slots:
             continue
         plan.set_path(path)
         for _ in range(2):
@@ -37,6 +40,6 @@ for label, fill in (('random', None), ('ones', 1), ('sparse', 0.1)):
         ms = e0.elapsed_time(e1) / 3
         out[path] = (ms, fit.clone())
         print(f'  {label:7s} {path:9s} {ms:8.2f} ms  {P/ms/1e6:8.3f} Ggenomes/s')
-    if len(out) == 2:
-        assert torch.equal(out['frontier'][1], out['unionfind'][1]), 'paths disagree'
+    for k in out:
+        assert torch.equal(out[k][1], out['unionfind'][1]), 'paths disagree'
     plan.set_path('auto')
