@@ -116,10 +116,14 @@ FXI bool fx_from_double(double d, fx192& out) {
     s = 0;
   }
   if (s + 53 > 192) return false;  // >= 2^64
-  int limb = s >> 6;
-  int off = s & 63;
-  out.w[limb] = mant << off;
-  if (off != 0 && limb + 1 < 3) out.w[limb + 1] = mant >> (64 - off);
+  // static-index placement (no dynamic limb indexing -> stays in registers)
+  const int limb = s >> 6;
+  const int off = s & 63;
+  const uint64_t lo = mant << off;
+  const uint64_t hi = off ? (mant >> (64 - off)) : 0ull;
+  out.w[0] = limb == 0 ? lo : 0ull;
+  out.w[1] = limb == 0 ? hi : (limb == 1 ? lo : 0ull);
+  out.w[2] = limb == 1 ? hi : (limb == 2 ? lo : 0ull);
   return exact;
 }
 
@@ -131,28 +135,37 @@ FXI int fx_clz64(uint64_t x) {
 #endif
 }
 
+// bits [s, s+64) of the 192-bit value (s in [0, 192)); static indexing only
+FXI uint64_t fx_window(const fx192& a, int s) {
+  const int l = s >> 6, o = s & 63;
+  const uint64_t x0 = l == 0 ? a.w[0] : (l == 1 ? a.w[1] : a.w[2]);
+  const uint64_t x1 = l == 0 ? a.w[1] : (l == 1 ? a.w[2] : 0ull);
+  return o ? ((x0 >> o) | (x1 << (64 - o))) : x0;
+}
+
+// any bit strictly below position s (s in [0, 192])
+FXI bool fx_any_below(const fx192& a, int s) {
+  const uint64_t m0 = s >= 64 ? ~0ull : ((1ull << s) - 1);
+  const uint64_t m1 = s >= 128 ? ~0ull : (s <= 64 ? 0ull : ((1ull << (s - 64)) - 1));
+  const uint64_t m2 = s >= 192 ? ~0ull : (s <= 128 ? 0ull : ((1ull << (s - 128)) - 1));
+  return ((a.w[0] & m0) | (a.w[1] & m1) | (a.w[2] & m2)) != 0ull;
+}
+
 // Round to the nearest double, ties to even (what math.fsum returns).
 FXI double fx_to_double(const fx192& a) {
-  int limb = a.w[2] ? 2 : (a.w[1] ? 1 : (a.w[0] ? 0 : -1));
+  const int limb = a.w[2] ? 2 : (a.w[1] ? 1 : (a.w[0] ? 0 : -1));
   if (limb < 0) return 0.0;
-  int p = limb * 64 + 63 - fx_clz64(a.w[limb]);  // index of the MSB
+  const uint64_t top = limb == 2 ? a.w[2] : (limb == 1 ? a.w[1] : a.w[0]);
+  int p = limb * 64 + 63 - fx_clz64(top);  // index of the MSB
   uint64_t m;
-  bool round_bit = false, sticky = false;
   if (p <= 52) {
     m = a.w[0];  // fits exactly; p <= 52 implies limb 0
   } else {
-    int sh = p - 52;  // drop `sh` low bits
-    // m = bits [sh, sh+53)
-    int l0 = sh >> 6, o0 = sh & 63;
-    m = a.w[l0] >> o0;
-    if (o0 != 0 && l0 + 1 < 3) m |= a.w[l0 + 1] << (64 - o0);
-    m &= (1ull << 53) - 1;
-    int rb = sh - 1;  // round bit index
-    round_bit = (a.w[rb >> 6] >> (rb & 63)) & 1ull;
-    // sticky: any bit below rb
-    int full = rb >> 6;
-    for (int i = 0; i < full; ++i) sticky |= a.w[i] != 0;
-    if (rb & 63) sticky |= (a.w[full] & ((1ull << (rb & 63)) - 1)) != 0;
+    const int sh = p - 52;  // drop `sh` low bits (1 <= sh <= 139)
+    const uint64_t win = fx_window(a, sh - 1);  // round bit at bit 0, mantissa above
+    m = (win >> 1) & ((1ull << 53) - 1);
+    const bool round_bit = win & 1ull;
+    const bool sticky = fx_any_below(a, sh - 1);
     if (round_bit && (sticky || (m & 1ull))) {
       m += 1;
       if (m == (1ull << 53)) {

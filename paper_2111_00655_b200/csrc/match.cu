@@ -195,7 +195,8 @@ __device__ bool constraints_hold(const MatchArgs& a, int32_t P, int32_t node) {
 // Walk pattern `p` anchored at `root`.  On success fills bind[0..npos) and
 // members[0..nmem) (sorted, unique) and returns true.
 __device__ bool match_walk(const MatchArgs& a, int32_t root, int32_t p, int32_t* bind,
-                           int32_t* members, int32_t& npos, int32_t& nmem) {
+                           int32_t* members, int32_t& npos, int32_t& nmem,
+                           const int32_t* s_row, int32_t s_deg) {
   const int32_t base = a.pat_pos_ptr[p];
   npos = a.pat_pos_ptr[p + 1] - base;
   nmem = 0;
@@ -205,8 +206,14 @@ __device__ bool match_walk(const MatchArgs& a, int32_t root, int32_t p, int32_t*
     if (i == 0) {
       node = root;
     } else {
-      const int32_t par = bind[a.pos_parent[P]];
-      node = __ldg(a.in_src + a.in_ptr[par] + a.pos_argidx[P]);
+      const int32_t pp = a.pos_parent[P];
+      const int32_t slot = a.pos_argidx[P];
+      if (pp == 0 && slot < s_deg) {
+        node = s_row[slot];  // the anchor's input row, staged by the warp
+      } else {
+        const int32_t par = bind[pp];
+        node = __ldg(a.in_src + a.in_ptr[par] + slot);
+      }
       if (node < 0) return false;  // graph input where an op is required
     }
     if (__ldg(a.kind + node) != a.pos_kind[P]) return false;
@@ -263,6 +270,11 @@ match_count_kernel(MatchArgs a, uint8_t* pair_ok, int32_t* pair_mem, int32_t* pa
   if (g >= a.n_groups) return;
   const int32_t root = a.group_anchor[g];
   const int32_t c0 = a.cand_ptr[g], c1 = a.cand_ptr[g + 1];
+  __shared__ int32_t s_in[MATCH_WARPS][STAGE_IN];
+  int32_t* s_row = s_in[threadIdx.x >> 5];
+  const int32_t s_deg = min(a.in_ptr[root + 1] - a.in_ptr[root], STAGE_IN);
+  if (lane < s_deg) s_row[lane] = a.in_src[a.in_ptr[root] + lane];
+  __syncwarp();
   int32_t bind[CB_MAXPOS];
   int32_t members[CB_MAXPOS];
   int32_t count = 0;
@@ -271,7 +283,7 @@ match_count_kernel(MatchArgs a, uint8_t* pair_ok, int32_t* pair_mem, int32_t* pa
     bool ok = false;
     int32_t npos = 0, nmem = 0;
     if (c < c1) {
-      ok = match_walk(a, root, a.cand_pat[c], bind, members, npos, nmem);
+      ok = match_walk(a, root, a.cand_pat[c], bind, members, npos, nmem, s_row, s_deg);
       pair_ok[c] = ok ? 1 : 0;
       pair_mem[c] = ok ? nmem : 0;
       pair_bind[c] = ok ? npos : 0;
@@ -293,6 +305,11 @@ match_fill_kernel(MatchArgs a, const uint8_t* pair_ok, const int32_t* mem_off,
   if (g >= a.n_groups) return;
   const int32_t root = a.group_anchor[g];
   const int32_t c0 = a.cand_ptr[g], c1 = a.cand_ptr[g + 1];
+  __shared__ int32_t s_in[MATCH_WARPS][STAGE_IN];
+  int32_t* s_row = s_in[threadIdx.x >> 5];
+  const int32_t s_deg = min(a.in_ptr[root + 1] - a.in_ptr[root], STAGE_IN);
+  if (lane < s_deg) s_row[lane] = a.in_src[a.in_ptr[root] + lane];
+  __syncwarp();
   int32_t bind[CB_MAXPOS];
   int32_t members[CB_MAXPOS];
   int32_t rank_base = group_ptr[g];
@@ -303,7 +320,7 @@ match_fill_kernel(MatchArgs a, const uint8_t* pair_ok, const int32_t* mem_off,
     if (ok) {
       int32_t npos, nmem;
       const int32_t p = a.cand_pat[c];
-      match_walk(a, root, p, bind, members, npos, nmem);
+      match_walk(a, root, p, bind, members, npos, nmem, s_row, s_deg);
       const int32_t m = rank_base + __popc(mask & ((1u << lane) - 1u));
       out_pat[m] = p;
       out_root[m] = root;

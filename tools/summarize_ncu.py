@@ -1,0 +1,69 @@
+"""Summarise gpurun_out/ ncu artefacts into profiles/ (run in the build
+container after tools/gpu_profile.sh).  Writes:
+  profiles/<tag>_launches.md          per-kernel share of the launch list
+  profiles/<tag>_fitness_ncu.json     full-set metrics of the fitness kernel
+  profiles/fitness_ncu_summary.json   traffic per genome (read by bench.py)
+"""
+import csv, json, os, subprocess, sys, collections
+
+tag = sys.argv[1] if len(sys.argv) > 1 else "r01"
+root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+out = os.path.join(root, "profiles")
+os.makedirs(out, exist_ok=True)
+
+# launch list
+rows = []
+with open(os.path.join(root, "gpurun_out", "launches.csv")) as fh:
+    lines = [l for l in fh if l.startswith('"')]
+rd = csv.reader(lines)
+hdr = next(rd)
+ix = {h: i for i, h in enumerate(hdr)}
+for r in rd:
+    if r[ix["Metric Name"]] != "gpu__time_duration.sum":
+        continue
+    name = r[ix["Kernel Name"]]
+    unit = r[ix["Metric Unit"]]
+    v = float(r[ix["Metric Value"]].replace(",", ""))
+    ns = v * {"nsecond": 1, "usecond": 1e3, "msecond": 1e6, "second": 1e9}.get(unit, 1)
+    rows.append((name.split("(")[0], ns))
+agg = collections.OrderedDict()
+for n, ns in rows:
+    a = agg.setdefault(n, [0, 0.0])
+    a[0] += 1
+    a[1] += ns
+tot = sum(a[1] for a in agg.values())
+with open(os.path.join(out, f"{tag}_launches.md"), "w") as fh:
+    fh.write(f"# {tag}: ncu launch list (gpu__time_duration.sum, --clock-control none)\n\n")
+    fh.write("Command: `ncu --metrics gpu__time_duration.sum --clock-control none -c 2000 "
+             "python bench.py --steps 3 --warmup 3 --no-cpu-baseline --e2e-steps 1 "
+             "--search-generations 3` (cold-cache, serialised: compare shares).\n\n")
+    fh.write("| kernel | launches | total ms | share |\n|---|---:|---:|---:|\n")
+    for n, (c, ns) in sorted(agg.items(), key=lambda kv: -kv[1][1]):
+        fh.write(f"| `{n}` | {c} | {ns / 1e6:.3f} | {100 * ns / tot:.1f}% |\n")
+print(open(os.path.join(out, f"{tag}_launches.md")).read())
+
+# full capture of the fitness kernel
+rep = os.path.join(root, "gpurun_out", "fitness_full.ncu-rep")
+if os.path.exists(rep):
+    raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True,
+                         text=True).stdout.splitlines()
+    r = list(csv.reader(raw))
+    names, units, vals = r[0], r[1], r[2]
+    want = ["Kernel Name", "launch__grid_size", "launch__block_size", "launch__registers_per_thread",
+            "gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
+            "sm__throughput.avg.pct_of_peak_sustained_elapsed",
+            "gpu__compute_memory_throughput.avg.pct_of_peak_sustained_elapsed",
+            "sm__warps_active.avg.pct_of_peak_sustained_active",
+            "smsp__inst_executed.sum", "smsp__issue_active.avg.pct_of_peak_sustained_active",
+            "l1tex__t_sector_hit_rate.pct", "lts__t_sector_hit_rate.pct"]
+    d = {}
+    for w in want:
+        if w in names:
+            i = names.index(w)
+            d[w] = {"value": vals[i], "unit": units[i]}
+    stalls = {n.replace("smsp__pcsamp_warps_issue_stalled_", ""): int(float(vals[i] or 0))
+              for i, n in enumerate(names)
+              if n.startswith("smsp__pcsamp_warps_issue_stalled_") and not n.endswith("not_issued")}
+    d["stall_samples"] = dict(sorted(stalls.items(), key=lambda kv: -kv[1])[:8])
+    json.dump(d, open(os.path.join(out, f"{tag}_fitness_ncu.json"), "w"), indent=1)
+    print(json.dumps(d, indent=1))
