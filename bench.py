@@ -186,8 +186,9 @@ def run_mine(args) -> None:
 
     # e2e through the public API with host buffers (pinned)
     rng = np.random.default_rng(rank)
+    # the population the timed ES steps produced, now host-resident (pinned)
     host = torch.empty((P, plan.words), dtype=torch.int64, pin_memory=True)
-    host.copy_(torch.from_numpy(rng.integers(-(1 << 62), 1 << 62, size=(P, plan.words))))
+    host.copy_(es.pop[es.cur])
     host_np = host.numpy().view(np.uint64)
     plan.evaluate_packed(host_np)  # warm
     barrier()
@@ -223,8 +224,10 @@ def run_mine(args) -> None:
                 traffic = d.get("dram_bytes_per_launch_per_genome", 0) * P or None
         except Exception:
             traffic = None
-    kernel_name = (f"fitness_frontier_kernel<{_slots(plan.info.frontier_slots)}>"
-                   if plan.info.frontier_slots else
+    f_slots = plan.info.frontier_slots
+    kernel_name = ((f"fitness_frontier2_kernel<{'uint32_t, 8' if f_slots <= 8 else 'uint64_t, 16'}>"
+                    if f_slots <= 16 else f"fitness_frontier_kernel<{_slots(f_slots)}>")
+                   if f_slots else
                    ("fitness_smem_kernel" if plan.info.smem_path else "fitness_global_kernel"))
     cpu = None
     if world == 1 and not args.no_cpu_baseline:

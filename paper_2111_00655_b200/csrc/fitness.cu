@@ -965,6 +965,35 @@ __device__ __forceinline__ int nib_first(LT m) {
   return __ffs((int)m) - 1 >> 2;
 }
 
+#define FR_QCAP 64
+
+// Price queue entry `idx` (exact region sum, kernel count, owner lane) and
+// add its term to the owner's accumulator (shared-memory multi-limb atomics:
+// an owner can have several entries in one batch).
+__device__ __forceinline__ void fr_price_entry(const uint64_t* qs0, const uint64_t* qs1,
+                                               const uint64_t* qs2, const uint64_t* qm, int idx,
+                                               const double* __restrict__ rt, const fx192& eps,
+                                               uint64_t* tacc0, uint64_t* tacc1, uint64_t* tacc2,
+                                               bool& inexact) {
+  const fx192 sum = {{qs0[idx], qs1[idx], qs2[idx]}};
+  const uint64_t m = qm[idx];
+  const double prod = __dmul_rn(fx_to_double(sum), __ldg(rt + (uint32_t)m));
+  fx192 term;
+  inexact |= !fx_from_double(prod, term);
+  fx_add(term, eps);
+  const int owner = (int)(m >> 32);
+  unsigned long long* w0 = reinterpret_cast<unsigned long long*>(tacc0 + owner);
+  unsigned long long* w1 = reinterpret_cast<unsigned long long*>(tacc1 + owner);
+  unsigned long long* w2 = reinterpret_cast<unsigned long long*>(tacc2 + owner);
+  const unsigned long long o0 = atomicAdd(w0, (unsigned long long)term.w[0]);
+  unsigned long long c = (o0 + term.w[0]) < o0;
+  const unsigned long long a1 = term.w[1] + c;
+  unsigned long long c1 = a1 < c;
+  const unsigned long long o1 = atomicAdd(w1, a1);
+  c1 += (o1 + a1) < o1;
+  atomicAdd(w2, (unsigned long long)(term.w[2] + c1));
+}
+
 template <typename LT, int F>
 __global__ void __launch_bounds__(FR_THREADS)
 fitness_frontier2_kernel(int32_t M, int32_t words, fx192 base_const, fx192 eps,
@@ -978,6 +1007,21 @@ fitness_frontier2_kernel(int32_t M, int32_t words, fx192 base_const, fx192 eps,
   uint64_t (*s2)[FR_THREADS] = s1 + F;
   uint64_t (*cs)[FR_THREADS] = s2 + F;  // low 32: kernel count, high 32: single unit or -1
   const int t = threadIdx.x;
+  const int lane = t & 31, warp = t >> 5;
+  // per-warp queue of closed regions + per-lane term accumulators
+  uint64_t* qbase = reinterpret_cast<uint64_t*>(cs + F) + (size_t)warp * 4 * FR_QCAP;
+  uint64_t* qs0 = qbase;
+  uint64_t* qs1 = qbase + FR_QCAP;
+  uint64_t* qs2 = qbase + 2 * FR_QCAP;
+  uint64_t* qm = qbase + 3 * FR_QCAP;  // low 32: kernel count, high 32: owner lane
+  uint64_t* tbase = reinterpret_cast<uint64_t*>(cs + F) + (size_t)(FR_THREADS / 32) * 4 * FR_QCAP +
+                    (size_t)warp * 96;
+  uint64_t* tacc0 = tbase;
+  uint64_t* tacc1 = tbase + 32;
+  uint64_t* tacc2 = tbase + 64;
+  tacc0[lane] = tacc1[lane] = tacc2[lane] = 0ull;
+  __syncwarp();
+  int qn = 0;
   bool inexact = false;
   const int64_t stride = (int64_t)gridDim.x * FR_THREADS;
   for (int64_t base = (int64_t)blockIdx.x * FR_THREADS + (t & ~31); base < n; base += stride) {
@@ -990,9 +1034,6 @@ fitness_frontier2_kernel(int32_t M, int32_t words, fx192 base_const, fx192 eps,
     LT lab = 0;  // nibble s: label of slot s
     LT act = 0;  // 0xF in nibble s while slot s is occupied
     fx192 total = base_const;
-    fx192 pend = fx_zero();
-    int32_t pend_cnt = 0;
-    bool pend_valid = false;
     int32_t cached_word = -1;
     uint64_t word = 0;
     for (int32_t p = 0; p < M; ++p) {
@@ -1066,21 +1107,7 @@ fitness_frontier2_kernel(int32_t M, int32_t words, fx192 base_const, fx192 eps,
                                 ((uint64_t)b2.y << 32) | b2.x}};
               fx_add(total, v);
             } else {
-              const fx192 cur = {{s0[e][t], s1[e][t], s2[e][t]}};
-              const int32_t ccnt = (int32_t)(uint32_t)cw;
-              if (!pend_valid) {
-                pend = cur;
-                pend_cnt = ccnt;
-                pend_valid = true;
-              } else {  // price the older region now, keep the new one queued
-                s0[e][t] = pend.w[0];
-                s1[e][t] = pend.w[1];
-                s2[e][t] = pend.w[2];
-                cs[e][t] = 0xffffffff00000000ull | (uint32_t)pend_cnt;
-                pend = cur;
-                pend_cnt = ccnt;
-                emit_slot = e;
-              }
+              emit_slot = e;  // multi-unit region: queued for warp-wide pricing
             }
           } else if (X == (uint32_t)e) {  // data moves to a member that stays
             const int tgt = nib_first<LT>(others);
@@ -1091,28 +1118,45 @@ fitness_frontier2_kernel(int32_t M, int32_t words, fx192 base_const, fx192 eps,
             lab = (lab & ~others) | (((LT)tgt * Nib<LT>::ONE) & others);
           }
         }
-        if (__any_sync(0xffffffffu, emit_slot >= 0)) {
+        // Closed multi-unit regions of all lanes go to the warp's queue; once
+        // 32 are waiting, every lane prices one (full-warp utilisation) and
+        // adds the term to its owner's accumulator.
+        const unsigned closing = __ballot_sync(0xffffffffu, emit_slot >= 0);
+        if (closing) {
           if (emit_slot >= 0) {
-            const fx192 sum = {{s0[emit_slot][t], s1[emit_slot][t], s2[emit_slot][t]}};
-            const double prod =
-                __dmul_rn(fx_to_double(sum), __ldg(rt + (uint32_t)cs[emit_slot][t]));
-            fx192 term;
-            inexact |= !fx_from_double(prod, term);
-            fx_add(total, term);
-            fx_add(total, eps);
+            const int at = qn + __popc(closing & ((1u << lane) - 1u));
+            qs0[at] = s0[emit_slot][t];
+            qs1[at] = s1[emit_slot][t];
+            qs2[at] = s2[emit_slot][t];
+            qm[at] = ((uint64_t)lane << 32) | (uint32_t)cs[emit_slot][t];
+          }
+          qn += __popc(closing);
+          if (qn >= 32) {
+            __syncwarp();
+            fr_price_entry(qs0, qs1, qs2, qm, lane, rt, eps, tacc0, tacc1, tacc2, inexact);
+            __syncwarp();
+            if (lane < qn - 32) {
+              qs0[lane] = qs0[32 + lane];
+              qs1[lane] = qs1[32 + lane];
+              qs2[lane] = qs2[32 + lane];
+              qm[lane] = qm[32 + lane];
+            }
+            __syncwarp();
+            qn -= 32;
           }
         }
       }
     }
-    if (__any_sync(0xffffffffu, pend_valid)) {
-      if (pend_valid) {
-        const double prod = __dmul_rn(fx_to_double(pend), __ldg(rt + pend_cnt));
-        fx192 term;
-        inexact |= !fx_from_double(prod, term);
-        fx_add(total, term);
-        fx_add(total, eps);
-      }
+    __syncwarp();
+    if (lane < qn) fr_price_entry(qs0, qs1, qs2, qm, lane, rt, eps, tacc0, tacc1, tacc2, inexact);
+    qn = 0;
+    __syncwarp();
+    {
+      const fx192 acc = {{tacc0[lane], tacc1[lane], tacc2[lane]}};
+      fx_add(total, acc);
+      tacc0[lane] = tacc1[lane] = tacc2[lane] = 0ull;
     }
+    __syncwarp();
     if (in_range) fit[i] = dead ? __longlong_as_double(0x7ff0000000000000ll) : fx_to_double(total);
   }
   if (inexact) atomicAdd(flags, 1ull);
@@ -1178,7 +1222,8 @@ static int launch_frontier_t(cb_es_plan* p, const uint64_t* d_pop, int64_t n, do
 template <typename LT, int F>
 static int launch_frontier2_t(cb_es_plan* p, const uint64_t* d_pop, int64_t n, double* d_fit,
                               cudaStream_t stream) {
-  const size_t smem = (size_t)4 * F * FR_THREADS * sizeof(uint64_t);
+  const size_t smem = ((size_t)4 * F * FR_THREADS + (size_t)(FR_THREADS / 32) * (4 * FR_QCAP + 96)) *
+                      sizeof(uint64_t);
   static bool configured = false;
   if (!configured) {
     CB_CUDA_TRY(cudaFuncSetAttribute(fitness_frontier2_kernel<LT, F>,

@@ -65,5 +65,16 @@ if os.path.exists(rep):
               for i, n in enumerate(names)
               if n.startswith("smsp__pcsamp_warps_issue_stalled_") and not n.endswith("not_issued")}
     d["stall_samples"] = dict(sorted(stalls.items(), key=lambda kv: -kv[1])[:8])
+    genomes = int(sys.argv[2]) if len(sys.argv) > 2 else 0
+    if genomes:
+        to_b = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+        rd = float(d["dram__bytes_read.sum"]["value"]) * to_b[d["dram__bytes_read.sum"]["unit"]]
+        wr = float(d["dram__bytes_write.sum"]["value"]) * to_b[d["dram__bytes_write.sum"]["unit"]]
+        d["genomes_in_launch"] = genomes
+        d["dram_bytes_per_genome"] = (rd + wr) / genomes
+        json.dump({"workload": "bert_base", "tag": tag, "genomes_in_launch": genomes,
+                   "dram_bytes_per_launch_per_genome": (rd + wr) / genomes,
+                   "source": f"profiles/{tag}_fitness_ncu.json"},
+                  open(os.path.join(out, "fitness_ncu_summary.json"), "w"), indent=1)
     json.dump(d, open(os.path.join(out, f"{tag}_fitness_ncu.json"), "w"), indent=1)
     print(json.dumps(d, indent=1))
