@@ -29,63 +29,7 @@
 #include <numeric>
 
 #include "cb_internal.cuh"
-
-// One record per dynamic unit of the frontier program (thread-per-genome
-// evaluation): the unit's costs, its genome bit, the frontier slot it
-// occupies while it still has unvisited neighbours, and the slots of its
-// earlier neighbours / of the units whose last neighbour it is.
-struct __align__(16) UnitRec {
-  fx192 rep;    // exact sum of its replacement kernels (region member value)
-  fx192 off;    // its own kernel cost + eps (removed when offloaded)
-  fx192 term1;  // round(rep) * r(cnt) + eps: its term as a region of one
-  int32_t bit;  // genome bit, -1 for always-on fixed units
-  int32_t cnt;  // kernels it contributes to a region
-  int32_t back_off, end_off;
-  uint8_t slot, nback, nend, pad;
-  uint8_t pad2[4];
-};
-
-struct cb_es_plan {
-  int32_t k = 0;       // genome bits
-  int32_t words = 0;   // uint64 words per genome
-  int32_t M = 0;       // dynamic units
-  int32_t n_virtual = 0;
-  int32_t E = 0;
-  int32_t infeasible_bits = 0;
-  fx192 base_const;    // static regions + every eligible kernel's cost + eps
-  fx192 eps;
-  double seed_cost = 0.0;
-  bool smem_path = true;
-  // host copies
-  std::vector<int32_t> slot_kernel, rep_match_ptr, rep_match;
-  std::vector<int8_t> rep_kind;
-  std::vector<int32_t> unit_slot;  // slot of unit u, -1 for virtual units
-  std::vector<fx192> unit_rep, unit_off;
-  std::vector<int32_t> unit_cnt;
-  std::vector<int2> edges;
-  std::vector<uint64_t> infeas_mask;
-  std::vector<double> rt;  // r(n) of the target backend, n = 0..max
-  // device copies
-  DBuf<int32_t> d_unit_slot, d_unit_cnt;
-  DBuf<fx192> d_unit_rep, d_unit_off;
-  DBuf<int2> d_edges;
-  DBuf<uint64_t> d_infeas;
-  DBuf<double> d_rt;
-  DBuf<unsigned long long> d_flags;
-  DBuf<uint8_t> d_scratch;
-  size_t scratch_per_group = 0;
-  int32_t scratch_groups = 0;
-  // staging for the host-buffer entry point
-  DBuf<uint64_t> d_pop_stage;
-  DBuf<double> d_fit_stage;
-  // frontier program (0 slots = not built / too wide)
-  int32_t F = 0;
-  std::vector<UnitRec> prog;
-  std::vector<uint8_t> prog_slots;
-  DBuf<UnitRec> d_prog;
-  DBuf<uint8_t> d_prog_slots;
-  int32_t force_path = -1;  // testing: 0 union-find, 1 frontier
-};
+#include "fitness_plan.cuh"
 
 #define FRONTIER_MAX 32
 
@@ -540,7 +484,8 @@ extern "C" int cb_es_plan_query(const cb_es_plan* p, cb_es_plan_info* info) {
 }
 
 extern "C" int cb_es_plan_set_path(cb_es_plan* p, int32_t path) {
-  CB_ARG_CHECK(p && path >= -1 && path <= 2, "cb_es_plan_set_path: bad arguments");
+  CB_ARG_CHECK(p && path >= -1 && path <= 3, "cb_es_plan_set_path: bad arguments");
+  CB_ARG_CHECK(path != 3 || p->jit_fn, "cb_es_plan_set_path: plan is not specialised");
   CB_ARG_CHECK(path < 1 || p->F > 0, "cb_es_plan_set_path: no frontier program for this plan");
   p->force_path = path;
   return CB_OK;
@@ -1246,6 +1191,8 @@ static int launch_frontier2_t(cb_es_plan* p, const uint64_t* d_pop, int64_t n, d
 static int launch_fitness(cb_es_plan* p, const uint64_t* d_pop, int64_t n, double* d_fit,
                           cudaStream_t stream) {
   if (n <= 0) return CB_OK;
+  if (p->jit_fn && (p->force_path == -1 || p->force_path == 3))
+    return cb_jit_launch(p, d_pop, n, d_fit, stream, sm_count());
   const bool frontier = p->F > 0 && p->force_path != 0;
   if (frontier) {
     if (p->force_path != 2) {

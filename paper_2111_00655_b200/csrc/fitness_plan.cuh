@@ -1,0 +1,69 @@
+// Fitness plan shared by fitness.cu (plan builder, generic kernels) and
+// jit.cu (plan-specialised kernel).
+#pragma once
+#include "cb_internal.cuh"
+
+// One record per dynamic unit of the frontier program (thread-per-genome
+// evaluation): the unit's costs, its genome bit, the frontier slot it
+// occupies while it still has unvisited neighbours, and the slots of its
+// earlier neighbours / of the units whose last neighbour it is.
+struct __align__(16) UnitRec {
+  fx192 rep;    // exact sum of its replacement kernels (region member value)
+  fx192 off;    // its own kernel cost + eps (removed when offloaded)
+  fx192 term1;  // round(rep) * r(cnt) + eps: its term as a region of one
+  int32_t bit;  // genome bit, -1 for always-on fixed units
+  int32_t cnt;  // kernels it contributes to a region
+  int32_t back_off, end_off;
+  uint8_t slot, nback, nend, pad;
+  uint8_t pad2[4];
+};
+
+struct cb_es_plan {
+  int32_t k = 0;       // genome bits
+  int32_t words = 0;   // uint64 words per genome
+  int32_t M = 0;       // dynamic units
+  int32_t n_virtual = 0;
+  int32_t E = 0;
+  int32_t infeasible_bits = 0;
+  fx192 base_const;    // static regions + every eligible kernel's cost + eps
+  fx192 eps;
+  double seed_cost = 0.0;
+  bool smem_path = true;
+  // host copies
+  std::vector<int32_t> slot_kernel, rep_match_ptr, rep_match;
+  std::vector<int8_t> rep_kind;
+  std::vector<int32_t> unit_slot;  // slot of unit u, -1 for virtual units
+  std::vector<fx192> unit_rep, unit_off;
+  std::vector<int32_t> unit_cnt;
+  std::vector<int2> edges;
+  std::vector<uint64_t> infeas_mask;
+  std::vector<double> rt;  // r(n) of the target backend, n = 0..max
+  // device copies
+  DBuf<int32_t> d_unit_slot, d_unit_cnt;
+  DBuf<fx192> d_unit_rep, d_unit_off;
+  DBuf<int2> d_edges;
+  DBuf<uint64_t> d_infeas;
+  DBuf<double> d_rt;
+  DBuf<unsigned long long> d_flags;
+  DBuf<uint8_t> d_scratch;
+  size_t scratch_per_group = 0;
+  int32_t scratch_groups = 0;
+  // staging for the host-buffer entry point
+  DBuf<uint64_t> d_pop_stage;
+  DBuf<double> d_fit_stage;
+  // frontier program (0 slots = not built / too wide)
+  int32_t F = 0;
+  std::vector<UnitRec> prog;
+  std::vector<uint8_t> prog_slots;
+  DBuf<UnitRec> d_prog;
+  DBuf<uint8_t> d_prog_slots;
+  int32_t force_path = -1;  // -1 auto, 0 union-find, 1 frontier, 2 frontier (smem labels), 3 jit
+  // plan-specialised kernel (jit.cu), null until cb_es_plan_specialize
+  void* jit_fn = nullptr;
+  DBuf<uint64_t> d_term1;
+};
+
+int cb_jit_specialize(cb_es_plan* P, double* compile_ms, std::string* source_out);
+int cb_jit_launch(cb_es_plan* P, const uint64_t* d_pop, int64_t n, double* d_fit, cudaStream_t stream,
+                  int sm_count);
+

@@ -9,7 +9,14 @@
 // its least significant bit is >= 2^-128 and it is < 2^64; anything else sets
 // the caller's `inexact` flag instead of silently losing bits.
 #pragma once
+#ifdef __CUDACC_RTC__  // NVRTC (jit.cu): no host headers
+typedef unsigned long long uint64_t;
+typedef unsigned int uint32_t;
+typedef int int32_t;
+typedef long long int64_t;
+#else
 #include <stdint.h>
+#endif
 
 #ifdef __CUDACC__
 #define FXI __host__ __device__ __forceinline__

@@ -158,4 +158,9 @@ def test_fitness_paths_agree_with_oracle(gpu, case):
         for path in ("frontier", "frontier_smem"):
             plan.set_path(path)
             assert np.array_equal(plan.evaluate(genomes), want), path
+    if 0 < plan.info.frontier_slots <= 16:
+        ms = plan.specialize()
+        assert ms is not None, getattr(plan, "specialize_error", "")
+        plan.set_path("jit")
+        assert np.array_equal(plan.evaluate(genomes), want), "jit"
     plan.set_path("auto")
