@@ -207,16 +207,8 @@ int cb_es_plan_query(const cb_es_plan* p, cb_es_plan_info* info);
 /* Evaluation path: -1 automatic (frontier program when available), 0 the
  * union-find kernels, 1 the frontier program (packed-label form when it has
  * <= 16 slots), 2 the frontier program in its shared-memory-label form.
- * 3 the plan-specialised kernel (after cb_es_plan_specialize).  For tests
- * and profiling; all paths return identical results. */
+ * For tests and profiling; all paths return identical results. */
 int cb_es_plan_set_path(cb_es_plan* p, int32_t path);
-/* Generate and compile (NVRTC, sm_100a) a fitness kernel specialised to this
- * plan's frontier program (<= 16 slots); afterwards the automatic path uses
- * it.  *compile_ms receives the generation + compile + load time.  Returns
- * CB_ERR_CUDA (plan unchanged) when run-time compilation is unavailable. */
-int cb_es_plan_specialize(cb_es_plan* p, double* compile_ms);
-/* The generated source (no GPU needed); *len receives its length. */
-int cb_es_plan_jit_source(cb_es_plan* p, char* buf, int64_t cap, int64_t* len);
 /* slot_kernel (host, genome_bits): canonical kernel index of each bit;
  * rep_kind (host, genome_bits): 0 infeasible, 1 same-set pattern,
  * 2 decomposed into singletons; rep_match_ptr/rep_match: replacement

@@ -484,8 +484,7 @@ extern "C" int cb_es_plan_query(const cb_es_plan* p, cb_es_plan_info* info) {
 }
 
 extern "C" int cb_es_plan_set_path(cb_es_plan* p, int32_t path) {
-  CB_ARG_CHECK(p && path >= -1 && path <= 3, "cb_es_plan_set_path: bad arguments");
-  CB_ARG_CHECK(path != 3 || p->jit_fn, "cb_es_plan_set_path: plan is not specialised");
+  CB_ARG_CHECK(p && path >= -1 && path <= 2, "cb_es_plan_set_path: bad arguments");
   CB_ARG_CHECK(path < 1 || p->F > 0, "cb_es_plan_set_path: no frontier program for this plan");
   p->force_path = path;
   return CB_OK;
@@ -1191,8 +1190,6 @@ static int launch_frontier2_t(cb_es_plan* p, const uint64_t* d_pop, int64_t n, d
 static int launch_fitness(cb_es_plan* p, const uint64_t* d_pop, int64_t n, double* d_fit,
                           cudaStream_t stream) {
   if (n <= 0) return CB_OK;
-  if (p->jit_fn && (p->force_path == -1 || p->force_path == 3))
-    return cb_jit_launch(p, d_pop, n, d_fit, stream, sm_count());
   const bool frontier = p->F > 0 && p->force_path != 0;
   if (frontier) {
     if (p->force_path != 2) {

@@ -1,5 +1,4 @@
-// Fitness plan shared by fitness.cu (plan builder, generic kernels) and
-// jit.cu (plan-specialised kernel).
+// Fitness plan: the host-built, genome-independent part of graph-level pricing.
 #pragma once
 #include "cb_internal.cuh"
 
@@ -57,13 +56,6 @@ struct cb_es_plan {
   std::vector<uint8_t> prog_slots;
   DBuf<UnitRec> d_prog;
   DBuf<uint8_t> d_prog_slots;
-  int32_t force_path = -1;  // -1 auto, 0 union-find, 1 frontier, 2 frontier (smem labels), 3 jit
-  // plan-specialised kernel (jit.cu), null until cb_es_plan_specialize
-  void* jit_fn = nullptr;
-  DBuf<uint64_t> d_term1;
+  int32_t force_path = -1;  // -1 auto, 0 union-find, 1 frontier, 2 frontier (smem labels)
 };
-
-int cb_jit_specialize(cb_es_plan* P, double* compile_ms, std::string* source_out);
-int cb_jit_launch(cb_es_plan* P, const uint64_t* d_pop, int64_t n, double* d_fit, cudaStream_t stream,
-                  int sm_count);
 

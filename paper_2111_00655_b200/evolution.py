@@ -208,29 +208,8 @@ class FitnessPlan:
         """'auto' | 'frontier' (thread per genome) | 'unionfind' (warp/CTA
         per genome); both give identical results, `auto` picks the frontier
         program whenever the plan has one."""
-        code = {"auto": -1, "unionfind": 0, "frontier": 1, "frontier_smem": 2, "jit": 3}[path]
+        code = {"auto": -1, "unionfind": 0, "frontier": 1, "frontier_smem": 2}[path]
         nat.check(nat.lib().cb_es_plan_set_path(self.handle.raw, code))
-
-    def specialize(self) -> float | None:
-        """Compile a fitness kernel specialised to this plan (NVRTC, sm_100a);
-        returns the compile time in ms, or None when the plan's frontier
-        program is too wide or run-time compilation is unavailable."""
-        if not 0 < self.info.frontier_slots <= 16:
-            return None
-        ms = ctypes.c_double()
-        rc = nat.lib().cb_es_plan_specialize(self.handle.raw, ctypes.byref(ms))
-        if rc != nat.CB_OK:
-            self.specialize_error = nat.last_error()
-            return None
-        return ms.value
-
-    def jit_source(self) -> str:
-        n = ctypes.c_int64()
-        nat.check(nat.lib().cb_es_plan_jit_source(self.handle.raw, None, 0, ctypes.byref(n)))
-        buf = ctypes.create_string_buffer(n.value + 1)
-        nat.check(nat.lib().cb_es_plan_jit_source(self.handle.raw, buf, n.value + 1,
-                                                  ctypes.byref(n)))
-        return buf.value.decode()
 
     def evaluate(self, genomes: Sequence[Sequence[int]]) -> np.ndarray:
         """Fitness of each genome (host buffers in, host results out)."""

@@ -176,12 +176,14 @@ def record_es(g, reg, measurer, eps, dp_placement, rng: random.Random, target: s
     k = len(eligible_slots(reg, dp_placement))
     genomes = [[0] * k, [1] * k] + [[rng.randrange(2) for _ in range(k)]
                                      for _ in range(n_genomes)]
-    fits = []
+    fits, decoded = [], []
     for bits in genomes:
         p = ref.decode_genome(g, reg, dp_placement, bits, target)
         fits.append(math.inf if p is None else ref.placement_cost_graphlevel(
             measurer, g, p, eps, reg.graph_backend_ids()))
-    out = {"graph_backend": target, "genome_length": k, "genomes": genomes, "fitness": fits}
+        decoded.append(None if p is None else kernels_json(p))
+    out = {"graph_backend": target, "genome_length": k, "genomes": genomes, "fitness": fits,
+           "decoded": decoded}
     if evolve_cfg is not None:
         cfg = ref.ESConfig(**evolve_cfg)
         es = ref.evolve(g, reg, measurer, dp_placement, eps, cfg, graph_backend=target)
