@@ -101,6 +101,7 @@ static void build_frontier_program(cb_es_plan* P, int32_t n_elig_units) {
     r.off = P->unit_off[u];
     fx_term(fx_to_double(r.rep), P->rt[P->unit_cnt[u]], P->eps, r.term1);
     r.bit = P->unit_slot[u];
+    r.bit2 = r.bit;
     r.cnt = P->unit_cnt[u];
     r.slot = (uint8_t)slot[p];
     r.back_off = (int32_t)P->prog_slots.size();
@@ -981,10 +982,10 @@ fitness_frontier2_kernel(int32_t M, int32_t words, fx192 base_const, fx192 eps,
     int32_t cached_word = -1;
     uint64_t word = 0;
     for (int32_t p = 0; p < M; ++p) {
-      const uint4* rp = reinterpret_cast<const uint4*>(prog + p);
-      const uint4 meta = __ldg(rp + 5);  // back_off, end_off, slot|nback|nend, -
-      const uint4 q4 = __ldg(rp + 4);    // term1.w2 (x,y), bit (z), cnt (w)
-      const int32_t bit = (int32_t)q4.z;
+      const UnitRec* r = prog + p;
+      const uint4 meta = __ldg(reinterpret_cast<const uint4*>(&r->back_off));
+      // meta: back_off, end_off, slot|nback|nend|-, bit
+      const int32_t bit = (int32_t)meta.w;
       bool on = !dead;
       if (bit >= 0) {
         const int32_t wi = bit >> 6;
@@ -999,20 +1000,14 @@ fitness_frontier2_kernel(int32_t M, int32_t words, fx192 base_const, fx192 eps,
       const int nend = (meta.z >> 16) & 0xff;
       const LT nibS = (LT)0xF << (4 * S);
       if (on) {
-        const uint4 r0 = __ldg(rp + 0);
-        const uint4 r1 = __ldg(rp + 1);
         if (bit >= 0) {
-          const uint4 r2 = __ldg(rp + 2);
-          fx192 off;
-          off.w[0] = ((uint64_t)r1.w << 32) | r1.z;
-          off.w[1] = ((uint64_t)r2.y << 32) | r2.x;
-          off.w[2] = ((uint64_t)r2.w << 32) | r2.z;
+          const fx192 off = {{__ldg(&r->off.w[0]), __ldg(&r->off.w[1]), __ldg(&r->off.w[2])}};
           fx_sub(total, off);
         }
-        s0[S][t] = ((uint64_t)r0.y << 32) | r0.x;
-        s1[S][t] = ((uint64_t)r0.w << 32) | r0.z;
-        s2[S][t] = ((uint64_t)r1.y << 32) | r1.x;
-        cs[S][t] = ((uint64_t)(uint32_t)p << 32) | q4.w;
+        s0[S][t] = __ldg(&r->rep.w[0]);
+        s1[S][t] = __ldg(&r->rep.w[1]);
+        s2[S][t] = __ldg(&r->rep.w[2]);
+        cs[S][t] = ((uint64_t)(uint32_t)p << 32) | (uint32_t)__ldg(&r->cnt);
         act |= nibS;
         lab = (lab & ~nibS) | ((LT)S << (4 * S));
       }
@@ -1045,10 +1040,9 @@ fitness_frontier2_kernel(int32_t M, int32_t words, fx192 base_const, fx192 eps,
             const uint64_t cw = cs[e][t];
             const int32_t one = (int32_t)(cw >> 32);
             if (one >= 0) {
-              const uint4* tp = reinterpret_cast<const uint4*>(prog + one);
-              const uint4 a = __ldg(tp + 3), b2 = __ldg(tp + 4);
-              const fx192 v = {{((uint64_t)a.y << 32) | a.x, ((uint64_t)a.w << 32) | a.z,
-                                ((uint64_t)b2.y << 32) | b2.x}};
+              const UnitRec* tp = prog + one;
+              const fx192 v = {{__ldg(&tp->term1.w[0]), __ldg(&tp->term1.w[1]),
+                                __ldg(&tp->term1.w[2])}};
               fx_add(total, v);
             } else {
               emit_slot = e;  // multi-unit region: queued for warp-wide pricing

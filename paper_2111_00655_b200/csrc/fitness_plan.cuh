@@ -14,7 +14,7 @@ struct __align__(16) UnitRec {
   int32_t cnt;  // kernels it contributes to a region
   int32_t back_off, end_off;
   uint8_t slot, nback, nend, pad;
-  uint8_t pad2[4];
+  int32_t bit2;  // copy of `bit` so one 16-byte load carries the step header
 };
 
 struct cb_es_plan {

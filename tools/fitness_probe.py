@@ -11,8 +11,6 @@ bs = workloads.paper_backends(g) if name != 'random100k' else workloads.random_b
 res = tp.optimize(g, bs.registry, bs.measurer, 0.01)
 plan = tp.FitnessPlan(g, bs.registry, bs.measurer, res.placement, 0.01, bs.graph_backend, res.kernel_matches)
 i = plan.info
-import time as _t
-_t0 = _t.time(); jit_ms = plan.specialize(); print('specialize ms', jit_ms, getattr(plan, 'specialize_error', ''), 'wall', _t.time() - _t0)
 print(name, 'k', plan.k, 'units', i.units, 'edges', i.edges, 'frontier', i.frontier_slots, 'dp', res.device)
 for label, fill in (('random', None), ('sparse', 0.1), ('dense', 0.9)):
     if fill is None:
@@ -27,10 +25,8 @@ for label, fill in (('random', None), ('sparse', 0.1), ('dense', 0.9)):
     pop &= torch.from_numpy(feas.view(np.int64)).cuda()
     fit = torch.empty(P, dtype=torch.float64, device='cuda')
     out = {}
-    for path in ('jit', 'frontier', 'unionfind'):
+    for path in ('frontier', 'unionfind'):
         if path.startswith('frontier') and not i.frontier_slots:
-            continue
-        if path == 'jit' and jit_ms is None:
             continue
         plan.set_path(path)
         for _ in range(2):
