@@ -29,6 +29,7 @@
 
 #define DP_NARROW_WARPS 16
 #define DP_WIDE_WARPS 8
+#define DP_STAGE_MAX (200 * 1024)
 
 struct DPArgs {
   // graph
@@ -115,7 +116,7 @@ __device__ bool solution_less(const DPArgs& a, int32_t r, int32_t k1, int32_t k2
       ++steps;
       const bool in1 = is_member(a, e.y, u);
       const bool in2 = is_member(a, e.z, u);
-      const int32_t cu = __ldcg(a.choice + u);
+      const int32_t cu = a.choice[u];
       const int32_t o1 = in1 ? e.y : cu;
       const int32_t o2 = in2 ? e.z : cu;
       if (o1 == o2) continue;
@@ -142,11 +143,11 @@ __device__ __forceinline__ bool candidate_value(const DPArgs& a, int32_t c, fx19
     for (int32_t j = a.pch_ptr[u]; j < a.pch_ptr[u + 1]; ++j) {
       const int32_t x = a.pch[j];
       if (is_member(a, c, x)) continue;
-      if (!__ldcg(a.feas + x)) return false;
-      fx192 o;
-      o.w[0] = __ldcg(&a.opt[x].w[0]);
-      o.w[1] = __ldcg(&a.opt[x].w[1]);
-      o.w[2] = __ldcg(&a.opt[x].w[2]);
+      // plain loads: values come from earlier launches or, inside one CTA,
+      // from earlier levels separated by __syncthreads (opt/feas may live in
+      // shared memory in the narrow-segment kernel)
+      if (!a.feas[x]) return false;
+      const fx192 o = a.opt[x];
       fx_add(val, o);
     }
   }
@@ -244,13 +245,40 @@ __device__ void dp_node(const DPArgs& a, int32_t r) {
   }
 }
 
+// One CTA walks a run of narrow levels.  When the graph is small enough the
+// per-node DP values (OPT, feasibility) are staged in shared memory for the
+// whole run, so each level's dependent reads of its post-dominator
+// children's values hit shared memory instead of L2; they are written back
+// to global memory for the nodes of this run at the end.
 __global__ void __launch_bounds__(DP_NARROW_WARPS * 32)
-dp_narrow_kernel(DPArgs a, const int32_t* __restrict__ level_ptr, int32_t lvl_begin, int32_t lvl_end) {
+dp_narrow_kernel(DPArgs a, const int32_t* __restrict__ level_ptr, int32_t lvl_begin, int32_t lvl_end,
+                 int32_t n_stage) {
+  extern __shared__ __align__(16) unsigned char dp_smem[];
   const int warp = threadIdx.x >> 5;
+  DPArgs b = a;
+  if (n_stage > 0) {
+    fx192* s_opt = reinterpret_cast<fx192*>(dp_smem);
+    uint8_t* s_feas = reinterpret_cast<uint8_t*>(s_opt + n_stage);
+    for (int32_t v = threadIdx.x; v < n_stage; v += blockDim.x) {
+      s_opt[v] = a.opt[v];
+      s_feas[v] = a.feas[v];
+    }
+    __syncthreads();
+    b.opt = s_opt;
+    b.feas = s_feas;
+  }
   for (int32_t l = lvl_begin; l < lvl_end; ++l) {
     const int32_t i0 = level_ptr[l], i1 = level_ptr[l + 1];
-    for (int32_t i = i0 + warp; i < i1; i += DP_NARROW_WARPS) dp_node(a, a.level_nodes[i]);
+    for (int32_t i = i0 + warp; i < i1; i += DP_NARROW_WARPS) dp_node(b, a.level_nodes[i]);
     __syncthreads();
+  }
+  if (n_stage > 0) {
+    const int32_t i0 = level_ptr[lvl_begin], i1 = level_ptr[lvl_end];
+    for (int32_t i = i0 + threadIdx.x; i < i1; i += blockDim.x) {
+      const int32_t v = a.level_nodes[i];
+      a.opt[v] = b.opt[v];
+      a.feas[v] = b.feas[v];
+    }
   }
 }
 
@@ -378,9 +406,18 @@ extern "C" int cb_dp_solve(cb_graph* g, cb_matches* m, double epsilon, int32_t* 
   cudaEventCreate(&ev1);
   cudaEventRecord(ev0);
   std::vector<LevelSegment> segs = cb_plan_levels(g, 2 * DP_NARROW_WARPS);
+  static bool smem_configured = false;
+  if (!smem_configured) {
+    CB_CUDA_TRY(cudaFuncSetAttribute(dp_narrow_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)DP_STAGE_MAX));
+    smem_configured = true;
+  }
   for (const LevelSegment& s : segs) {
     if (s.narrow) {
-      dp_narrow_kernel<<<1, DP_NARROW_WARPS * 32>>>(a, d_level_ptr.p, s.lvl_begin, s.lvl_end);
+      const size_t stage_bytes = (size_t)n * (sizeof(fx192) + 1);
+      const int32_t n_stage = stage_bytes <= DP_STAGE_MAX ? n : 0;
+      dp_narrow_kernel<<<1, DP_NARROW_WARPS * 32, n_stage ? stage_bytes : 0>>>(
+          a, d_level_ptr.p, s.lvl_begin, s.lvl_end, n_stage);
     } else {
       int32_t i0 = g->level_ptr[s.lvl_begin], i1 = g->level_ptr[s.lvl_end];
       int32_t blocks = (i1 - i0 + DP_WIDE_WARPS - 1) / DP_WIDE_WARPS;

@@ -65,17 +65,24 @@ class DPResult:
 
 def _new_frontiers(g: ComputationGraph) -> int:
     """Largest number of nodes first enqueued by a single pop (pop order is
-    (depth, id)); mirrors the reference counter."""
-    rank = {v: i for i, v in enumerate(sorted(g.nodes, key=lambda v: (g.depth(v), v)))}
-    first: dict[int, int] = {}
-    for c in g.nodes:
-        preds = g.node_predecessors(c)
-        if preds:
-            first[c] = min(preds, key=rank.__getitem__)
-    counts: dict[int, int] = {}
-    for p in first.values():
-        counts[p] = counts.get(p, 0) + 1
-    return max(counts.values(), default=0)
+    (depth, id)); mirrors the reference counter (vectorised over the CSR)."""
+    n = len(g.nodes)
+    if n == 0:
+        return 0
+    order = np.lexsort((np.arange(n), g._depth_arr))  # pop order over node indices
+    rank = np.empty(n, dtype=np.int64)
+    rank[order] = np.arange(n)
+    src = g._in_src.astype(np.int64)
+    dst = np.repeat(np.arange(n), np.diff(g._in_ptr))
+    keep = src >= 0
+    src, dst = src[keep], dst[keep]
+    if src.size == 0:
+        return 0
+    # for every consumer, the predecessor that pops first enqueues it
+    best = np.full(n, np.iinfo(np.int64).max)
+    np.minimum.at(best, dst, rank[src])
+    firsts = best[best != np.iinfo(np.int64).max]
+    return int(np.bincount(firsts).max())
 
 
 def optimize(g: ComputationGraph, registry: PatternRegistry, measurer: Measurer,
