@@ -190,11 +190,12 @@ def run_mine(args) -> None:
     host = torch.empty((P, plan.words), dtype=torch.int64, pin_memory=True)
     host.copy_(es.pop[es.cur])
     host_np = host.numpy().view(np.uint64)
-    plan.evaluate_packed(host_np)  # warm
+    host_fit = torch.empty(P, dtype=torch.float64, pin_memory=True).numpy()
+    plan.evaluate_packed(host_np, host_fit)  # warm
     barrier()
     t0 = time.perf_counter()
     for _ in range(args.e2e_steps):
-        fit = plan.evaluate_packed(host_np)
+        fit = plan.evaluate_packed(host_np, host_fit)
     e2e_s = time.perf_counter() - t0
     barrier()
 

@@ -1237,10 +1237,52 @@ extern "C" int cb_fitness_host(cb_es_plan* p, const uint64_t* h_pop, int64_t n, 
   const size_t words = (size_t)n * p->words;
   if (p->d_pop_stage.n < words) CB_CUDA_TRY(p->d_pop_stage.alloc(words));
   if (p->d_fit_stage.n < (size_t)n) CB_CUDA_TRY(p->d_fit_stage.alloc((size_t)n));
-  CB_CUDA_TRY(cudaMemcpy(p->d_pop_stage.p, h_pop, words * sizeof(uint64_t), cudaMemcpyHostToDevice));
-  int rc = launch_fitness(p, p->d_pop_stage.p, n, p->d_fit_stage.p, 0);
+  // Chunked pipeline over three streams: the H2D copy of chunk i+1 and the
+  // D2H copy of chunk i-1 overlap the fitness kernel of chunk i (copies are
+  // asynchronous when the host buffers are pinned).
+  const int64_t chunk = std::max<int64_t>(1 << 18, (n + 15) / 16);
+  cudaStream_t s_in, s_run, s_out;
+  CB_CUDA_TRY(cudaStreamCreateWithFlags(&s_in, cudaStreamNonBlocking));
+  CB_CUDA_TRY(cudaStreamCreateWithFlags(&s_run, cudaStreamNonBlocking));
+  CB_CUDA_TRY(cudaStreamCreateWithFlags(&s_out, cudaStreamNonBlocking));
+  std::vector<cudaEvent_t> copied, priced;
+  int rc = CB_OK;
+  for (int64_t lo = 0; lo < n && rc == CB_OK; lo += chunk) {
+    const int64_t cnt = std::min<int64_t>(chunk, n - lo);
+    cudaEvent_t e_in, e_run;
+    cudaEventCreateWithFlags(&e_in, cudaEventDisableTiming);
+    cudaEventCreateWithFlags(&e_run, cudaEventDisableTiming);
+    copied.push_back(e_in);
+    priced.push_back(e_run);
+    uint64_t* dpop = p->d_pop_stage.p + (size_t)lo * p->words;
+    double* dfit = p->d_fit_stage.p + lo;
+    if (cudaMemcpyAsync(dpop, h_pop + (size_t)lo * p->words, (size_t)cnt * p->words * sizeof(uint64_t),
+                        cudaMemcpyHostToDevice, s_in) != cudaSuccess) {
+      rc = CB_ERR_CUDA;
+      break;
+    }
+    cudaEventRecord(e_in, s_in);
+    cudaStreamWaitEvent(s_run, e_in, 0);
+    rc = launch_fitness(p, dpop, cnt, dfit, s_run);
+    cudaEventRecord(e_run, s_run);
+    cudaStreamWaitEvent(s_out, e_run, 0);
+    if (cudaMemcpyAsync(h_fit + lo, dfit, (size_t)cnt * sizeof(double), cudaMemcpyDeviceToHost,
+                        s_out) != cudaSuccess)
+      rc = CB_ERR_CUDA;
+  }
+  cudaError_t se = cudaStreamSynchronize(s_out);
+  cudaStreamSynchronize(s_run);
+  cudaStreamSynchronize(s_in);
+  for (cudaEvent_t e : copied) cudaEventDestroy(e);
+  for (cudaEvent_t e : priced) cudaEventDestroy(e);
+  cudaStreamDestroy(s_in);
+  cudaStreamDestroy(s_run);
+  cudaStreamDestroy(s_out);
+  if (rc == CB_ERR_CUDA || se != cudaSuccess) {
+    cb_set_error(std::string("cb_fitness_host: ") + cudaGetErrorString(cudaGetLastError()));
+    return CB_ERR_CUDA;
+  }
   if (rc != CB_OK) return rc;
-  CB_CUDA_TRY(cudaMemcpy(h_fit, p->d_fit_stage.p, (size_t)n * sizeof(double), cudaMemcpyDeviceToHost));
   unsigned long long flags[2] = {0, 0};
   CB_CUDA_TRY(cudaMemcpy(flags, p->d_flags.p, sizeof(flags), cudaMemcpyDeviceToHost));
   if (flags[0]) {

@@ -216,9 +216,14 @@ class FitnessPlan:
         pop = pack_genomes(genomes, self.k, self.words)
         return self.evaluate_packed(pop)
 
-    def evaluate_packed(self, pop: np.ndarray) -> np.ndarray:
+    def evaluate_packed(self, pop: np.ndarray, out: np.ndarray | None = None) -> np.ndarray:
+        """Fitness of packed genome rows held in host memory: chunked H2D /
+        kernel / D2H pipeline (fully overlapped when `pop` and `out` are
+        pinned, e.g. views of `torch.empty(..., pin_memory=True)`)."""
         pop = np.ascontiguousarray(pop, dtype=np.uint64)
-        out = np.empty(pop.shape[0], dtype=np.float64)
+        if out is None:
+            out = np.empty(pop.shape[0], dtype=np.float64)
+        assert out.dtype == np.float64 and out.flags.c_contiguous and len(out) == pop.shape[0]
         if pop.shape[0]:
             nat.check(nat.lib().cb_fitness_host(self.handle.raw, nat.ptr(pop, nat.c_uint64),
                                                 pop.shape[0], nat.ptr(out, nat.c_double)))
