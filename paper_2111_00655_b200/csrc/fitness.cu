@@ -111,6 +111,14 @@ static void build_frontier_program(cb_es_plan* P, int32_t n_elig_units) {
     r.end_off = (int32_t)P->prog_slots.size();
     for (int32_t q : ends_at[p]) P->prog_slots.push_back((uint8_t)slot[q]);
     r.nend = (uint8_t)(P->prog_slots.size() - r.end_off);
+    r.hot.x = (uint32_t)r.bit;
+    r.hot.y = (uint32_t)r.slot | ((uint32_t)r.nback << 8) | ((uint32_t)r.nend << 16);
+    r.hot.z = r.hot.w = 0u;
+    if (r.nback > 8 || r.nend > 8) P->packed_ok = false;
+    for (int j = 0; j < r.nback && j < 8; ++j)
+      r.hot.z |= (uint32_t)(P->prog_slots[r.back_off + j] & 0xF) << (4 * j);
+    for (int j = 0; j < r.nend && j < 8; ++j)
+      r.hot.w |= (uint32_t)(P->prog_slots[r.end_off + j] & 0xF) << (4 * j);
     P->prog[p] = r;
   }
   if (P->prog_slots.empty()) P->prog_slots.push_back(0);
@@ -983,9 +991,8 @@ fitness_frontier2_kernel(int32_t M, int32_t words, fx192 base_const, fx192 eps,
     uint64_t word = 0;
     for (int32_t p = 0; p < M; ++p) {
       const UnitRec* r = prog + p;
-      const uint4 meta = __ldg(reinterpret_cast<const uint4*>(&r->back_off));
-      // meta: back_off, end_off, slot|nback|nend|-, bit
-      const int32_t bit = (int32_t)meta.w;
+      const uint4 hot = __ldg(&r->hot);  // bit, slot|nback|nend, back nibbles, end nibbles
+      const int32_t bit = (int32_t)hot.x;
       bool on = !dead;
       if (bit >= 0) {
         const int32_t wi = bit >> 6;
@@ -995,9 +1002,9 @@ fitness_frontier2_kernel(int32_t M, int32_t words, fx192 base_const, fx192 eps,
         }
         on = (word >> (bit & 63)) & 1ull;
       }
-      const int S = meta.z & 0xff;
-      const int nback = (meta.z >> 8) & 0xff;
-      const int nend = (meta.z >> 16) & 0xff;
+      const int S = hot.y & 0xff;
+      const int nback = (hot.y >> 8) & 0xff;
+      const int nend = (hot.y >> 16) & 0xff;
       const LT nibS = (LT)0xF << (4 * S);
       if (on) {
         if (bit >= 0) {
@@ -1012,7 +1019,7 @@ fitness_frontier2_kernel(int32_t M, int32_t words, fx192 base_const, fx192 eps,
         lab = (lab & ~nibS) | ((LT)S << (4 * S));
       }
       for (int j = 0; j < nback; ++j) {
-        const int b = __ldg(slots + meta.x + j);
+        const int b = (hot.z >> (4 * j)) & 0xF;
         const uint32_t B = (uint32_t)(lab >> (4 * b)) & 0xF;
         const bool merge = on && ((act >> (4 * b)) & 1) && B != (uint32_t)S;
         if (merge) {
@@ -1029,7 +1036,7 @@ fitness_frontier2_kernel(int32_t M, int32_t words, fx192 base_const, fx192 eps,
         }
       }
       for (int j = 0; j < nend; ++j) {
-        const int e = __ldg(slots + meta.y + j);
+        const int e = (hot.w >> (4 * j)) & 0xF;
         const LT nibE = (LT)0xF << (4 * e);
         int emit_slot = -1;
         if (act & nibE) {
@@ -1186,7 +1193,7 @@ static int launch_fitness(cb_es_plan* p, const uint64_t* d_pop, int64_t n, doubl
   if (n <= 0) return CB_OK;
   const bool frontier = p->F > 0 && p->force_path != 0;
   if (frontier) {
-    if (p->force_path != 2) {
+    if (p->force_path != 2 && p->packed_ok) {
       if (p->F <= 8) return launch_frontier2_t<uint32_t, 8>(p, d_pop, n, d_fit, stream);
       if (p->F <= 16) return launch_frontier2_t<uint64_t, 16>(p, d_pop, n, d_fit, stream);
     }

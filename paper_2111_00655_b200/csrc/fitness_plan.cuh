@@ -14,7 +14,11 @@ struct __align__(16) UnitRec {
   int32_t cnt;  // kernels it contributes to a region
   int32_t back_off, end_off;
   uint8_t slot, nback, nend, pad;
-  int32_t bit2;  // copy of `bit` so one 16-byte load carries the step header
+  int32_t bit2;  // copy of `bit`
+  // packed step header of the packed-label kernel (one 16-byte load):
+  // x = bit, y = slot | nback << 8 | nend << 16, z = back slots (4 bits
+  // each, <= 8), w = end slots (4 bits each, <= 8)
+  uint4 hot;
 };
 
 struct cb_es_plan {
@@ -56,6 +60,7 @@ struct cb_es_plan {
   std::vector<uint8_t> prog_slots;
   DBuf<UnitRec> d_prog;
   DBuf<uint8_t> d_prog_slots;
+  bool packed_ok = true;     // every unit's back / end lists fit the packed header
   int32_t force_path = -1;  // -1 auto, 0 union-find, 1 frontier, 2 frontier (smem labels)
 };
 

@@ -38,6 +38,15 @@ FXI bool fx_is_zero(const fx192& a) { return (a.w[0] | a.w[1] | a.w[2]) == 0; }
 
 // a += b (mod 2^192)
 FXI void fx_add(fx192& a, const fx192& b) {
+#ifdef __CUDA_ARCH__
+  // one carry chain (IADD3 with carry predicates) instead of compare-based carries
+  asm("add.cc.u64 %0, %0, %3;\n\t"
+      "addc.cc.u64 %1, %1, %4;\n\t"
+      "addc.u64 %2, %2, %5;"
+      : "+l"(a.w[0]), "+l"(a.w[1]), "+l"(a.w[2])
+      : "l"(b.w[0]), "l"(b.w[1]), "l"(b.w[2]));
+  return;
+#endif
   uint64_t s0 = a.w[0] + b.w[0];
   uint64_t c0 = s0 < a.w[0];
   uint64_t t1 = a.w[1] + b.w[1];
@@ -51,6 +60,14 @@ FXI void fx_add(fx192& a, const fx192& b) {
 
 // a -= b (mod 2^192); exact whenever the true result is non-negative
 FXI void fx_sub(fx192& a, const fx192& b) {
+#ifdef __CUDA_ARCH__
+  asm("sub.cc.u64 %0, %0, %3;\n\t"
+      "subc.cc.u64 %1, %1, %4;\n\t"
+      "subc.u64 %2, %2, %5;"
+      : "+l"(a.w[0]), "+l"(a.w[1]), "+l"(a.w[2])
+      : "l"(b.w[0]), "l"(b.w[1]), "l"(b.w[2]));
+  return;
+#endif
   uint64_t d0 = a.w[0] - b.w[0];
   uint64_t br0 = a.w[0] < b.w[0];
   uint64_t t1 = a.w[1] - b.w[1];
