@@ -226,7 +226,8 @@ def run_mine(args) -> None:
         except Exception:
             traffic = None
     f_slots = plan.info.frontier_slots
-    kernel_name = ((f"fitness_frontier2_kernel<{'uint32_t, 8' if f_slots <= 8 else 'uint64_t, 16'}>"
+    f2 = next(f for f in (4, 6, 8, 12, 16, 99) if f_slots <= f)
+    kernel_name = ((f"fitness_frontier2_kernel<{'uint32_t' if f2 <= 8 else 'uint64_t'}, {f2}>"
                     if f_slots <= 16 else f"fitness_frontier_kernel<{_slots(f_slots)}>")
                    if f_slots else
                    ("fitness_smem_kernel" if plan.info.smem_path else "fitness_global_kernel"))

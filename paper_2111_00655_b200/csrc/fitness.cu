@@ -1194,7 +1194,11 @@ static int launch_fitness(cb_es_plan* p, const uint64_t* d_pop, int64_t n, doubl
   const bool frontier = p->F > 0 && p->force_path != 0;
   if (frontier) {
     if (p->force_path != 2 && p->packed_ok) {
+      // smallest slot count that fits: less shared memory, more resident warps
+      if (p->F <= 4) return launch_frontier2_t<uint32_t, 4>(p, d_pop, n, d_fit, stream);
+      if (p->F <= 6) return launch_frontier2_t<uint32_t, 6>(p, d_pop, n, d_fit, stream);
       if (p->F <= 8) return launch_frontier2_t<uint32_t, 8>(p, d_pop, n, d_fit, stream);
+      if (p->F <= 12) return launch_frontier2_t<uint64_t, 12>(p, d_pop, n, d_fit, stream);
       if (p->F <= 16) return launch_frontier2_t<uint64_t, 16>(p, d_pop, n, d_fit, stream);
     }
     if (p->F <= 8) return launch_frontier_t<8>(p, d_pop, n, d_fit, stream);
