@@ -209,6 +209,18 @@ int cb_es_plan_query(const cb_es_plan* p, cb_es_plan_info* info);
  * <= 16 slots), 2 the frontier program in its shared-memory-label form.
  * For tests and profiling; all paths return identical results. */
 int cb_es_plan_set_path(cb_es_plan* p, int32_t path);
+/* Merged-component pool entries per genome of the anchor kernel (1..24,
+ * default min(frontier slots, 16)); genomes that need more are priced by
+ * the warp-per-genome kernel.  A tuning / testing knob: results are
+ * identical for every value. */
+int cb_es_plan_set_pool(cb_es_plan* p, int32_t entries);
+/* The dynamic unit graph (diagnostics and tests; any pointer may be NULL):
+ * unit_bit[units] genome bit of each unit (-1 = fixed unit), unit_cnt[units]
+ * kernels each unit contributes to a region, edges[2*edges] unit pairs
+ * (a < b), frontier_needed = slots the frontier program needs (may exceed
+ * the kernels' cap, in which case frontier_slots is 0). */
+int cb_es_plan_units(const cb_es_plan* p, int32_t* unit_bit, int32_t* unit_cnt,
+                     int32_t* edges, int32_t* frontier_needed);
 /* slot_kernel (host, genome_bits): canonical kernel index of each bit;
  * rep_kind (host, genome_bits): 0 infeasible, 1 same-set pattern,
  * 2 decomposed into singletons; rep_match_ptr/rep_match: replacement

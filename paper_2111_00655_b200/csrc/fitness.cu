@@ -31,7 +31,8 @@
 #include "cb_internal.cuh"
 #include "fitness_plan.cuh"
 
-#define FRONTIER_MAX 32
+#define FRONTIER_MAX 32   // slot cap of the thread-per-genome kernels
+#define WIDE_MAX 128      // slot cap of the program (warp-per-genome sparse kernel)
 
 static bool fx_term(double base, double r, const fx192& eps, fx192& out);
 
@@ -85,12 +86,26 @@ static void build_frontier_program(cb_es_plan* P, int32_t n_elig_units) {
       free_slots.push_back(slot[q]);
     }
     std::sort(free_slots.begin(), free_slots.end(), std::greater<int32_t>());
-    if (used > FRONTIER_MAX) {
-      P->F = 0;
-      return;
-    }
+  }
+  P->F_needed = used;
+  if (used > WIDE_MAX) {
+    P->F = 0;
+    return;
   }
   P->F = used;
+  P->pool_entries = std::min(used, 16);
+  // sparse walk: program position of every genome bit, fixed-unit positions
+  P->prog_last.assign(last.begin(), last.end());
+  P->pos_of_bit.assign((size_t)std::max(P->k, 1), -1);
+  P->fixed_pos.clear();
+  for (int32_t p = 0; p < M; ++p) {
+    const int32_t b = P->unit_slot[order[p]];
+    if (b >= 0)
+      P->pos_of_bit[b] = p;
+    else
+      P->fixed_pos.push_back(p);
+  }
+  P->fixed_pos.push_back(M);  // sentinel
   P->prog.resize(M);
   P->prog_slots.clear();
   for (int32_t p = 0; p < M; ++p) {
@@ -114,7 +129,7 @@ static void build_frontier_program(cb_es_plan* P, int32_t n_elig_units) {
     r.hot.x = (uint32_t)r.bit;
     r.hot.y = (uint32_t)r.slot | ((uint32_t)r.nback << 8) | ((uint32_t)r.nend << 16);
     r.hot.z = r.hot.w = 0u;
-    if (r.nback > 8 || r.nend > 8) P->packed_ok = false;
+    if (r.nback > 8 || r.nend > 8 || used > 16) P->packed_ok = false;
     for (int j = 0; j < r.nback && j < 8; ++j)
       r.hot.z |= (uint32_t)(P->prog_slots[r.back_off + j] & 0xF) << (4 * j);
     for (int j = 0; j < r.nend && j < 8; ++j)
@@ -469,6 +484,13 @@ extern "C" int cb_es_plan_create(cb_graph* g, cb_matches* m, int32_t n_kernels,
   if (P->F > 0) {
     if ((e = P->d_prog.upload(P->prog)) != cudaSuccess) return fail_cuda(e);
     if ((e = P->d_prog_slots.upload(P->prog_slots)) != cudaSuccess) return fail_cuda(e);
+    if ((e = P->d_prog_last.upload(P->prog_last)) != cudaSuccess) return fail_cuda(e);
+    if ((e = P->d_pos_of_bit.upload(P->pos_of_bit)) != cudaSuccess) return fail_cuda(e);
+    if ((e = P->d_fixed_pos.upload(P->fixed_pos)) != cudaSuccess) return fail_cuda(e);
+  }
+  if ((rc = build_anchor_plan(P)) != CB_OK) {
+    delete P;
+    return rc;
   }
   if ((e = P->d_flags.alloc(2)) != cudaSuccess) return fail_cuda(e);
   cudaMemset(P->d_flags.p, 0, 2 * sizeof(unsigned long long));
@@ -492,9 +514,33 @@ extern "C" int cb_es_plan_query(const cb_es_plan* p, cb_es_plan_info* info) {
   return CB_OK;
 }
 
+extern "C" int cb_es_plan_units(const cb_es_plan* p, int32_t* unit_bit, int32_t* unit_cnt,
+                                int32_t* edges, int32_t* frontier_needed) {
+  CB_ARG_CHECK(p, "cb_es_plan_units: null plan");
+  if (unit_bit) std::copy(p->unit_slot.begin(), p->unit_slot.end(), unit_bit);
+  if (unit_cnt) std::copy(p->unit_cnt.begin(), p->unit_cnt.end(), unit_cnt);
+  if (edges)
+    for (size_t i = 0; i < p->edges.size(); ++i) {
+      edges[2 * i] = p->edges[i].x;
+      edges[2 * i + 1] = p->edges[i].y;
+    }
+  if (frontier_needed) *frontier_needed = p->F_needed;
+  return CB_OK;
+}
+
+extern "C" int cb_es_plan_set_pool(cb_es_plan* p, int32_t entries) {
+  CB_ARG_CHECK(p && entries >= 1 && entries <= 24, "cb_es_plan_set_pool: entries must be in [1, 24]");
+  p->pool_entries = entries;
+  return CB_OK;
+}
+
 extern "C" int cb_es_plan_set_path(cb_es_plan* p, int32_t path) {
-  CB_ARG_CHECK(p && path >= -1 && path <= 2, "cb_es_plan_set_path: bad arguments");
+  CB_ARG_CHECK(p && path >= -1 && path <= 4, "cb_es_plan_set_path: bad arguments");
+  CB_ARG_CHECK(path != 4 || p->anchor_ok,
+               "cb_es_plan_set_path: no anchor program (> 64 slots or values outside a 128-bit window)");
   CB_ARG_CHECK(path < 1 || p->F > 0, "cb_es_plan_set_path: no frontier program for this plan");
+  CB_ARG_CHECK(path < 1 || path > 2 || p->F <= FRONTIER_MAX,
+               "cb_es_plan_set_path: the thread-per-genome kernels need <= 32 frontier slots");
   p->force_path = path;
   return CB_OK;
 }
@@ -1192,6 +1238,10 @@ static int launch_fitness(cb_es_plan* p, const uint64_t* d_pop, int64_t n, doubl
                           cudaStream_t stream) {
   if (n <= 0) return CB_OK;
   const bool frontier = p->F > 0 && p->force_path != 0;
+  if (frontier && p->force_path == 3) return launch_fitness_wide(p, d_pop, n, d_fit, stream);
+  if (frontier && (p->force_path == 4 || (p->force_path == -1 && !p->packed_ok)))
+    return p->anchor_ok ? launch_fitness_anchor(p, d_pop, n, d_fit, stream)
+                        : launch_fitness_wide(p, d_pop, n, d_fit, stream);
   if (frontier) {
     if (p->force_path != 2 && p->packed_ok) {
       // smallest slot count that fits: less shared memory, more resident warps

@@ -56,11 +56,42 @@ struct cb_es_plan {
   DBuf<double> d_fit_stage;
   // frontier program (0 slots = not built / too wide)
   int32_t F = 0;
+  int32_t F_needed = 0;  // width of the program before the FRONTIER_MAX cap
   std::vector<UnitRec> prog;
   std::vector<uint8_t> prog_slots;
   DBuf<UnitRec> d_prog;
   DBuf<uint8_t> d_prog_slots;
+  // sparse walk (fitness_wide.cu): last neighbour position of each program
+  // position, program position of each genome bit (-1 infeasible), program
+  // positions of the fixed units followed by the sentinel M
+  std::vector<int32_t> prog_last, pos_of_bit, fixed_pos;
+  DBuf<int32_t> d_prog_last, d_pos_of_bit, d_fixed_pos;
+  // anchor kernel (fitness_anchor.cu): 128-bit window (values carried as
+  // X = v >> anchor_shift), per-position step headers and 128-bit constants,
+  // merged-component pool entries per genome, and the list of genomes that
+  // overflowed it
+  bool anchor_ok = false;
+  int32_t anchor_shift = 0;
+  DBuf<uint8_t> d_ahot;     // AHot[M]
+  DBuf<uint64_t> d_acold;   // [M][6]: rep, off, term1 as 128-bit X
+  DBuf<int32_t> d_acnt;     // [M]
+  int32_t pool_entries = 16;
+  DBuf<int64_t> d_ovf_list;
+  DBuf<int32_t> d_ovf_count;
   bool packed_ok = true;     // every unit's back / end lists fit the packed header
-  int32_t force_path = -1;  // -1 auto, 0 union-find, 1 frontier, 2 frontier (smem labels)
+  int32_t force_path = -1;  // -1 auto, 0 union-find, 1 frontier, 2 frontier (smem labels),
+                            // 3 sparse warp-per-genome walk, 4 anchor walk (thread per genome)
 };
+
+// fitness_wide.cu: warp-per-genome sparse walk of the frontier program (F <= 128)
+int launch_fitness_wide(cb_es_plan* p, const uint64_t* d_pop, int64_t n, double* d_fit,
+                        cudaStream_t stream);
+// the same over the genome indices list[0 .. *list_count) (count on the device)
+int launch_fitness_wide_list(cb_es_plan* p, const uint64_t* d_pop, int64_t n_max, double* d_fit,
+                             const int64_t* list, const int32_t* list_count, cudaStream_t stream);
+// fitness_anchor.cu: 128-bit window analysis + step headers (plan time);
+// thread-per-genome anchor walk (F <= 64), overflow to the wide kernel
+int build_anchor_plan(cb_es_plan* p);
+int launch_fitness_anchor(cb_es_plan* p, const uint64_t* d_pop, int64_t n, double* d_fit,
+                          cudaStream_t stream);
 

@@ -210,3 +210,54 @@ FXI double fx_to_double(const fx192& a) {
   if (ex > 1023) return fx_double_of(0x7ff0000000000000ull);
   return fx_double_of(((uint64_t)(ex + 1023) << 52) | frac);
 }
+
+// ---------------------------------------------------------------- windows
+// Plans whose every value is a multiple of 2^(s-128) and small enough can be
+// carried as 128-bit integers X = v >> s (value X * 2^(s-128)); these move
+// between the two forms exactly.
+
+// a << s (0 <= s < 192), bits past 2^192 dropped; static indexing only
+FXI fx192 fx_shl(const fx192& a, int s) {
+  const int q = s >> 6, r = s & 63;
+  const uint64_t b0 = q == 0 ? a.w[0] : 0ull;
+  const uint64_t b1 = q == 0 ? a.w[1] : (q == 1 ? a.w[0] : 0ull);
+  const uint64_t b2 = q == 0 ? a.w[2] : (q == 1 ? a.w[1] : a.w[0]);
+  fx192 o;
+  o.w[0] = b0 << r;
+  o.w[1] = (b1 << r) | (r ? b0 >> (64 - r) : 0ull);
+  o.w[2] = (b2 << r) | (r ? b1 >> (64 - r) : 0ull);
+  return o;
+}
+
+// a >> s (0 <= s < 192), logical
+FXI fx192 fx_shr(const fx192& a, int s) {
+  const int q = s >> 6, r = s & 63;
+  const uint64_t b0 = q == 0 ? a.w[0] : (q == 1 ? a.w[1] : a.w[2]);
+  const uint64_t b1 = q == 0 ? a.w[1] : (q == 1 ? a.w[2] : 0ull);
+  const uint64_t b2 = q == 0 ? a.w[2] : 0ull;
+  fx192 o;
+  o.w[0] = (b0 >> r) | (r ? b1 << (64 - r) : 0ull);
+  o.w[1] = (b1 >> r) | (r ? b2 << (64 - r) : 0ull);
+  o.w[2] = b2 >> r;
+  return o;
+}
+
+// index of the lowest set bit (192 if zero) / highest set bit (-1 if zero)
+FXI int fx_lowest_bit(const fx192& a) {
+  for (int l = 0; l < 3; ++l)
+    if (a.w[l]) {
+      uint64_t x = a.w[l];
+      int b = 0;
+      while (!(x & 1ull)) {
+        x >>= 1;
+        ++b;
+      }
+      return l * 64 + b;
+    }
+  return 192;
+}
+FXI int fx_highest_bit(const fx192& a) {
+  for (int l = 2; l >= 0; --l)
+    if (a.w[l]) return l * 64 + 63 - fx_clz64(a.w[l]);
+  return -1;
+}

@@ -184,6 +184,21 @@ class FitnessPlan:
         self.rep_match = rep
         self.slot_kernel = slot_kernel[:self.k]
 
+    def unit_graph(self) -> dict:
+        """The plan's dynamic unit graph: genome bit per unit (-1 = fixed
+        target-backend component), kernels per unit, edges (a < b) and the
+        frontier width the thread-per-genome program needs."""
+        m, e = self.info.units, self.info.edges
+        bit = np.empty(max(m, 1), np.int32)
+        cnt = np.empty(max(m, 1), np.int32)
+        edges = np.empty((max(e, 1), 2), np.int32)
+        need = nat.c_int32(0)
+        nat.check(nat.lib().cb_es_plan_units(self.handle.raw, nat.ptr(bit, nat.c_int32),
+                                             nat.ptr(cnt, nat.c_int32),
+                                             nat.ptr(edges, nat.c_int32), ctypes.byref(need)))
+        return {"unit_bit": bit[:m], "unit_cnt": cnt[:m], "edges": edges[:e],
+                "frontier_needed": int(need.value)}
+
     def _locate(self, placement: PlacementStrategy) -> np.ndarray:
         """Match-table index of every assignment (same backend, same nodes)."""
         g, table = self.g, self.table
@@ -205,11 +220,20 @@ class FitnessPlan:
         return out
 
     def set_path(self, path: str) -> None:
-        """'auto' | 'frontier' (thread per genome) | 'unionfind' (warp/CTA
-        per genome); both give identical results, `auto` picks the frontier
-        program whenever the plan has one."""
-        code = {"auto": -1, "unionfind": 0, "frontier": 1, "frontier_smem": 2}[path]
+        """'auto' | 'frontier' / 'frontier_smem' (thread per genome, <= 32
+        frontier slots) | 'anchor' (thread per genome, <= 64 slots) | 'wide'
+        (warp per genome, sparse walk, <= 128 slots) | 'unionfind'
+        (warp/CTA per genome, any plan).  All give identical results;
+        `auto` picks the packed-label frontier kernel for <= 16 slots, the
+        anchor kernel up to 64, the wide kernel up to 128, else union-find."""
+        code = {"auto": -1, "unionfind": 0, "frontier": 1, "frontier_smem": 2, "wide": 3,
+                "anchor": 4}[path]
         nat.check(nat.lib().cb_es_plan_set_path(self.handle.raw, code))
+
+    def set_pool(self, entries: int) -> None:
+        """Merged-component pool entries per genome of the anchor kernel
+        (tuning / testing; results do not depend on it)."""
+        nat.check(nat.lib().cb_es_plan_set_pool(self.handle.raw, int(entries)))
 
     def evaluate(self, genomes: Sequence[Sequence[int]]) -> np.ndarray:
         """Fitness of each genome (host buffers in, host results out)."""

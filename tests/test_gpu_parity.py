@@ -155,6 +155,13 @@ def test_fitness_paths_agree_with_oracle(gpu, case):
     plan.set_path("unionfind")
     assert np.array_equal(plan.evaluate(genomes), want)
     if plan.info.frontier_slots:
+        for path in ("wide", "anchor"):
+            plan.set_path(path)
+            assert np.array_equal(plan.evaluate(genomes), want), path
+        plan.set_pool(1)
+        assert np.array_equal(plan.evaluate(genomes), want), "anchor, pool of 1"
+        plan.set_pool(16)
+    if 0 < plan.info.frontier_slots <= 32:
         for path in ("frontier", "frontier_smem"):
             plan.set_path(path)
             assert np.array_equal(plan.evaluate(genomes), want), path

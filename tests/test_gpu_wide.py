@@ -1,0 +1,85 @@
+"""Wide frontier programs (17..128 slots: random DAGs with long-range
+edges, like the 100k-op config) evaluated by the sparse warp-per-genome
+kernel, bit-exact against the CPU oracle (oracle/oracle.c, the reference's
+graph-level pricing restated) and against the union-find kernels."""
+
+import json
+
+import numpy as np
+import pytest
+
+import paper_2111_00655_b200 as tp
+from paper_2111_00655_b200 import workloads
+from paper_2111_00655_b200.cost import profile_to_json
+from paper_2111_00655_b200.graph import graph_to_json
+from oracle import OracleCase
+
+pytestmark = pytest.mark.gpu
+
+
+def _case(g, bs, eps):
+    return json.loads(json.dumps({
+        "graph": graph_to_json(g),
+        "backends": [[b.id, b.kind.value] for b in bs.registry.backends.values()],
+        "patterns": [[bp.backend, bp.text(), bp.source.value] for bp in bs.registry.patterns],
+        "profiles": {b: profile_to_json(p) for b, p in bs.measurer.profiles.items()},
+        "epsilon": eps}))
+
+
+def _genomes(plan, rng, rows_per_density=300):
+    feasible = np.array([k != 0 for k in plan.rep_kind], dtype=np.uint8)
+    rows = []
+    for d in (0.02, 0.1, 0.3, 0.5, 0.8, 1.0):
+        x = (rng.random((rows_per_density, plan.k)) < d).astype(np.uint8)
+        x[: rows_per_density // 2] &= feasible  # half guaranteed feasible
+        rows.append(x)
+    rows.append(np.zeros((1, plan.k), np.uint8))
+    rows.append(feasible[None, :])
+    return np.concatenate(rows)
+
+
+@pytest.mark.parametrize("seed,n,window", [(0, 2000, 64), (1, 3000, 64), (2, 1500, 128),
+                                           (3, 800, 24)])
+def test_wide_plan_matches_oracle(gpu, seed, n, window):
+    g = workloads.random_dag(n, seed=seed, ops=workloads.RANDOM_OPS, window=window)
+    bs = workloads.random_backends(g, n_backends=8, n_graph=1, seed=seed)
+    res = tp.optimize(g, bs.registry, bs.measurer, 0.01)
+    plan = tp.FitnessPlan(g, bs.registry, bs.measurer, res.placement, 0.01, bs.graph_backend,
+                          res.kernel_matches)
+    ug = plan.unit_graph()
+    assert plan.info.frontier_slots == ug["frontier_needed"]
+    genomes = _genomes(plan, np.random.default_rng(seed))
+    oc = OracleCase(_case(g, bs, 0.01))
+    oc.price()
+    kernels = [[a.backend_pattern.order, a.root, sorted(a.nodes)]
+               for a in res.placement.assignments]
+    want = oc.fitness(kernels, bs.graph_backend, genomes, threads=8)
+    got = plan.evaluate(genomes)  # auto: wide kernel for > 16 slots
+    assert np.array_equal(got, want)
+    for path in ("wide", "anchor"):
+        plan.set_path(path)
+        assert np.array_equal(plan.evaluate(genomes), want), path
+    # tiny pools: most genomes overflow to the warp-per-genome kernel
+    for entries in (1, 2, 5):
+        plan.set_pool(entries)
+        assert np.array_equal(plan.evaluate(genomes), want), entries
+    plan.set_pool(16)
+    plan.set_path("unionfind")
+    assert np.array_equal(plan.evaluate(genomes), want)
+    plan.set_path("auto")
+
+
+@pytest.mark.parametrize("name", ["resnet50", "bert_base", "nasnet_a", "nasrnn"])
+def test_wide_kernel_agrees_on_models(gpu, name):
+    g = workloads.CONFIGS[name]()
+    bs = workloads.paper_backends(g)
+    res = tp.optimize(g, bs.registry, bs.measurer, 0.01)
+    plan = tp.FitnessPlan(g, bs.registry, bs.measurer, res.placement, 0.01, bs.graph_backend,
+                          res.kernel_matches)
+    genomes = _genomes(plan, np.random.default_rng(5), 2000)
+    plan.set_path("auto")
+    want = plan.evaluate(genomes)
+    for path in ("wide", "anchor"):
+        plan.set_path(path)
+        assert np.array_equal(plan.evaluate(genomes), want), path
+    plan.set_path("auto")

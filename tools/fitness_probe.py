@@ -6,6 +6,7 @@ import paper_2111_00655_b200 as tp
 from paper_2111_00655_b200 import workloads
 name = sys.argv[1] if len(sys.argv) > 1 else 'bert_base'
 P = int(sys.argv[2]) if len(sys.argv) > 2 else 1 << 22
+PATHS = sys.argv[3].split(',') if len(sys.argv) > 3 else ['auto', 'wide', 'unionfind']
 g = workloads.CONFIGS[name]()
 bs = workloads.paper_backends(g) if name != 'random100k' else workloads.random_backends(g, 8, 1, 0)
 res = tp.optimize(g, bs.registry, bs.measurer, 0.01)
@@ -25,8 +26,8 @@ for label, fill in (('random', None), ('sparse', 0.1), ('dense', 0.9)):
     pop &= torch.from_numpy(feas.view(np.int64)).cuda()
     fit = torch.empty(P, dtype=torch.float64, device='cuda')
     out = {}
-    for path in ('frontier', 'unionfind'):
-        if path.startswith('frontier') and not i.frontier_slots:
+    for path in PATHS:
+        if path.startswith('frontier') and not 0 < i.frontier_slots <= 32 or path == 'wide' and not i.frontier_slots:
             continue
         plan.set_path(path)
         for _ in range(2):
@@ -39,7 +40,7 @@ for label, fill in (('random', None), ('sparse', 0.1), ('dense', 0.9)):
         e1.record(); torch.cuda.synchronize()
         ms = e0.elapsed_time(e1) / 3
         out[path] = (ms, fit.clone())
-        print(f'  {label:7s} {path:9s} {ms:8.2f} ms  {P/ms/1e6:8.3f} Ggenomes/s')
+        print(f'  {label:7s} {path:9s} {ms:8.2f} ms  {P/ms/1e3:10.3f} Mgenomes/s', flush=True)
     for k in out:
-        assert torch.equal(out[k][1], out['unionfind'][1]), 'paths disagree'
+        assert torch.equal(out[k][1], out[PATHS[0]][1]), 'paths disagree'
     plan.set_path('auto')
