@@ -69,6 +69,8 @@ class ESPlanInfo(ctypes.Structure):
         ("smem_path", c_int32),
         ("frontier_slots", c_int32),
         ("seed_cost", c_double),
+        ("window_shift", c_int32),
+        ("packed_labels", c_int32),
     ]
 
 

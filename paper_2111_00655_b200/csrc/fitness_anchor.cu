@@ -16,9 +16,8 @@
 //   survivor.  A pointer always targets a slot that ends no earlier, so no
 //   active slot ever points to a released one.
 // * Sums only where needed.  A one-unit component is described by its unit
-//   (rep, cnt, term1 come from the program position of the slot's occupant,
-//   which is the same for the whole warp: a per-warp table updated each
-//   step).  Only merged components hold an exact sum, in a per-thread pool;
+//   (rep, cnt, term1 come from its program position, kept in the label).
+//   Only merged components hold an exact sum, in a per-thread pool;
 //   the anchor's label word carries the pool index and the kernel count.  A
 //   genome that needs more live merged components than the pool holds is
 //   listed for the warp-per-genome kernel (fitness_wide.cu) instead.
@@ -49,11 +48,13 @@ struct __align__(16) AHot {
 };
 static_assert(sizeof(AHot) == 32, "AHot layout");
 
-// label word: non-anchor: parent slot (bit 31 clear)
-//             anchor:      bit 31 | single << 30 | cnt << 8 | pool entry
+// label word: non-anchor:    parent slot (bit 31 clear)
+//             single anchor: bit 31 | bit 30 | program position of its unit
+//             merged anchor: bit 31 | cnt << 8 | pool entry
 constexpr uint32_t L_ANCHOR = 0x80000000u;
 constexpr uint32_t L_SINGLE = 0x40000000u;
 constexpr uint32_t L_CNT_MAX = (1u << 22) - 1u;
+constexpr uint32_t L_POS_MASK = (1u << 30) - 1u;  // single anchors: program position of the unit
 
 struct X128 {
   uint64_t lo, hi;
@@ -109,6 +110,13 @@ __device__ __forceinline__ void an_price(const uint64_t* ql, const uint64_t* qh,
   atomicAdd(w1, (unsigned long long)(term.hi + ((o0 + term.lo) < o0)));
 }
 
+// slot j of a short back+end list: byte j of the header's list (word 3 + j / 4)
+__device__ __forceinline__ int hdr_slot(const uint4& h0, const uint4& h1, int j) {
+  const int k = j >> 2;
+  const uint32_t w = k == 0 ? h0.w : (k == 1 ? h1.x : (k == 2 ? h1.y : (k == 3 ? h1.z : h1.w)));
+  return (int)((w >> (8 * (j & 3))) & 0xffu);
+}
+
 template <int C>
 __global__ void __launch_bounds__(AN_THREADS)
 fitness_anchor_kernel(AnArgs a, const uint64_t* __restrict__ pop, int64_t n, double* __restrict__ fit) {
@@ -118,8 +126,7 @@ fitness_anchor_kernel(AnArgs a, const uint64_t* __restrict__ pop, int64_t n, dou
   uint64_t* PH = PL + C * T;                             // [C][T] high word
   uint64_t* qall = PH + C * T;                           // [W][3][QCAP] region queue
   uint64_t* tall = qall + W * 3 * AN_QCAP;               // [W][2][32] owner accumulators
-  int32_t* occ_all = reinterpret_cast<int32_t*>(tall + W * 64);  // [W][64] occupant position
-  int32_t* end_all = occ_all + W * 64;                             // [W][64] occupant end
+  int32_t* end_all = reinterpret_cast<int32_t*>(tall + W * 64);  // [W][64] end of the slot's unit
   uint32_t* LAB = reinterpret_cast<uint32_t*>(end_all + W * 64);  // [F][T] labels
   const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
   uint64_t* ql = qall + warp * 3 * AN_QCAP;
@@ -127,8 +134,10 @@ fitness_anchor_kernel(AnArgs a, const uint64_t* __restrict__ pop, int64_t n, dou
   uint64_t* qm = qh + AN_QCAP;
   uint64_t* tlo = tall + warp * 64;
   uint64_t* thi = tlo + 32;
-  int32_t* occ = occ_all + warp * 64;
   int32_t* endw = end_all + warp * 64;
+  uint32_t* lab = LAB + t;  // this thread's column: lab[slot * T]
+  uint64_t* pl = PL + t;
+  uint64_t* ph = PH + t;
   tlo[lane] = thi[lane] = 0ull;
   __syncwarp();
   int qn = 0;
@@ -150,11 +159,13 @@ fitness_anchor_kernel(AnArgs a, const uint64_t* __restrict__ pop, int64_t n, dou
     for (int32_t p = 0; p < a.M; ++p) {
       const AHot* hp = a.hot + p;
       const uint4 h0 = __ldg(reinterpret_cast<const uint4*>(hp));
+      const uint4 h1 = __ldg(reinterpret_cast<const uint4*>(hp) + 1);
       const int32_t bit = (int32_t)h0.x;
       const int S = h0.z & 0xff;
       const int nback = (h0.z >> 8) & 0xff;
       const int nend = (h0.z >> 16) & 0xff;
-      const uint8_t* lst = (h0.z >> 31) ? a.slots + h0.w : hp->list;
+      const bool long_list = (h0.z >> 31) != 0u;
+      const uint8_t* lst = a.slots + h0.w;  // long lists only
       bool on = !dead;
       if (bit >= 0) {
         const int32_t wi = bit >> 6;
@@ -164,50 +175,47 @@ fitness_anchor_kernel(AnArgs a, const uint64_t* __restrict__ pop, int64_t n, dou
         }
         on = (word >> (bit & 63)) & 1ull;
       }
-      if (lane == 0) {
-        occ[S] = p;
-        endw[S] = (int32_t)h0.y;
-      }
+      if (lane == 0) endw[S] = (int32_t)h0.y;
       __syncwarp();
       if (on) {
         if (bit >= 0) x_sub(total, ld_x(a.cold + (size_t)p * 6 + 2));
         act |= 1ull << S;
-        LAB[S * T + t] = L_ANCHOR | L_SINGLE;
+        lab[S * T] = L_ANCHOR | L_SINGLE | (uint32_t)p;
       }
       int A = S;  // root slot of the new unit's component
       for (int j = 0; j < nback; ++j) {
-        const int b = __ldg(lst + j);
+        const int b = long_list ? __ldg(lst + j) : hdr_slot(h0, h1, j);
         if (!on || !((act >> b) & 1ull)) continue;
         int x = b;
-        uint32_t lx = LAB[x * T + t];
+        uint32_t lx = lab[x * T];
         while (!(lx & L_ANCHOR)) {
           x = (int)(lx & 0xff);
-          lx = LAB[x * T + t];
+          lx = lab[x * T];
         }
-        if (x != b) LAB[b * T + t] = (uint32_t)x;  // path compression
+        if (x != b) lab[b * T] = (uint32_t)x;  // path compression
         if (x == A) continue;
-        const uint32_t lA = LAB[A * T + t];
+        const uint32_t lA = lab[A * T];
         const bool keepA = endw[A] >= endw[x];  // the later-ending anchor survives
         const int Wn = keepA ? A : x, Xn = keepA ? x : A;
         const uint32_t lW = keepA ? lA : lx, lX = keepA ? lx : lA;
         X128 sW, sX;
         uint32_t cW, cX;
         if (lW & L_SINGLE) {
-          const int32_t u = occ[Wn];
+          const uint32_t u = lW & L_POS_MASK;
           sW = ld_x(a.cold + (size_t)u * 6);
           cW = (uint32_t)__ldg(a.cnt + u);
         } else {
           const int e = lW & 0x3f;
-          sW = {PL[e * T + t], PH[e * T + t]};
+          sW = {pl[e * T], ph[e * T]};
           cW = (lW >> 8) & L_CNT_MAX;
         }
         if (lX & L_SINGLE) {
-          const int32_t u = occ[Xn];
+          const uint32_t u = lX & L_POS_MASK;
           sX = ld_x(a.cold + (size_t)u * 6);
           cX = (uint32_t)__ldg(a.cnt + u);
         } else {
           const int e = lX & 0x3f;
-          sX = {PL[e * T + t], PH[e * T + t]};
+          sX = {pl[e * T], ph[e * T]};
           cX = (lX >> 8) & L_CNT_MAX;
         }
         x_add(sW, sX);
@@ -226,22 +234,22 @@ fitness_anchor_kernel(AnArgs a, const uint64_t* __restrict__ pop, int64_t n, dou
           e = 0;
         }
         ovf |= c > L_CNT_MAX;
-        PL[e * T + t] = sW.lo;
-        PH[e * T + t] = sW.hi;
-        LAB[Wn * T + t] = L_ANCHOR | ((c & L_CNT_MAX) << 8) | (uint32_t)e;
-        LAB[Xn * T + t] = (uint32_t)Wn;
+        pl[e * T] = sW.lo;
+        ph[e * T] = sW.hi;
+        lab[Wn * T] = L_ANCHOR | ((c & L_CNT_MAX) << 8) | (uint32_t)e;
+        lab[Xn * T] = (uint32_t)Wn;
         A = Wn;
       }
       for (int j = 0; j < nend; ++j) {
-        const int e = __ldg(lst + nback + j);
+        const int e = long_list ? __ldg(lst + nback + j) : hdr_slot(h0, h1, nback + j);
         bool emit = false;
         uint32_t le = 0u;
         if ((act >> e) & 1ull) {
           act &= ~(1ull << e);
-          le = LAB[e * T + t];
+          le = lab[e * T];
           if (le & L_ANCHOR) {  // the anchor leaves: its region is complete
             if (le & L_SINGLE) {
-              x_add(total, ld_x(a.cold + (size_t)occ[e] * 6 + 4));
+              x_add(total, ld_x(a.cold + (size_t)(le & L_POS_MASK) * 6 + 4));
             } else {
               emit = true;
               pfree |= 1u << (le & 0x3f);
@@ -254,8 +262,8 @@ fitness_anchor_kernel(AnArgs a, const uint64_t* __restrict__ pop, int64_t n, dou
           if (emit) {
             const int at = qn + __popc(closing & ((1u << lane) - 1u));
             const int pe = le & 0x3f;
-            ql[at] = PL[pe * T + t];
-            qh[at] = PH[pe * T + t];
+            ql[at] = pl[pe * T];
+            qh[at] = ph[pe * T];
             qm[at] = ((uint64_t)lane << 32) | ((le >> 8) & L_CNT_MAX);
           }
           qn += __popc(closing);
@@ -313,7 +321,7 @@ int sm_count_anchor() {
 
 size_t anchor_smem(int C, int F) {
   constexpr int T = AN_THREADS, W = AN_THREADS / 32;
-  return (size_t)2 * C * T * 8 + (size_t)W * (3 * AN_QCAP + 64) * 8 + (size_t)W * 128 * 4 +
+  return (size_t)2 * C * T * 8 + (size_t)W * (3 * AN_QCAP + 64) * 8 + (size_t)W * 64 * 4 +
          (size_t)F * T * 4;
 }
 

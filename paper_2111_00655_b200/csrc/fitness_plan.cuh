@@ -80,7 +80,8 @@ struct cb_es_plan {
   DBuf<int32_t> d_ovf_count;
   bool packed_ok = true;     // every unit's back / end lists fit the packed header
   int32_t force_path = -1;  // -1 auto, 0 union-find, 1 frontier, 2 frontier (smem labels),
-                            // 3 sparse warp-per-genome walk, 4 anchor walk (thread per genome)
+                            // 3 sparse warp-per-genome walk, 4 anchor walk (thread per genome),
+                            // 5 packed-label walk in the 128-bit window
 };
 
 // fitness_wide.cu: warp-per-genome sparse walk of the frontier program (F <= 128)
@@ -92,6 +93,9 @@ int launch_fitness_wide_list(cb_es_plan* p, const uint64_t* d_pop, int64_t n_max
 // fitness_anchor.cu: 128-bit window analysis + step headers (plan time);
 // thread-per-genome anchor walk (F <= 64), overflow to the wide kernel
 int build_anchor_plan(cb_es_plan* p);
+// fitness_packed128.cu: packed-label walk (<= 16 slots) in the 128-bit window
+int launch_fitness_packed128(cb_es_plan* p, const uint64_t* d_pop, int64_t n, double* d_fit,
+                             cudaStream_t stream);
 int launch_fitness_anchor(cb_es_plan* p, const uint64_t* d_pop, int64_t n, double* d_fit,
                           cudaStream_t stream);
 

@@ -221,14 +221,21 @@ class FitnessPlan:
 
     def set_path(self, path: str) -> None:
         """'auto' | 'frontier' / 'frontier_smem' (thread per genome, <= 32
-        frontier slots) | 'anchor' (thread per genome, <= 64 slots) | 'wide'
+        frontier slots; 'packed128': the packed-label walk in the plan's
+        128-bit window) | 'anchor' (thread per genome, <= 64 slots) | 'wide'
         (warp per genome, sparse walk, <= 128 slots) | 'unionfind'
         (warp/CTA per genome, any plan).  All give identical results;
-        `auto` picks the packed-label frontier kernel for <= 16 slots, the
+        `auto` picks the packed-label frontier kernel for <= 16 slots (in
+        the 128-bit window when the plan fits one), the
         anchor kernel up to 64, the wide kernel up to 128, else union-find."""
         code = {"auto": -1, "unionfind": 0, "frontier": 1, "frontier_smem": 2, "wide": 3,
-                "anchor": 4}[path]
+                "anchor": 4, "packed128": 5}[path]
         nat.check(nat.lib().cb_es_plan_set_path(self.handle.raw, code))
+
+    def has_packed128(self) -> bool:
+        """Whether the 'packed128' path applies (<= 16 frontier slots and
+        every plan value inside a 128-bit window)."""
+        return bool(self.info.packed_labels) and self.info.window_shift >= 0
 
     def set_pool(self, entries: int) -> None:
         """Merged-component pool entries per genome of the anchor kernel

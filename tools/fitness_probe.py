@@ -26,10 +26,12 @@ for label, fill in (('random', None), ('sparse', 0.1), ('dense', 0.9)):
     pop &= torch.from_numpy(feas.view(np.int64)).cuda()
     fit = torch.empty(P, dtype=torch.float64, device='cuda')
     out = {}
-    for path in PATHS:
+    for spec in PATHS:
+        path, _, pool = spec.partition(':')
         if path.startswith('frontier') and not 0 < i.frontier_slots <= 32 or path == 'wide' and not i.frontier_slots:
             continue
         plan.set_path(path)
+        plan.set_pool(int(pool) if pool else 16)
         for _ in range(2):
             plan.evaluate_device(pop.data_ptr(), P, fit.data_ptr())
         torch.cuda.synchronize()
@@ -39,8 +41,8 @@ for label, fill in (('random', None), ('sparse', 0.1), ('dense', 0.9)):
             plan.evaluate_device(pop.data_ptr(), P, fit.data_ptr())
         e1.record(); torch.cuda.synchronize()
         ms = e0.elapsed_time(e1) / 3
-        out[path] = (ms, fit.clone())
-        print(f'  {label:7s} {path:9s} {ms:8.2f} ms  {P/ms/1e3:10.3f} Mgenomes/s', flush=True)
+        out[spec] = (ms, fit.clone())
+        print(f'  {label:7s} {spec:9s} {ms:8.2f} ms  {P/ms/1e3:10.3f} Mgenomes/s', flush=True)
     for k in out:
         assert torch.equal(out[k][1], out[PATHS[0]][1]), 'paths disagree'
     plan.set_path('auto')
