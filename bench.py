@@ -103,10 +103,6 @@ def build_workload(name: str):
     return tp, g, bs
 
 
-def _slots(f: int) -> int:
-    return 4 if f <= 4 else 8 if f <= 8 else 16 if f <= 16 else 32
-
-
 def shard_size(words: int, requested: int | None) -> int:
     if requested:
         return requested
@@ -225,15 +221,13 @@ def run_mine(args) -> None:
                 traffic = d.get("dram_bytes_per_launch_per_genome", 0) * P or None
         except Exception:
             traffic = None
-    f_slots = plan.info.frontier_slots
-    f2 = next(f for f in (4, 6, 8, 12, 16, 99) if f_slots <= f)
-    kernel_name = ((f"fitness_frontier2_kernel<{'uint32_t' if f2 <= 8 else 'uint64_t'}, {f2}>"
-                    if f_slots <= 16 else f"fitness_frontier_kernel<{_slots(f_slots)}>")
-                   if f_slots else
-                   ("fitness_smem_kernel" if plan.info.smem_path else "fitness_global_kernel"))
+    kernel_name = plan.kernel_name()
     cpu = None
     if world == 1 and not args.no_cpu_baseline:
         cpu = cpu_baseline(g, bs, res, plan, args)
+    sweep = None
+    if world == 1 and not args.no_configs:
+        sweep = config_sweep(dev)
     line = {
         "metric": "fitness_evals_per_sec",
         "value": evals_per_s,
@@ -245,7 +239,7 @@ def run_mine(args) -> None:
         "higher_is_better": True,
         "scaling": "weak",
         "vs_baseline": None,
-        "dtype": "u64 bit-genomes, exact 192-bit fixed-point costs",
+        "dtype": "u64 bit-genomes, exact fixed-point costs (128-bit plan window)",
         "data": "synthetic (BERT-base graph built op by op; simulated backend cost tables)",
         "config": {"workload": f"{args.workload}: op-level DP + evolutionary search",
                    "nodes": len(g.nodes), "dp_kernels": len(res.placement),
@@ -269,6 +263,8 @@ def run_mine(args) -> None:
     }
     if cpu is not None:
         line["cpu_baseline"] = cpu
+    if sweep is not None:
+        line["configs"] = sweep
     print(json.dumps(line), flush=True)
     if world > 1:
         import torch.distributed as dist
@@ -306,6 +302,87 @@ def cpu_baseline(g, bs, res, plan, args) -> dict:
     return {"value": sample / dt, "unit": "genomes/s", "cores": threads, "kind": "port",
             "sample": f"{sample} random genomes of the {args.workload} DP placement "
                       f"({plan.k} bits), oracle/oracle.c or_fitness with {threads} OpenMP threads"}
+
+
+# per-config sweep (BASELINE.json's five configs), one GPU: population for
+# the search wall time, generations, population for the fitness rate, CPU
+# sample for the oracle rate, and whether the oracle's covered-set DP (the
+# reference's algorithm) is run for a parity check
+SWEEP = {
+    "resnet50": dict(search_pop=65536, gens=50, fit_pop=1 << 22, cpu=200_000, ref_dp=True),
+    "bert_base": dict(search_pop=65536, gens=50, fit_pop=1 << 22, cpu=100_000, ref_dp=True),
+    "nasnet_a": dict(search_pop=65536, gens=50, fit_pop=1 << 20, cpu=20_000, ref_dp=True),
+    "nasrnn": dict(search_pop=65536, gens=50, fit_pop=65536, cpu=50_000, ref_dp=True),
+    "random100k": dict(search_pop=65536, gens=10, fit_pop=1 << 20, cpu=200, ref_dp=False),
+}
+
+
+def config_sweep(dev) -> dict:
+    """Search wall time, DP time, fitness rate and CPU-oracle rate for each
+    BASELINE.json config (supplementary to the headline line)."""
+    import numpy as np
+    import torch
+    from paper_2111_00655_b200.es_device import DeviceEvolution
+    out = {}
+    for name, cfg in SWEEP.items():
+        tp, g, bs = build_workload(name)
+        row = {"nodes": len(g.nodes)}
+        for rep in range(2):  # first pass warms module loads / first launches
+            bs.registry._tables.clear()
+            torch.cuda.synchronize(dev)
+            t0 = time.perf_counter()
+            res = tp.optimize(g, bs.registry, bs.measurer, 0.01, validate=False)
+            t1 = time.perf_counter()
+            plan = tp.FitnessPlan(g, bs.registry, bs.measurer, res.placement, 0.01, bs.graph_backend,
+                                  res.kernel_matches)
+            es = DeviceEvolution(plan, cfg["search_pop"] if rep else 1024, seed=0, device=dev)
+            es.initialize()
+            for _ in range(cfg["gens"] if rep else 1):
+                es.step()
+            torch.cuda.synchronize(dev)
+            t2 = time.perf_counter()
+        best, _ = es.best()
+        row.update(search_wall_s=t2 - t0, dp_s=t1 - t0, dp_device_ms=res.device["device_ms"],
+                   es_population=cfg["search_pop"], es_generations=cfg["gens"],
+                   dp_kernels=len(res.placement), dp_cost_ms=res.cost_ms, es_best_cost_ms=best,
+                   rounding_window_safe=res.device["rounding_window_safe"],
+                   genome_bits=plan.k, frontier_slots=plan.info.frontier_slots,
+                   fitness_kernel=plan.kernel_name())
+        P = cfg["fit_pop"]
+        es = DeviceEvolution(plan, P, seed=1, device=dev)
+        es.initialize()
+        es.step()
+        es.enable_kernel_timing(True)
+        gens = 3
+        for _ in range(gens):
+            es.step()
+        torch.cuda.synchronize(dev)
+        kt = es.kernel_times_ms()
+        fit_ms = sum(kt["fitness"]) / len(kt["fitness"])
+        row.update(fitness_population=P, fitness_ms_per_generation=fit_ms,
+                   fitness_evals_per_s=P / (fit_ms / 1e3))
+        del es
+        torch.cuda.empty_cache()
+        # CPU oracle (reference algorithm in C), bounded sample, all host threads
+        oc = _oracle_case(g, bs)
+        oc.price()
+        kernels = [[a.backend_pattern.order, a.root, sorted(a.nodes)] for a in res.placement.assignments]
+        threads = os.cpu_count() or 1
+        pop = np.random.default_rng(3).integers(0, 2, size=(cfg["cpu"], plan.k), dtype=np.uint8)
+        t0 = time.perf_counter()
+        oc.fitness(kernels, bs.graph_backend, pop, threads=threads)
+        row["cpu_oracle_fitness_per_s"] = cfg["cpu"] / (time.perf_counter() - t0)
+        row["cpu_threads"] = threads
+        if cfg["ref_dp"]:
+            t0 = time.perf_counter()
+            status, cost, ref_kernels = oc.dp(max_states=200_000)
+            row["reference_dp"] = {"status": status, "s": time.perf_counter() - t0,
+                                   "placement_identical": status == "ok" and ref_kernels == kernels
+                                   and cost == res.cost_ms}
+        else:
+            row["reference_dp"] = {"status": "not run (covered-set state space of a 100k-node graph)"}
+        out[name] = row
+    return out
 
 
 def run_reference(args) -> None:
@@ -380,6 +457,7 @@ def main() -> None:
     ap.add_argument("--cpu-sample", type=int, default=200_000)
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-configs", action="store_true", help="skip the five-config sweep")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

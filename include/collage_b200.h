@@ -216,6 +216,9 @@ int cb_es_plan_set_path(cb_es_plan* p, int32_t path);
  * the warp-per-genome kernel.  A tuning / testing knob: results are
  * identical for every value. */
 int cb_es_plan_set_pool(cb_es_plan* p, int32_t entries);
+/* Name of the fitness kernel the current path setting dispatches to
+ * (static string; for reports and profiles). */
+const char* cb_es_plan_kernel(const cb_es_plan* p);
 /* The dynamic unit graph (diagnostics and tests; any pointer may be NULL):
  * unit_bit[units] genome bit of each unit (-1 = fixed unit), unit_cnt[units]
  * kernels each unit contributes to a region, edges[2*edges] unit pairs

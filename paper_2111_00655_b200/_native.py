@@ -114,6 +114,7 @@ _SIGNATURES = {
     "cb_es_plan_slots": (c_int, [c_void_p, _P_I32, _P_I8, _P_I32, _P_I32]),
     "cb_es_plan_set_path": (c_int, [c_void_p, c_int32]),
     "cb_es_plan_set_pool": (c_int, [c_void_p, c_int32]),
+    "cb_es_plan_kernel": (c_char_p, [c_void_p]),
     "cb_es_plan_units": (c_int, [c_void_p, _P_I32, _P_I32, _P_I32, _P_I32]),
     "cb_es_plan_destroy": (None, [c_void_p]),
     "cb_fitness_device": (c_int, [c_void_p, c_void_p, c_int64, c_void_p, c_void_p]),

@@ -530,6 +530,26 @@ extern "C" int cb_es_plan_units(const cb_es_plan* p, int32_t* unit_bit, int32_t*
   return CB_OK;
 }
 
+extern "C" const char* cb_es_plan_kernel(const cb_es_plan* p) {
+  // the kernel launch_fitness dispatches to (mirrors its decision order)
+  if (!p) return "";
+  const bool frontier = p->F > 0 && p->force_path != 0;
+  if (frontier && p->force_path == 3) return "fitness_wide_kernel";
+  if (frontier && p->packed_ok && p->anchor_ok && (p->force_path == 5 || p->force_path == -1)) {
+    static const char* pk[] = {"fitness_packed128_kernel<uint32_t, 4>", "fitness_packed128_kernel<uint32_t, 6>",
+                               "fitness_packed128_kernel<uint32_t, 8>", "fitness_packed128_kernel<uint64_t, 12>",
+                               "fitness_packed128_kernel<uint64_t, 16>"};
+    return pk[p->F <= 4 ? 0 : p->F <= 6 ? 1 : p->F <= 8 ? 2 : p->F <= 12 ? 3 : 4];
+  }
+  if (frontier && (p->force_path == 4 || (p->force_path == -1 && !p->packed_ok)))
+    return p->anchor_ok ? "fitness_anchor_kernel" : "fitness_wide_kernel";
+  if (frontier) {
+    if (p->force_path != 2 && p->packed_ok) return "fitness_frontier2_kernel";
+    return "fitness_frontier_kernel";
+  }
+  return p->smem_path ? "fitness_smem_kernel" : "fitness_global_kernel";
+}
+
 extern "C" int cb_es_plan_set_pool(cb_es_plan* p, int32_t entries) {
   CB_ARG_CHECK(p && entries >= 1 && entries <= 24, "cb_es_plan_set_pool: entries must be in [1, 24]");
   p->pool_entries = entries;

@@ -232,6 +232,10 @@ class FitnessPlan:
                 "anchor": 4, "packed128": 5}[path]
         nat.check(nat.lib().cb_es_plan_set_path(self.handle.raw, code))
 
+    def kernel_name(self) -> str:
+        """The fitness kernel evaluate / evaluate_device launch."""
+        return nat.lib().cb_es_plan_kernel(self.handle.raw).decode()
+
     def has_packed128(self) -> bool:
         """Whether the 'packed128' path applies (<= 16 frontier slots and
         every plan value inside a 128-bit window)."""
