@@ -78,3 +78,47 @@ if os.path.exists(rep):
                   open(os.path.join(out, "fitness_ncu_summary.json"), "w"), indent=1)
     json.dump(d, open(os.path.join(out, f"{tag}_fitness_ncu.json"), "w"), indent=1)
     print(json.dumps(d, indent=1))
+
+
+# every full capture: one row per kernel launch (HBM roofline of each kernel)
+def _rows(rep):
+    raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True,
+                         text=True).stdout.splitlines()
+    r = list(csv.reader(raw))
+    if len(r) < 3:
+        return []
+    names, units = r[0], r[1]
+    to_b = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "B": 1, "KB": 1e3, "MB": 1e6, "GB": 1e9}
+    to_us = {"nsecond": 1e-3, "ns": 1e-3, "usecond": 1, "us": 1, "msecond": 1e3, "ms": 1e3, "second": 1e6, "s": 1e6}
+    out = []
+    for vals in r[2:]:
+        g = lambda k: vals[names.index(k)] if k in names else ""
+        u = lambda k: units[names.index(k)] if k in names else ""
+        dur = float(g("gpu__time_duration.sum").replace(",", "")) * to_us[u("gpu__time_duration.sum")]
+        rd = float(g("dram__bytes_read.sum").replace(",", "")) * to_b[u("dram__bytes_read.sum")]
+        wr = float(g("dram__bytes_write.sum").replace(",", "")) * to_b[u("dram__bytes_write.sum")]
+        out.append((g("Kernel Name").split("(")[0], g("launch__grid_size"), dur, rd + wr,
+                    g("smsp__issue_active.avg.pct_of_peak_sustained_active"),
+                    g("sm__warps_active.avg.pct_of_peak_sustained_active"),
+                    g("smsp__inst_executed.sum")))
+    return out
+
+peak = json.load(open(os.path.join(root, "MEASURED_PEAKS.json")))["hbm_gbs"]
+rows = []
+for rep, what in (("fitness_full.ncu-rep", "bench workload (BERT-base)"),
+                  ("search_full.ncu-rep", "search phase (BERT-base)"),
+                  ("anchor_full.ncu-rep", "random 100k DAG, 65536 random genomes")):
+    path = os.path.join(root, "gpurun_out", rep)
+    if os.path.exists(path):
+        rows += [(what,) + x for x in _rows(path)]
+with open(os.path.join(out, f"{tag}_kernels.md"), "w") as fh:
+    fh.write(f"# {tag}: per-kernel DRAM traffic and HBM roofline (ncu --set full, one launch each)\n\n")
+    fh.write(f"Peak: {peak} GB/s (MEASURED_PEAKS.json).  ncu serialises launches and runs with cold "
+             "caches; durations are for reading shares and ratios, not bench values.\n\n")
+    fh.write("| workload | kernel | grid | duration us | DRAM bytes | GB/s | % of HBM peak | issue active % "
+             "| warps active % | warp instructions |\n|---|---|---:|---:|---:|---:|---:|---:|---:|---:|\n")
+    for what, k, grid, dur, b, iss, wa, inst in rows:
+        gbs = b / (dur * 1e-6) / 1e9 if dur else 0.0
+        fh.write(f"| {what} | `{k}` | {grid} | {dur:.1f} | {b:.0f} | {gbs:.2f} | {100 * gbs / peak:.4f}% "
+                 f"| {iss} | {wa} | {inst} |\n")
+print(open(os.path.join(out, f"{tag}_kernels.md")).read())
