@@ -347,6 +347,7 @@ def config_sweep(dev) -> dict:
                    dp_kernels=len(res.placement), dp_cost_ms=res.cost_ms, es_best_cost_ms=best,
                    rounding_window_safe=res.device["rounding_window_safe"],
                    genome_bits=plan.k, frontier_slots=plan.info.frontier_slots,
+                   window_shift=plan.info.window_shift,
                    fitness_kernel=plan.kernel_name())
         P = cfg["fit_pop"]
         es = DeviceEvolution(plan, P, seed=1, device=dev)
