@@ -136,15 +136,16 @@ def optimize(g: ComputationGraph, registry: PatternRegistry, measurer: Measurer,
                                     "compatibly by the registered patterns")
     chosen = kernels[:res.n_kernels]
     patterns = registry.patterns
-    assignments = [Assignment(table.node_set(int(m)), patterns[int(table.pat[m])],
-                              g.id_of(int(table.root[m]))) for m in chosen]
+    root_ids = np.asarray(g._ids)[table.root[chosen]].tolist()
+    assignments = [Assignment(table.node_set(m), patterns[p], r)
+                   for m, p, r in zip(chosen.tolist(), table.pat[chosen].tolist(), root_ids)]
     stats.improvements = len(assignments)
     placement = PlacementStrategy(assignments)
     if validate or (validate is None and len(g.nodes) <= VALIDATE_MAX_NODES):
         validate_placement(g, placement)
     order = {a.nodes: i for i, a in enumerate(placement.assignments)}
     canon = np.empty(len(chosen), dtype=np.int32)
-    for m in chosen:
-        canon[order[table.node_set(int(m))]] = m
+    for m in chosen.tolist():
+        canon[order[table.node_set(m)]] = m
     return DPResult(placement, res.cost_ms, stats,
                     {frozenset(g.nodes): res.cost_ms, frozenset(): 0.0}, device, canon)

@@ -88,6 +88,7 @@ class MatchTable:
             nat.ptr(self.bind_ptr, I32), nat.ptr(self.binds, I32)))
         self._objs: dict[int, Match] = {}
         self._sets: dict[int, frozenset[int]] = {}
+        self._lists = None
 
     @classmethod
     def all_anchors(cls, g: ComputationGraph, pats: NativePatterns) -> "MatchTable":
@@ -113,8 +114,11 @@ class MatchTable:
     def node_set(self, m: int) -> frozenset[int]:
         s = self._sets.get(m)
         if s is None:
-            ids = self.graph._ids
-            s = frozenset(int(ids[v]) for v in self.members[self.mem_ptr[m]:self.mem_ptr[m + 1]])
+            if self._lists is None:  # Python-int views, built once per table
+                self._lists = (self.members.tolist(), self.mem_ptr.tolist(),
+                               np.asarray(self.graph._ids).tolist())
+            mem, ptr, ids = self._lists
+            s = frozenset([ids[v] for v in mem[ptr[m]:ptr[m + 1]]])
             self._sets[m] = s
         return s
 
