@@ -203,7 +203,8 @@ typedef struct {
   int32_t frontier_slots;/* thread/genome frontier program width (0 = none) */
   double seed_cost;      /* graph-level cost of the all-zero genome */
   int32_t window_shift;  /* 128-bit window: values carried as v >> shift (-1 = none) */
-  int32_t packed_labels; /* frontier fits the packed-label kernels (<= 16 slots) */
+  int32_t packed_labels; /* 1: frontier fits the packed-label kernels (<= 16 slots),
+                            2: also the packed anchor kernel (<= 8 slots) */
 } cb_es_plan_info;
 int cb_es_plan_query(const cb_es_plan* p, cb_es_plan_info* info);
 /* Evaluation path: -1 automatic (frontier program when available), 0 the

@@ -512,7 +512,7 @@ extern "C" int cb_es_plan_query(const cb_es_plan* p, cb_es_plan_info* info) {
   info->frontier_slots = p->F;
   info->seed_cost = p->seed_cost;
   info->window_shift = p->anchor_ok ? p->anchor_shift : -1;
-  info->packed_labels = p->F > 0 && p->packed_ok ? 1 : 0;
+  info->packed_labels = p->F > 0 && p->packed_ok ? (p->pa_ok && p->anchor_ok ? 2 : 1) : 0;
   return CB_OK;
 }
 
@@ -535,6 +535,8 @@ extern "C" const char* cb_es_plan_kernel(const cb_es_plan* p) {
   if (!p) return "";
   const bool frontier = p->F > 0 && p->force_path != 0;
   if (frontier && p->force_path == 3) return "fitness_wide_kernel";
+  if (frontier && p->pa_ok && p->anchor_ok && (p->force_path == 6 || p->force_path == -1))
+    return p->F <= 4 ? "fitness_pa_kernel<4>" : p->F <= 6 ? "fitness_pa_kernel<6>" : "fitness_pa_kernel<8>";
   if (frontier && p->packed_ok && p->anchor_ok && (p->force_path == 5 || p->force_path == -1)) {
     static const char* pk[] = {"fitness_packed128_kernel<uint32_t, 4>", "fitness_packed128_kernel<uint32_t, 6>",
                                "fitness_packed128_kernel<uint32_t, 8>", "fitness_packed128_kernel<uint64_t, 12>",
@@ -557,7 +559,9 @@ extern "C" int cb_es_plan_set_pool(cb_es_plan* p, int32_t entries) {
 }
 
 extern "C" int cb_es_plan_set_path(cb_es_plan* p, int32_t path) {
-  CB_ARG_CHECK(p && path >= -1 && path <= 5, "cb_es_plan_set_path: bad arguments");
+  CB_ARG_CHECK(p && path >= -1 && path <= 6, "cb_es_plan_set_path: bad arguments");
+  CB_ARG_CHECK(path != 6 || (p->pa_ok && p->anchor_ok),
+               "cb_es_plan_set_path: no packed anchor program (> 8 slots or values outside a 128-bit window)");
   CB_ARG_CHECK(path != 5 || (p->packed_ok && p->anchor_ok),
                "cb_es_plan_set_path: no packed 128-bit program (> 16 slots or values outside a 128-bit window)");
   CB_ARG_CHECK(path != 4 || p->anchor_ok,
@@ -1263,6 +1267,8 @@ static int launch_fitness(cb_es_plan* p, const uint64_t* d_pop, int64_t n, doubl
   if (n <= 0) return CB_OK;
   const bool frontier = p->F > 0 && p->force_path != 0;
   if (frontier && p->force_path == 3) return launch_fitness_wide(p, d_pop, n, d_fit, stream);
+  if (frontier && p->pa_ok && p->anchor_ok && (p->force_path == 6 || p->force_path == -1))
+    return launch_fitness_packed_anchor(p, d_pop, n, d_fit, stream);
   if (frontier && p->packed_ok && p->anchor_ok && (p->force_path == 5 || p->force_path == -1))
     return launch_fitness_packed128(p, d_pop, n, d_fit, stream);
   if (frontier && (p->force_path == 4 || (p->force_path == -1 && !p->packed_ok)))

@@ -427,7 +427,43 @@ int build_anchor_plan(cb_es_plan* P) {
     }
     cnt[p] = r.cnt;
   }
+  // packed anchor headers (F <= 8): bit | slot | nback | nend, back / end
+  // slot nibbles, and the end rank of every slot's current unit (slots
+  // ordered by their unit's last neighbour, ties by slot)
+  P->pa_ok = P->F <= 8 && P->k < 0xFFFFF;
+  std::vector<uint32_t> pah;
+  if (P->pa_ok) {
+    pah.resize((size_t)M * 4);
+    std::vector<int32_t> occ_last(P->F, -1);
+    for (int32_t p = 0; p < M && P->pa_ok; ++p) {
+      const UnitRec& r = P->prog[p];
+      if (r.nback > 8 || r.nend > 8) {
+        P->pa_ok = false;
+        break;
+      }
+      occ_last[r.slot] = P->prog_last[p];
+      uint32_t x = (r.bit >= 0 ? (uint32_t)r.bit : 0xFFFFFu) | ((uint32_t)r.slot << 20) |
+                   ((uint32_t)r.nback << 24) | ((uint32_t)r.nend << 28);
+      uint32_t yb = 0, ze = 0, wr = 0;
+      for (int j = 0; j < r.nback; ++j) yb |= (uint32_t)(P->prog_slots[r.back_off + j] & 0xF) << (4 * j);
+      for (int j = 0; j < r.nend; ++j) ze |= (uint32_t)(P->prog_slots[r.end_off + j] & 0xF) << (4 * j);
+      for (int s = 0; s < P->F; ++s) {
+        int rank = 0;
+        for (int q = 0; q < P->F; ++q)
+          if (occ_last[q] < occ_last[s] || (occ_last[q] == occ_last[s] && q < s)) ++rank;
+        wr |= (uint32_t)rank << (4 * s);
+      }
+      pah[(size_t)p * 4 + 0] = x;
+      pah[(size_t)p * 4 + 1] = yb;
+      pah[(size_t)p * 4 + 2] = ze;
+      pah[(size_t)p * 4 + 3] = wr;
+    }
+  }
   cudaError_t e;
+  if (P->pa_ok && (e = P->d_pahdr.upload(pah)) != cudaSuccess) {
+    cb_set_error(std::string("CUDA error in plan upload: ") + cudaGetErrorString(e));
+    return CB_ERR_CUDA;
+  }
   if ((e = P->d_ahot.upload(reinterpret_cast<const uint8_t*>(hot.data()), hot.size() * sizeof(AHot))) !=
           cudaSuccess ||
       (e = P->d_acold.upload(cold)) != cudaSuccess || (e = P->d_acnt.upload(cnt)) != cudaSuccess) {

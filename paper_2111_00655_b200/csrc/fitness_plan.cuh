@@ -76,12 +76,15 @@ struct cb_es_plan {
   DBuf<uint64_t> d_acold;   // [M][6]: rep, off, term1 as 128-bit X
   DBuf<int32_t> d_acnt;     // [M]
   int32_t pool_entries = 16;
+  // packed anchor walk (fitness_packed128.cu, <= 8 slots): 16-byte step headers
+  bool pa_ok = false;
+  DBuf<uint32_t> d_pahdr;
   DBuf<int64_t> d_ovf_list;
   DBuf<int32_t> d_ovf_count;
   bool packed_ok = true;     // every unit's back / end lists fit the packed header
   int32_t force_path = -1;  // -1 auto, 0 union-find, 1 frontier, 2 frontier (smem labels),
                             // 3 sparse warp-per-genome walk, 4 anchor walk (thread per genome),
-                            // 5 packed-label walk in the 128-bit window
+                            // 5 packed-label walk in the 128-bit window, 6 packed anchor walk
 };
 
 // fitness_wide.cu: warp-per-genome sparse walk of the frontier program (F <= 128)
@@ -96,6 +99,8 @@ int build_anchor_plan(cb_es_plan* p);
 // fitness_packed128.cu: packed-label walk (<= 16 slots) in the 128-bit window
 int launch_fitness_packed128(cb_es_plan* p, const uint64_t* d_pop, int64_t n, double* d_fit,
                              cudaStream_t stream);
+int launch_fitness_packed_anchor(cb_es_plan* p, const uint64_t* d_pop, int64_t n, double* d_fit,
+                                 cudaStream_t stream);
 int launch_fitness_anchor(cb_es_plan* p, const uint64_t* d_pop, int64_t n, double* d_fit,
                           cudaStream_t stream);
 

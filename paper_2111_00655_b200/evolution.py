@@ -222,14 +222,16 @@ class FitnessPlan:
     def set_path(self, path: str) -> None:
         """'auto' | 'frontier' / 'frontier_smem' (thread per genome, <= 32
         frontier slots; 'packed128': the packed-label walk in the plan's
-        128-bit window) | 'anchor' (thread per genome, <= 64 slots) | 'wide'
+        128-bit window; 'packed_anchor': the same with anchor labels, <= 8
+        slots) | 'anchor' (thread per genome, <= 64 slots) | 'wide'
         (warp per genome, sparse walk, <= 128 slots) | 'unionfind'
         (warp/CTA per genome, any plan).  All give identical results;
-        `auto` picks the packed-label frontier kernel for <= 16 slots (in
-        the 128-bit window when the plan fits one), the
+        `auto` picks the packed anchor kernel for <= 8 slots, the
+        packed-label frontier kernel for <= 16 slots (in the 128-bit window
+        when the plan fits one), the
         anchor kernel up to 64, the wide kernel up to 128, else union-find."""
         code = {"auto": -1, "unionfind": 0, "frontier": 1, "frontier_smem": 2, "wide": 3,
-                "anchor": 4, "packed128": 5}[path]
+                "anchor": 4, "packed128": 5, "packed_anchor": 6}[path]
         nat.check(nat.lib().cb_es_plan_set_path(self.handle.raw, code))
 
     def kernel_name(self) -> str:
@@ -240,6 +242,11 @@ class FitnessPlan:
         """Whether the 'packed128' path applies (<= 16 frontier slots and
         every plan value inside a 128-bit window)."""
         return bool(self.info.packed_labels) and self.info.window_shift >= 0
+
+    def has_packed_anchor(self) -> bool:
+        """Whether the 'packed_anchor' path applies (<= 8 frontier slots,
+        128-bit window)."""
+        return self.info.packed_labels == 2 and self.info.window_shift >= 0
 
     def set_pool(self, entries: int) -> None:
         """Merged-component pool entries per genome of the anchor kernel

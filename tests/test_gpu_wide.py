@@ -79,7 +79,7 @@ def test_wide_kernel_agrees_on_models(gpu, name):
     genomes = _genomes(plan, np.random.default_rng(5), 2000)
     plan.set_path("auto")
     want = plan.evaluate(genomes)
-    for path in ("wide", "anchor", "frontier") + (("packed128",) if plan.has_packed128() else ()):
+    for path in ("wide", "anchor", "frontier") + (("packed128",) if plan.has_packed128() else ()) + (("packed_anchor",) if plan.has_packed_anchor() else ()):
         plan.set_path(path)
         assert np.array_equal(plan.evaluate(genomes), want), path
     plan.set_path("auto")
