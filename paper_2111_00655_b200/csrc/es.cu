@@ -13,7 +13,7 @@
 // of the child from the two parents with segment masks (coalesced rows).
 #include <cub/cub.cuh>
 
-#include "cb_internal.cuh"
+#include "fitness_plan.cuh"
 
 // Philox4x32-10
 struct Philox {
@@ -187,7 +187,7 @@ breed_kernel(int32_t k, int32_t words, const uint64_t* __restrict__ parents,
 template <int W>
 __global__ void __launch_bounds__(256)
 breed_thread_kernel(int32_t k, const uint64_t* __restrict__ parents, const double* __restrict__ fit,
-                    int64_t n_parents, uint64_t* __restrict__ children, int64_t n_children,
+                    const uint32_t* __restrict__ keys, int64_t n_parents, uint64_t* __restrict__ children, int64_t n_children,
                     const uint64_t* __restrict__ keep, int64_t n_keep, uint64_t seed,
                     uint32_t generation, uint32_t stream_id, int32_t tournament, double rate,
                     double log1m_rate) {
@@ -203,14 +203,16 @@ breed_thread_kernel(int32_t k, const uint64_t* __restrict__ parents, const doubl
                  stream_id);
       int64_t pa = 0, pb = 0;
       for (int t = 0; t < 2; ++t) {
+        // compare the 32-bit order keys (high word of the non-negative
+        // fitness, an L2-resident array), the full doubles only on a key tie
         int64_t best = rng.below((uint32_t)n_parents);
-        double bf = __ldg(fit + best);
+        uint32_t bk = __ldg(keys + best);
         for (int j = 1; j < tournament; ++j) {
           const int64_t i = rng.below((uint32_t)n_parents);
-          const double f = __ldg(fit + i);
-          if (f < bf) {
+          const uint32_t ki = __ldg(keys + i);
+          if (ki < bk || (ki == bk && __ldg(fit + i) < __ldg(fit + best))) {
             best = i;
-            bf = f;
+            bk = ki;
           }
         }
         if (t == 0) pa = best;
@@ -255,18 +257,25 @@ breed_thread_kernel(int32_t k, const uint64_t* __restrict__ parents, const doubl
   }
 }
 
-struct cb_es_plan;
-extern "C" int cb_es_plan_query(const cb_es_plan* p, cb_es_plan_info* info);
+
+// Tournament order keys: the high word of each fitness (non-negative doubles
+// and +inf order like their bit patterns), half the bytes of the fitness
+// array so that a large population's keys stay in L2 for the random gathers.
+__global__ void fitness_keys_kernel(const double* __restrict__ fit, int64_t n, uint32_t* __restrict__ keys) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride)
+    keys[i] = (uint32_t)((unsigned long long)__double_as_longlong(__ldg(fit + i)) >> 32);
+}
 
 template <int W>
 static void launch_breed_thread(int32_t k, const uint64_t* parents, const double* fit,
-                                int64_t n_parents, uint64_t* children, int64_t n_children,
+                                const uint32_t* keys, int64_t n_parents, uint64_t* children, int64_t n_children,
                                 const uint64_t* keep, int64_t n_keep, uint64_t seed, uint32_t gen,
                                 uint32_t sid, int32_t tournament, double rate, double log1m,
                                 cudaStream_t s) {
   int64_t blocks = (n_children + 255) / 256;
   if (blocks > 148 * 8) blocks = 148 * 8;
-  breed_thread_kernel<W><<<(unsigned)blocks, 256, 0, s>>>(k, parents, fit, n_parents, children,
+  breed_thread_kernel<W><<<(unsigned)blocks, 256, 0, s>>>(k, parents, fit, keys, n_parents, children,
                                                            n_children, keep, n_keep, seed, gen,
                                                            sid, tournament, rate, log1m);
 }
@@ -286,10 +295,17 @@ extern "C" int cb_es_breed(cb_es_plan* p, const uint64_t* d_parents, const doubl
   double log1m = (mutation_rate > 0.0 && mutation_rate < 1.0) ? log1p(-mutation_rate) : -1.0;
   cudaStream_t s = (cudaStream_t)stream;
   const uint32_t gen = (uint32_t)generation, sid = (uint32_t)stream_id;
+  uint32_t* keys = nullptr;
+  if (info.words <= 8) {
+    if (p->d_keys.n < (size_t)n_parents) CB_CUDA_TRY(p->d_keys.alloc((size_t)n_parents));
+    keys = p->d_keys.p;
+    const int64_t kb = std::min<int64_t>((n_parents + 255) / 256, 148 * 16);
+    fitness_keys_kernel<<<(unsigned)kb, 256, 0, s>>>(d_parent_fit, n_parents, keys);
+  }
   switch (info.words) {
 #define CB_BREED_CASE(Wn)                                                                   \
   case Wn:                                                                                  \
-    launch_breed_thread<Wn>(info.genome_bits, d_parents, d_parent_fit, n_parents, d_children, \
+    launch_breed_thread<Wn>(info.genome_bits, d_parents, d_parent_fit, keys, n_parents, d_children, \
                             n_children, d_keep, n_keep, seed, gen, sid, tournament,          \
                             mutation_rate, log1m, s);                                        \
     CB_CUDA_TRY(cudaGetLastError());                                                         \

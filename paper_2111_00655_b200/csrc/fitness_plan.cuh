@@ -76,6 +76,8 @@ struct cb_es_plan {
   DBuf<uint64_t> d_acold;   // [M][6]: rep, off, term1 as 128-bit X
   DBuf<int32_t> d_acnt;     // [M]
   int32_t pool_entries = 16;
+  // tournament order keys of the parent population (es.cu)
+  DBuf<uint32_t> d_keys;
   // packed anchor walk (fitness_packed128.cu, <= 8 slots): 16-byte step headers
   bool pa_ok = false;
   DBuf<uint32_t> d_pahdr;
