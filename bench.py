@@ -119,12 +119,19 @@ def run_mine(args) -> None:
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # one GPU per rank; CB_BENCH_DIST_BACKEND=gloo (test only) lets several
+    # ranks share the GPUs of a smaller box to exercise the N > 1 code path
+    backend = os.environ.get("CB_BENCH_DIST_BACKEND", "nccl")
+    local = local % max(torch.cuda.device_count(), 1) if backend != "nccl" else local
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     group = None
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=dev)
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(backend)
         group = dist.group.WORLD
 
     def barrier():
@@ -245,7 +252,8 @@ def run_mine(args) -> None:
                    "nodes": len(g.nodes), "dp_kernels": len(res.placement),
                    "genome_bits": plan.k, "genome_words": plan.words,
                    "population_per_gpu": P, "global_population": P * world,
-                   "parallelism": f"population sharded over {world} GPU(s), NCCL all-gather of elites",
+                   "parallelism": f"population sharded over {world} GPU(s), "
+                                  f"{'NCCL' if backend == 'nccl' else backend} all-gather of elites",
                    "l2": "population > L2 (no flush)"},
         "search": {"wall_s": search_s, "dp_s": search_t["dp_s"], "es_s": search_t["es_s"],
                    "es_population_per_gpu": args.search_population,
