@@ -12,6 +12,9 @@
 // ------------------------------------------------------------- error state
 void cb_set_error(const std::string& msg);
 
+// Streaming multiprocessors of the current device (148 on B200), cached.
+int cb_sm_count();
+
 #define CB_CUDA_TRY(expr)                                                  \
   do {                                                                     \
     cudaError_t _e = (expr);                                               \

@@ -274,7 +274,7 @@ static void launch_breed_thread(int32_t k, const uint64_t* parents, const double
                                 uint32_t sid, int32_t tournament, double rate, double log1m,
                                 cudaStream_t s) {
   int64_t blocks = (n_children + 255) / 256;
-  if (blocks > 148 * 8) blocks = 148 * 8;
+  if (blocks > (int64_t)cb_sm_count() * 8) blocks = (int64_t)cb_sm_count() * 8;
   breed_thread_kernel<W><<<(unsigned)blocks, 256, 0, s>>>(k, parents, fit, keys, n_parents, children,
                                                            n_children, keep, n_keep, seed, gen,
                                                            sid, tournament, rate, log1m);
@@ -299,7 +299,7 @@ extern "C" int cb_es_breed(cb_es_plan* p, const uint64_t* d_parents, const doubl
   if (info.words <= 8) {
     if (p->d_keys.n < (size_t)n_parents) CB_CUDA_TRY(p->d_keys.alloc((size_t)n_parents));
     keys = p->d_keys.p;
-    const int64_t kb = std::min<int64_t>((n_parents + 255) / 256, 148 * 16);
+    const int64_t kb = std::min<int64_t>((n_parents + 255) / 256, (int64_t)cb_sm_count() * 16);
     fitness_keys_kernel<<<(unsigned)kb, 256, 0, s>>>(d_parent_fit, n_parents, keys);
   }
   switch (info.words) {
@@ -323,7 +323,7 @@ extern "C" int cb_es_breed(cb_es_plan* p, const uint64_t* d_parents, const doubl
       break;
   }
   int64_t blocks = (n_children + BREED_WARPS - 1) / BREED_WARPS;
-  if (blocks > 148 * 16) blocks = 148 * 16;
+  if (blocks > (int64_t)cb_sm_count() * 16) blocks = (int64_t)cb_sm_count() * 16;
   breed_kernel<<<(unsigned)blocks, BREED_WARPS * 32, 0, (cudaStream_t)stream>>>(
       info.genome_bits, info.words, d_parents, d_parent_fit, n_parents, d_children, n_children,
       d_keep, n_keep, seed, (uint32_t)generation, (uint32_t)stream_id, tournament, mutation_rate,

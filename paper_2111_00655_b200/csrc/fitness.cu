@@ -1204,7 +1204,7 @@ static FitArgs make_args(cb_es_plan* p) {
   return a;
 }
 
-static int sm_count() {
+int cb_sm_count() {
   static int cached = 0;
   if (!cached) {
     int dev = 0;
@@ -1230,7 +1230,7 @@ static int launch_frontier_t(cb_es_plan* p, const uint64_t* d_pop, int64_t n, do
                                                             FR_THREADS, smem));
   if (per_sm < 1) per_sm = 1;
   const int64_t want = (n + FR_THREADS - 1) / FR_THREADS;
-  const int64_t grid = std::min<int64_t>(want, (int64_t)per_sm * sm_count());
+  const int64_t grid = std::min<int64_t>(want, (int64_t)per_sm * cb_sm_count());
   fitness_frontier_kernel<F><<<(unsigned)grid, FR_THREADS, smem, stream>>>(
       p->M, p->words, p->base_const, p->eps, p->d_prog.p, p->d_prog_slots.p, p->d_infeas.p,
       p->d_rt.p, d_pop, n, d_fit, p->d_flags.p);
@@ -1254,7 +1254,7 @@ static int launch_frontier2_t(cb_es_plan* p, const uint64_t* d_pop, int64_t n, d
                                                             FR_THREADS, smem));
   if (per_sm < 1) per_sm = 1;
   const int64_t want = (n + FR_THREADS - 1) / FR_THREADS;
-  const int64_t grid = std::min<int64_t>(want, (int64_t)per_sm * sm_count());
+  const int64_t grid = std::min<int64_t>(want, (int64_t)per_sm * cb_sm_count());
   fitness_frontier2_kernel<LT, F><<<(unsigned)grid, FR_THREADS, smem, stream>>>(
       p->M, p->words, p->base_const, p->eps, p->d_prog.p, p->d_prog_slots.p, p->d_infeas.p,
       p->d_rt.p, d_pop, n, d_fit, p->d_flags.p);
@@ -1301,11 +1301,11 @@ static int launch_fitness(cb_es_plan* p, const uint64_t* d_pop, int64_t n, doubl
                                                               FIT_WARPS * 32, smem));
     if (per_sm < 1) per_sm = 1;
     int64_t want = (n + FIT_WARPS - 1) / FIT_WARPS;
-    int64_t grid = std::min<int64_t>(want, (int64_t)per_sm * sm_count());
+    int64_t grid = std::min<int64_t>(want, (int64_t)per_sm * cb_sm_count());
     fitness_smem_kernel<<<(unsigned)grid, FIT_WARPS * 32, smem, stream>>>(a, d_pop, n, d_fit);
   } else {
     const size_t per_group = ((size_t)p->M * (sizeof(fx192) + 8) + 255) & ~(size_t)255;
-    int64_t grid = std::min<int64_t>(n, (int64_t)4 * sm_count());
+    int64_t grid = std::min<int64_t>(n, (int64_t)4 * cb_sm_count());
     if (p->scratch_per_group != per_group || p->scratch_groups < grid) {
       CB_CUDA_TRY(p->d_scratch.alloc(per_group * grid));
       p->scratch_per_group = per_group;

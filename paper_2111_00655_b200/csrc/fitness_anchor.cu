@@ -308,17 +308,6 @@ fitness_anchor_kernel(AnArgs a, const uint64_t* __restrict__ pop, int64_t n, dou
   if (inexact) atomicAdd(a.flags, 1ull);
 }
 
-int sm_count_anchor() {
-  static int cached = 0;
-  if (!cached) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&cached, cudaDevAttrMultiProcessorCount, dev);
-    if (cached <= 0) cached = 148;
-  }
-  return cached;
-}
-
 size_t anchor_smem(int C, int F) {
   constexpr int T = AN_THREADS, W = AN_THREADS / 32;
   return (size_t)2 * C * T * 8 + (size_t)W * (3 * AN_QCAP + 64) * 8 + (size_t)W * 64 * 4 +
@@ -354,7 +343,7 @@ int launch_anchor_t(cb_es_plan* p, const uint64_t* d_pop, int64_t n, double* d_f
   a.ovf_count = p->d_ovf_count.p;
   a.ovf_list = p->d_ovf_list.p;
   const int64_t want = (n + AN_THREADS - 1) / AN_THREADS;
-  const int64_t grid = std::min<int64_t>(want, (int64_t)per_sm * sm_count_anchor());
+  const int64_t grid = std::min<int64_t>(want, (int64_t)per_sm * cb_sm_count());
   fitness_anchor_kernel<C><<<(unsigned)grid, AN_THREADS, smem, stream>>>(a, d_pop, n, d_fit);
   CB_CUDA_TRY(cudaGetLastError());
   // genomes that ran out of pool entries: warp-per-genome kernel over the list

@@ -392,17 +392,6 @@ PkArgs make_pk_args(cb_es_plan* p) {
   return a;
 }
 
-int sm_count_pk() {
-  static int cached = 0;
-  if (!cached) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&cached, cudaDevAttrMultiProcessorCount, dev);
-    if (cached <= 0) cached = 148;
-  }
-  return cached;
-}
-
 template <typename LT, int F>
 int launch_pk_t(cb_es_plan* p, const uint64_t* d_pop, int64_t n, double* d_fit, cudaStream_t stream) {
   const size_t smem = ((size_t)3 * F * PK_THREADS + (size_t)(PK_THREADS / 32) * (3 * PK_QCAP + 64)) *
@@ -419,7 +408,7 @@ int launch_pk_t(cb_es_plan* p, const uint64_t* d_pop, int64_t n, double* d_fit, 
   if (per_sm < 1) per_sm = 1;
   PkArgs a = make_pk_args(p);
   const int64_t want = (n + PK_THREADS - 1) / PK_THREADS;
-  const int64_t grid = std::min<int64_t>(want, (int64_t)per_sm * sm_count_pk());
+  const int64_t grid = std::min<int64_t>(want, (int64_t)per_sm * cb_sm_count());
   fitness_packed128_kernel<LT, F><<<(unsigned)grid, PK_THREADS, smem, stream>>>(a, d_pop, n, d_fit);
   CB_CUDA_TRY(cudaGetLastError());
   return CB_OK;
@@ -440,7 +429,7 @@ int launch_pa_t(cb_es_plan* p, const uint64_t* d_pop, int64_t n, double* d_fit, 
   if (per_sm < 1) per_sm = 1;
   PkArgs a = make_pk_args(p);
   const int64_t want = (n + PK_THREADS - 1) / PK_THREADS;
-  const int64_t grid = std::min<int64_t>(want, (int64_t)per_sm * sm_count_pk());
+  const int64_t grid = std::min<int64_t>(want, (int64_t)per_sm * cb_sm_count());
   fitness_pa_kernel<F><<<(unsigned)grid, PK_THREADS, smem, stream>>>(
       a, reinterpret_cast<const uint4*>(p->d_pahdr.p), d_pop, n, d_fit);
   CB_CUDA_TRY(cudaGetLastError());

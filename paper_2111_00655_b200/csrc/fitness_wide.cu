@@ -293,17 +293,6 @@ fitness_wide_kernel(WideArgs a, const uint64_t* __restrict__ pop, int64_t n, dou
   if (__any_sync(0xffffffffu, inexact) && lane == 0) atomicAdd(a.flags, 1ull);
 }
 
-int sm_count_wide() {
-  static int cached = 0;
-  if (!cached) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&cached, cudaDevAttrMultiProcessorCount, dev);
-    if (cached <= 0) cached = 148;
-  }
-  return cached;
-}
-
 template <int SPL>
 int launch_wide_t(cb_es_plan* p, const uint64_t* d_pop, int64_t n, double* d_fit, cudaStream_t stream,
                   const int64_t* list = nullptr, const int32_t* list_count = nullptr) {
@@ -325,7 +314,7 @@ int launch_wide_t(cb_es_plan* p, const uint64_t* d_pop, int64_t n, double* d_fit
   CB_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fitness_wide_kernel<SPL>, WD_THREADS, 0));
   if (per_sm < 1) per_sm = 1;
   const int64_t want = (n + WD_THREADS / 32 - 1) / (WD_THREADS / 32);
-  const int64_t grid = std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)per_sm * sm_count_wide()));
+  const int64_t grid = std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)per_sm * cb_sm_count()));
   fitness_wide_kernel<SPL><<<(unsigned)grid, WD_THREADS, 0, stream>>>(a, d_pop, n, d_fit, list, list_count);
   CB_CUDA_TRY(cudaGetLastError());
   return CB_OK;
@@ -344,7 +333,7 @@ int launch_fitness_wide_list(cb_es_plan* p, const uint64_t* d_pop, int64_t n_max
                              const int64_t* list, const int32_t* list_count, cudaStream_t stream) {
   // the count lives on the device: size the grid for the worst case, idle
   // warps exit at once
-  const int64_t n = std::min<int64_t>(n_max, (int64_t)4 * 148 * 16);
+  const int64_t n = std::min<int64_t>(n_max, (int64_t)4 * cb_sm_count() * 16);
   if (p->F <= 32) return launch_wide_t<1>(p, d_pop, n, d_fit, stream, list, list_count);
   if (p->F <= 64) return launch_wide_t<2>(p, d_pop, n, d_fit, stream, list, list_count);
   return launch_wide_t<4>(p, d_pop, n, d_fit, stream, list, list_count);
