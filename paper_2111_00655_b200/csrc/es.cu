@@ -227,7 +227,9 @@ breed_thread_kernel(int32_t k, const uint64_t* __restrict__ parents, const doubl
 #pragma unroll
       for (int w = 0; w < W; ++w) {
         const uint64_t mb = seg_mask(ci, cj, w);
-        v[w] = (__ldg(parents + pa * W + w) & ~mb) | (__ldg(parents + pb * W + w) & mb);
+        // parent rows and child rows stream through L2 with evict-first
+        // priority so the tournament keys stay resident
+        v[w] = (__ldcs(parents + pa * W + w) & ~mb) | (__ldcs(parents + pb * W + w) & mb);
       }
       if (rate >= 1.0 || rate * (double)k > 8.0) {
         for (int64_t bit = 0; bit < k; ++bit) {
@@ -253,7 +255,7 @@ breed_thread_kernel(int32_t k, const uint64_t* __restrict__ parents, const doubl
       if (k % 64) v[(k - 1) >> 6] &= (1ull << (k % 64)) - 1ull;
     }
 #pragma unroll
-    for (int w = 0; w < W; ++w) children[child * W + w] = v[w];
+    for (int w = 0; w < W; ++w) __stcs(children + child * W + w, v[w]);
   }
 }
 
