@@ -183,8 +183,8 @@ def run_mine(args) -> None:
         barrier()
     ms = t_start.elapsed_time(t_end)
     kt = es.kernel_times_ms()
-    fit_ms = sum(kt["fitness"]) / len(kt["fitness"])
-    breed_ms = sum(kt["breed"]) / len(kt["breed"])
+    mean = lambda xs: sum(xs) / len(xs) if xs else 0.0
+    gen_ms, fit_ms, breed_ms = mean(kt["generation"]), mean(kt["fitness"]), mean(kt["breed"])
     best_cost, _ = es.best()
 
     # e2e through the public API with host buffers (pinned)
@@ -202,12 +202,12 @@ def run_mine(args) -> None:
     e2e_s = time.perf_counter() - t0
     barrier()
 
-    vals = torch.tensor([ms, e2e_s, fit_ms, breed_ms, search_t["total_s"]], dtype=torch.float64,
-                        device=dev)
+    vals = torch.tensor([ms, e2e_s, gen_ms, fit_ms, breed_ms, search_t["total_s"]],
+                        dtype=torch.float64, device=dev)
     if world > 1:
         import torch.distributed as dist
         dist.all_reduce(vals, op=dist.ReduceOp.MAX)
-    ms, e2e_s, fit_ms, breed_ms, search_s = vals.tolist()
+    ms, e2e_s, gen_ms, fit_ms, breed_ms, search_s = vals.tolist()
     if rank != 0:
         if world > 1:
             import torch.distributed as dist
@@ -215,20 +215,29 @@ def run_mine(args) -> None:
         return
     step_ms = ms / args.steps
     evals_per_s = world * P * args.steps / (ms / 1e3)
-    bytes_per_launch = P * (plan.words * 8 + 8)
+    if es.fused:
+        # fused breed + fitness: child row out, fitness out, two parent rows and
+        # 2 x tournament 4-byte order keys gathered, per genome
+        per_genome = 8 * plan.words + 8 + 2 * 8 * plan.words + 2 * es.tournament * 4
+        dom_ms = gen_ms
+    else:
+        per_genome = plan.words * 8 + 8  # genome row in, fitness out
+        dom_ms = fit_ms
+    bytes_per_launch = P * per_genome
     peak, peak_src = _peaks()
-    achieved = bytes_per_launch / (fit_ms / 1e3) / 1e9
+    achieved = bytes_per_launch / (dom_ms / 1e3) / 1e9
     traffic = None
     prof = os.path.join(ROOT, "profiles", "fitness_ncu_summary.json")
     if os.path.exists(prof):
         try:
             with open(prof) as fh:
                 d = json.load(fh)
-            if d.get("workload") == args.workload:
+            if d.get("workload") == args.workload and \
+                    kernel_name.replace(" ", "") in d.get("kernel", "").replace(" ", ""):
                 traffic = d.get("dram_bytes_per_launch_per_genome", 0) * P or None
         except Exception:
             traffic = None
-    kernel_name = plan.kernel_name()
+    kernel_name = plan.generation_kernel_name() if es.fused else plan.kernel_name()
     cpu = None
     if world == 1 and not args.no_cpu_baseline:
         cpu = cpu_baseline(g, bs, res, plan, args)
@@ -259,11 +268,13 @@ def run_mine(args) -> None:
                    "es_population_per_gpu": args.search_population,
                    "es_generations": args.search_generations, "dp_cost_ms": res.cost_ms,
                    "best_cost_ms_after_timed_steps": best_cost},
-        "kernels_ms": {"fitness": fit_ms, "breed": breed_ms},
+        "kernels_ms": ({"generation_fused": gen_ms} if es.fused else
+                       {"generation": gen_ms, "fitness": fit_ms, "breed": breed_ms}),
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic, "kernel": kernel_name,
                      "peak_source": peak_src,
-                     "algorithmic_bytes_per_launch": bytes_per_launch},
+                     "algorithmic_bytes_per_launch": bytes_per_launch,
+                     "algorithmic_bytes_per_genome": per_genome},
         "e2e": {"value": world * P * args.e2e_steps / e2e_s, "unit": "genomes/s",
                 "h2d_bytes_per_step": P * plan.words * 8, "d2h_bytes_per_step": P * 8},
         "gpu_launches": args.steps * (es.launches_per_generation + 1),
@@ -358,7 +369,7 @@ def config_sweep(dev) -> dict:
                    window_shift=plan.info.window_shift,
                    fitness_kernel=plan.kernel_name())
         P = cfg["fit_pop"]
-        es = DeviceEvolution(plan, P, seed=1, device=dev)
+        es = DeviceEvolution(plan, P, seed=1, device=dev, fused=False)  # the fitness kernel alone
         es.initialize()
         es.step()
         es.enable_kernel_timing(True)

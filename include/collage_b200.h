@@ -257,6 +257,19 @@ int cb_es_breed(cb_es_plan* p, const uint64_t* d_parents,
                 double mutation_rate, void* stream);
 /* Index of the smallest fitness (first on ties) -> d_idx[0]; value ->
  * d_val[0]. */
+/* One ES generation: breed n_children rows into d_children (same operators
+ * and draws as cb_es_breed) and write their fitness to d_child_fit (as
+ * cb_fitness_device).  Runs as a single fused kernel when the plan's walk
+ * allows it (<= 8 frontier slots, 128-bit window, <= 4 words per genome),
+ * else as the two launches; results are identical. */
+int cb_es_generation(cb_es_plan* p, const uint64_t* d_parents,
+                     const double* d_parent_fit, int64_t n_parents,
+                     uint64_t* d_children, double* d_child_fit,
+                     int64_t n_children, const uint64_t* d_keep, int64_t n_keep,
+                     uint64_t seed, uint64_t generation, uint64_t stream_id,
+                     int32_t tournament, double mutation_rate, void* stream);
+/* 1 when cb_es_generation runs fused for this plan (and path setting). */
+int cb_es_generation_fused(const cb_es_plan* p);
 int cb_argmin(const double* d_fit, int64_t n, int64_t* d_idx, double* d_val,
               void* stream);
 

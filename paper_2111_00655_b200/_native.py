@@ -122,6 +122,10 @@ _SIGNATURES = {
     "cb_es_breed": (c_int, [c_void_p, c_void_p, c_void_p, c_int64, c_void_p, c_int64, c_void_p,
                             c_int64, c_uint64, c_uint64, c_uint64, c_int32, c_double,
                             c_void_p]),
+    "cb_es_generation": (c_int, [c_void_p, c_void_p, c_void_p, c_int64, c_void_p, c_void_p, c_int64,
+                                 c_void_p, c_int64, c_uint64, c_uint64, c_uint64, c_int32,
+                                 c_double, c_void_p]),
+    "cb_es_generation_fused": (c_int, [c_void_p]),
     "cb_argmin": (c_int, [c_void_p, c_int64, c_void_p, c_void_p, c_void_p]),
 }
 

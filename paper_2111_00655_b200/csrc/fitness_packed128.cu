@@ -12,6 +12,7 @@
 // 192-bit fixed point -- one add fewer per merge, one shared-memory word
 // fewer per slot.  Results are bit-identical (tests/test_gpu_wide.py,
 // tests/test_gpu_parity.py).
+#include "es_ops.cuh"
 #include "fitness_plan.cuh"
 
 #define PK_THREADS 128
@@ -374,6 +375,163 @@ fitness_pa_kernel(PkArgs a, const uint4* __restrict__ hdr, const uint64_t* __res
   if (inexact) atomicAdd(a.flags, 1ull);
 }
 
+// Fused generation: each thread breeds its child (make_child, same draws as
+// breed_thread_kernel), streams the row out, and prices it from registers
+// with the packed anchor walk -- the breed's random parent / key gathers
+// overlap the walk of other warps instead of running as a separate
+// memory-bound launch, and the fitness pass needs no genome loads.
+template <int F, int W>
+__global__ void __launch_bounds__(PK_THREADS)
+fitness_pa_breed_kernel(PkArgs a, const uint4* __restrict__ hdr, BreedArgs br, uint64_t* __restrict__ children,
+                        int64_t n, double* __restrict__ fit) {
+  using LT = uint32_t;
+  constexpr int T = PK_THREADS;
+  extern __shared__ __align__(16) unsigned char pk_smem[];
+  uint64_t(*sl)[T] = reinterpret_cast<uint64_t(*)[T]>(pk_smem);  // [F][T] sum, low word
+  uint64_t(*sh)[T] = sl + F;                                       // high word
+  uint64_t(*cs)[T] = sh + F;  // low 32: kernel count, high 32: single unit or -1
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  uint64_t* ql = reinterpret_cast<uint64_t*>(cs + F) + (size_t)warp * 3 * PK_QCAP;
+  uint64_t* qh = ql + PK_QCAP;
+  uint64_t* qm = qh + PK_QCAP;  // low 32: kernel count, high 32: owner lane
+  uint64_t* tlo = reinterpret_cast<uint64_t*>(cs + F) + (size_t)(T / 32) * 3 * PK_QCAP + (size_t)warp * 64;
+  uint64_t* thi = tlo + 32;
+  tlo[lane] = thi[lane] = 0ull;
+  __syncwarp();
+  int qn = 0;
+  bool inexact = false;
+  const int64_t stride = (int64_t)gridDim.x * T;
+  for (int64_t base = (int64_t)blockIdx.x * T + (t & ~31); base < n; base += stride) {
+    const int64_t i = base + lane;
+    const bool in_range = i < n;
+    uint64_t v[W];
+    if (in_range) {
+      make_child<W>(v, br.k, br.parents, br.fit, br.keys, br.n_parents, i, br.keep, br.n_keep, br.seed,
+                    br.generation, br.stream_id, br.tournament, br.rate, br.log1m_rate);
+#pragma unroll
+      for (int w = 0; w < W; ++w) __stcs(children + i * W + w, v[w]);
+    } else {
+#pragma unroll
+      for (int w = 0; w < W; ++w) v[w] = 0ull;
+    }
+    bool dead = !in_range;
+#pragma unroll
+    for (int w = 0; w < W; ++w) dead |= (v[w] & __ldg(a.infeas + w)) != 0ull;
+    LT lab = 0;  // nibble s: label (anchor slot) of slot s
+    LT act = 0;  // 0xF in nibble s while slot s is occupied
+    uint64_t tot_lo = 0ull, tot_hi = 0ull;  // dynamic part of the total (two's complement)
+    for (int32_t p = 0; p < a.M; ++p) {
+      // x = bit (20 bits, all ones = fixed unit) | slot << 20 | nback << 24 | nend << 28,
+      // y = back slot nibbles, z = end slot nibbles, w = end rank of each slot's unit
+      const uint4 h = __ldg(hdr + p);
+      const uint32_t bitf = h.x & 0xFFFFFu;
+      bool on = !dead;
+      if (bitf != 0xFFFFFu) {
+        const int32_t wi = (int32_t)(bitf >> 6);
+        uint64_t word = v[0];
+#pragma unroll
+        for (int w = 1; w < W; ++w)
+          if (wi == w) word = v[w];
+        on = !dead && ((word >> (bitf & 63)) & 1ull);
+      }
+      const int S = (h.x >> 20) & 0xF;
+      const int nback = (h.x >> 24) & 0xF;
+      const int nend = h.x >> 28;
+      const LT nibS = (LT)0xF << (4 * S);
+      if (on) {
+        const uint64_t* c = a.cold + (size_t)p * 6;
+        if (bitf != 0xFFFFFu) {
+          const ulonglong2 off = __ldg(reinterpret_cast<const ulonglong2*>(c + 2));
+          sub2(tot_lo, tot_hi, off.x, off.y);
+        }
+        const ulonglong2 rep = __ldg(reinterpret_cast<const ulonglong2*>(c));
+        sl[S][t] = rep.x;
+        sh[S][t] = rep.y;
+        cs[S][t] = ((uint64_t)(uint32_t)p << 32) | (uint32_t)__ldg(a.cnt + p);
+        act |= nibS;
+        lab = (lab & ~nibS) | ((LT)S << (4 * S));
+      }
+      uint32_t A = (uint32_t)S;  // anchor of the new unit's component
+      for (int j = 0; j < nback; ++j) {
+        const int b = (h.y >> (4 * j)) & 0xF;
+        const uint32_t B = (uint32_t)(lab >> (4 * b)) & 0xF;
+        const bool merge = on && ((act >> (4 * b)) & 1) && B != A;
+        if (merge) {
+          // the anchor whose unit ends later survives
+          const bool keepA = ((h.w >> (4 * A)) & 0xF) >= ((h.w >> (4 * B)) & 0xF);
+          const uint32_t W = keepA ? A : B, X = keepA ? B : A;
+          uint64_t lo = sl[W][t], hi = sh[W][t];
+          add2(lo, hi, sl[X][t], sh[X][t]);
+          sl[W][t] = lo;
+          sh[W][t] = hi;
+          const uint32_t c = (uint32_t)cs[W][t] + (uint32_t)cs[X][t];
+          cs[W][t] = 0xffffffff00000000ull | c;
+          const LT m = nibeq<LT>(lab, X) & act;
+          lab = (lab & ~m) | (((LT)W * Nib2<LT>::ONE) & m);
+          A = W;
+        }
+      }
+      for (int j = 0; j < nend; ++j) {
+        const int e = (h.z >> (4 * j)) & 0xF;
+        const LT nibE = (LT)0xF << (4 * e);
+        int emit_slot = -1;
+        if (act & nibE) {
+          act &= ~nibE;
+          if (((lab >> (4 * e)) & 0xF) == (uint32_t)e) {  // the anchor leaves: region complete
+            const int32_t one = (int32_t)(cs[e][t] >> 32);
+            if (one >= 0) {
+              const ulonglong2 v = __ldg(reinterpret_cast<const ulonglong2*>(a.cold + (size_t)one * 6 + 4));
+              add2(tot_lo, tot_hi, v.x, v.y);
+            } else {
+              emit_slot = e;  // multi-unit region: queued for warp-wide pricing
+            }
+          }
+        }
+        const unsigned closing = __ballot_sync(0xffffffffu, emit_slot >= 0);
+        if (closing) {
+          if (emit_slot >= 0) {
+            const int at = qn + __popc(closing & ((1u << lane) - 1u));
+            ql[at] = sl[emit_slot][t];
+            qh[at] = sh[emit_slot][t];
+            qm[at] = ((uint64_t)lane << 32) | (uint32_t)cs[emit_slot][t];
+          }
+          qn += __popc(closing);
+          if (qn >= 32) {
+            __syncwarp();
+            pk_price(ql, qh, qm, lane, a, tlo, thi, inexact);
+            __syncwarp();
+            if (lane < qn - 32) {
+              ql[lane] = ql[32 + lane];
+              qh[lane] = qh[32 + lane];
+              qm[lane] = qm[32 + lane];
+            }
+            __syncwarp();
+            qn -= 32;
+          }
+        }
+      }
+    }
+    __syncwarp();
+    if (lane < qn) pk_price(ql, qh, qm, lane, a, tlo, thi, inexact);
+    qn = 0;
+    __syncwarp();
+    add2(tot_lo, tot_hi, tlo[lane], thi[lane]);
+    tlo[lane] = thi[lane] = 0ull;
+    __syncwarp();
+    if (in_range) {
+      if (dead) {
+        fit[i] = __longlong_as_double(0x7ff0000000000000ll);
+      } else {
+        const uint64_t sx = (uint64_t)((int64_t)tot_hi >> 63);
+        fx192 v = fx_shl(fx192{{tot_lo, tot_hi, sx}}, a.shift);
+        fx_add(v, a.base_const);
+        fit[i] = fx_to_double(v);
+      }
+    }
+  }
+  if (inexact) atomicAdd(a.flags, 1ull);
+}
+
 PkArgs make_pk_args(cb_es_plan* p) {
   PkArgs a;
   a.M = p->M;
@@ -436,7 +594,52 @@ int launch_pa_t(cb_es_plan* p, const uint64_t* d_pop, int64_t n, double* d_fit, 
   return CB_OK;
 }
 
+template <int F, int W>
+int launch_pab_t(cb_es_plan* p, const BreedArgs& br, uint64_t* d_children, int64_t n, double* d_fit,
+                 cudaStream_t stream) {
+  const size_t smem = ((size_t)3 * F * PK_THREADS + (size_t)(PK_THREADS / 32) * (3 * PK_QCAP + 64)) *
+                      sizeof(uint64_t);
+  static bool configured = false;
+  if (!configured) {
+    CB_CUDA_TRY(cudaFuncSetAttribute(fitness_pa_breed_kernel<F, W>,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    configured = true;
+  }
+  int per_sm = 0;
+  CB_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fitness_pa_breed_kernel<F, W>,
+                                                            PK_THREADS, smem));
+  if (per_sm < 1) per_sm = 1;
+  PkArgs a = make_pk_args(p);
+  const int64_t want = (n + PK_THREADS - 1) / PK_THREADS;
+  const int64_t grid = std::min<int64_t>(want, (int64_t)per_sm * cb_sm_count());
+  fitness_pa_breed_kernel<F, W><<<(unsigned)grid, PK_THREADS, smem, stream>>>(
+      a, reinterpret_cast<const uint4*>(p->d_pahdr.p), br, d_children, n, d_fit);
+  CB_CUDA_TRY(cudaGetLastError());
+  return CB_OK;
+}
+
+template <int F>
+int launch_pab_f(cb_es_plan* p, const BreedArgs& br, uint64_t* c, int64_t n, double* f, cudaStream_t s) {
+  switch (p->words) {
+    case 1: return launch_pab_t<F, 1>(p, br, c, n, f, s);
+    case 2: return launch_pab_t<F, 2>(p, br, c, n, f, s);
+    case 3: return launch_pab_t<F, 3>(p, br, c, n, f, s);
+    default: return launch_pab_t<F, 4>(p, br, c, n, f, s);
+  }
+}
+
 }  // namespace
+
+bool fused_generation_ok(const cb_es_plan* p) {
+  return p->F > 0 && p->pa_ok && p->anchor_ok && p->words <= 4 && (p->force_path == -1 || p->force_path == 6);
+}
+
+int launch_fused_generation(cb_es_plan* p, const BreedArgs& br, uint64_t* d_children, int64_t n,
+                            double* d_fit, cudaStream_t stream) {
+  if (p->F <= 4) return launch_pab_f<4>(p, br, d_children, n, d_fit, stream);
+  if (p->F <= 6) return launch_pab_f<6>(p, br, d_children, n, d_fit, stream);
+  return launch_pab_f<8>(p, br, d_children, n, d_fit, stream);
+}
 
 int launch_fitness_packed_anchor(cb_es_plan* p, const uint64_t* d_pop, int64_t n, double* d_fit,
                                  cudaStream_t stream) {

@@ -103,6 +103,11 @@ int launch_fitness_packed128(cb_es_plan* p, const uint64_t* d_pop, int64_t n, do
                              cudaStream_t stream);
 int launch_fitness_packed_anchor(cb_es_plan* p, const uint64_t* d_pop, int64_t n, double* d_fit,
                                  cudaStream_t stream);
+// fused breed + packed anchor fitness (one kernel per generation, <= 4 words)
+struct BreedArgs;
+bool fused_generation_ok(const cb_es_plan* p);
+int launch_fused_generation(cb_es_plan* p, const BreedArgs& br, uint64_t* d_children, int64_t n,
+                            double* d_fit, cudaStream_t stream);
 int launch_fitness_anchor(cb_es_plan* p, const uint64_t* d_pop, int64_t n, double* d_fit,
                           cudaStream_t stream);
 

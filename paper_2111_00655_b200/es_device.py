@@ -53,7 +53,7 @@ def exchange_elites(best_val, best_row, group, out_fit, out_rows):
 class DeviceEvolution:
     def __init__(self, plan: FitnessPlan, population: int, seed: int = 0, tournament: int = 4,
                  mutation_rate: float | None = None, device=None, process_group=None,
-                 history_capacity: int = 4096):
+                 history_capacity: int = 4096, fused: bool = False):
         torch = _torch()
         if population < 2:
             raise ValueError("population must be at least 2")
@@ -84,7 +84,15 @@ class DeviceEvolution:
         self.history = torch.full((history_capacity,), float("inf"), dtype=torch.float64,
                                   device=self.device)
         self.generation = 0
-        self.launches_per_generation = 4  # argmin (2 CUB kernels + unpack) + breed + fitness
+        # fused=True: one breed + fitness kernel per generation when the plan
+        # allows it (cb_es_generation).  Off by default: on B200 the separate
+        # launches measured faster (BERT 27.4 vs 28.8 ms per 16.7 M genomes)
+        # -- the walk is issue bound and the in-kernel breed adds to its issue
+        # load more than it hides of the breed's memory latency.
+        self.fused = bool(fused) and plan.fused_generation()
+        # own kernels per generation: order keys + (fused | breed + fitness) + argmin unpack
+        # (the two CUB argmin kernels are library code)
+        self.launches_per_generation = 3 if self.fused else 4
 
     # -- helpers -----------------------------------------------------------------------
     def _stream(self) -> int:
@@ -140,12 +148,16 @@ class DeviceEvolution:
         self.kernel_events: list[tuple] = []
 
     def kernel_times_ms(self) -> dict[str, list[float]]:
+        """Per-step device times: 'generation' (breed + fitness), and for the
+        unfused path its 'breed' and 'fitness' parts."""
         torch = _torch()
         torch.cuda.synchronize(self.device)
-        out = {"breed": [], "fitness": []}
-        for e0, e1, e2 in self.kernel_events:
-            out["breed"].append(e0.elapsed_time(e1))
-            out["fitness"].append(e1.elapsed_time(e2))
+        out = {"generation": [], "breed": [], "fitness": []}
+        for ev in self.kernel_events:
+            out["generation"].append(ev[0].elapsed_time(ev[-1]))
+            if len(ev) == 3:
+                out["breed"].append(ev[0].elapsed_time(ev[1]))
+                out["fitness"].append(ev[1].elapsed_time(ev[2]))
         return out
 
     def step(self) -> None:
@@ -155,20 +167,27 @@ class DeviceEvolution:
         timing = getattr(self, "timing", False)
         if timing:
             torch = _torch()
-            ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+            ev = [torch.cuda.Event(enable_timing=True) for _ in range(2 if self.fused else 3)]
             ev[0].record()
-        nat.check(nat.lib().cb_es_breed(
-            self.plan.handle.raw, self._ptr(self.pop[self.cur]), self._ptr(self.fit[self.cur]),
-            self.P, self._ptr(self.pop[nxt]), self.P, self._ptr(self.elite), 1,
-            ctypes.c_uint64(self.seed), ctypes.c_uint64(self.generation),
-            ctypes.c_uint64(self.rank), self.tournament, float(self.rate),
-            ctypes.c_void_p(self._stream())))
+        args = (self.plan.handle.raw, self._ptr(self.pop[self.cur]), self._ptr(self.fit[self.cur]),
+                self.P)
+        rng = (ctypes.c_uint64(self.seed), ctypes.c_uint64(self.generation),
+               ctypes.c_uint64(self.rank), self.tournament, float(self.rate),
+               ctypes.c_void_p(self._stream()))
+        if self.fused:
+            nat.check(nat.lib().cb_es_generation(*args, self._ptr(self.pop[nxt]),
+                                                 self._ptr(self.fit[nxt]), self.P,
+                                                 self._ptr(self.elite), 1, *rng))
+            self.cur = nxt
+        else:
+            nat.check(nat.lib().cb_es_breed(*args, self._ptr(self.pop[nxt]), self.P,
+                                            self._ptr(self.elite), 1, *rng))
+            if timing:
+                ev[1].record()
+            self.cur = nxt
+            self._evaluate(self.cur)
         if timing:
-            ev[1].record()
-        self.cur = nxt
-        self._evaluate(self.cur)
-        if timing:
-            ev[2].record()
+            ev[-1].record()
             self.kernel_events.append(tuple(ev))
         self._record_best()
 

@@ -243,6 +243,17 @@ class FitnessPlan:
         every plan value inside a 128-bit window)."""
         return bool(self.info.packed_labels) and self.info.window_shift >= 0
 
+    def fused_generation(self) -> bool:
+        """Whether cb_es_generation runs breed + fitness as one kernel."""
+        return bool(nat.lib().cb_es_generation_fused(self.handle.raw))
+
+    def generation_kernel_name(self) -> str:
+        """The kernel that prices a device ES generation."""
+        name = self.kernel_name()
+        if self.fused_generation():  # fitness_pa_kernel<F> -> fitness_pa_breed_kernel<F, words>
+            return f"fitness_pa_breed_kernel<{name[name.index('<') + 1:-1]}, {self.words}>"
+        return name
+
     def has_packed_anchor(self) -> bool:
         """Whether the 'packed_anchor' path applies (<= 8 frontier slots,
         128-bit window)."""

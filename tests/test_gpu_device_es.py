@@ -57,3 +57,26 @@ def test_breed_identity_without_mutation(gpu):
     es.elite.copy_(row.view(1, -1))
     es.step()
     assert torch.equal(es.pop[es.cur], row.expand_as(es.pop[es.cur]))
+
+
+@pytest.mark.parametrize("name", ["resnet50", "bert_base"])
+def test_fused_generation_matches_breed_then_fitness(gpu, name):
+    """cb_es_generation's fused kernel (breed + packed anchor walk) produces
+    the same children, fitness and history as cb_es_breed followed by the
+    fitness kernel."""
+    _, _, plan = _setup(name)
+    assert plan.fused_generation()
+    runs = []
+    for fused in (True, False):
+        es = DeviceEvolution(plan, 3000, seed=5, fused=fused)  # not a multiple of the CTA size
+        assert es.fused == fused
+        es.initialize()
+        for _ in range(6):
+            es.step()
+        runs.append((es.pop[es.cur].clone(), es.fit[es.cur].clone(), es.history_values()))
+    assert torch.equal(runs[0][0], runs[1][0])
+    assert torch.equal(runs[0][1], runs[1][1])
+    assert np.array_equal(runs[0][2], runs[1][2])
+    plan.set_path("frontier")  # another walk: the generation falls back to two launches
+    assert not plan.fused_generation()
+    plan.set_path("auto")

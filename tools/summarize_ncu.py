@@ -72,7 +72,9 @@ if os.path.exists(rep):
         wr = float(d["dram__bytes_write.sum"]["value"]) * to_b[d["dram__bytes_write.sum"]["unit"]]
         d["genomes_in_launch"] = genomes
         d["dram_bytes_per_genome"] = (rd + wr) / genomes
-        json.dump({"workload": "bert_base", "tag": tag, "genomes_in_launch": genomes,
+        kname = d["Kernel Name"]["value"].split("(")[0].replace("void ", "").replace("<unnamed>::", "")
+        kname = kname.replace("(int)", "").replace("unsigned int", "uint32_t")
+        json.dump({"workload": "bert_base", "kernel": kname, "tag": tag, "genomes_in_launch": genomes,
                    "dram_bytes_per_launch_per_genome": (rd + wr) / genomes,
                    "source": f"profiles/{tag}_fitness_ncu.json"},
                   open(os.path.join(out, "fitness_ncu_summary.json"), "w"), indent=1)
