@@ -230,7 +230,10 @@ fitness_packed128_kernel(PkArgs a, const uint64_t* __restrict__ pop, int64_t n, 
 // ends last (the header's end-rank nibbles order the slots' current units by
 // their last neighbour), so a non-anchor release is a bit clear and an
 // anchor release closes the region -- no member test, no data move.
-template <int F>
+// W in 1..4: the genome's words are held in registers and loaded one genome
+// ahead (the next row's loads overlap the current walk); W = 0 loads words
+// on demand (longer genomes).
+template <int F, int W>
 __global__ void __launch_bounds__(PK_THREADS)
 fitness_pa_kernel(PkArgs a, const uint4* __restrict__ hdr, const uint64_t* __restrict__ pop, int64_t n,
                   double* __restrict__ fit) {
@@ -251,13 +254,31 @@ fitness_pa_kernel(PkArgs a, const uint4* __restrict__ hdr, const uint64_t* __res
   int qn = 0;
   bool inexact = false;
   const int64_t stride = (int64_t)gridDim.x * T;
+  constexpr int WR = W > 0 ? W : 1;
+  uint64_t pre[WR];
+  if (W > 0) {
+    const int64_t i0 = (int64_t)blockIdx.x * T + t;
+#pragma unroll
+    for (int w = 0; w < WR; ++w) pre[w] = i0 < n ? __ldcs(pop + i0 * W + w) : 0ull;
+  }
   for (int64_t base = (int64_t)blockIdx.x * T + (t & ~31); base < n; base += stride) {
     const int64_t i = base + lane;
     const bool in_range = i < n;
     const uint64_t* gen = pop + (in_range ? i : 0) * a.words;
     bool dead = !in_range;
-    if (in_range)
+    uint64_t cur[WR];
+    if (W > 0) {
+#pragma unroll
+      for (int w = 0; w < WR; ++w) {
+        cur[w] = pre[w];
+        dead |= (cur[w] & __ldg(a.infeas + w)) != 0ull;
+      }
+      const int64_t inext = i + stride;  // prefetch the next genome of this thread
+#pragma unroll
+      for (int w = 0; w < WR; ++w) pre[w] = inext < n ? __ldcs(pop + inext * W + w) : 0ull;
+    } else if (in_range) {
       for (int32_t w = 0; w < a.words; ++w) dead |= (__ldg(gen + w) & __ldg(a.infeas + w)) != 0ull;
+    }
     LT lab = 0;  // nibble s: label (anchor slot) of slot s
     LT act = 0;  // 0xF in nibble s while slot s is occupied
     uint64_t tot_lo = 0ull, tot_hi = 0ull;  // dynamic part of the total (two's complement)
@@ -271,8 +292,16 @@ fitness_pa_kernel(PkArgs a, const uint4* __restrict__ hdr, const uint64_t* __res
       bool on = !dead;
       if (bitf != 0xFFFFFu) {
         const int32_t wi = (int32_t)(bitf >> 6);
-        if (wi != cached_word) {
-          word = dead ? 0ull : __ldg(gen + wi);
+        if (wi != cached_word) {  // warp uniform: the lanes walk the same program
+          if (W > 0) {
+            word = cur[0];
+#pragma unroll
+            for (int w = 1; w < WR; ++w)
+              if (wi == w) word = cur[w];
+            if (dead) word = 0ull;
+          } else {
+            word = dead ? 0ull : __ldg(gen + wi);
+          }
           cached_word = wi;
         }
         on = (word >> (bitf & 63)) & 1ull;
@@ -572,26 +601,37 @@ int launch_pk_t(cb_es_plan* p, const uint64_t* d_pop, int64_t n, double* d_fit, 
   return CB_OK;
 }
 
-template <int F>
+template <int F, int W>
 int launch_pa_t(cb_es_plan* p, const uint64_t* d_pop, int64_t n, double* d_fit, cudaStream_t stream) {
   const size_t smem = ((size_t)3 * F * PK_THREADS + (size_t)(PK_THREADS / 32) * (3 * PK_QCAP + 64)) *
                       sizeof(uint64_t);
   static bool configured = false;
   if (!configured) {
-    CB_CUDA_TRY(cudaFuncSetAttribute(fitness_pa_kernel<F>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    CB_CUDA_TRY(cudaFuncSetAttribute(fitness_pa_kernel<F, W>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      (int)smem));
     configured = true;
   }
   int per_sm = 0;
-  CB_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fitness_pa_kernel<F>, PK_THREADS, smem));
+  CB_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fitness_pa_kernel<F, W>, PK_THREADS, smem));
   if (per_sm < 1) per_sm = 1;
   PkArgs a = make_pk_args(p);
   const int64_t want = (n + PK_THREADS - 1) / PK_THREADS;
   const int64_t grid = std::min<int64_t>(want, (int64_t)per_sm * cb_sm_count());
-  fitness_pa_kernel<F><<<(unsigned)grid, PK_THREADS, smem, stream>>>(
+  fitness_pa_kernel<F, W><<<(unsigned)grid, PK_THREADS, smem, stream>>>(
       a, reinterpret_cast<const uint4*>(p->d_pahdr.p), d_pop, n, d_fit);
   CB_CUDA_TRY(cudaGetLastError());
   return CB_OK;
+}
+
+template <int F>
+int launch_pa_w(cb_es_plan* p, const uint64_t* d_pop, int64_t n, double* d_fit, cudaStream_t stream) {
+  switch (p->words) {
+    case 1: return launch_pa_t<F, 1>(p, d_pop, n, d_fit, stream);
+    case 2: return launch_pa_t<F, 2>(p, d_pop, n, d_fit, stream);
+    case 3: return launch_pa_t<F, 3>(p, d_pop, n, d_fit, stream);
+    case 4: return launch_pa_t<F, 4>(p, d_pop, n, d_fit, stream);
+    default: return launch_pa_t<F, 0>(p, d_pop, n, d_fit, stream);
+  }
 }
 
 template <int F, int W>
@@ -643,9 +683,9 @@ int launch_fused_generation(cb_es_plan* p, const BreedArgs& br, uint64_t* d_chil
 
 int launch_fitness_packed_anchor(cb_es_plan* p, const uint64_t* d_pop, int64_t n, double* d_fit,
                                  cudaStream_t stream) {
-  if (p->F <= 4) return launch_pa_t<4>(p, d_pop, n, d_fit, stream);
-  if (p->F <= 6) return launch_pa_t<6>(p, d_pop, n, d_fit, stream);
-  return launch_pa_t<8>(p, d_pop, n, d_fit, stream);
+  if (p->F <= 4) return launch_pa_w<4>(p, d_pop, n, d_fit, stream);
+  if (p->F <= 6) return launch_pa_w<6>(p, d_pop, n, d_fit, stream);
+  return launch_pa_w<8>(p, d_pop, n, d_fit, stream);
 }
 
 int launch_fitness_packed128(cb_es_plan* p, const uint64_t* d_pop, int64_t n, double* d_fit,
