@@ -155,7 +155,7 @@ fitness_anchor_kernel(AnArgs a, const uint64_t* __restrict__ pop, int64_t n, dou
     bool ovf = false;
     X128 total = {0ull, 0ull};
     int32_t cached_word = -1;
-    uint64_t word = 0ull;
+    uint64_t word = 0ull, next_word = a.words > 0 ? __ldg(gen) : 0ull;
     for (int32_t p = 0; p < a.M; ++p) {
       const AHot* hp = a.hot + p;
       const uint4 h0 = __ldg(reinterpret_cast<const uint4*>(hp));
@@ -169,8 +169,10 @@ fitness_anchor_kernel(AnArgs a, const uint64_t* __restrict__ pop, int64_t n, dou
       bool on = !dead;
       if (bit >= 0) {
         const int32_t wi = bit >> 6;
-        if (wi != cached_word) {
-          word = dead ? 0ull : __ldg(gen + wi);
+        if (wi != cached_word) {  // warp uniform; the next word is loaded one word ahead
+          word = wi == cached_word + 1 ? next_word : __ldg(gen + wi);
+          if (dead) word = 0ull;
+          next_word = wi + 1 < a.words ? __ldg(gen + wi + 1) : 0ull;
           cached_word = wi;
         }
         on = (word >> (bit & 63)) & 1ull;

@@ -283,7 +283,7 @@ fitness_pa_kernel(PkArgs a, const uint4* __restrict__ hdr, const uint64_t* __res
     LT act = 0;  // 0xF in nibble s while slot s is occupied
     uint64_t tot_lo = 0ull, tot_hi = 0ull;  // dynamic part of the total (two's complement)
     int32_t cached_word = -1;
-    uint64_t word = 0;
+    uint64_t word = 0, next_word = W == 0 && a.words > 0 ? __ldg(gen) : 0ull;
     for (int32_t p = 0; p < a.M; ++p) {
       // x = bit (20 bits, all ones = fixed unit) | slot << 20 | nback << 24 | nend << 28,
       // y = back slot nibbles, z = end slot nibbles, w = end rank of each slot's unit
@@ -299,8 +299,10 @@ fitness_pa_kernel(PkArgs a, const uint4* __restrict__ hdr, const uint64_t* __res
             for (int w = 1; w < WR; ++w)
               if (wi == w) word = cur[w];
             if (dead) word = 0ull;
-          } else {
-            word = dead ? 0ull : __ldg(gen + wi);
+          } else {  // long genomes: the next word is loaded one word ahead
+            word = wi == cached_word + 1 ? next_word : __ldg(gen + wi);
+            if (dead) word = 0ull;
+            next_word = wi + 1 < a.words ? __ldg(gen + wi + 1) : 0ull;
           }
           cached_word = wi;
         }
