@@ -156,10 +156,21 @@ fitness_anchor_kernel(AnArgs a, const uint64_t* __restrict__ pop, int64_t n, dou
     X128 total = {0ull, 0ull};
     int32_t cached_word = -1;
     uint64_t word = 0ull, next_word = a.words > 0 ? __ldg(gen) : 0ull;
+    // the step header and the unit's removed-kernel term are loaded one step
+    // ahead: a wide program lives in L2, not L1, and its loads head every
+    // step's dependency chain
+    uint4 nh0 = __ldg(reinterpret_cast<const uint4*>(a.hot));
+    uint4 nh1 = __ldg(reinterpret_cast<const uint4*>(a.hot) + 1);
+    X128 noff = ld_x(a.cold + 2);
     for (int32_t p = 0; p < a.M; ++p) {
       const AHot* hp = a.hot + p;
-      const uint4 h0 = __ldg(reinterpret_cast<const uint4*>(hp));
-      const uint4 h1 = __ldg(reinterpret_cast<const uint4*>(hp) + 1);
+      const uint4 h0 = nh0, h1 = nh1;
+      const X128 off = noff;
+      if (p + 1 < a.M) {
+        nh0 = __ldg(reinterpret_cast<const uint4*>(hp + 1));
+        nh1 = __ldg(reinterpret_cast<const uint4*>(hp + 1) + 1);
+        noff = ld_x(a.cold + (size_t)(p + 1) * 6 + 2);
+      }
       const int32_t bit = (int32_t)h0.x;
       const int S = h0.z & 0xff;
       const int nback = (h0.z >> 8) & 0xff;
@@ -180,7 +191,7 @@ fitness_anchor_kernel(AnArgs a, const uint64_t* __restrict__ pop, int64_t n, dou
       if (lane == 0) endw[S] = (int32_t)h0.y;
       __syncwarp();
       if (on) {
-        if (bit >= 0) x_sub(total, ld_x(a.cold + (size_t)p * 6 + 2));
+        if (bit >= 0) x_sub(total, off);
         act |= 1ull << S;
         lab[S * T] = L_ANCHOR | L_SINGLE | (uint32_t)p;
       }
