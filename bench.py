@@ -303,6 +303,17 @@ def _oracle_case(g, bs):
     return OracleCase(json.loads(json.dumps(case)))
 
 
+def _random_packed(n: int, k: int, seed: int):
+    """n random genomes of k bits as packed uint64 rows (padding bits clear)."""
+    import numpy as np
+    words = max(1, (k + 63) // 64)
+    rows = np.random.default_rng(seed).integers(0, 1 << 63, size=(n, words), dtype=np.uint64)
+    rows ^= np.random.default_rng(seed + 1).integers(0, 2, size=(n, words), dtype=np.uint64) << np.uint64(63)
+    if k % 64:
+        rows[:, -1] &= np.uint64((1 << (k % 64)) - 1)
+    return rows
+
+
 def cpu_baseline(g, bs, res, plan, args) -> dict:
     """The reference algorithm restated in C (oracle) on the host cores,
     bounded sample: fitness of `sample` random genomes."""
@@ -311,15 +322,14 @@ def cpu_baseline(g, bs, res, plan, args) -> dict:
     oc.price()
     kernels = [[a.backend_pattern.order, a.root, sorted(a.nodes)] for a in res.placement.assignments]
     threads = os.cpu_count() or 1
-    rng = np.random.default_rng(1)
     sample = args.cpu_sample
-    pop = rng.integers(0, 2, size=(sample, plan.k), dtype=np.uint8)
+    pop = _random_packed(sample, plan.k, 1)
     oc.fitness(kernels, bs.graph_backend, pop[:64], threads=threads)
     t0 = time.perf_counter()
     oc.fitness(kernels, bs.graph_backend, pop, threads=threads)
     dt = time.perf_counter() - t0
     return {"value": sample / dt, "unit": "genomes/s", "cores": threads, "kind": "port",
-            "sample": f"{sample} random genomes of the {args.workload} DP placement "
+            "sample": f"{sample} random packed genomes of the {args.workload} DP placement "
                       f"({plan.k} bits), oracle/oracle.c or_fitness with {threads} OpenMP threads"}
 
 
@@ -425,14 +435,12 @@ def run_reference(args) -> None:
           if kind == "graph_inference_library"}
     order_backend = [bp.backend for bp in bs.registry.patterns]
     k = sum(1 for o, _, _ in kernels if order_backend[o] not in gb)
-    rng = np.random.default_rng(2)
-    sample = args.cpu_sample
+    sample = args.ref_sample
     for _ in range(args.warmup):
-        oc.fitness(kernels, bs.graph_backend, rng.integers(0, 2, size=(256, k), dtype=np.uint8),
-                   threads=threads)
+        oc.fitness(kernels, bs.graph_backend, _random_packed(256, k, 2), threads=threads)
     times = []
-    for _ in range(args.steps):
-        pop = rng.integers(0, 2, size=(sample, k), dtype=np.uint8)
+    for step in range(args.steps):
+        pop = _random_packed(sample, k, 100 + step)  # packed rows, as the GPU arm reads them
         t0 = time.perf_counter()
         oc.fitness(kernels, bs.graph_backend, pop, threads=threads)
         times.append(time.perf_counter() - t0)
@@ -455,7 +463,7 @@ def run_reference(args) -> None:
                    "nodes": len(g.nodes), "genome_bits": k, "dp_status": status,
                    "dp_cost_ms": cost, "dp_s": dp_s},
         "cpu_baseline": {"value": value, "unit": "genomes/s", "cores": threads, "kind": "port",
-                         "sample": f"{sample} random genomes per step, oracle/oracle.c "
+                         "sample": f"{sample} random packed genomes per step, oracle/oracle.c "
                                    f"(reference algorithm restated in C), {threads} threads"},
         "e2e": {"value": value, "unit": "genomes/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
@@ -474,7 +482,10 @@ def main() -> None:
     ap.add_argument("--search-population", type=int, default=65536)
     ap.add_argument("--search-generations", type=int, default=50)
     ap.add_argument("--e2e-steps", type=int, default=5)
-    ap.add_argument("--cpu-sample", type=int, default=200_000)
+    ap.add_argument("--cpu-sample", type=int, default=2_000_000,
+                    help="genomes in the CPU-baseline sample (~10 s of CPU work on BERT)")
+    ap.add_argument("--ref-sample", type=int, default=400_000,
+                    help="genomes per step of the --impl reference arm")
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-configs", action="store_true", help="skip the five-config sweep")
