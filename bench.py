@@ -371,6 +371,24 @@ def config_sweep(dev) -> dict:
             torch.cuda.synchronize(dev)
             t2 = time.perf_counter()
         best, _ = es.best()
+        # the matcher and pricing on their own (table cache cleared), host wall with syncs
+        from paper_2111_00655_b200.cost import price_matches
+        bs.registry._tables.clear()
+        torch.cuda.synchronize(dev)
+        m0 = time.perf_counter()
+        table = bs.registry.match_table(g)
+        torch.cuda.synchronize(dev)
+        m1 = time.perf_counter()
+        price_matches(bs.measurer, bs.registry, table)
+        torch.cuda.synchronize(dev)
+        m2 = time.perf_counter()
+        row.update(matcher={"anchors": len(g.nodes), "patterns": len(bs.registry.patterns),
+                            "matches": int(table.n_matches), "wall_ms": 1e3 * (m1 - m0),
+                            "anchors_per_s": len(g.nodes) / (m1 - m0)},
+                   pricing={"matches": int(table.n_matches), "wall_ms": 1e3 * (m2 - m1)},
+                   dp={"nodes": len(g.nodes), "device_ms": res.device["device_ms"],
+                       "levels": res.device["levels"], "launches": res.device["launches"],
+                       "nodes_per_s": len(g.nodes) / (res.device["device_ms"] / 1e3)})
         row.update(search_wall_s=t2 - t0, dp_s=t1 - t0, dp_device_ms=res.device["device_ms"],
                    es_population=cfg["search_pop"], es_generations=cfg["gens"],
                    dp_kernels=len(res.placement), dp_cost_ms=res.cost_ms, es_best_cost_ms=best,
