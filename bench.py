@@ -373,19 +373,24 @@ def config_sweep(dev) -> dict:
         best, _ = es.best()
         # the matcher and pricing on their own (table cache cleared), host wall with syncs
         from paper_2111_00655_b200.cost import price_matches
-        bs.registry._tables.clear()
-        torch.cuda.synchronize(dev)
-        m0 = time.perf_counter()
-        table = bs.registry.match_table(g)
-        torch.cuda.synchronize(dev)
-        m1 = time.perf_counter()
-        price_matches(bs.measurer, bs.registry, table)
-        torch.cuda.synchronize(dev)
-        m2 = time.perf_counter()
+        tm, tpr = [], []
+        for _ in range(3):  # best of 3 (the first pays buffer allocation)
+            bs.registry._tables.clear()
+            torch.cuda.synchronize(dev)
+            m0 = time.perf_counter()
+            table = bs.registry.match_table(g)
+            torch.cuda.synchronize(dev)
+            m1 = time.perf_counter()
+            price_matches(bs.measurer, bs.registry, table)
+            torch.cuda.synchronize(dev)
+            m2 = time.perf_counter()
+            tm.append(m1 - m0)
+            tpr.append(m2 - m1)
         row.update(matcher={"anchors": len(g.nodes), "patterns": len(bs.registry.patterns),
-                            "matches": int(table.n_matches), "wall_ms": 1e3 * (m1 - m0),
-                            "anchors_per_s": len(g.nodes) / (m1 - m0)},
-                   pricing={"matches": int(table.n_matches), "wall_ms": 1e3 * (m2 - m1)},
+                            "matches": int(table.n_matches), "wall_ms": 1e3 * min(tm),
+                            "anchors_per_s": len(g.nodes) / min(tm),
+                            "note": "host wall incl. download of the match table"},
+                   pricing={"matches": int(table.n_matches), "wall_ms": 1e3 * min(tpr)},
                    dp={"nodes": len(g.nodes), "device_ms": res.device["device_ms"],
                        "levels": res.device["levels"], "launches": res.device["launches"],
                        "nodes_per_s": len(g.nodes) / (res.device["device_ms"] / 1e3)})

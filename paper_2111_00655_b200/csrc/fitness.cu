@@ -25,6 +25,7 @@
 // region terms and removed op-kernel terms into a 192-bit total that a
 // shuffle reduction finishes and rounds once.
 #include <algorithm>
+#include <cstdio>
 #include <cstring>
 #include <numeric>
 
@@ -535,8 +536,13 @@ extern "C" const char* cb_es_plan_kernel(const cb_es_plan* p) {
   if (!p) return "";
   const bool frontier = p->F > 0 && p->force_path != 0;
   if (frontier && p->force_path == 3) return "fitness_wide_kernel";
-  if (frontier && p->pa_ok && p->anchor_ok && (p->force_path == 6 || p->force_path == -1))
-    return p->F <= 4 ? "fitness_pa_kernel<4>" : p->F <= 6 ? "fitness_pa_kernel<6>" : "fitness_pa_kernel<8>";
+  if (frontier && p->pa_ok && p->anchor_ok && (p->force_path == 6 || p->force_path == -1)) {
+    // fitness_pa_kernel<F, W>: W = genome words held in registers (0 = loaded on demand)
+    static thread_local char buf[48];
+    std::snprintf(buf, sizeof(buf), "fitness_pa_kernel<%d, %d>", p->F <= 4 ? 4 : p->F <= 6 ? 6 : 8,
+                  p->words <= 4 ? p->words : 0);
+    return buf;
+  }
   if (frontier && p->packed_ok && p->anchor_ok && (p->force_path == 5 || p->force_path == -1)) {
     static const char* pk[] = {"fitness_packed128_kernel<uint32_t, 4>", "fitness_packed128_kernel<uint32_t, 6>",
                                "fitness_packed128_kernel<uint32_t, 8>", "fitness_packed128_kernel<uint64_t, 12>",

@@ -250,8 +250,9 @@ class FitnessPlan:
     def generation_kernel_name(self) -> str:
         """The kernel that prices a device ES generation."""
         name = self.kernel_name()
-        if self.fused_generation():  # fitness_pa_kernel<F> -> fitness_pa_breed_kernel<F, words>
-            return f"fitness_pa_breed_kernel<{name[name.index('<') + 1:-1]}, {self.words}>"
+        if self.fused_generation():  # fitness_pa_kernel<F, W> -> fitness_pa_breed_kernel<F, words>
+            f = name[name.index('<') + 1:].split(',')[0]
+            return f"fitness_pa_breed_kernel<{f}, {self.words}>"
         return name
 
     def has_packed_anchor(self) -> bool:

@@ -83,3 +83,38 @@ def test_wide_kernel_agrees_on_models(gpu, name):
         plan.set_path(path)
         assert np.array_equal(plan.evaluate(genomes), want), path
     plan.set_path("auto")
+
+
+def test_plan_outside_the_128_bit_window_uses_192_bit_kernels(gpu):
+    """Costs spanning ~160 bits (1e-18 .. 1e12 ms) leave no 128-bit window:
+    the automatic path falls back to the 192-bit walks, still bit-exact."""
+    from paper_2111_00655_b200.cost import OpCost, SimMeasurer, SimProfile
+    g = workloads.random_dag(300, seed=4, ops=workloads.RANDOM_OPS, window=16)
+    bs = workloads.random_backends(g, n_backends=4, n_graph=1, seed=4)
+    profiles = {}
+    for bid, p in bs.measurer.profiles.items():
+        scale = 1e12 if bid == bs.graph_backend else 1e-18
+        profiles[bid] = SimProfile(bid, {op: OpCost(0.0, oc.overhead * scale)
+                                         for op, oc in p.op_costs.items()},
+                                   fusion_discount=p.fusion_discount, region_alpha=p.region_alpha,
+                                   region_floor=p.region_floor)
+    meas = SimMeasurer(profiles)
+    res = tp.optimize(g, bs.registry, meas, 0.01)
+    plan = tp.FitnessPlan(g, bs.registry, meas, res.placement, 0.01, bs.graph_backend,
+                          res.kernel_matches)
+    assert plan.k > 0
+    assert plan.info.window_shift == -1 and not plan.has_packed128()
+    genomes = _genomes(plan, np.random.default_rng(9), 200)
+    class _B:  # the oracle reads profiles from the backend set
+        registry, measurer = bs.registry, meas
+    oc = OracleCase(_case(g, _B, 0.01))
+    oc.price()
+    kernels = [[a.backend_pattern.order, a.root, sorted(a.nodes)] for a in res.placement.assignments]
+    want = oc.fitness(kernels, bs.graph_backend, genomes)
+    assert np.array_equal(plan.evaluate(genomes), want)
+    assert plan.kernel_name() in ("fitness_frontier2_kernel", "fitness_wide_kernel",
+                                  "fitness_frontier_kernel")
+    for path in ("unionfind", "wide"):
+        plan.set_path(path)
+        assert np.array_equal(plan.evaluate(genomes), want), path
+    plan.set_path("auto")
