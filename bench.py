@@ -227,6 +227,7 @@ def run_mine(args) -> None:
     peak, peak_src = _peaks()
     achieved = bytes_per_launch / (dom_ms / 1e3) / 1e9
     traffic = None
+    inst_per_genome = None
     prof = os.path.join(ROOT, "profiles", "fitness_ncu_summary.json")
     if os.path.exists(prof):
         try:
@@ -235,6 +236,7 @@ def run_mine(args) -> None:
             if d.get("workload") == args.workload and \
                     kernel_name.replace(" ", "") in d.get("kernel", "").replace(" ", ""):
                 traffic = d.get("dram_bytes_per_launch_per_genome", 0) * P or None
+                inst_per_genome = d.get("warp_instructions_per_genome")
         except Exception:
             traffic = None
     kernel_name = plan.generation_kernel_name() if es.fused else plan.kernel_name()
@@ -282,6 +284,18 @@ def run_mine(args) -> None:
     }
     if cpu is not None:
         line["cpu_baseline"] = cpu
+    if inst_per_genome:
+        # the bound that binds: warp-instruction issue (4 schedulers per SM, one
+        # instruction per cycle each), instructions per genome from the ncu capture
+        # of the same kernel (profiles/fitness_ncu_summary.json)
+        sms = torch.cuda.get_device_properties(dev).multi_processor_count
+        mhz = line["clocks"].get("sm_mhz") or 1965.0
+        peak_issue = sms * 4 * mhz * 1e6
+        achieved_issue = inst_per_genome * P / (dom_ms / 1e3)
+        line["issue_roofline"] = {"bound": "issue", "achieved": achieved_issue, "peak": peak_issue,
+                                  "unit": "warp instructions/s", "frac": achieved_issue / peak_issue,
+                                  "warp_instructions_per_genome": inst_per_genome,
+                                  "source": "profiles/fitness_ncu_summary.json"}
     if sweep is not None:
         line["configs"] = sweep
     print(json.dumps(line), flush=True)

@@ -74,8 +74,10 @@ if os.path.exists(rep):
         d["dram_bytes_per_genome"] = (rd + wr) / genomes
         kname = d["Kernel Name"]["value"].split("(")[0].replace("void ", "").replace("<unnamed>::", "")
         kname = kname.replace("(int)", "").replace("unsigned int", "uint32_t")
+        inst = float(d["smsp__inst_executed.sum"]["value"].replace(",", ""))
         json.dump({"workload": "bert_base", "kernel": kname, "tag": tag, "genomes_in_launch": genomes,
                    "dram_bytes_per_launch_per_genome": (rd + wr) / genomes,
+                   "warp_instructions_per_genome": inst / genomes,
                    "source": f"profiles/{tag}_fitness_ncu.json"},
                   open(os.path.join(out, "fitness_ncu_summary.json"), "w"), indent=1)
     json.dump(d, open(os.path.join(out, f"{tag}_fitness_ncu.json"), "w"), indent=1)
