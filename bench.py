@@ -226,6 +226,7 @@ def run_mine(args) -> None:
     bytes_per_launch = P * per_genome
     peak, peak_src = _peaks()
     achieved = bytes_per_launch / (dom_ms / 1e3) / 1e9
+    kernel_name = plan.generation_kernel_name() if es.fused else plan.kernel_name()
     traffic = None
     inst_per_genome = None
     prof = os.path.join(ROOT, "profiles", "fitness_ncu_summary.json")
@@ -237,9 +238,8 @@ def run_mine(args) -> None:
                     kernel_name.replace(" ", "") in d.get("kernel", "").replace(" ", ""):
                 traffic = d.get("dram_bytes_per_launch_per_genome", 0) * P or None
                 inst_per_genome = d.get("warp_instructions_per_genome")
-        except Exception:
+        except (OSError, ValueError, KeyError):
             traffic = None
-    kernel_name = plan.generation_kernel_name() if es.fused else plan.kernel_name()
     cpu = None
     if world == 1 and not args.no_cpu_baseline:
         cpu = cpu_baseline(g, bs, res, plan, args)
