@@ -118,3 +118,52 @@ def test_plan_outside_the_128_bit_window_uses_192_bit_kernels(gpu):
         plan.set_path(path)
         assert np.array_equal(plan.evaluate(genomes), want), path
     plan.set_path("auto")
+
+
+def _scaled(bs, scale_of):
+    from paper_2111_00655_b200.cost import OpCost, SimMeasurer, SimProfile
+    return SimMeasurer({bid: SimProfile(bid, {op: OpCost(oc.coeff, oc.overhead * scale_of(bid))
+                                              for op, oc in p.op_costs.items()},
+                                        fusion_discount=p.fusion_discount,
+                                        region_alpha=p.region_alpha, region_floor=p.region_floor)
+                        for bid, p in bs.measurer.profiles.items()})
+
+
+@pytest.mark.parametrize("n_rows", [1, 31, 33, 1000])
+def test_edge_plans_every_path(gpu, n_rows):
+    """Degenerate plans through every kernel path, against the oracle:
+    no genome bits (everything on the graph backend), every kernel offloadable
+    with a cheap graph backend (long regions), and odd population sizes."""
+    g = workloads.random_dag(200, seed=6, ops=workloads.RANDOM_OPS, window=12)
+    bs = workloads.random_backends(g, n_backends=4, n_graph=1, seed=6)
+    for name, scale in (("all-graph", lambda b: 1e-3 if b == bs.graph_backend else 1.0),
+                        ("cheap-graph", lambda b: 0.5 if b == bs.graph_backend else 1.0),
+                        ("no-graph", lambda b: 1e3 if b == bs.graph_backend else 1.0)):
+        meas = _scaled(bs, scale)
+        res = tp.optimize(g, bs.registry, meas, 0.01)
+        plan = tp.FitnessPlan(g, bs.registry, meas, res.placement, 0.01, bs.graph_backend,
+                              res.kernel_matches)
+        assert (plan.k == 0) == (name == "all-graph"), (name, plan.k)
+        rng = np.random.default_rng(n_rows)
+        genomes = (rng.random((n_rows, plan.k)) < 0.5).astype(np.uint8)
+
+        class _B:
+            registry, measurer = bs.registry, meas
+        oc = OracleCase(_case(g, _B, 0.01))
+        oc.price()
+        kernels = [[a.backend_pattern.order, a.root, sorted(a.nodes)]
+                   for a in res.placement.assignments]
+        want = oc.fitness(kernels, bs.graph_backend, genomes)
+        paths = ["auto", "unionfind"]
+        if plan.info.frontier_slots:
+            paths += ["wide", "anchor"] if plan.info.window_shift >= 0 else ["wide"]
+        if 0 < plan.info.frontier_slots <= 32:
+            paths += ["frontier", "frontier_smem"]
+        if plan.has_packed128():
+            paths.append("packed128")
+        if plan.has_packed_anchor():
+            paths.append("packed_anchor")
+        for path in paths:
+            plan.set_path(path)
+            assert np.array_equal(plan.evaluate(genomes), want), (name, path)
+        plan.set_path("auto")
