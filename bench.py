@@ -279,7 +279,7 @@ def run_mine(args) -> None:
                      "algorithmic_bytes_per_genome": per_genome},
         "e2e": {"value": world * P * args.e2e_steps / e2e_s, "unit": "genomes/s",
                 "h2d_bytes_per_step": P * plan.words * 8, "d2h_bytes_per_step": P * 8},
-        "gpu_launches": args.steps * (es.launches_per_generation + 1),
+        "gpu_launches": args.steps * es.launches_per_generation,
         "clocks": clocks.summary(),
     }
     if cpu is not None:
