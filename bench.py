@@ -465,7 +465,6 @@ def run_reference(args) -> None:
     status, cost, kernels = oc.dp(max_states=2_000_000)
     dp_s = time.perf_counter() - t0
     threads = os.cpu_count() or 1
-    from paper_2111_00655_b200.evolution import pack_genomes  # noqa: F401  (layout only)
     k = sum(1 for _, _, _ in kernels) if kernels else 0
     # genome length: kernels not on graph backends
     gb = {b for b, kind in [[b.id, b.kind.value] for b in bs.registry.backends.values()]

@@ -1,7 +1,6 @@
 """GPU path (libcollage_b200 through the package API) against the reference's
 golden outputs and the CPU oracle: bit-exact matches, placements and costs."""
 
-import math
 
 import numpy as np
 import pytest

@@ -9,7 +9,6 @@ GPU box).  Writes profiles/r01_reference_python.json:
   population 32, 200 generations) where the DP finishes.
 """
 import json
-import math
 import os
 import random
 import sys
