@@ -12,6 +12,8 @@
 // 192-bit fixed point -- one add fewer per merge, one shared-memory word
 // fewer per slot.  Results are bit-identical (tests/test_gpu_wide.py,
 // tests/test_gpu_parity.py).
+#include <type_traits>
+
 #include "es_ops.cuh"
 #include "fitness_plan.cuh"
 
@@ -19,6 +21,9 @@
 #define PK_QCAP 64
 
 namespace {
+
+template <int V>
+using IC = std::integral_constant<int, V>;
 
 template <typename LT>
 struct Nib2;
@@ -325,64 +330,79 @@ fitness_pa_kernel(PkArgs a, const uint4* __restrict__ hdr, const uint64_t* __res
         act |= nibS;
         lab = (lab & ~nibS) | ((LT)S << (4 * S));
       }
-      uint32_t A = (uint32_t)S;  // anchor of the new unit's component
-      for (int j = 0; j < nback; ++j) {
-        const int b = (h.y >> (4 * j)) & 0xF;
-        const uint32_t B = (uint32_t)(lab >> (4 * b)) & 0xF;
-        const bool merge = on && ((act >> (4 * b)) & 1) && B != A;
-        if (merge) {
-          // the anchor whose unit ends later survives
-          const bool keepA = ((h.w >> (4 * A)) & 0xF) >= ((h.w >> (4 * B)) & 0xF);
-          const uint32_t W = keepA ? A : B, X = keepA ? B : A;
-          uint64_t lo = sl[W][t], hi = sh[W][t];
-          add2(lo, hi, sl[X][t], sh[X][t]);
-          sl[W][t] = lo;
-          sh[W][t] = hi;
-          const uint32_t c = (uint32_t)cs[W][t] + (uint32_t)cs[X][t];
-          cs[W][t] = 0xffffffff00000000ull | c;
-          const LT m = nibeq<LT>(lab, X) & act;
-          lab = (lab & ~m) | (((LT)W * Nib2<LT>::ONE) & m);
-          A = W;
+      // back / end lists: straight-line code for the common (nback, nend)
+      // shapes (warp-uniform switch on the header), a loop otherwise
+      auto step_lists = [&](auto nb_c, auto ne_c) {
+        constexpr int NB = decltype(nb_c)::value, NE = decltype(ne_c)::value;
+        uint32_t A = (uint32_t)S;  // anchor of the new unit's component
+        for (int j = 0; j < (NB >= 0 ? NB : nback); ++j) {  // constant trip counts unroll
+          const int b = (h.y >> (4 * j)) & 0xF;
+          const uint32_t B = (uint32_t)(lab >> (4 * b)) & 0xF;
+          const bool merge = on && ((act >> (4 * b)) & 1) && B != A;
+          if (merge) {
+            // the anchor whose unit ends later survives
+            const bool keepA = ((h.w >> (4 * A)) & 0xF) >= ((h.w >> (4 * B)) & 0xF);
+            const uint32_t W = keepA ? A : B, X = keepA ? B : A;
+            uint64_t lo = sl[W][t], hi = sh[W][t];
+            add2(lo, hi, sl[X][t], sh[X][t]);
+            sl[W][t] = lo;
+            sh[W][t] = hi;
+            const uint32_t c = (uint32_t)cs[W][t] + (uint32_t)cs[X][t];
+            cs[W][t] = 0xffffffff00000000ull | c;
+            const LT m = nibeq<LT>(lab, X) & act;
+            lab = (lab & ~m) | (((LT)W * Nib2<LT>::ONE) & m);
+            A = W;
+          }
         }
-      }
-      for (int j = 0; j < nend; ++j) {
-        const int e = (h.z >> (4 * j)) & 0xF;
-        const LT nibE = (LT)0xF << (4 * e);
-        int emit_slot = -1;
-        if (act & nibE) {
-          act &= ~nibE;
-          if (((lab >> (4 * e)) & 0xF) == (uint32_t)e) {  // the anchor leaves: region complete
-            const int32_t one = (int32_t)(cs[e][t] >> 32);
-            if (one >= 0) {
-              const ulonglong2 v = __ldg(reinterpret_cast<const ulonglong2*>(a.cold + (size_t)one * 6 + 4));
-              add2(tot_lo, tot_hi, v.x, v.y);
-            } else {
-              emit_slot = e;  // multi-unit region: queued for warp-wide pricing
+        for (int j = 0; j < (NE >= 0 ? NE : nend); ++j) {
+          const int e = (h.z >> (4 * j)) & 0xF;
+          const LT nibE = (LT)0xF << (4 * e);
+          int emit_slot = -1;
+          if (act & nibE) {
+            act &= ~nibE;
+            if (((lab >> (4 * e)) & 0xF) == (uint32_t)e) {  // the anchor leaves: region complete
+              const int32_t one = (int32_t)(cs[e][t] >> 32);
+              if (one >= 0) {
+                const ulonglong2 v = __ldg(reinterpret_cast<const ulonglong2*>(a.cold + (size_t)one * 6 + 4));
+                add2(tot_lo, tot_hi, v.x, v.y);
+              } else {
+                emit_slot = e;  // multi-unit region: queued for warp-wide pricing
+              }
+            }
+          }
+          const unsigned closing = __ballot_sync(0xffffffffu, emit_slot >= 0);
+          if (closing) {
+            if (emit_slot >= 0) {
+              const int at = qn + __popc(closing & ((1u << lane) - 1u));
+              ql[at] = sl[emit_slot][t];
+              qh[at] = sh[emit_slot][t];
+              qm[at] = ((uint64_t)lane << 32) | (uint32_t)cs[emit_slot][t];
+            }
+            qn += __popc(closing);
+            if (qn >= 32) {
+              __syncwarp();
+              pk_price(ql, qh, qm, lane, a, tlo, thi, inexact);
+              __syncwarp();
+              if (lane < qn - 32) {
+                ql[lane] = ql[32 + lane];
+                qh[lane] = qh[32 + lane];
+                qm[lane] = qm[32 + lane];
+              }
+              __syncwarp();
+              qn -= 32;
             }
           }
         }
-        const unsigned closing = __ballot_sync(0xffffffffu, emit_slot >= 0);
-        if (closing) {
-          if (emit_slot >= 0) {
-            const int at = qn + __popc(closing & ((1u << lane) - 1u));
-            ql[at] = sl[emit_slot][t];
-            qh[at] = sh[emit_slot][t];
-            qm[at] = ((uint64_t)lane << 32) | (uint32_t)cs[emit_slot][t];
-          }
-          qn += __popc(closing);
-          if (qn >= 32) {
-            __syncwarp();
-            pk_price(ql, qh, qm, lane, a, tlo, thi, inexact);
-            __syncwarp();
-            if (lane < qn - 32) {
-              ql[lane] = ql[32 + lane];
-              qh[lane] = qh[32 + lane];
-              qm[lane] = qm[32 + lane];
-            }
-            __syncwarp();
-            qn -= 32;
-          }
-        }
+      };
+      switch ((nback << 4) | nend) {
+        case 0x11: step_lists(IC<1>{}, IC<1>{}); break;
+        case 0x10: step_lists(IC<1>{}, IC<0>{}); break;
+        case 0x22: step_lists(IC<2>{}, IC<2>{}); break;
+        case 0x21: step_lists(IC<2>{}, IC<1>{}); break;
+        case 0x00: step_lists(IC<0>{}, IC<0>{}); break;
+        case 0x32: step_lists(IC<3>{}, IC<2>{}); break;
+        case 0x33: step_lists(IC<3>{}, IC<3>{}); break;
+        default: step_lists(IC<-1>{}, IC<-1>{}); break;
       }
     }
     __syncwarp();
