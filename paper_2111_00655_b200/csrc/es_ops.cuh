@@ -98,6 +98,32 @@ struct BreedArgs {
   double rate, log1m_rate;
 };
 
+// Two tournaments of size TOUR (same draws and winners as the loop form:
+// first draw leads, a challenger wins only when strictly fitter).
+template <int TOUR>
+__device__ __forceinline__ void tournament_pair(Philox& rng, int64_t n_parents, const uint32_t* __restrict__ keys,
+                                                const double* __restrict__ fit, int64_t& pa, int64_t& pb) {
+  uint32_t idx[2 * TOUR], kv[2 * TOUR];
+#pragma unroll
+  for (int q = 0; q < 2 * TOUR; ++q) idx[q] = rng.below((uint32_t)n_parents);
+#pragma unroll
+  for (int q = 0; q < 2 * TOUR; ++q) kv[q] = __ldg(keys + idx[q]);
+#pragma unroll
+  for (int t = 0; t < 2; ++t) {
+    uint32_t best = idx[t * TOUR], bk = kv[t * TOUR];
+#pragma unroll
+    for (int j = 1; j < TOUR; ++j) {
+      const uint32_t i = idx[t * TOUR + j], ki = kv[t * TOUR + j];
+      if (ki < bk || (ki == bk && __ldg(fit + i) < __ldg(fit + best))) {
+        best = i;
+        bk = ki;
+      }
+    }
+    if (t == 0) pa = best;
+    else pb = best;
+  }
+}
+
 // Child row `child` of a generation into v[0..W): the kept elite rows first,
 // then tournament / crossover / mutation children (Philox keyed by seed,
 // countered by child, generation and stream).
@@ -114,21 +140,27 @@ __device__ __forceinline__ void make_child(uint64_t (&v)[W], int32_t k, const ui
     Philox rng(seed, (uint32_t)child, (uint32_t)(child >> 32) ^ (generation * 0x9E3779B9u),
                stream_id);
     int64_t pa = 0, pb = 0;
-    for (int t = 0; t < 2; ++t) {
-      // compare the 32-bit order keys (high word of the non-negative
-      // fitness, an L2-resident array), the full doubles only on a key tie
-      int64_t best = rng.below((uint32_t)n_parents);
-      uint32_t bk = __ldg(keys + best);
-      for (int j = 1; j < tournament; ++j) {
-        const int64_t i = rng.below((uint32_t)n_parents);
-        const uint32_t ki = __ldg(keys + i);
-        if (ki < bk || (ki == bk && __ldg(fit + i) < __ldg(fit + best))) {
-          best = i;
-          bk = ki;
+    // tournaments compare the 32-bit order keys (high word of the
+    // non-negative fitness, an L2-resident array), the full doubles only on a
+    // key tie; the default size draws all indices first so the key gathers
+    // are in flight together
+    if (tournament == 4) {
+      tournament_pair<4>(rng, n_parents, keys, fit, pa, pb);
+    } else {
+      for (int t = 0; t < 2; ++t) {
+        int64_t best = rng.below((uint32_t)n_parents);
+        uint32_t bk = __ldg(keys + best);
+        for (int j = 1; j < tournament; ++j) {
+          const int64_t i = rng.below((uint32_t)n_parents);
+          const uint32_t ki = __ldg(keys + i);
+          if (ki < bk || (ki == bk && __ldg(fit + i) < __ldg(fit + best))) {
+            best = i;
+            bk = ki;
+          }
         }
+        if (t == 0) pa = best;
+        else pb = best;
       }
-      if (t == 0) pa = best;
-      else pb = best;
     }
     int64_t ci = 0, cj = 0;
     if (k >= 2) {
