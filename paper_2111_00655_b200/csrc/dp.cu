@@ -23,6 +23,7 @@
 // the smallest kernel of the symmetric difference, found by walking the two
 // candidate solutions down the post-dominator tree until they agree.
 #include <algorithm>
+#include <climits>
 #include <cstring>
 
 #include "cb_internal.cuh"
@@ -30,6 +31,7 @@
 #define DP_NARROW_WARPS 16
 #define DP_WIDE_WARPS 8
 #define DP_STAGE_MAX (200 * 1024)
+#define DP_WSTACK 64  // per-warp tie-walk stack entries in shared memory
 
 struct DPArgs {
   // graph
@@ -99,18 +101,20 @@ __device__ bool same_members(const DPArgs& a, int32_t k1, int32_t k2) {
 }
 
 // True when the subtree solution that roots r with k1 sorts before the one
-// rooting r with k2 (both equal in cost).  Executed by a single thread.
-__device__ bool solution_less(const DPArgs& a, int32_t r, int32_t k1, int32_t k2) {
-  if (same_members(a, k1, k2)) return a.pat[k1] < a.pat[k2];
-  while (atomicCAS(a.lock, 0, 1) != 0) {
-  }
-  __threadfence();
+// rooting r with k2 (both equal in cost).  Executed by a single thread: a
+// depth-first walk of the post-dominator subtree that only descends where the
+// two solutions' owning kernels differ, tracking the smallest kernel each side
+// holds outside the other.  The walk uses the warp's own shared-memory stack;
+// a walk deeper than that restarts on the global stack under a lock.
+__device__ bool solution_walk(const DPArgs& a, int32_t r, int32_t k1, int32_t k2, int4* stack,
+                              int64_t cap, bool& overflow) {
   int32_t best1 = k1, best2 = k2;
   int64_t top = 0;
   unsigned long long steps = 0;
-  a.stack[top++] = make_int4(r, k1, k2, 0);
+  stack[top++] = make_int4(r, k1, k2, 0);
+  overflow = false;
   while (top > 0) {
-    int4 e = a.stack[--top];
+    int4 e = stack[--top];
     for (int32_t j = a.pch_ptr[e.x]; j < a.pch_ptr[e.x + 1]; ++j) {
       const int32_t u = a.pch[j];
       ++steps;
@@ -122,13 +126,29 @@ __device__ bool solution_less(const DPArgs& a, int32_t r, int32_t k1, int32_t k2
       if (o1 == o2) continue;
       if (!in1 && cu >= 0 && elem_less(a, cu, best1)) best1 = cu;
       if (!in2 && cu >= 0 && elem_less(a, cu, best2)) best2 = cu;
-      a.stack[top++] = make_int4(u, o1, o2, 0);
+      if (top == cap) {
+        overflow = true;
+        return false;
+      }
+      stack[top++] = make_int4(u, o1, o2, 0);
     }
   }
   atomicAdd(a.counters + 1, steps);
+  return elem_less(a, best1, best2);
+}
+
+__device__ bool solution_less(const DPArgs& a, int32_t r, int32_t k1, int32_t k2, int4* wstack) {
+  if (same_members(a, k1, k2)) return a.pat[k1] < a.pat[k2];
+  bool overflow = false;
+  const bool less = solution_walk(a, r, k1, k2, wstack, DP_WSTACK, overflow);
+  if (!overflow) return less;
+  while (atomicCAS(a.lock, 0, 1) != 0) {
+  }
+  __threadfence();
+  const bool res = solution_walk(a, r, k1, k2, a.stack, INT64_MAX, overflow);
   __threadfence();
   atomicExch(a.lock, 0);
-  return elem_less(a, best1, best2);
+  return res;
 }
 
 // Value of candidate c for root r; returns false when some required
@@ -154,8 +174,8 @@ __device__ __forceinline__ bool candidate_value(const DPArgs& a, int32_t c, fx19
   return true;
 }
 
-// Whole warp relaxes node r.
-__device__ void dp_node(const DPArgs& a, int32_t r) {
+// Whole warp relaxes node r (`wstack`: the warp's tie-walk stack).
+__device__ void dp_node(const DPArgs& a, int32_t r, int4* wstack) {
   const int lane = threadIdx.x & 31;
   const int32_t c0 = a.group_ptr[r], c1 = a.group_ptr[r + 1];
   bool inexact = false;
@@ -228,7 +248,7 @@ __device__ void dp_node(const DPArgs& a, int32_t r) {
           winner = cand;
         } else {
           ++ties;
-          if (solution_less(a, r, cand, winner)) winner = cand;
+          if (solution_less(a, r, cand, winner, wstack)) winner = cand;
         }
       }
     }
@@ -254,6 +274,7 @@ __global__ void __launch_bounds__(DP_NARROW_WARPS * 32)
 dp_narrow_kernel(DPArgs a, const int32_t* __restrict__ level_ptr, int32_t lvl_begin, int32_t lvl_end,
                  int32_t n_stage) {
   extern __shared__ __align__(16) unsigned char dp_smem[];
+  __shared__ int4 s_stack[DP_NARROW_WARPS][DP_WSTACK];
   const int warp = threadIdx.x >> 5;
   DPArgs b = a;
   if (n_stage > 0) {
@@ -269,7 +290,7 @@ dp_narrow_kernel(DPArgs a, const int32_t* __restrict__ level_ptr, int32_t lvl_be
   }
   for (int32_t l = lvl_begin; l < lvl_end; ++l) {
     const int32_t i0 = level_ptr[l], i1 = level_ptr[l + 1];
-    for (int32_t i = i0 + warp; i < i1; i += DP_NARROW_WARPS) dp_node(b, a.level_nodes[i]);
+    for (int32_t i = i0 + warp; i < i1; i += DP_NARROW_WARPS) dp_node(b, a.level_nodes[i], s_stack[warp]);
     __syncthreads();
   }
   if (n_stage > 0) {
@@ -284,8 +305,9 @@ dp_narrow_kernel(DPArgs a, const int32_t* __restrict__ level_ptr, int32_t lvl_be
 
 __global__ void __launch_bounds__(DP_WIDE_WARPS * 32)
 dp_wide_kernel(DPArgs a, int32_t i0, int32_t i1) {
+  __shared__ int4 s_stack[DP_WIDE_WARPS][DP_WSTACK];
   const int32_t i = i0 + blockIdx.x * DP_WIDE_WARPS + (threadIdx.x >> 5);
-  if (i < i1) dp_node(a, a.level_nodes[i]);
+  if (i < i1) dp_node(a, a.level_nodes[i], s_stack[threadIdx.x >> 5]);
 }
 
 // Sum of OPT over post-dominator-tree roots + global minimum regret.

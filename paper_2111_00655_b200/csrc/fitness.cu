@@ -109,7 +109,6 @@ static void build_frontier_program(cb_es_plan* P, int32_t n_elig_units) {
   P->fixed_pos.push_back(M);  // sentinel
   P->prog.resize(M);
   P->prog_slots.clear();
-  P->prog_end_pos.clear();
   for (int32_t p = 0; p < M; ++p) {
     const int32_t u = order[p];
     UnitRec r;
@@ -126,10 +125,7 @@ static void build_frontier_program(cb_es_plan* P, int32_t n_elig_units) {
       if (pos[q] < p) P->prog_slots.push_back((uint8_t)slot[pos[q]]);
     r.nback = (uint8_t)(P->prog_slots.size() - r.back_off);
     r.end_off = (int32_t)P->prog_slots.size();
-    for (int32_t q : ends_at[p]) {
-      P->prog_slots.push_back((uint8_t)slot[q]);
-      P->prog_end_pos.push_back(q);
-    }
+    for (int32_t q : ends_at[p]) P->prog_slots.push_back((uint8_t)slot[q]);
     r.nend = (uint8_t)(P->prog_slots.size() - r.end_off);
     r.hot.x = (uint32_t)r.bit;
     r.hot.y = (uint32_t)r.slot | ((uint32_t)r.nback << 8) | ((uint32_t)r.nend << 16);

@@ -78,7 +78,6 @@ struct AnArgs {
   const AHot* __restrict__ hot;
   const uint64_t* __restrict__ cold;  // [M][6] rep, off, term1
   const int32_t* __restrict__ cnt;
-  const uint64_t* __restrict__ endterm;  // [end entries][2] term1 of each ending unit
   const uint8_t* __restrict__ slots;
   const uint64_t* __restrict__ infeas;
   const double* __restrict__ rt;
@@ -167,7 +166,6 @@ fitness_anchor_kernel(AnArgs a, const uint64_t* __restrict__ pop, int64_t n, dou
     uint4 nh0 = __ldg(reinterpret_cast<const uint4*>(a.hot));
     uint4 nh1 = __ldg(reinterpret_cast<const uint4*>(a.hot) + 1);
     X128 noff = ld_x(a.cold + 2);
-    int32_t eo = 0;  // end-list entries of the steps before p
     for (int32_t p = 0; p < a.M; ++p) {
       const AHot* hp = a.hot + p;
       const uint4 h0 = nh0, h1 = nh1;
@@ -271,8 +269,8 @@ fitness_anchor_kernel(AnArgs a, const uint64_t* __restrict__ pop, int64_t n, dou
             act &= ~(1ull << e);
             le = lab[e * T];
             if (le & L_ANCHOR) {  // the anchor leaves: its region is complete
-              if (le & L_SINGLE) {  // one unit: the unit ending here
-                x_add(total, ld_x(a.endterm + 2 * (size_t)(eo + j)));
+              if (le & L_SINGLE) {
+                x_add(total, ld_x(a.cold + (size_t)(le & L_POS_MASK) * 6 + 4));
               } else {
                 emit = true;
                 pfree |= 1u << (le & 0x3f);
@@ -315,7 +313,6 @@ fitness_anchor_kernel(AnArgs a, const uint64_t* __restrict__ pop, int64_t n, dou
         case 0x21: step_lists(IC<2>{}, IC<1>{}); break;
         default: step_lists(IC<-1>{}, IC<-1>{}); break;
       }
-      eo += nend;
     }
     __syncwarp();
     if (lane < qn) an_price(ql, qh, qm, lane, a, tlo, thi, inexact);
@@ -371,7 +368,6 @@ int launch_anchor_t(cb_es_plan* p, const uint64_t* d_pop, int64_t n, double* d_f
   a.hot = reinterpret_cast<const AHot*>(p->d_ahot.p);
   a.cold = p->d_acold.p;
   a.cnt = p->d_acnt.p;
-  a.endterm = p->d_aendterm.p;
   a.slots = p->d_prog_slots.p;
   a.infeas = p->d_infeas.p;
   a.rt = p->d_rt.p;
@@ -484,19 +480,7 @@ int build_anchor_plan(cb_es_plan* P) {
       pah[(size_t)p * 4 + 3] = wr;
     }
   }
-  // term1 of the unit of every end-list entry (a region of one closes with its
-  // unit's own term: its address is then known without reading the slot)
-  std::vector<uint64_t> endterm(std::max<size_t>(P->prog_end_pos.size(), 1) * 2, 0ull);
-  for (size_t i = 0; i < P->prog_end_pos.size(); ++i) {
-    const fx192 x = fx_shr(P->prog[P->prog_end_pos[i]].term1, lo);
-    endterm[2 * i] = x.w[0];
-    endterm[2 * i + 1] = x.w[1];
-  }
   cudaError_t e;
-  if ((e = P->d_aendterm.upload(endterm)) != cudaSuccess) {
-    cb_set_error(std::string("CUDA error in plan upload: ") + cudaGetErrorString(e));
-    return CB_ERR_CUDA;
-  }
   if (P->pa_ok && (e = P->d_pahdr.upload(pah)) != cudaSuccess) {
     cb_set_error(std::string("CUDA error in plan upload: ") + cudaGetErrorString(e));
     return CB_ERR_CUDA;

@@ -65,8 +65,6 @@ struct cb_es_plan {
   // position, program position of each genome bit (-1 infeasible), program
   // positions of the fixed units followed by the sentinel M
   std::vector<int32_t> prog_last, pos_of_bit, fixed_pos;
-  // program position of the unit of every end-list entry, in program order
-  std::vector<int32_t> prog_end_pos;
   DBuf<int32_t> d_prog_last, d_pos_of_bit, d_fixed_pos;
   // anchor kernel (fitness_anchor.cu): 128-bit window (values carried as
   // X = v >> anchor_shift), per-position step headers and 128-bit constants,
@@ -76,7 +74,6 @@ struct cb_es_plan {
   int32_t anchor_shift = 0;
   DBuf<uint8_t> d_ahot;     // AHot[M]
   DBuf<uint64_t> d_acold;   // [M][6]: rep, off, term1 as 128-bit X
-  DBuf<uint64_t> d_aendterm;  // [end entries][2]: term1 (128-bit X) of each ending unit
   DBuf<int32_t> d_acnt;     // [M]
   int32_t pool_entries = 16;
   // tournament order keys of the parent population (es.cu)
