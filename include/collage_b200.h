@@ -268,6 +268,11 @@ int cb_es_generation(cb_es_plan* p, const uint64_t* d_parents,
                      int64_t n_children, const uint64_t* d_keep, int64_t n_keep,
                      uint64_t seed, uint64_t generation, uint64_t stream_id,
                      int32_t tournament, double mutation_rate, void* stream);
+/* cb_argmin plus, when d_pop is given, the best row copied to d_elite
+ * (words uint64) and the best value to *d_history_slot (if not NULL). */
+int cb_argmin_elite(const double* d_fit, int64_t n, const uint64_t* d_pop,
+                    int32_t words, int64_t* d_idx, double* d_val,
+                    uint64_t* d_elite, double* d_history_slot, void* stream);
 /* 1 when cb_es_generation runs fused for this plan (and path setting). */
 int cb_es_generation_fused(const cb_es_plan* p);
 int cb_argmin(const double* d_fit, int64_t n, int64_t* d_idx, double* d_val,

@@ -126,6 +126,8 @@ _SIGNATURES = {
                                  c_void_p, c_int64, c_uint64, c_uint64, c_uint64, c_int32,
                                  c_double, c_void_p]),
     "cb_es_generation_fused": (c_int, [c_void_p]),
+    "cb_argmin_elite": (c_int, [c_void_p, c_int64, c_void_p, c_int32, c_void_p, c_void_p, c_void_p,
+                                c_void_p, c_void_p]),
     "cb_argmin": (c_int, [c_void_p, c_int64, c_void_p, c_void_p, c_void_p]),
 }
 

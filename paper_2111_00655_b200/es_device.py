@@ -130,6 +130,15 @@ class DeviceEvolution:
                                   self._stream())
 
     def _record_best(self) -> None:
+        if self.world == 1:
+            # argmin, elite row and history entry in one native call
+            hist = (ctypes.c_void_p(self.history[self.generation:].data_ptr())
+                    if self.generation < self.history.numel() else ctypes.c_void_p())
+            nat.check(nat.lib().cb_argmin_elite(
+                self._ptr(self.fit[self.cur]), self.P, self._ptr(self.pop[self.cur]), self.W,
+                self._ptr(self.best_idx), self._ptr(self.best_val), self._ptr(self.elite), hist,
+                ctypes.c_void_p(self._stream())))
+            return
         nat.check(nat.lib().cb_argmin(self._ptr(self.fit[self.cur]), self.P,
                                       self._ptr(self.best_idx), self._ptr(self.best_val),
                                       ctypes.c_void_p(self._stream())))
