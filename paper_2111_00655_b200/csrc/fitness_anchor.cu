@@ -31,7 +31,6 @@
 #include <algorithm>
 #include <cmath>
 #include <cstring>
-#include <type_traits>
 
 #include "fitness_plan.cuh"
 
@@ -39,9 +38,6 @@
 #define AN_QCAP 64
 
 namespace {
-
-template <int V>
-using IC = std::integral_constant<int, V>;
 
 // Per-position step header, one 32-byte uniform load per step.
 struct __align__(16) AHot {
@@ -199,119 +195,104 @@ fitness_anchor_kernel(AnArgs a, const uint64_t* __restrict__ pop, int64_t n, dou
         act |= 1ull << S;
         lab[S * T] = L_ANCHOR | L_SINGLE | (uint32_t)p;
       }
-      // back / end lists: straight-line code for the common (nback, nend)
-      // shapes (warp-uniform switch on the header), a loop otherwise
-      auto step_lists = [&](auto nb_c, auto ne_c) {
-        constexpr int NB = decltype(nb_c)::value, NE = decltype(ne_c)::value;
-        int A = S;  // root slot of the new unit's component
-        for (int j = 0; j < (NB >= 0 ? NB : nback); ++j) {  // constant trip counts unroll
-          const int b = long_list ? __ldg(lst + j) : hdr_slot(h0, h1, j);
-          if (!on || !((act >> b) & 1ull)) continue;
-          int x = b;
-          uint32_t lx = lab[x * T];
-          while (!(lx & L_ANCHOR)) {
-            x = (int)(lx & 0xff);
-            lx = lab[x * T];
-          }
-          if (x != b) lab[b * T] = (uint32_t)x;  // path compression
-          if (x == A) continue;
-          const uint32_t lA = lab[A * T];
-          const bool keepA = endw[A] >= endw[x];  // the later-ending anchor survives
-          const int Wn = keepA ? A : x, Xn = keepA ? x : A;
-          const uint32_t lW = keepA ? lA : lx, lX = keepA ? lx : lA;
-          X128 sW, sX;
-          uint32_t cW, cX;
-          if (lW & L_SINGLE) {
-            const uint32_t u = lW & L_POS_MASK;
-            sW = ld_x(a.cold + (size_t)u * 6);
-            cW = (uint32_t)__ldg(a.cnt + u);
-          } else {
-            const int e = lW & 0x3f;
-            sW = {pl[e * T], ph[e * T]};
-            cW = (lW >> 8) & L_CNT_MAX;
-          }
-          if (lX & L_SINGLE) {
-            const uint32_t u = lX & L_POS_MASK;
-            sX = ld_x(a.cold + (size_t)u * 6);
-            cX = (uint32_t)__ldg(a.cnt + u);
-          } else {
-            const int e = lX & 0x3f;
-            sX = {pl[e * T], ph[e * T]};
-            cX = (lX >> 8) & L_CNT_MAX;
-          }
-          x_add(sW, sX);
-          const uint32_t c = cW + cX;
-          int e;
-          if (!(lW & L_SINGLE)) {
-            e = lW & 0x3f;
-            if (!(lX & L_SINGLE)) pfree |= 1u << (lX & 0x3f);
-          } else if (!(lX & L_SINGLE)) {
-            e = lX & 0x3f;
-          } else if (pfree) {
-            e = __ffs(pfree) - 1;
-            pfree &= pfree - 1u;
-          } else {
-            ovf = true;  // pool exhausted: the genome goes to the fallback kernel
-            e = 0;
-          }
-          ovf |= c > L_CNT_MAX;
-          pl[e * T] = sW.lo;
-          ph[e * T] = sW.hi;
-          lab[Wn * T] = L_ANCHOR | ((c & L_CNT_MAX) << 8) | (uint32_t)e;
-          lab[Xn * T] = (uint32_t)Wn;
-          A = Wn;
+      int A = S;  // root slot of the new unit's component
+      for (int j = 0; j < nback; ++j) {
+        const int b = long_list ? __ldg(lst + j) : hdr_slot(h0, h1, j);
+        if (!on || !((act >> b) & 1ull)) continue;
+        int x = b;
+        uint32_t lx = lab[x * T];
+        while (!(lx & L_ANCHOR)) {
+          x = (int)(lx & 0xff);
+          lx = lab[x * T];
         }
-        for (int j = 0; j < (NE >= 0 ? NE : nend); ++j) {
-          const int e = long_list ? __ldg(lst + nback + j) : hdr_slot(h0, h1, nback + j);
-          bool emit = false;
-          uint32_t le = 0u;
-          if ((act >> e) & 1ull) {
-            act &= ~(1ull << e);
-            le = lab[e * T];
-            if (le & L_ANCHOR) {  // the anchor leaves: its region is complete
-              if (le & L_SINGLE) {
-                x_add(total, ld_x(a.cold + (size_t)(le & L_POS_MASK) * 6 + 4));
-              } else {
-                emit = true;
-                pfree |= 1u << (le & 0x3f);
-              }
-            }
-          }
-          // closed multi-unit regions of all lanes are priced 32 at a time
-          const unsigned closing = __ballot_sync(0xffffffffu, emit);
-          if (closing) {
-            if (emit) {
-              const int at = qn + __popc(closing & ((1u << lane) - 1u));
-              const int pe = le & 0x3f;
-              ql[at] = pl[pe * T];
-              qh[at] = ph[pe * T];
-              qm[at] = ((uint64_t)lane << 32) | ((le >> 8) & L_CNT_MAX);
-            }
-            qn += __popc(closing);
-            if (qn >= 32) {
-              __syncwarp();
-              an_price(ql, qh, qm, lane, a, tlo, thi, inexact);
-              __syncwarp();
-              if (lane < qn - 32) {
-                ql[lane] = ql[32 + lane];
-                qh[lane] = qh[32 + lane];
-                qm[lane] = qm[32 + lane];
-              }
-              __syncwarp();
-              qn -= 32;
+        if (x != b) lab[b * T] = (uint32_t)x;  // path compression
+        if (x == A) continue;
+        const uint32_t lA = lab[A * T];
+        const bool keepA = endw[A] >= endw[x];  // the later-ending anchor survives
+        const int Wn = keepA ? A : x, Xn = keepA ? x : A;
+        const uint32_t lW = keepA ? lA : lx, lX = keepA ? lx : lA;
+        X128 sW, sX;
+        uint32_t cW, cX;
+        if (lW & L_SINGLE) {
+          const uint32_t u = lW & L_POS_MASK;
+          sW = ld_x(a.cold + (size_t)u * 6);
+          cW = (uint32_t)__ldg(a.cnt + u);
+        } else {
+          const int e = lW & 0x3f;
+          sW = {pl[e * T], ph[e * T]};
+          cW = (lW >> 8) & L_CNT_MAX;
+        }
+        if (lX & L_SINGLE) {
+          const uint32_t u = lX & L_POS_MASK;
+          sX = ld_x(a.cold + (size_t)u * 6);
+          cX = (uint32_t)__ldg(a.cnt + u);
+        } else {
+          const int e = lX & 0x3f;
+          sX = {pl[e * T], ph[e * T]};
+          cX = (lX >> 8) & L_CNT_MAX;
+        }
+        x_add(sW, sX);
+        const uint32_t c = cW + cX;
+        int e;
+        if (!(lW & L_SINGLE)) {
+          e = lW & 0x3f;
+          if (!(lX & L_SINGLE)) pfree |= 1u << (lX & 0x3f);
+        } else if (!(lX & L_SINGLE)) {
+          e = lX & 0x3f;
+        } else if (pfree) {
+          e = __ffs(pfree) - 1;
+          pfree &= pfree - 1u;
+        } else {
+          ovf = true;  // pool exhausted: the genome goes to the fallback kernel
+          e = 0;
+        }
+        ovf |= c > L_CNT_MAX;
+        pl[e * T] = sW.lo;
+        ph[e * T] = sW.hi;
+        lab[Wn * T] = L_ANCHOR | ((c & L_CNT_MAX) << 8) | (uint32_t)e;
+        lab[Xn * T] = (uint32_t)Wn;
+        A = Wn;
+      }
+      for (int j = 0; j < nend; ++j) {
+        const int e = long_list ? __ldg(lst + nback + j) : hdr_slot(h0, h1, nback + j);
+        bool emit = false;
+        uint32_t le = 0u;
+        if ((act >> e) & 1ull) {
+          act &= ~(1ull << e);
+          le = lab[e * T];
+          if (le & L_ANCHOR) {  // the anchor leaves: its region is complete
+            if (le & L_SINGLE) {
+              x_add(total, ld_x(a.cold + (size_t)(le & L_POS_MASK) * 6 + 4));
+            } else {
+              emit = true;
+              pfree |= 1u << (le & 0x3f);
             }
           }
         }
-      };
-      switch (long_list ? -1 : (nback << 4) | nend) {
-        case 0x11: step_lists(IC<1>{}, IC<1>{}); break;
-        case 0x12: step_lists(IC<1>{}, IC<2>{}); break;
-        case 0x10: step_lists(IC<1>{}, IC<0>{}); break;
-        case 0x00: step_lists(IC<0>{}, IC<0>{}); break;
-        case 0x22: step_lists(IC<2>{}, IC<2>{}); break;
-        case 0x01: step_lists(IC<0>{}, IC<1>{}); break;
-        case 0x21: step_lists(IC<2>{}, IC<1>{}); break;
-        default: step_lists(IC<-1>{}, IC<-1>{}); break;
+        // closed multi-unit regions of all lanes are priced 32 at a time
+        const unsigned closing = __ballot_sync(0xffffffffu, emit);
+        if (closing) {
+          if (emit) {
+            const int at = qn + __popc(closing & ((1u << lane) - 1u));
+            const int pe = le & 0x3f;
+            ql[at] = pl[pe * T];
+            qh[at] = ph[pe * T];
+            qm[at] = ((uint64_t)lane << 32) | ((le >> 8) & L_CNT_MAX);
+          }
+          qn += __popc(closing);
+          if (qn >= 32) {
+            __syncwarp();
+            an_price(ql, qh, qm, lane, a, tlo, thi, inexact);
+            __syncwarp();
+            if (lane < qn - 32) {
+              ql[lane] = ql[32 + lane];
+              qh[lane] = qh[32 + lane];
+              qm[lane] = qm[32 + lane];
+            }
+            __syncwarp();
+            qn -= 32;
+          }
+        }
       }
     }
     __syncwarp();
