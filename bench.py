@@ -440,6 +440,17 @@ def config_sweep(dev) -> dict:
         oc.fitness(kernels, bs.graph_backend, pop, threads=threads)
         row["cpu_oracle_fitness_per_s"] = cfg["cpu"] / (time.perf_counter() - t0)
         row["cpu_threads"] = threads
+        if name in ("resnet50", "bert_base"):
+            # the reference's own search API, drop-in: tp.evolve with the default
+            # ESConfig (population 32, 200 generations; reference draws replayed
+            # exactly, each generation priced in one GPU batch)
+            t0 = time.perf_counter()
+            r2 = tp.optimize(g, bs.registry, bs.measurer, 0.01)
+            ev = tp.evolve(g, bs.registry, bs.measurer, r2.placement, 0.01, tp.ESConfig(),
+                           graph_backend=bs.graph_backend, kernel_matches=r2.kernel_matches)
+            row["evolve_default"] = {"s": time.perf_counter() - t0, "cost_ms": ev.cost_ms,
+                                     "evaluations": ev.evaluations,
+                                     "note": "optimize + evolve(ESConfig()) through the public API"}
         if cfg["ref_dp"]:
             t0 = time.perf_counter()
             status, cost, ref_kernels = oc.dp(max_states=200_000)

@@ -89,3 +89,21 @@ def test_random_dag_100k_end_to_end(gpu):
         want = math.inf if dec is None else tp.placement_cost_graphlevel(
             bs.measurer, g, dec, 0.01, bs.registry.graph_backend_ids())
         assert f == want
+
+
+def test_nasrnn_cell_matches_oracle_beyond_reference_cap(gpu):
+    """One NasRNN cell (47 nodes): the reference DP exceeds 200 000 states; the
+    CPU oracle's covered-set DP solves it with a 30 M-state cap
+    (tests/golden/make_oracle_large.py) and the device DP must return the
+    identical placement and cost."""
+    import json
+    import os
+    from conftest import GOLDEN, build_case, kernels_of
+    with open(os.path.join(GOLDEN, "oracle_large.json")) as fh:
+        cases = json.load(fh)
+    for case in cases:
+        g, reg, meas = build_case(case)
+        res = tp.optimize(g, reg, meas, case["epsilon"])
+        want = case["oracle_dp"]
+        assert res.cost_ms == want["cost"], case["name"]
+        assert kernels_of(res.placement) == want["kernels"], case["name"]

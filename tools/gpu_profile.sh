@@ -12,7 +12,7 @@ timeout 900 ncu --set full --clock-control none -k regex:"dp_narrow|match_count|
   -o gpurun_out/search_full python bench.py $ARGS > gpurun_out/ncu_search_run.log 2>&1
 tail -2 gpurun_out/ncu_search_run.log
 ls -la gpurun_out
-# the wide-program kernel (random 100k DAG, 65536 random genomes)
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:fitness_anchor -c 1 \
-  -o gpurun_out/anchor_full python tools/fitness_probe.py random100k 65536 anchor > gpurun_out/ncu_anchor_run.log 2>&1
+# the wide-program kernel (random 100k DAG, a 262 144-genome ES population after one generation)
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:fitness_anchor -s 2 -c 1 \
+  -o gpurun_out/anchor_full python tools/es_fitness_probe.py random100k 262144 > gpurun_out/ncu_anchor_run.log 2>&1
 tail -2 gpurun_out/ncu_anchor_run.log

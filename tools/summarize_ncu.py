@@ -111,7 +111,7 @@ peak = json.load(open(os.path.join(root, "MEASURED_PEAKS.json")))["hbm_gbs"]
 rows = []
 for rep, what in (("fitness_full.ncu-rep", "bench workload (BERT-base)"),
                   ("search_full.ncu-rep", "search phase (BERT-base)"),
-                  ("anchor_full.ncu-rep", "random 100k DAG, 65536 random genomes")):
+                  ("anchor_full.ncu-rep", "random 100k DAG, 262 144-genome ES population")):
     path = os.path.join(root, "gpurun_out", rep)
     if os.path.exists(path):
         rows += [(what,) + x for x in _rows(path)]
