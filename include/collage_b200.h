@@ -17,6 +17,11 @@
  *                     tensorplace/cost.py:320-373 placement_cost_graphlevel
  *   cb_es_breed       tensorplace/evolution.py:373-428 selection / crossover /
  *                     mutation (device variant, counter-based RNG)
+ *   cb_es_generation  tensorplace/evolution.py:233-247 one generation (breed +
+ *                     evaluate), optionally as one fused kernel
+ *   cb_argmin*        tensorplace/evolution.py:228-230, :245-247 best tracking
+ *   cb_es_plan_units / _kernel / _set_path / _set_pool: diagnostics and tuning
+ *                     knobs of this implementation (no reference counterpart)
  *
  * Conventions: plain pointers and sizes only; arrays marked "host" live in
  * host memory, "device" arrays are CUDA device pointers; `stream` is a
@@ -255,9 +260,8 @@ int cb_es_breed(cb_es_plan* p, const uint64_t* d_parents,
                 const uint64_t* d_keep, int64_t n_keep, uint64_t seed,
                 uint64_t generation, uint64_t stream_id, int32_t tournament,
                 double mutation_rate, void* stream);
-/* Index of the smallest fitness (first on ties) -> d_idx[0]; value ->
- * d_val[0]. */
-/* One ES generation: breed n_children rows into d_children (same operators
+/* One ES generation (tensorplace/evolution.py:233-247: breed the next
+ * population, evaluate it): breed n_children rows into d_children (same operators
  * and draws as cb_es_breed) and write their fitness to d_child_fit (as
  * cb_fitness_device).  Runs as a single fused kernel when the plan's walk
  * allows it (<= 8 frontier slots, 128-bit window, <= 4 words per genome),
@@ -269,12 +273,15 @@ int cb_es_generation(cb_es_plan* p, const uint64_t* d_parents,
                      uint64_t seed, uint64_t generation, uint64_t stream_id,
                      int32_t tournament, double mutation_rate, void* stream);
 /* cb_argmin plus, when d_pop is given, the best row copied to d_elite
- * (words uint64) and the best value to *d_history_slot (if not NULL). */
+ * (words uint64) and the best value to *d_history_slot (if not NULL):
+ * the best-so-far / history bookkeeping of tensorplace/evolution.py:245-247. */
 int cb_argmin_elite(const double* d_fit, int64_t n, const uint64_t* d_pop,
                     int32_t words, int64_t* d_idx, double* d_val,
                     uint64_t* d_elite, double* d_history_slot, void* stream);
 /* 1 when cb_es_generation runs fused for this plan (and path setting). */
 int cb_es_generation_fused(const cb_es_plan* p);
+/* Index of the smallest fitness (first on ties) -> d_idx[0]; value ->
+ * d_val[0] (tensorplace/evolution.py:228-230, :245-247 best tracking). */
 int cb_argmin(const double* d_fit, int64_t n, int64_t* d_idx, double* d_val,
               void* stream);
 
