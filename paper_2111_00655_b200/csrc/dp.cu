@@ -270,30 +270,63 @@ __device__ void dp_node(const DPArgs& a, int32_t r, int4* wstack) {
 // whole run, so each level's dependent reads of its post-dominator
 // children's values hit shared memory instead of L2; they are written back
 // to global memory for the nodes of this run at the end.
+// Sizes of the read-only arrays a narrow run may stage in shared memory.
+struct DPStage {
+  int32_t n_stage;     // nodes whose OPT / feasibility are staged (0 = none)
+  int32_t n_groups;    // graph nodes (group_ptr has n_groups + 1 entries)
+  int32_t n_matches;   // 0 = match tables not staged
+  int32_t n_members;
+  int32_t n_pch;
+};
+
 __global__ void __launch_bounds__(DP_NARROW_WARPS * 32)
 dp_narrow_kernel(DPArgs a, const int32_t* __restrict__ level_ptr, int32_t lvl_begin, int32_t lvl_end,
-                 int32_t n_stage) {
+                 DPStage st) {
   extern __shared__ __align__(16) unsigned char dp_smem[];
-  __shared__ int4 s_stack[DP_NARROW_WARPS][DP_WSTACK];
+  __shared__ int4 s_stack[DP_WSTACK * DP_NARROW_WARPS];
   const int warp = threadIdx.x >> 5;
   DPArgs b = a;
-  if (n_stage > 0) {
-    fx192* s_opt = reinterpret_cast<fx192*>(dp_smem);
-    uint8_t* s_feas = reinterpret_cast<uint8_t*>(s_opt + n_stage);
-    for (int32_t v = threadIdx.x; v < n_stage; v += blockDim.x) {
+  unsigned char* cur = dp_smem;
+  if (st.n_stage > 0) {
+    fx192* s_opt = reinterpret_cast<fx192*>(cur);
+    uint8_t* s_feas = reinterpret_cast<uint8_t*>(s_opt + st.n_stage);
+    for (int32_t v = threadIdx.x; v < st.n_stage; v += blockDim.x) {
       s_opt[v] = a.opt[v];
       s_feas[v] = a.feas[v];
     }
-    __syncthreads();
     b.opt = s_opt;
     b.feas = s_feas;
+    cur = reinterpret_cast<unsigned char*>(s_feas) + ((st.n_stage + 15) & ~15);
   }
+  if (st.n_matches > 0) {
+    // the match tables and the post-dominator tree are read by every
+    // relaxation of the run: stage them so the dependent chains of a
+    // candidate's value (group -> members -> children -> OPT) stay on chip
+    auto stage_i32 = [&](const int32_t* src, int32_t count) -> const int32_t* {
+      int32_t* dst = reinterpret_cast<int32_t*>(cur);
+      for (int32_t i = threadIdx.x; i < count; i += blockDim.x) dst[i] = src[i];
+      cur += ((size_t)count * 4 + 15) & ~(size_t)15;
+      return dst;
+    };
+    double* s_cost = reinterpret_cast<double*>(cur);
+    for (int32_t i = threadIdx.x; i < st.n_matches; i += blockDim.x) s_cost[i] = a.cost[i];
+    cur += ((size_t)st.n_matches * 8 + 15) & ~(size_t)15;
+    b.cost = s_cost;
+    b.group_ptr = stage_i32(a.group_ptr, st.n_groups + 1);
+    b.pat = stage_i32(a.pat, st.n_matches);
+    b.mem_ptr = stage_i32(a.mem_ptr, st.n_matches + 1);
+    b.members = stage_i32(a.members, st.n_members);
+    b.pch_ptr = stage_i32(a.pch_ptr, st.n_groups + 1);
+    b.pch = stage_i32(a.pch, st.n_pch);
+  }
+  __syncthreads();
   for (int32_t l = lvl_begin; l < lvl_end; ++l) {
     const int32_t i0 = level_ptr[l], i1 = level_ptr[l + 1];
-    for (int32_t i = i0 + warp; i < i1; i += DP_NARROW_WARPS) dp_node(b, a.level_nodes[i], s_stack[warp]);
+    for (int32_t i = i0 + warp; i < i1; i += DP_NARROW_WARPS)
+      dp_node(b, a.level_nodes[i], s_stack + warp * DP_WSTACK);
     __syncthreads();
   }
-  if (n_stage > 0) {
+  if (st.n_stage > 0) {
     const int32_t i0 = level_ptr[lvl_begin], i1 = level_ptr[lvl_end];
     for (int32_t i = i0 + threadIdx.x; i < i1; i += blockDim.x) {
       const int32_t v = a.level_nodes[i];
@@ -305,9 +338,9 @@ dp_narrow_kernel(DPArgs a, const int32_t* __restrict__ level_ptr, int32_t lvl_be
 
 __global__ void __launch_bounds__(DP_WIDE_WARPS * 32)
 dp_wide_kernel(DPArgs a, int32_t i0, int32_t i1) {
-  __shared__ int4 s_stack[DP_WIDE_WARPS][DP_WSTACK];
+  __shared__ int4 s_stack[DP_WIDE_WARPS * DP_WSTACK];
   const int32_t i = i0 + blockIdx.x * DP_WIDE_WARPS + (threadIdx.x >> 5);
-  if (i < i1) dp_node(a, a.level_nodes[i], s_stack[threadIdx.x >> 5]);
+  if (i < i1) dp_node(a, a.level_nodes[i], s_stack + (threadIdx.x >> 5) * DP_WSTACK);
 }
 
 // Sum of OPT over post-dominator-tree roots + global minimum regret.
@@ -436,10 +469,25 @@ extern "C" int cb_dp_solve(cb_graph* g, cb_matches* m, double epsilon, int32_t* 
   }
   for (const LevelSegment& s : segs) {
     if (s.narrow) {
-      const size_t stage_bytes = (size_t)n * (sizeof(fx192) + 1);
-      const int32_t n_stage = stage_bytes <= DP_STAGE_MAX ? n : 0;
-      dp_narrow_kernel<<<1, DP_NARROW_WARPS * 32, n_stage ? stage_bytes : 0>>>(
-          a, d_level_ptr.p, s.lvl_begin, s.lvl_end, n_stage);
+      auto al = [](size_t b) { return (b + 15) & ~(size_t)15; };
+      DPStage st{};
+      size_t bytes = 0;
+      const size_t opt_bytes = (size_t)n * sizeof(fx192) + al((size_t)n);
+      if (opt_bytes <= DP_STAGE_MAX) {
+        st.n_stage = n;
+        bytes = opt_bytes;
+      }
+      const size_t tab_bytes = al((size_t)m->n_matches * 8) + al(((size_t)n + 1) * 4) * 2 +
+                               al((size_t)m->n_matches * 4) + al(((size_t)m->n_matches + 1) * 4) +
+                               al((size_t)m->n_members * 4) + al(g->pch.size() * 4);
+      if (st.n_stage && bytes + tab_bytes <= DP_STAGE_MAX) {
+        st.n_groups = n;
+        st.n_matches = (int32_t)m->n_matches;
+        st.n_members = (int32_t)m->n_members;
+        st.n_pch = (int32_t)g->pch.size();
+        bytes += tab_bytes;
+      }
+      dp_narrow_kernel<<<1, DP_NARROW_WARPS * 32, bytes>>>(a, d_level_ptr.p, s.lvl_begin, s.lvl_end, st);
     } else {
       int32_t i0 = g->level_ptr[s.lvl_begin], i1 = g->level_ptr[s.lvl_end];
       int32_t blocks = (i1 - i0 + DP_WIDE_WARPS - 1) / DP_WIDE_WARPS;
