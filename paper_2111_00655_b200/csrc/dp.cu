@@ -182,12 +182,16 @@ __device__ void dp_node(const DPArgs& a, int32_t r, int4* wstack) {
   // pass 1: minimum and second minimum (distinct) over feasible candidates
   fx192 best = fx_max(), second = fx_max();
   bool any = false;
+  fx192 last_v = fx_max();
+  bool last_ok = false;
   for (int32_t base = c0; base < c1; base += 32) {
     const int32_t c = base + lane;
     fx192 v = fx_max();
     bool ok = false;
     if (c < c1) ok = candidate_value(a, c, v, inexact);
     if (!ok) v = fx_max();
+    last_v = v;
+    last_ok = ok;
     // warp min of v
     fx192 mn = v;
     for (int off = 16; off > 0; off >>= 1) {
@@ -229,14 +233,19 @@ __device__ void dp_node(const DPArgs& a, int32_t r, int4* wstack) {
     return;
   }
   // pass 2: candidates attaining the minimum, settled by the key order
+  // (a single chunk reuses its pass-1 values instead of recomputing them)
   int32_t winner = -1;
   int ties = 0;
+  const bool one_chunk = c1 - c0 <= 32;
   for (int32_t base = c0; base < c1; base += 32) {
     const int32_t c = base + lane;
-    fx192 v;
-    bool ok = false;
+    fx192 v = last_v;
+    bool ok = last_ok;
     bool dummy = false;
-    if (c < c1) ok = candidate_value(a, c, v, dummy);
+    if (!one_chunk) {
+      ok = false;
+      if (c < c1) ok = candidate_value(a, c, v, dummy);
+    }
     const bool hit = ok && fx_eq(v, best);
     unsigned mask = __ballot_sync(0xffffffffu, hit);
     if (lane == 0) {
