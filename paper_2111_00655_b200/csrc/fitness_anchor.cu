@@ -481,6 +481,7 @@ int launch_fitness_anchor(cb_es_plan* p, const uint64_t* d_pop, int64_t n, doubl
   const int C = p->pool_entries;
   if (C <= 8) return launch_anchor_t<8>(p, d_pop, n, d_fit, stream);
   if (C <= 12) return launch_anchor_t<12>(p, d_pop, n, d_fit, stream);
+  if (C <= 14) return launch_anchor_t<14>(p, d_pop, n, d_fit, stream);
   if (C <= 16) return launch_anchor_t<16>(p, d_pop, n, d_fit, stream);
   return launch_anchor_t<24>(p, d_pop, n, d_fit, stream);
 }

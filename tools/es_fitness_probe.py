@@ -11,6 +11,9 @@ g = workloads.CONFIGS[name]()
 bs = workloads.paper_backends(g) if name != 'random100k' else workloads.random_backends(g, 8, 1, 0)
 res = tp.optimize(g, bs.registry, bs.measurer, 0.01, validate=False)
 plan = tp.FitnessPlan(g, bs.registry, bs.measurer, res.placement, 0.01, bs.graph_backend, res.kernel_matches)
+import os
+if os.environ.get('CB_POOL'):
+    plan.set_pool(int(os.environ['CB_POOL']))
 es = DeviceEvolution(plan, P, seed=1, fused=False)
 es.initialize()
 es.step()
