@@ -564,6 +564,7 @@ extern "C" const char* cb_es_plan_kernel(const cb_es_plan* p) {
 extern "C" int cb_es_plan_set_pool(cb_es_plan* p, int32_t entries) {
   CB_ARG_CHECK(p && entries >= 1 && entries <= 24, "cb_es_plan_set_pool: entries must be in [1, 24]");
   p->pool_entries = entries;
+  p->pool_auto = false;
   return CB_OK;
 }
 

@@ -359,6 +359,14 @@ int launch_anchor_t(cb_es_plan* p, const uint64_t* d_pop, int64_t n, double* d_f
   const int64_t grid = std::min<int64_t>(want, (int64_t)per_sm * cb_sm_count());
   fitness_anchor_kernel<C><<<(unsigned)grid, AN_THREADS, smem, stream>>>(a, d_pop, n, d_fit);
   CB_CUDA_TRY(cudaGetLastError());
+  if (p->pool_auto) {  // let the next launch see this one's overflow count
+    if (!p->h_ovf) {
+      CB_CUDA_TRY(cudaHostAlloc((void**)&p->h_ovf, sizeof(int32_t), cudaHostAllocDefault));
+      *p->h_ovf = 0;
+    }
+    CB_CUDA_TRY(cudaMemcpyAsync(p->h_ovf, p->d_ovf_count.p, sizeof(int32_t), cudaMemcpyDeviceToHost, stream));
+    p->last_anchor_n = n;
+  }
   // genomes that ran out of pool entries: warp-per-genome kernel over the list
   return launch_fitness_wide_list(p, d_pop, n, d_fit, p->d_ovf_list.p, p->d_ovf_count.p, stream);
 }
@@ -478,7 +486,17 @@ int build_anchor_plan(cb_es_plan* P) {
 
 int launch_fitness_anchor(cb_es_plan* p, const uint64_t* d_pop, int64_t n, double* d_fit,
                           cudaStream_t stream) {
-  const int C = p->pool_entries;
+  int C = p->pool_entries;
+  if (p->pool_auto) {
+    // 14 entries fit 8 CTAs of 64 threads per SM on a 36-slot program; when
+    // more than 1 % of the previous launch's genomes overflowed (dense
+    // populations) use 16.  The count is read without synchronising: it is
+    // the last launch that finished, a hint only -- results never depend on C.
+    const volatile int32_t* h = p->h_ovf;
+    if (h && p->last_anchor_n > 0)
+      p->auto_pool = (int64_t)*h * 100 > p->last_anchor_n ? 16 : 14;
+    C = std::min(p->pool_entries, p->auto_pool);
+  }
   if (C <= 8) return launch_anchor_t<8>(p, d_pop, n, d_fit, stream);
   if (C <= 12) return launch_anchor_t<12>(p, d_pop, n, d_fit, stream);
   if (C <= 14) return launch_anchor_t<14>(p, d_pop, n, d_fit, stream);

@@ -76,6 +76,15 @@ struct cb_es_plan {
   DBuf<uint64_t> d_acold;   // [M][6]: rep, off, term1 as 128-bit X
   DBuf<int32_t> d_acnt;     // [M]
   int32_t pool_entries = 16;
+  // pool_auto: the pool size follows the overflow rate of earlier launches,
+  // read back asynchronously into pinned memory (never synchronised on)
+  bool pool_auto = true;
+  int32_t* h_ovf = nullptr;       // pinned: overflow count of the last finished launch
+  int64_t last_anchor_n = 0;
+  int32_t auto_pool = 14;
+  ~cb_es_plan() {
+    if (h_ovf) cudaFreeHost(h_ovf);
+  }
   // tournament order keys of the parent population (es.cu)
   DBuf<uint32_t> d_keys;
   // packed anchor walk (fitness_packed128.cu, <= 8 slots): 16-byte step headers

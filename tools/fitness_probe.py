@@ -31,7 +31,8 @@ for label, fill in (('random', None), ('sparse', 0.1), ('dense', 0.9)):
         if path.startswith('frontier') and not 0 < i.frontier_slots <= 32 or path == 'wide' and not i.frontier_slots:
             continue
         plan.set_path(path)
-        plan.set_pool(int(pool) if pool and path == 'anchor' else 16)
+        if pool and path == 'anchor':
+            plan.set_pool(int(pool))
         for _ in range(2):
             plan.evaluate_device(pop.data_ptr(), P, fit.data_ptr())
         torch.cuda.synchronize()
