@@ -35,6 +35,9 @@ import time
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
+# the CPU oracle's OpenMP threads sleep when idle instead of spinning next to
+# host-side timings (set before libgomp loads)
+os.environ.setdefault("OMP_WAIT_POLICY", "PASSIVE")
 
 L2_BYTES = 126 * 1024 * 1024
 
@@ -240,12 +243,12 @@ def run_mine(args) -> None:
                 inst_per_genome = d.get("warp_instructions_per_genome")
         except (OSError, ValueError, KeyError):
             traffic = None
-    cpu = None
-    if world == 1 and not args.no_cpu_baseline:
-        cpu = cpu_baseline(g, bs, res, plan, args)
     sweep = None
     if world == 1 and not args.no_configs:
         sweep = config_sweep(dev)
+    cpu = None  # last: its OpenMP pool must not compete with the sweep's host-side timings
+    if world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_baseline(g, bs, res, plan, args)
     line = {
         "metric": "fitness_evals_per_sec",
         "value": evals_per_s,

@@ -134,18 +134,20 @@ def optimize(g: ComputationGraph, registry: PatternRegistry, measurer: Measurer,
                 f"candidate matches", op_kinds=(kind,), node_ids=(nid,))
         raise UncoverableGraphError("no full placement found; some nodes cannot be covered "
                                     "compatibly by the registered patterns")
-    chosen = kernels[:res.n_kernels]
+    chosen = kernels[:res.n_kernels].tolist()
     patterns = registry.patterns
-    root_ids = np.asarray(g._ids)[table.root[chosen]].tolist()
-    assignments = [Assignment(table.node_set(m), patterns[p], r)
-                   for m, p, r in zip(chosen.tolist(), table.pat[chosen].tolist(), root_ids)]
+    # canonical order (sorted node tuple) computed once for the placement and
+    # for the match indices the fitness plan takes
+    sets = table.node_sets(chosen)
+    keys = [tuple(sorted(x)) for x in sets]
+    order = sorted(range(len(chosen)), key=keys.__getitem__)
+    pats = table.pat[chosen].tolist() if chosen else []
+    roots = np.asarray(g._ids)[table.root[chosen]].tolist() if chosen else []
+    assignments = [Assignment.fast(sets[i], patterns[pats[i]], roots[i]) for i in order]
     stats.improvements = len(assignments)
-    placement = PlacementStrategy(assignments)
+    placement = PlacementStrategy.from_canonical(assignments)
     if validate or (validate is None and len(g.nodes) <= VALIDATE_MAX_NODES):
         validate_placement(g, placement)
-    order = {a.nodes: i for i, a in enumerate(placement.assignments)}
-    canon = np.empty(len(chosen), dtype=np.int32)
-    for m in chosen.tolist():
-        canon[order[table.node_set(m)]] = m
+    canon = np.asarray([chosen[i] for i in order], dtype=np.int32)
     return DPResult(placement, res.cost_ms, stats,
                     {frozenset(g.nodes): res.cost_ms, frozenset(): 0.0}, device, canon)

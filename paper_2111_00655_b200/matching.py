@@ -111,6 +111,14 @@ class MatchTable:
     def group(self, gi: int) -> range:
         return range(int(self.group_ptr[gi]), int(self.group_ptr[gi + 1]))
 
+    def node_sets(self, ms: list[int]) -> list[frozenset[int]]:
+        """node_set for many matches at once (no per-match cache lookups)."""
+        if self._lists is None:
+            self._lists = (self.members.tolist(), self.mem_ptr.tolist(),
+                           np.asarray(self.graph._ids).tolist())
+        mem, ptr, ids = self._lists
+        return [frozenset([ids[v] for v in mem[ptr[m]:ptr[m + 1]]]) for m in ms]
+
     def node_set(self, m: int) -> frozenset[int]:
         s = self._sets.get(m)
         if s is None:
