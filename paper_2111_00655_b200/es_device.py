@@ -212,3 +212,34 @@ class DeviceEvolution:
 
     def history_values(self) -> np.ndarray:
         return self.history[:min(self.generation + 1, self.history.numel())].cpu().numpy()
+
+
+def evolve_device(g, registry, measurer, dp_placement, epsilon: float, population: int = 65536,
+                  generations: int = 50, seed: int = 0, graph_backend: str | None = None,
+                  kernel_matches=None, tournament: int = 4, mutation_rate: float | None = None,
+                  device=None, process_group=None):
+    """Population-scale graph-level search on the GPU (the device counterpart
+    of `evolve`, tensorplace/evolution.py:195-250): the DP placement seeds
+    row 0, every generation breeds and prices the whole population on the
+    device (one shard per rank when `process_group` spans several GPUs, with
+    an all-gather of the rank elites), and the best genome is decoded back
+    into a placement.  Returns an `ESResult`; `evaluations` counts every
+    priced genome (no fitness cache, unlike `evolve`)."""
+    from .evolution import ESResult, FitnessPlan, resolve_graph_backend
+    target = resolve_graph_backend(registry, graph_backend)
+    plan = FitnessPlan(g, registry, measurer, dp_placement, epsilon, target, kernel_matches)
+    seed_cost = plan.seed_cost
+    if plan.k == 0:
+        return ESResult(dp_placement, seed_cost, seed_cost, (), 0, 0)
+    es = DeviceEvolution(plan, population, seed=seed, tournament=tournament,
+                         mutation_rate=mutation_rate, device=device, process_group=process_group,
+                         history_capacity=max(generations + 1, 1))
+    es.initialize()
+    for _ in range(generations):
+        es.step()
+    best, bits = es.best()
+    placement = plan.decode(bits.tolist(), dp_placement)
+    assert placement is not None  # the elite never regresses below the feasible seed
+    hist = es.history_values()
+    history = tuple((i, float(v)) for i, v in enumerate(hist))
+    return ESResult(placement, best, seed_cost, history, population * (generations + 1), plan.k)

@@ -80,3 +80,22 @@ def test_fused_generation_matches_breed_then_fitness(gpu, name):
     plan.set_path("frontier")  # another walk: the generation falls back to two launches
     assert not plan.fused_generation()
     plan.set_path("auto")
+
+
+@pytest.mark.parametrize("name", ["resnet50", "bert_base"])
+def test_evolve_device_public_api(gpu, name):
+    """evolve_device: DP-seeded device search through the package API; the
+    decoded placement prices (host reference pricing) to the reported cost,
+    which never exceeds the DP seed and reaches the reference evolve's
+    result on these graphs."""
+    case, res, plan = _setup(name)
+    g, reg, meas = build_case(case)
+    res = tp.optimize(g, reg, meas, case["epsilon"])
+    out = tp.evolve_device(g, reg, meas, res.placement, case["epsilon"], population=8192,
+                           generations=30, graph_backend=case["es"]["graph_backend"],
+                           kernel_matches=res.kernel_matches)
+    assert out.cost_ms <= out.seed_cost_ms
+    assert out.cost_ms == tp.placement_cost_graphlevel(meas, g, out.placement, case["epsilon"],
+                                                       reg.graph_backend_ids())
+    assert [c for _, c in out.history] == sorted((c for _, c in out.history), reverse=True)
+    assert out.genome_length == plan.k and out.evaluations == 8192 * 31
