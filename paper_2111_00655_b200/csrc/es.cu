@@ -251,41 +251,28 @@ extern "C" int cb_es_generation(cb_es_plan* p, const uint64_t* d_parents, const 
 
 extern "C" int cb_es_generation_fused(const cb_es_plan* p) { return p && fused_generation_ok(p) ? 1 : 0; }
 
-__global__ void unpack_kv(const cub::KeyValuePair<int, double>* kv, int64_t* idx, double* val) {
-  *idx = kv->key;
-  *val = kv->value;
-}
-
-// best index / value -> idx, val; with a row source also the best row -> elite and
-// the value -> history slot (one launch instead of three host-side copies)
-__global__ void unpack_elite(const cub::KeyValuePair<int, double>* kv, int64_t* idx, double* val,
-                             const uint64_t* __restrict__ pop, int32_t words, uint64_t* elite,
-                             double* hist) {
-  const int64_t i = kv->key;
-  if (threadIdx.x == 0) {
-    *idx = i;
-    *val = kv->value;
-    if (hist) *hist = kv->value;
-  }
-  if (pop)
-    for (int32_t w = threadIdx.x; w < words; w += blockDim.x) elite[w] = pop[i * words + w];
-}
-
-static int argmin_kv(const double* d_fit, int64_t n, cudaStream_t s, cub::KeyValuePair<int, double>** out) {
+// index of the smallest fitness (first on ties) -> *d_idx, value -> *d_val
+static int argmin_to(const double* d_fit, int64_t n, int64_t* d_idx, double* d_val, cudaStream_t s) {
   static thread_local void* tmp = nullptr;
   static thread_local size_t tmp_bytes = 0;
-  static thread_local cub::KeyValuePair<int, double>* kv = nullptr;
   size_t bytes = 0;
-  if (!kv) CB_CUDA_TRY(cudaMalloc((void**)&kv, sizeof(*kv)));
-  CB_CUDA_TRY(cub::DeviceReduce::ArgMin(nullptr, bytes, d_fit, kv, (int)n, s));
+  CB_CUDA_TRY(cub::DeviceReduce::ArgMin(nullptr, bytes, d_fit, d_val, d_idx, n, s));
   if (bytes > tmp_bytes) {
     if (tmp) cudaFree(tmp);
     CB_CUDA_TRY(cudaMalloc(&tmp, bytes));
     tmp_bytes = bytes;
   }
-  CB_CUDA_TRY(cub::DeviceReduce::ArgMin(tmp, bytes, d_fit, kv, (int)n, s));
-  *out = kv;
+  CB_CUDA_TRY(cub::DeviceReduce::ArgMin(tmp, bytes, d_fit, d_val, d_idx, n, s));
   return CB_OK;
+}
+
+// best row -> elite, best value -> history slot (one launch instead of three
+// host-side copies)
+__global__ void copy_elite(const int64_t* idx, const double* val, const uint64_t* __restrict__ pop,
+                           int32_t words, uint64_t* elite, double* hist) {
+  const int64_t i = *idx;
+  if (threadIdx.x == 0 && hist) *hist = *val;
+  for (int32_t w = threadIdx.x; w < words; w += blockDim.x) elite[w] = pop[i * words + w];
 }
 
 extern "C" int cb_argmin_elite(const double* d_fit, int64_t n, const uint64_t* d_pop, int32_t words,
@@ -293,33 +280,18 @@ extern "C" int cb_argmin_elite(const double* d_fit, int64_t n, const uint64_t* d
                                void* stream) {
   CB_ARG_CHECK(d_fit && d_idx && d_val && n > 0 && (!d_pop || (d_elite && words > 0)),
                "cb_argmin_elite: bad arguments");
-  CB_ARG_CHECK(n < (int64_t)0x7fffffff, "cb_argmin_elite: too many rows");
   cudaStream_t s = (cudaStream_t)stream;
-  cub::KeyValuePair<int, double>* kv = nullptr;
-  int rc = argmin_kv(d_fit, n, s, &kv);
+  int rc = argmin_to(d_fit, n, d_idx, d_val, s);
   if (rc != CB_OK) return rc;
-  unpack_elite<<<1, 32, 0, s>>>(kv, d_idx, d_val, d_pop, words, d_elite, d_history_slot);
-  CB_CUDA_TRY(cudaGetLastError());
+  if (d_pop || d_history_slot) {
+    copy_elite<<<1, 32, 0, s>>>(d_idx, d_val, d_pop, d_pop ? words : 0, d_elite, d_history_slot);
+    CB_CUDA_TRY(cudaGetLastError());
+  }
   return CB_OK;
 }
 
 extern "C" int cb_argmin(const double* d_fit, int64_t n, int64_t* d_idx, double* d_val,
                          void* stream) {
   CB_ARG_CHECK(d_fit && d_idx && d_val && n > 0, "cb_argmin: bad arguments");
-  static thread_local void* tmp = nullptr;
-  static thread_local size_t tmp_bytes = 0;
-  static thread_local cub::KeyValuePair<int, double>* kv = nullptr;
-  size_t bytes = 0;
-  cudaStream_t s = (cudaStream_t)stream;
-  if (!kv) CB_CUDA_TRY(cudaMalloc((void**)&kv, sizeof(*kv)));
-  CB_CUDA_TRY(cub::DeviceReduce::ArgMin(nullptr, bytes, d_fit, kv, (int)n, s));
-  if (bytes > tmp_bytes) {
-    if (tmp) cudaFree(tmp);
-    CB_CUDA_TRY(cudaMalloc(&tmp, bytes));
-    tmp_bytes = bytes;
-  }
-  CB_CUDA_TRY(cub::DeviceReduce::ArgMin(tmp, bytes, d_fit, kv, (int)n, s));
-  unpack_kv<<<1, 1, 0, s>>>(kv, d_idx, d_val);
-  CB_CUDA_TRY(cudaGetLastError());
-  return CB_OK;
+  return argmin_to(d_fit, n, d_idx, d_val, (cudaStream_t)stream);
 }

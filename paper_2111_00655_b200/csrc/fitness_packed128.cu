@@ -342,16 +342,16 @@ fitness_pa_kernel(PkArgs a, const uint4* __restrict__ hdr, const uint64_t* __res
           if (merge) {
             // the anchor whose unit ends later survives
             const bool keepA = ((h.w >> (4 * A)) & 0xF) >= ((h.w >> (4 * B)) & 0xF);
-            const uint32_t W = keepA ? A : B, X = keepA ? B : A;
-            uint64_t lo = sl[W][t], hi = sh[W][t];
-            add2(lo, hi, sl[X][t], sh[X][t]);
-            sl[W][t] = lo;
-            sh[W][t] = hi;
-            const uint32_t c = (uint32_t)cs[W][t] + (uint32_t)cs[X][t];
-            cs[W][t] = 0xffffffff00000000ull | c;
-            const LT m = nibeq<LT>(lab, X) & act;
-            lab = (lab & ~m) | (((LT)W * Nib2<LT>::ONE) & m);
-            A = W;
+            const uint32_t win = keepA ? A : B, los = keepA ? B : A;
+            uint64_t lo = sl[win][t], hi = sh[win][t];
+            add2(lo, hi, sl[los][t], sh[los][t]);
+            sl[win][t] = lo;
+            sh[win][t] = hi;
+            const uint32_t c = (uint32_t)cs[win][t] + (uint32_t)cs[los][t];
+            cs[win][t] = 0xffffffff00000000ull | c;
+            const LT m = nibeq<LT>(lab, los) & act;
+            lab = (lab & ~m) | (((LT)win * Nib2<LT>::ONE) & m);
+            A = win;
           }
         }
         for (int j = 0; j < (NE >= 0 ? NE : nend); ++j) {
@@ -510,16 +510,16 @@ fitness_pa_breed_kernel(PkArgs a, const uint4* __restrict__ hdr, BreedArgs br, u
         if (merge) {
           // the anchor whose unit ends later survives
           const bool keepA = ((h.w >> (4 * A)) & 0xF) >= ((h.w >> (4 * B)) & 0xF);
-          const uint32_t W = keepA ? A : B, X = keepA ? B : A;
-          uint64_t lo = sl[W][t], hi = sh[W][t];
-          add2(lo, hi, sl[X][t], sh[X][t]);
-          sl[W][t] = lo;
-          sh[W][t] = hi;
-          const uint32_t c = (uint32_t)cs[W][t] + (uint32_t)cs[X][t];
-          cs[W][t] = 0xffffffff00000000ull | c;
-          const LT m = nibeq<LT>(lab, X) & act;
-          lab = (lab & ~m) | (((LT)W * Nib2<LT>::ONE) & m);
-          A = W;
+          const uint32_t win = keepA ? A : B, los = keepA ? B : A;
+          uint64_t lo = sl[win][t], hi = sh[win][t];
+          add2(lo, hi, sl[los][t], sh[los][t]);
+          sl[win][t] = lo;
+          sh[win][t] = hi;
+          const uint32_t c = (uint32_t)cs[win][t] + (uint32_t)cs[los][t];
+          cs[win][t] = 0xffffffff00000000ull | c;
+          const LT m = nibeq<LT>(lab, los) & act;
+          lab = (lab & ~m) | (((LT)win * Nib2<LT>::ONE) & m);
+          A = win;
         }
       }
       for (int j = 0; j < nend; ++j) {
