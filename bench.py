@@ -25,6 +25,7 @@ tensorplace, oracle/oracle.c) on the host cores for the same workload.
 from __future__ import annotations
 
 import argparse
+import gc
 import json
 import os
 import statistics
@@ -373,17 +374,18 @@ def config_sweep(dev) -> dict:
     for name, cfg in SWEEP.items():
         tp, g, bs = build_workload(name)
         row = {"nodes": len(g.nodes)}
-        for rep in range(2):  # first pass warms module loads / first launches
+        for rep in range(2):  # first pass warms module loads, launches and allocations
             bs.registry._tables.clear()
+            gc.collect()
             torch.cuda.synchronize(dev)
             t0 = time.perf_counter()
             res = tp.optimize(g, bs.registry, bs.measurer, 0.01, validate=False)
             t1 = time.perf_counter()
             plan = tp.FitnessPlan(g, bs.registry, bs.measurer, res.placement, 0.01, bs.graph_backend,
                                   res.kernel_matches)
-            es = DeviceEvolution(plan, cfg["search_pop"] if rep else 1024, seed=0, device=dev)
+            es = DeviceEvolution(plan, cfg["search_pop"], seed=0, device=dev)
             es.initialize()
-            for _ in range(cfg["gens"] if rep else 1):
+            for _ in range(cfg["gens"] if rep else 2):
                 es.step()
             torch.cuda.synchronize(dev)
             t2 = time.perf_counter()
