@@ -17,13 +17,19 @@
 // "dynamic unit" graph: one unit per feasible eligible kernel plus one unit
 // per connected component of fixed target-backend kernels (always on).
 //
-// Evaluation (device): one warp per genome (units fit in shared memory) or
-// one CTA per genome (large graphs, scratch in global memory / L2).  Lanes
-// switch units on from the genome bits, hook the union-find over dynamic
-// edges with shared-memory CAS (lock-free, smaller root wins), accumulate
-// exact region sums with multi-limb shared-memory atomics, and add the
-// region terms and removed op-kernel terms into a 192-bit total that a
-// shuffle reduction finishes and rounds once.
+// Evaluation (device).  The plan orders the units into a "frontier
+// program" (each unit holds a slot from its position to its last
+// neighbour's) and launch_fitness picks the kernel by the program's width F:
+//   F <= 8   fitness_pa_kernel          (fitness_packed128.cu) packed anchor labels
+//   F <= 16  fitness_packed128_kernel / fitness_frontier2_kernel (this file)
+//   F <= 64  fitness_anchor_kernel      (fitness_anchor.cu) union-find anchors
+//   F <= 128 fitness_wide_kernel        (fitness_wide.cu) warp per genome
+//   wider    fitness_smem_kernel / fitness_global_kernel (this file): warp or
+//            CTA per genome, lock-free union-find over the dynamic edges
+//            (shared-memory CAS, smaller root wins), exact region sums with
+//            multi-limb atomics, a shuffle reduction of the 192-bit total.
+// All of them return bit-identical fitness (values in the plan's 128-bit
+// window where it exists, else 192-bit fixed point, rounded once).
 #include <algorithm>
 #include <cstdio>
 #include <cstring>
