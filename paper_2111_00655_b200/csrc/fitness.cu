@@ -1350,6 +1350,24 @@ extern "C" int cb_fitness_host(cb_es_plan* p, const uint64_t* h_pop, int64_t n, 
   // D2H copy of chunk i-1 overlap the fitness kernel of chunk i (copies are
   // asynchronous when the host buffers are pinned).
   const int64_t chunk = std::max<int64_t>(1 << 18, (n + 15) / 16);
+  if (n <= chunk) {
+    // one chunk (small batches, e.g. one `evolve` generation): copy in, price,
+    // copy out on the plan's own stream -- no per-call stream / event setup
+    if (!p->host_stream) CB_CUDA_TRY(cudaStreamCreateWithFlags(&p->host_stream, cudaStreamNonBlocking));
+    cudaStream_t s1 = p->host_stream;
+    CB_CUDA_TRY(cudaMemcpyAsync(p->d_pop_stage.p, h_pop, words * sizeof(uint64_t), cudaMemcpyHostToDevice, s1));
+    int rc1 = launch_fitness(p, p->d_pop_stage.p, n, p->d_fit_stage.p, s1);
+    if (rc1 != CB_OK) return rc1;
+    CB_CUDA_TRY(cudaMemcpyAsync(h_fit, p->d_fit_stage.p, (size_t)n * sizeof(double), cudaMemcpyDeviceToHost, s1));
+    CB_CUDA_TRY(cudaStreamSynchronize(s1));
+    unsigned long long flags1[2] = {0, 0};
+    CB_CUDA_TRY(cudaMemcpy(flags1, p->d_flags.p, sizeof(flags1), cudaMemcpyDeviceToHost));
+    if (flags1[0]) {
+      cb_set_error("a region cost fell outside the exact accumulator range");
+      return CB_ERR_INEXACT;
+    }
+    return CB_OK;
+  }
   cudaStream_t s_in, s_run, s_out;
   CB_CUDA_TRY(cudaStreamCreateWithFlags(&s_in, cudaStreamNonBlocking));
   CB_CUDA_TRY(cudaStreamCreateWithFlags(&s_run, cudaStreamNonBlocking));

@@ -82,8 +82,10 @@ struct cb_es_plan {
   int32_t* h_ovf = nullptr;       // pinned: overflow count of the last finished launch
   int64_t last_anchor_n = 0;
   int32_t auto_pool = 14;
+  cudaStream_t host_stream = nullptr;  // single-chunk cb_fitness_host calls
   ~cb_es_plan() {
     if (h_ovf) cudaFreeHost(h_ovf);
+    if (host_stream) cudaStreamDestroy(host_stream);
   }
   // tournament order keys of the parent population (es.cu)
   DBuf<uint32_t> d_keys;
