@@ -71,6 +71,7 @@ class ESPlanInfo(ctypes.Structure):
         ("seed_cost", c_double),
         ("window_shift", c_int32),
         ("packed_labels", c_int32),
+        ("fsm_transitions", c_int32),
     ]
 
 

@@ -31,6 +31,7 @@
 // All of them return bit-identical fitness (values in the plan's 128-bit
 // window where it exists, else 192-bit fixed point, rounded once).
 #include <algorithm>
+#include <climits>
 #include <cstdio>
 #include <cstring>
 #include <numeric>
@@ -498,7 +499,7 @@ extern "C" int cb_es_plan_create(cb_graph* g, cb_matches* m, int32_t n_kernels,
     if ((e = P->d_pos_of_bit.upload(P->pos_of_bit)) != cudaSuccess) return fail_cuda(e);
     if ((e = P->d_fixed_pos.upload(P->fixed_pos)) != cudaSuccess) return fail_cuda(e);
   }
-  if ((rc = build_anchor_plan(P)) != CB_OK) {
+  if ((rc = build_anchor_plan(P)) != CB_OK || (rc = build_fsm_plan(P)) != CB_OK) {
     delete P;
     return rc;
   }
@@ -523,6 +524,7 @@ extern "C" int cb_es_plan_query(const cb_es_plan* p, cb_es_plan_info* info) {
   info->seed_cost = p->seed_cost;
   info->window_shift = p->anchor_ok ? p->anchor_shift : -1;
   info->packed_labels = p->F > 0 && p->packed_ok ? (p->pa_ok && p->anchor_ok ? 2 : 1) : 0;
+  info->fsm_transitions = p->fsm_ok ? (int32_t)std::min<int64_t>(p->fsm_entries, INT32_MAX) : 0;
   return CB_OK;
 }
 
@@ -545,6 +547,12 @@ extern "C" const char* cb_es_plan_kernel(const cb_es_plan* p) {
   if (!p) return "";
   const bool frontier = p->F > 0 && p->force_path != 0;
   if (frontier && p->force_path == 3) return "fitness_wide_kernel";
+  if (frontier && p->fsm_ok && (p->force_path == 7 || (p->force_path == -1 && p->fsm_auto))) {
+    static thread_local char fbuf[48];
+    std::snprintf(fbuf, sizeof(fbuf), "fitness_fsm_kernel<%d, %d>", p->F <= 4 ? 4 : p->F <= 6 ? 6 : 8,
+                  p->words <= 4 ? p->words : 0);
+    return fbuf;
+  }
   if (frontier && p->pa_ok && p->anchor_ok && (p->force_path == 6 || p->force_path == -1)) {
     // fitness_pa_kernel<F, W>: W = genome words held in registers (0 = loaded on demand)
     static thread_local char buf[48];
@@ -575,7 +583,8 @@ extern "C" int cb_es_plan_set_pool(cb_es_plan* p, int32_t entries) {
 }
 
 extern "C" int cb_es_plan_set_path(cb_es_plan* p, int32_t path) {
-  CB_ARG_CHECK(p && path >= -1 && path <= 6, "cb_es_plan_set_path: bad arguments");
+  CB_ARG_CHECK(p && path >= -1 && path <= 7, "cb_es_plan_set_path: bad arguments");
+  CB_ARG_CHECK(path != 7 || p->fsm_ok, "cb_es_plan_set_path: no finite-state program for this plan");
   CB_ARG_CHECK(path != 6 || (p->pa_ok && p->anchor_ok),
                "cb_es_plan_set_path: no packed anchor program (> 8 slots or values outside a 128-bit window)");
   CB_ARG_CHECK(path != 5 || (p->packed_ok && p->anchor_ok),
@@ -1283,6 +1292,8 @@ static int launch_fitness(cb_es_plan* p, const uint64_t* d_pop, int64_t n, doubl
   if (n <= 0) return CB_OK;
   const bool frontier = p->F > 0 && p->force_path != 0;
   if (frontier && p->force_path == 3) return launch_fitness_wide(p, d_pop, n, d_fit, stream);
+  if (frontier && p->fsm_ok && (p->force_path == 7 || (p->force_path == -1 && p->fsm_auto)))
+    return launch_fitness_fsm(p, d_pop, n, d_fit, stream);
   if (frontier && p->pa_ok && p->anchor_ok && (p->force_path == 6 || p->force_path == -1))
     return launch_fitness_packed_anchor(p, d_pop, n, d_fit, stream);
   if (frontier && p->packed_ok && p->anchor_ok && (p->force_path == 5 || p->force_path == -1))

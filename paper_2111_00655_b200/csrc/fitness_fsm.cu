@@ -1,0 +1,459 @@
+// Frontier walk as a finite-state machine (thread per genome, <= 8 slots).
+//
+// Same semantics as every fitness kernel here (tensorplace/evolution.py:
+// 256-371 decode, tensorplace/cost.py:320-373 graph-level pricing).  The
+// packed-label kernels recompute, for every genome and step, which frontier
+// slots are occupied and how they are grouped into components -- the
+// connectivity part of the walk, which is most of its instructions.  That
+// part depends only on the frontier *state* (the partition of the occupied
+// slots into components, plus whether each component already holds more
+// than one unit) and on the step's genome bit, and the number of reachable
+// states is small (BERT-base: at most 62 per step, 5 798 transitions in
+// all; NasNet-A: 2 784 per step).  So the plan enumerates the reachable
+// states step by step and tabulates every transition: next state plus the
+// arithmetic it implies -- store the unit's sum in its slot, add component
+// sums into the surviving anchor slot, close a one-unit region (its unit's
+// precomputed term) or queue a multi-unit region for pricing.  The kernel
+// then does per step: one table load indexed by (state, bit), and only the
+// listed 128-bit adds.  Components keep their data at their anchor (the
+// member whose unit ends last), as in fitness_pa_kernel.
+#include <algorithm>
+#include <cstring>
+#include <unordered_map>
+
+#include "fitness_plan.cuh"
+
+#define FSM_THREADS 128
+#define FSM_QCAP 64
+
+namespace {
+
+struct FsmArgs {
+  int32_t M, words, shift;
+  fx192 base_const;
+  uint64_t eps_lo, eps_hi;
+  const uint4* __restrict__ hdr;       // [M]: table offset, bit, slot | nend << 8
+  const uint4* __restrict__ table;     // transitions
+  const uint64_t* __restrict__ cold;   // [M][6] rep, off, term1 (128-bit X)
+  const int32_t* __restrict__ cnt;     // [M]
+  const uint64_t* __restrict__ endterm;  // [end entries][2] term1 of each ending unit
+  const uint64_t* __restrict__ infeas;
+  const double* __restrict__ rt;
+  unsigned long long* flags;
+};
+
+__device__ __forceinline__ void fadd2(uint64_t& lo, uint64_t& hi, uint64_t blo, uint64_t bhi) {
+  asm("add.cc.u64 %0, %0, %2;\n\taddc.u64 %1, %1, %3;" : "+l"(lo), "+l"(hi) : "l"(blo), "l"(bhi));
+}
+__device__ __forceinline__ void fsub2(uint64_t& lo, uint64_t& hi, uint64_t blo, uint64_t bhi) {
+  asm("sub.cc.u64 %0, %0, %2;\n\tsubc.u64 %1, %1, %3;" : "+l"(lo), "+l"(hi) : "l"(blo), "l"(bhi));
+}
+
+// Price queue entry `idx` and add its term to the owner lane's accumulator.
+__device__ __forceinline__ void fsm_price(const uint64_t* ql, const uint64_t* qh, const uint64_t* qm, int idx,
+                                          const FsmArgs& a, uint64_t* tlo, uint64_t* thi, bool& inexact) {
+  const fx192 sum = fx_shl(fx192{{ql[idx], qh[idx], 0ull}}, a.shift);
+  const uint64_t m = qm[idx];
+  const double prod = __dmul_rn(fx_to_double(sum), __ldg(a.rt + (uint32_t)m));
+  fx192 t;
+  inexact |= !fx_from_double(prod, t);
+  inexact |= fx_any_below(t, a.shift);
+  const fx192 tx = fx_shr(t, a.shift);
+  inexact |= tx.w[2] != 0ull;
+  uint64_t lo = tx.w[0], hi = tx.w[1];
+  fadd2(lo, hi, a.eps_lo, a.eps_hi);
+  const int owner = (int)(m >> 32);
+  const unsigned long long o0 = atomicAdd(reinterpret_cast<unsigned long long*>(tlo + owner), lo);
+  atomicAdd(reinterpret_cast<unsigned long long*>(thi + owner), hi + ((o0 + lo) < o0));
+}
+
+// Transition entry: x = next | open << 16 | n_merge << 17 | n_emit << 20 | n_single << 23,
+// y = merges (src 3 bits | dst 3 bits) x 5, z = emit anchor slots (3 bits) x 5 |
+// single-close end-list indices (3 bits) x 5 << 15.
+template <int F, int W>
+__global__ void __launch_bounds__(FSM_THREADS)
+fitness_fsm_kernel(FsmArgs a, const uint64_t* __restrict__ pop, int64_t n, double* __restrict__ fit) {
+  constexpr int T = FSM_THREADS;
+  extern __shared__ __align__(16) unsigned char fsm_smem[];
+  uint64_t(*sl)[T] = reinterpret_cast<uint64_t(*)[T]>(fsm_smem);  // [F][T] anchor sums, low word
+  uint64_t(*sh)[T] = sl + F;                                         // high word
+  uint64_t* ql0 = reinterpret_cast<uint64_t*>(sh + F);
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  uint64_t* ql = ql0 + (size_t)warp * 3 * FSM_QCAP;
+  uint64_t* qh = ql + FSM_QCAP;
+  uint64_t* qm = qh + FSM_QCAP;  // low 32: kernel count, high 32: owner lane
+  uint64_t* tlo = ql0 + (size_t)(T / 32) * 3 * FSM_QCAP + (size_t)warp * 64;
+  uint64_t* thi = tlo + 32;
+  uint32_t(*sc)[T] = reinterpret_cast<uint32_t(*)[T]>(ql0 + (size_t)(T / 32) * (3 * FSM_QCAP + 64));
+  tlo[lane] = thi[lane] = 0ull;
+  __syncwarp();
+  int qn = 0;
+  bool inexact = false;
+  const int64_t stride = (int64_t)gridDim.x * T;
+  constexpr int WR = W > 0 ? W : 1;
+  uint64_t pre[WR];
+  if (W > 0) {
+    const int64_t i0 = (int64_t)blockIdx.x * T + t;
+#pragma unroll
+    for (int w = 0; w < WR; ++w) pre[w] = i0 < n ? __ldcs(pop + i0 * W + w) : 0ull;
+  }
+  for (int64_t base = (int64_t)blockIdx.x * T + (t & ~31); base < n; base += stride) {
+    const int64_t i = base + lane;
+    const bool in_range = i < n;
+    const uint64_t* gen = pop + (in_range ? i : 0) * a.words;
+    bool dead = !in_range;
+    uint64_t cur[WR];
+    if (W > 0) {
+#pragma unroll
+      for (int w = 0; w < WR; ++w) {
+        cur[w] = pre[w];
+        dead |= (cur[w] & __ldg(a.infeas + w)) != 0ull;
+      }
+      const int64_t inext = i + stride;  // prefetch the next genome of this thread
+#pragma unroll
+      for (int w = 0; w < WR; ++w) pre[w] = inext < n ? __ldcs(pop + inext * W + w) : 0ull;
+    } else if (in_range) {
+      for (int32_t w = 0; w < a.words; ++w) dead |= (__ldg(gen + w) & __ldg(a.infeas + w)) != 0ull;
+    }
+    uint32_t state = 0u;
+    uint64_t tot_lo = 0ull, tot_hi = 0ull;
+    int32_t cached_word = -1, eo = 0;
+    uint64_t word = 0ull, next_word = W == 0 && a.words > 0 ? __ldg(gen) : 0ull;
+    for (int32_t p = 0; p < a.M; ++p) {
+      const uint4 h = __ldg(a.hdr + p);  // x = table offset, y = bit, z = slot | nend << 8
+      const int32_t bit = (int32_t)h.y;
+      bool on = !dead;
+      if (bit >= 0) {
+        const int32_t wi = bit >> 6;
+        if (wi != cached_word) {  // warp uniform
+          if (W > 0) {
+            word = cur[0];
+#pragma unroll
+            for (int w = 1; w < WR; ++w)
+              if (wi == w) word = cur[w];
+          } else {
+            word = wi == cached_word + 1 ? next_word : __ldg(gen + wi);
+            next_word = wi + 1 < a.words ? __ldg(gen + wi + 1) : 0ull;
+          }
+          if (dead) word = 0ull;
+          cached_word = wi;
+        }
+        on = (word >> (bit & 63)) & 1ull;
+      }
+      const uint4 e = __ldg(a.table + h.x + 2 * state + (on ? 1u : 0u));
+      state = e.x & 0xFFFFu;
+      const int S = h.z & 0xFF;
+      const uint64_t* c = a.cold + (size_t)p * 6;
+      if (on && bit >= 0) {
+        const ulonglong2 off = __ldg(reinterpret_cast<const ulonglong2*>(c + 2));
+        fsub2(tot_lo, tot_hi, off.x, off.y);
+      }
+      if ((e.x >> 16) & 1u) {  // the unit opens its slot (it has a later neighbour or closes later)
+        const ulonglong2 rep = __ldg(reinterpret_cast<const ulonglong2*>(c));
+        sl[S][t] = rep.x;
+        sh[S][t] = rep.y;
+        sc[S][t] = (uint32_t)__ldg(a.cnt + p);
+      }
+      const int nm = (e.x >> 17) & 7;
+      for (int k = 0; k < nm; ++k) {  // component sums into the surviving anchor
+        const int src = (e.y >> (6 * k)) & 7, dst = (e.y >> (6 * k + 3)) & 7;
+        uint64_t lo = sl[dst][t], hi = sh[dst][t];
+        fadd2(lo, hi, sl[src][t], sh[src][t]);
+        sl[dst][t] = lo;
+        sh[dst][t] = hi;
+        sc[dst][t] += sc[src][t];
+      }
+      const int ns = (e.x >> 23) & 7;
+      for (int k = 0; k < ns; ++k) {  // one-unit regions close: their unit's own term
+        const int j = (e.z >> (15 + 3 * k)) & 7;
+        const ulonglong2 v = __ldg(reinterpret_cast<const ulonglong2*>(a.endterm) + eo + j);
+        fadd2(tot_lo, tot_hi, v.x, v.y);
+      }
+      const int ne = (e.x >> 20) & 7;
+      const int nemax = __reduce_max_sync(0xffffffffu, (unsigned)ne);
+      for (int k = 0; k < nemax; ++k) {  // multi-unit regions close: queued for pricing
+        const bool emit = k < ne;
+        const int slot = (e.z >> (3 * k)) & 7;
+        const unsigned closing = __ballot_sync(0xffffffffu, emit);
+        if (closing) {
+          if (emit) {
+            const int at = qn + __popc(closing & ((1u << lane) - 1u));
+            ql[at] = sl[slot][t];
+            qh[at] = sh[slot][t];
+            qm[at] = ((uint64_t)lane << 32) | sc[slot][t];
+          }
+          qn += __popc(closing);
+          if (qn >= 32) {
+            __syncwarp();
+            fsm_price(ql, qh, qm, lane, a, tlo, thi, inexact);
+            __syncwarp();
+            if (lane < qn - 32) {
+              ql[lane] = ql[32 + lane];
+              qh[lane] = qh[32 + lane];
+              qm[lane] = qm[32 + lane];
+            }
+            __syncwarp();
+            qn -= 32;
+          }
+        }
+      }
+      eo += (h.z >> 8) & 0xFF;
+    }
+    __syncwarp();
+    if (lane < qn) fsm_price(ql, qh, qm, lane, a, tlo, thi, inexact);
+    qn = 0;
+    __syncwarp();
+    fadd2(tot_lo, tot_hi, tlo[lane], thi[lane]);
+    tlo[lane] = thi[lane] = 0ull;
+    __syncwarp();
+    if (in_range) {
+      if (dead) {
+        fit[i] = __longlong_as_double(0x7ff0000000000000ll);
+      } else {
+        const uint64_t sx = (uint64_t)((int64_t)tot_hi >> 63);
+        fx192 v = fx_shl(fx192{{tot_lo, tot_hi, sx}}, a.shift);
+        fx_add(v, a.base_const);
+        fit[i] = fx_to_double(v);
+      }
+    }
+  }
+  if (inexact) atomicAdd(a.flags, 1ull);
+}
+
+template <int F, int W>
+int launch_fsm_t(cb_es_plan* p, const uint64_t* d_pop, int64_t n, double* d_fit, cudaStream_t stream) {
+  const size_t smem = (size_t)2 * F * FSM_THREADS * 8 + (size_t)(FSM_THREADS / 32) * (3 * FSM_QCAP + 64) * 8 +
+                      (size_t)F * FSM_THREADS * 4;
+  static bool configured = false;
+  if (!configured) {
+    CB_CUDA_TRY(cudaFuncSetAttribute(fitness_fsm_kernel<F, W>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)smem));
+    configured = true;
+  }
+  int per_sm = 0;
+  CB_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fitness_fsm_kernel<F, W>, FSM_THREADS, smem));
+  if (per_sm < 1) per_sm = 1;
+  FsmArgs a;
+  a.M = p->M;
+  a.words = p->words;
+  a.shift = p->anchor_shift;
+  a.base_const = p->base_const;
+  const fx192 ex = fx_shr(p->eps, p->anchor_shift);
+  a.eps_lo = ex.w[0];
+  a.eps_hi = ex.w[1];
+  a.hdr = reinterpret_cast<const uint4*>(p->d_fsm_hdr.p);
+  a.table = reinterpret_cast<const uint4*>(p->d_fsm_table.p);
+  a.cold = p->d_acold.p;
+  a.cnt = p->d_acnt.p;
+  a.endterm = p->d_fsm_endterm.p;
+  a.infeas = p->d_infeas.p;
+  a.rt = p->d_rt.p;
+  a.flags = p->d_flags.p;
+  const int64_t want = (n + FSM_THREADS - 1) / FSM_THREADS;
+  const int64_t grid = std::min<int64_t>(want, (int64_t)per_sm * cb_sm_count());
+  fitness_fsm_kernel<F, W><<<(unsigned)grid, FSM_THREADS, smem, stream>>>(a, d_pop, n, d_fit);
+  CB_CUDA_TRY(cudaGetLastError());
+  return CB_OK;
+}
+
+template <int F>
+int launch_fsm_w(cb_es_plan* p, const uint64_t* d_pop, int64_t n, double* d_fit, cudaStream_t stream) {
+  switch (p->words) {
+    case 1: return launch_fsm_t<F, 1>(p, d_pop, n, d_fit, stream);
+    case 2: return launch_fsm_t<F, 2>(p, d_pop, n, d_fit, stream);
+    case 3: return launch_fsm_t<F, 3>(p, d_pop, n, d_fit, stream);
+    case 4: return launch_fsm_t<F, 4>(p, d_pop, n, d_fit, stream);
+    default: return launch_fsm_t<F, 0>(p, d_pop, n, d_fit, stream);
+  }
+}
+
+// ------------------------------------------------------------ plan time
+
+// A state: component label per slot (4 bits, 0 = free) and a multi-unit flag
+// per component (bit c-1 for label c); labels numbered by first slot.
+struct FsmState {
+  uint32_t lab = 0, multi = 0;
+  uint64_t key() const { return (uint64_t)lab | ((uint64_t)multi << 32); }
+};
+
+FsmState canonical(const int* lab, const bool* multi_of_label, int F) {
+  int remap[16];
+  for (int i = 0; i < 16; ++i) remap[i] = 0;
+  int next = 0;
+  FsmState s;
+  for (int slot = 0; slot < F; ++slot) {
+    const int l = lab[slot];
+    if (!l) continue;
+    if (!remap[l]) {
+      remap[l] = ++next;
+      if (multi_of_label[l]) s.multi |= 1u << (next - 1);
+    }
+    s.lab |= (uint32_t)remap[l] << (4 * slot);
+  }
+  return s;
+}
+
+}  // namespace
+
+// Enumerate the reachable frontier states step by step and tabulate every
+// (state, bit) transition.  Leaves fsm_ok false when the program is wider
+// than 8 slots, a transition needs more actions than an entry encodes, or
+// the table would exceed 64 MB.
+int build_fsm_plan(cb_es_plan* P) {
+  P->fsm_ok = false;
+  if (!P->anchor_ok || P->F <= 0 || P->F > 8 || P->M == 0) return CB_OK;
+  const int32_t M = P->M, F = P->F;
+  std::vector<std::vector<int32_t>> ends(M);
+  for (int32_t q = 0; q < M; ++q) ends[P->prog_last[q]].push_back(q);
+  std::vector<uint4> table;
+  std::vector<uint4> hdr(M);
+  std::vector<uint64_t> endterm;
+  std::vector<int32_t> occ_end(F, -1);
+  std::vector<FsmState> cur(1);  // the empty frontier
+  std::unordered_map<uint64_t, int32_t> next_ids;
+  std::vector<FsmState> nxt;
+  const size_t cap = (size_t)64 << 20;
+  for (int32_t p = 0; p < M; ++p) {
+    const UnitRec& r = P->prog[p];
+    const int S = r.slot;
+    occ_end[S] = P->prog_last[p];
+    if ((int)ends[p].size() != r.nend) return CB_OK;  // program / end lists disagree
+    for (int32_t q : ends[p]) {
+      const fx192 x = fx_shr(P->prog[q].term1, P->anchor_shift);
+      endterm.push_back(x.w[0]);
+      endterm.push_back(x.w[1]);
+    }
+    hdr[p] = make_uint4((uint32_t)table.size(), (uint32_t)r.bit, (uint32_t)S | ((uint32_t)r.nend << 8), 0u);
+    if ((table.size() + 2 * cur.size()) * sizeof(uint4) > cap) return CB_OK;
+    next_ids.clear();
+    nxt.clear();
+    for (const FsmState& st : cur) {
+      for (int on = 0; on < 2; ++on) {
+        int lab[8];
+        bool multi[17];
+        for (int i = 0; i < 17; ++i) multi[i] = false;
+        for (int s = 0; s < F; ++s) {
+          lab[s] = (st.lab >> (4 * s)) & 0xF;
+          if (lab[s]) multi[lab[s]] = (st.multi >> (lab[s] - 1)) & 1u;
+        }
+        uint32_t open = 0, merges = 0, emits = 0, singles = 0;
+        int n_merge = 0, n_emit = 0, n_single = 0;
+        auto anchor_of = [&](int label) {  // member whose unit ends last (ties: larger slot)
+          int best = -1;
+          for (int s = 0; s < F; ++s)
+            if (lab[s] == label && (best < 0 || occ_end[s] > occ_end[best] || (occ_end[s] == occ_end[best] && s > best)))
+              best = s;
+          return best;
+        };
+        if (on) {
+          int join[8], nj = 0;
+          for (int j = 0; j < r.nback; ++j) {
+            const int b = P->prog_slots[r.back_off + j];
+            const int l = lab[b];
+            if (!l) continue;
+            bool seen = false;
+            for (int k = 0; k < nj; ++k) seen |= join[k] == l;
+            if (!seen) join[nj++] = l;
+          }
+          int anchors[8];
+          for (int k = 0; k < nj; ++k) anchors[k] = anchor_of(join[k]);
+          const int L = 16;  // temporary label of the new component
+          lab[S] = L;
+          multi[L] = nj > 0;
+          for (int k = 0; k < nj; ++k)
+            for (int s = 0; s < F; ++s)
+              if (lab[s] == join[k]) lab[s] = L;
+          const int Wn = anchor_of(L);
+          open = 1;
+          auto add_merge = [&](int src) {
+            if (n_merge >= 5) return false;
+            merges |= ((uint32_t)src | ((uint32_t)Wn << 3)) << (6 * n_merge);
+            ++n_merge;
+            return true;
+          };
+          for (int k = 0; k < nj; ++k)
+            if (anchors[k] != Wn && !add_merge(anchors[k])) return CB_OK;
+          if (S != Wn && !add_merge(S)) return CB_OK;
+        }
+        // releases: a component closes when its last member leaves; its data
+        // is at the anchor it had when the step's releases began (the anchor
+        // ends last, so members still present then end at this step too)
+        int anchor_at[17];
+        for (int l = 0; l < 17; ++l) anchor_at[l] = -1;
+        for (int s = 0; s < F; ++s)
+          if (lab[s] && anchor_at[lab[s]] < 0) anchor_at[lab[s]] = anchor_of(lab[s]);
+        for (int j = 0; j < r.nend; ++j) {
+          const int e = P->prog_slots[r.end_off + j];
+          const int l = lab[e];
+          if (!l) continue;
+          const int A = anchor_at[l];
+          lab[e] = 0;
+          bool left = false;
+          for (int s = 0; s < F; ++s) left |= lab[s] == l;
+          if (left) continue;
+          if (multi[l]) {
+            if (n_emit >= 5) return CB_OK;
+            emits |= (uint32_t)A << (3 * n_emit);
+            ++n_emit;
+          } else {
+            if (n_single >= 5) return CB_OK;
+            singles |= (uint32_t)j << (3 * n_single);  // the unit ending as end-list entry j
+            ++n_single;
+          }
+        }
+        // the new component's label may be 16: remap before canonicalising
+        int lab2[8];
+        bool multi2[17];
+        for (int i = 0; i < 17; ++i) multi2[i] = multi[i];
+        for (int s = 0; s < F; ++s) lab2[s] = lab[s];
+        if (on) {
+          int freel = 1;
+          bool used[17] = {false};
+          for (int s = 0; s < F; ++s) used[lab2[s]] = true;
+          while (used[freel]) ++freel;
+          for (int s = 0; s < F; ++s)
+            if (lab2[s] == 16) lab2[s] = freel;
+          multi2[freel] = multi[16];
+        }
+        const FsmState ns = canonical(lab2, multi2, F);
+        auto it = next_ids.find(ns.key());
+        int32_t nid;
+        if (it == next_ids.end()) {
+          nid = (int32_t)nxt.size();
+          if (nid > 0xFFFF) return CB_OK;
+          next_ids.emplace(ns.key(), nid);
+          nxt.push_back(ns);
+        } else {
+          nid = it->second;
+        }
+        table.push_back(make_uint4((uint32_t)nid | (open << 16) | ((uint32_t)n_merge << 17) |
+                                       ((uint32_t)n_emit << 20) | ((uint32_t)n_single << 23),
+                                   merges, emits | (singles << 15), 0u));
+      }
+    }
+    cur.swap(nxt);
+  }
+  if (endterm.empty()) endterm.assign(2, 0ull);
+  cudaError_t e;
+  if ((e = P->d_fsm_hdr.upload(reinterpret_cast<const uint32_t*>(hdr.data()), hdr.size() * 4)) != cudaSuccess ||
+      (e = P->d_fsm_table.upload(reinterpret_cast<const uint32_t*>(table.data()), table.size() * 4)) !=
+          cudaSuccess ||
+      (e = P->d_fsm_endterm.upload(endterm)) != cudaSuccess) {
+    cb_set_error(std::string("CUDA error in plan upload: ") + cudaGetErrorString(e));
+    return CB_ERR_CUDA;
+  }
+  P->fsm_states_max = 0;
+  P->fsm_entries = (int64_t)table.size();
+  P->fsm_ok = true;
+  // automatic selection only while the table stays cache-resident (NasNet-A's
+  // 13.8 MB table makes every step an L2 round trip: slower than the
+  // packed-label walk); `set_path("fsm")` still forces it
+  P->fsm_auto = table.size() * sizeof(uint4) <= ((size_t)1 << 20);
+  return CB_OK;
+}
+
+int launch_fitness_fsm(cb_es_plan* p, const uint64_t* d_pop, int64_t n, double* d_fit, cudaStream_t stream) {
+  if (p->F <= 4) return launch_fsm_w<4>(p, d_pop, n, d_fit, stream);
+  if (p->F <= 6) return launch_fsm_w<6>(p, d_pop, n, d_fit, stream);
+  return launch_fsm_w<8>(p, d_pop, n, d_fit, stream);
+}

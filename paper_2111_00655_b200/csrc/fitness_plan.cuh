@@ -87,6 +87,14 @@ struct cb_es_plan {
     if (h_ovf) cudaFreeHost(h_ovf);
     if (host_stream) cudaStreamDestroy(host_stream);
   }
+  // finite-state walk (fitness_fsm.cu, <= 8 slots): per-step headers,
+  // transition table, term of every end-list entry's unit
+  bool fsm_ok = false;
+  bool fsm_auto = false;  // chosen by the automatic path (table <= 1 MB)
+  DBuf<uint32_t> d_fsm_hdr, d_fsm_table;
+  DBuf<uint64_t> d_fsm_endterm;
+  int32_t fsm_states_max = 0;
+  int64_t fsm_entries = 0;
   // tournament order keys of the parent population (es.cu)
   DBuf<uint32_t> d_keys;
   // packed anchor walk (fitness_packed128.cu, <= 8 slots): 16-byte step headers
@@ -97,7 +105,8 @@ struct cb_es_plan {
   bool packed_ok = true;     // every unit's back / end lists fit the packed header
   int32_t force_path = -1;  // -1 auto, 0 union-find, 1 frontier, 2 frontier (smem labels),
                             // 3 sparse warp-per-genome walk, 4 anchor walk (thread per genome),
-                            // 5 packed-label walk in the 128-bit window, 6 packed anchor walk
+                            // 5 packed-label walk in the 128-bit window, 6 packed anchor walk,
+                            // 7 finite-state walk
 };
 
 // fitness_wide.cu: warp-per-genome sparse walk of the frontier program (F <= 128)
@@ -114,6 +123,9 @@ int launch_fitness_packed128(cb_es_plan* p, const uint64_t* d_pop, int64_t n, do
                              cudaStream_t stream);
 int launch_fitness_packed_anchor(cb_es_plan* p, const uint64_t* d_pop, int64_t n, double* d_fit,
                                  cudaStream_t stream);
+// fitness_fsm.cu: frontier states enumerated at plan time, walk by table
+int build_fsm_plan(cb_es_plan* p);
+int launch_fitness_fsm(cb_es_plan* p, const uint64_t* d_pop, int64_t n, double* d_fit, cudaStream_t stream);
 // fused breed + packed anchor fitness (one kernel per generation, <= 4 words)
 struct BreedArgs;
 bool fused_generation_ok(const cb_es_plan* p);

@@ -231,7 +231,7 @@ class FitnessPlan:
         when the plan fits one), the
         anchor kernel up to 64, the wide kernel up to 128, else union-find."""
         code = {"auto": -1, "unionfind": 0, "frontier": 1, "frontier_smem": 2, "wide": 3,
-                "anchor": 4, "packed128": 5, "packed_anchor": 6}[path]
+                "anchor": 4, "packed128": 5, "packed_anchor": 6, "fsm": 7}[path]
         nat.check(nat.lib().cb_es_plan_set_path(self.handle.raw, code))
 
     def kernel_name(self) -> str:
@@ -254,6 +254,10 @@ class FitnessPlan:
             f = name[name.index('<') + 1:].split(',')[0]
             return f"fitness_pa_breed_kernel<{f}, {self.words}>"
         return name
+
+    def has_fsm(self) -> bool:
+        """Whether the 'fsm' path applies (finite-state program built)."""
+        return self.info.fsm_transitions > 0
 
     def has_packed_anchor(self) -> bool:
         """Whether the 'packed_anchor' path applies (<= 8 frontier slots,

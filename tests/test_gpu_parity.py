@@ -161,7 +161,7 @@ def test_fitness_paths_agree_with_oracle(gpu, case):
         assert np.array_equal(plan.evaluate(genomes), want), "anchor, pool of 1"
         plan.set_pool(16)
     if 0 < plan.info.frontier_slots <= 32:
-        for path in ("frontier", "frontier_smem") + (("packed128",) if plan.has_packed128() else ()) + (("packed_anchor",) if plan.has_packed_anchor() else ()):
+        for path in ("frontier", "frontier_smem") + (("packed128",) if plan.has_packed128() else ()) + (("packed_anchor",) if plan.has_packed_anchor() else ()) + (("fsm",) if plan.has_fsm() else ()):
             plan.set_path(path)
             assert np.array_equal(plan.evaluate(genomes), want), path
     plan.set_path("auto")

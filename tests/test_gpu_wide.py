@@ -79,7 +79,7 @@ def test_wide_kernel_agrees_on_models(gpu, name):
     genomes = _genomes(plan, np.random.default_rng(5), 2000)
     plan.set_path("auto")
     want = plan.evaluate(genomes)
-    for path in ("wide", "anchor", "frontier") + (("packed128",) if plan.has_packed128() else ()) + (("packed_anchor",) if plan.has_packed_anchor() else ()):
+    for path in ("wide", "anchor", "frontier") + (("packed128",) if plan.has_packed128() else ()) + (("packed_anchor",) if plan.has_packed_anchor() else ()) + (("fsm",) if plan.has_fsm() else ()):
         plan.set_path(path)
         assert np.array_equal(plan.evaluate(genomes), want), path
     plan.set_path("auto")
@@ -163,6 +163,8 @@ def test_edge_plans_every_path(gpu, n_rows):
             paths.append("packed128")
         if plan.has_packed_anchor():
             paths.append("packed_anchor")
+        if plan.has_fsm():
+            paths.append("fsm")
         for path in paths:
             plan.set_path(path)
             assert np.array_equal(plan.evaluate(genomes), want), (name, path)

@@ -26,6 +26,8 @@ for name, g, bs in (
         paths.append("packed128")
     if plan.has_packed_anchor():
         paths.append("packed_anchor")
+    if plan.has_fsm():
+        paths.append("fsm")
     for path in paths:
         plan.set_path(path)
         got = plan.evaluate(genomes)
