@@ -12,10 +12,11 @@
 // all; NasNet-A: 2 784 per step).  So the plan enumerates the reachable
 // states step by step and tabulates every transition: next state plus the
 // arithmetic it implies -- store the unit's sum in its slot, add component
-// sums into the surviving anchor slot, close a one-unit region (its unit's
-// precomputed term) or queue a multi-unit region for pricing.  The kernel
-// then does per step: one table load indexed by (state, bit), and only the
-// listed 128-bit adds.  Components keep their data at their anchor (the
+// sums into the surviving anchor slot, queue closed multi-unit regions for
+// pricing -- and one exact delta folding every genome-independent term of
+// the transition (closed one-unit regions, the removed kernel term).  The
+// kernel then does per step: one 32-byte table load indexed by (state, bit),
+// one 128-bit add, and only the listed sum moves.  Components keep their data at their anchor (the
 // member whose unit ends last), as in fitness_pa_kernel.
 #include <algorithm>
 #include <cstring>
@@ -36,7 +37,6 @@ struct FsmArgs {
   const uint4* __restrict__ table;     // transitions
   const uint64_t* __restrict__ cold;   // [M][6] rep, off, term1 (128-bit X)
   const int32_t* __restrict__ cnt;     // [M]
-  const uint64_t* __restrict__ endterm;  // [end entries][2] term1 of each ending unit
   const uint64_t* __restrict__ infeas;
   const double* __restrict__ rt;
   unsigned long long* flags;
@@ -44,9 +44,6 @@ struct FsmArgs {
 
 __device__ __forceinline__ void fadd2(uint64_t& lo, uint64_t& hi, uint64_t blo, uint64_t bhi) {
   asm("add.cc.u64 %0, %0, %2;\n\taddc.u64 %1, %1, %3;" : "+l"(lo), "+l"(hi) : "l"(blo), "l"(bhi));
-}
-__device__ __forceinline__ void fsub2(uint64_t& lo, uint64_t& hi, uint64_t blo, uint64_t bhi) {
-  asm("sub.cc.u64 %0, %0, %2;\n\tsubc.u64 %1, %1, %3;" : "+l"(lo), "+l"(hi) : "l"(blo), "l"(bhi));
 }
 
 // Price queue entry `idx` and add its term to the owner lane's accumulator.
@@ -67,9 +64,10 @@ __device__ __forceinline__ void fsm_price(const uint64_t* ql, const uint64_t* qh
   atomicAdd(reinterpret_cast<unsigned long long*>(thi + owner), hi + ((o0 + lo) < o0));
 }
 
-// Transition entry: x = next | open << 16 | n_merge << 17 | n_emit << 20 | n_single << 23,
-// y = merges (src 3 bits | dst 3 bits) x 5, z = emit anchor slots (3 bits) x 5 |
-// single-close end-list indices (3 bits) x 5 << 15.
+// Transition entry (32 bytes): x = next | open << 16 | n_merge << 17 | n_emit << 20,
+// y = merges (src 3 bits | dst 3 bits) x 5, z = emit anchor slots (3 bits) x 5;
+// then the transition's exact 128-bit delta: the terms of the one-unit
+// regions it closes minus the removed op-kernel term of an offloaded unit.
 template <int F, int W>
 __global__ void __launch_bounds__(FSM_THREADS)
 fitness_fsm_kernel(FsmArgs a, const uint64_t* __restrict__ pop, int64_t n, double* __restrict__ fit) {
@@ -117,7 +115,7 @@ fitness_fsm_kernel(FsmArgs a, const uint64_t* __restrict__ pop, int64_t n, doubl
     }
     uint32_t state = 0u;
     uint64_t tot_lo = 0ull, tot_hi = 0ull;
-    int32_t cached_word = -1, eo = 0;
+    int32_t cached_word = -1;
     uint64_t word = 0ull, next_word = W == 0 && a.words > 0 ? __ldg(gen) : 0ull;
     for (int32_t p = 0; p < a.M; ++p) {
       const uint4 h = __ldg(a.hdr + p);  // x = table offset, y = bit, z = slot | nend << 8
@@ -140,16 +138,14 @@ fitness_fsm_kernel(FsmArgs a, const uint64_t* __restrict__ pop, int64_t n, doubl
         }
         on = (word >> (bit & 63)) & 1ull;
       }
-      const uint4 e = __ldg(a.table + h.x + 2 * state + (on ? 1u : 0u));
+      const uint4* ent = a.table + 2 * ((size_t)h.x + 2 * state + (on ? 1u : 0u));
+      const uint4 e = __ldg(ent);
+      const uint4 dv = __ldg(ent + 1);  // exact delta: closed one-unit regions' terms - removed term
       state = e.x & 0xFFFFu;
       const int S = h.z & 0xFF;
-      const uint64_t* c = a.cold + (size_t)p * 6;
-      if (on && bit >= 0) {
-        const ulonglong2 off = __ldg(reinterpret_cast<const ulonglong2*>(c + 2));
-        fsub2(tot_lo, tot_hi, off.x, off.y);
-      }
-      if ((e.x >> 16) & 1u) {  // the unit opens its slot (it has a later neighbour or closes later)
-        const ulonglong2 rep = __ldg(reinterpret_cast<const ulonglong2*>(c));
+      fadd2(tot_lo, tot_hi, ((uint64_t)dv.y << 32) | dv.x, ((uint64_t)dv.w << 32) | dv.z);
+      if ((e.x >> 16) & 1u) {  // the unit opens its slot
+        const ulonglong2 rep = __ldg(reinterpret_cast<const ulonglong2*>(a.cold + (size_t)p * 6));
         sl[S][t] = rep.x;
         sh[S][t] = rep.y;
         sc[S][t] = (uint32_t)__ldg(a.cnt + p);
@@ -162,12 +158,6 @@ fitness_fsm_kernel(FsmArgs a, const uint64_t* __restrict__ pop, int64_t n, doubl
         sl[dst][t] = lo;
         sh[dst][t] = hi;
         sc[dst][t] += sc[src][t];
-      }
-      const int ns = (e.x >> 23) & 7;
-      for (int k = 0; k < ns; ++k) {  // one-unit regions close: their unit's own term
-        const int j = (e.z >> (15 + 3 * k)) & 7;
-        const ulonglong2 v = __ldg(reinterpret_cast<const ulonglong2*>(a.endterm) + eo + j);
-        fadd2(tot_lo, tot_hi, v.x, v.y);
       }
       const int ne = (e.x >> 20) & 7;
       const int nemax = __reduce_max_sync(0xffffffffu, (unsigned)ne);
@@ -197,7 +187,6 @@ fitness_fsm_kernel(FsmArgs a, const uint64_t* __restrict__ pop, int64_t n, doubl
           }
         }
       }
-      eo += (h.z >> 8) & 0xFF;
     }
     __syncwarp();
     if (lane < qn) fsm_price(ql, qh, qm, lane, a, tlo, thi, inexact);
@@ -245,7 +234,6 @@ int launch_fsm_t(cb_es_plan* p, const uint64_t* d_pop, int64_t n, double* d_fit,
   a.table = reinterpret_cast<const uint4*>(p->d_fsm_table.p);
   a.cold = p->d_acold.p;
   a.cnt = p->d_acnt.p;
-  a.endterm = p->d_fsm_endterm.p;
   a.infeas = p->d_infeas.p;
   a.rt = p->d_rt.p;
   a.flags = p->d_flags.p;
@@ -307,7 +295,6 @@ int build_fsm_plan(cb_es_plan* P) {
   for (int32_t q = 0; q < M; ++q) ends[P->prog_last[q]].push_back(q);
   std::vector<uint4> table;
   std::vector<uint4> hdr(M);
-  std::vector<uint64_t> endterm;
   std::vector<int32_t> occ_end(F, -1);
   std::vector<FsmState> cur(1);  // the empty frontier
   std::unordered_map<uint64_t, int32_t> next_ids;
@@ -318,13 +305,8 @@ int build_fsm_plan(cb_es_plan* P) {
     const int S = r.slot;
     occ_end[S] = P->prog_last[p];
     if ((int)ends[p].size() != r.nend) return CB_OK;  // program / end lists disagree
-    for (int32_t q : ends[p]) {
-      const fx192 x = fx_shr(P->prog[q].term1, P->anchor_shift);
-      endterm.push_back(x.w[0]);
-      endterm.push_back(x.w[1]);
-    }
-    hdr[p] = make_uint4((uint32_t)table.size(), (uint32_t)r.bit, (uint32_t)S | ((uint32_t)r.nend << 8), 0u);
-    if ((table.size() + 2 * cur.size()) * sizeof(uint4) > cap) return CB_OK;
+    hdr[p] = make_uint4((uint32_t)(table.size() / 2), (uint32_t)r.bit, (uint32_t)S | ((uint32_t)r.nend << 8), 0u);
+    if ((table.size() + 4 * cur.size()) * sizeof(uint4) > cap) return CB_OK;
     next_ids.clear();
     nxt.clear();
     for (const FsmState& st : cur) {
@@ -336,8 +318,9 @@ int build_fsm_plan(cb_es_plan* P) {
           lab[s] = (st.lab >> (4 * s)) & 0xF;
           if (lab[s]) multi[lab[s]] = (st.multi >> (lab[s] - 1)) & 1u;
         }
-        uint32_t open = 0, merges = 0, emits = 0, singles = 0;
-        int n_merge = 0, n_emit = 0, n_single = 0;
+        uint32_t open = 0, merges = 0, emits = 0;
+        int n_merge = 0, n_emit = 0;
+        fx192 delta = fx_zero();  // terms of the one-unit regions closed by this transition
         auto anchor_of = [&](int label) {  // member whose unit ends last (ties: larger slot)
           int best = -1;
           for (int s = 0; s < F; ++s)
@@ -396,9 +379,7 @@ int build_fsm_plan(cb_es_plan* P) {
             emits |= (uint32_t)A << (3 * n_emit);
             ++n_emit;
           } else {
-            if (n_single >= 5) return CB_OK;
-            singles |= (uint32_t)j << (3 * n_single);  // the unit ending as end-list entry j
-            ++n_single;
+            fx_add(delta, P->prog[ends[p][j]].term1);  // its unit: end-list entry j
           }
         }
         // the new component's label may be 16: remap before canonicalising
@@ -426,24 +407,41 @@ int build_fsm_plan(cb_es_plan* P) {
         } else {
           nid = it->second;
         }
+        // exact delta of the transition: terms of the one-unit regions it
+        // closes minus the removed op-kernel term of an offloaded unit
+        if (on && r.bit >= 0) fx_sub(delta, r.off);
+        // to the 128-bit window: shift the magnitude, then restore the sign
+        const bool neg = (delta.w[2] >> 63) != 0;
+        fx192 mag = delta;
+        if (neg) {
+          mag = fx_zero();
+          fx_sub(mag, delta);
+        }
+        fx192 dx = fx_shr(mag, P->anchor_shift);
+        if (dx.w[2] != 0 || (dx.w[1] >> 62) != 0) return CB_OK;  // outside the window
+        if (neg) {
+          const fx192 m2 = dx;
+          dx = fx_zero();
+          fx_sub(dx, m2);
+        }
         table.push_back(make_uint4((uint32_t)nid | (open << 16) | ((uint32_t)n_merge << 17) |
-                                       ((uint32_t)n_emit << 20) | ((uint32_t)n_single << 23),
-                                   merges, emits | (singles << 15), 0u));
+                                       ((uint32_t)n_emit << 20),
+                                   merges, emits, 0u));
+        table.push_back(make_uint4((uint32_t)dx.w[0], (uint32_t)(dx.w[0] >> 32), (uint32_t)dx.w[1],
+                                   (uint32_t)(dx.w[1] >> 32)));
       }
     }
     cur.swap(nxt);
   }
-  if (endterm.empty()) endterm.assign(2, 0ull);
   cudaError_t e;
   if ((e = P->d_fsm_hdr.upload(reinterpret_cast<const uint32_t*>(hdr.data()), hdr.size() * 4)) != cudaSuccess ||
       (e = P->d_fsm_table.upload(reinterpret_cast<const uint32_t*>(table.data()), table.size() * 4)) !=
-          cudaSuccess ||
-      (e = P->d_fsm_endterm.upload(endterm)) != cudaSuccess) {
+          cudaSuccess) {
     cb_set_error(std::string("CUDA error in plan upload: ") + cudaGetErrorString(e));
     return CB_ERR_CUDA;
   }
   P->fsm_states_max = 0;
-  P->fsm_entries = (int64_t)table.size();
+  P->fsm_entries = (int64_t)table.size() / 2;
   P->fsm_ok = true;
   // automatic selection only while the table stays cache-resident (NasNet-A's
   // 13.8 MB table makes every step an L2 round trip: slower than the

@@ -87,12 +87,11 @@ struct cb_es_plan {
     if (h_ovf) cudaFreeHost(h_ovf);
     if (host_stream) cudaStreamDestroy(host_stream);
   }
-  // finite-state walk (fitness_fsm.cu, <= 8 slots): per-step headers,
-  // transition table, term of every end-list entry's unit
+  // finite-state walk (fitness_fsm.cu, <= 8 slots): per-step headers and
+  // the transition table
   bool fsm_ok = false;
   bool fsm_auto = false;  // chosen by the automatic path (table <= 1 MB)
   DBuf<uint32_t> d_fsm_hdr, d_fsm_table;
-  DBuf<uint64_t> d_fsm_endterm;
   int32_t fsm_states_max = 0;
   int64_t fsm_entries = 0;
   // tournament order keys of the parent population (es.cu)
