@@ -92,16 +92,10 @@ __device__ __forceinline__ X128 ld_x(const uint64_t* p) {
 // have several entries in one batch).
 __device__ __forceinline__ void an_price(const uint64_t* ql, const uint64_t* qh, const uint64_t* qm, int idx,
                                          const AnArgs& a, uint64_t* tlo, uint64_t* thi, bool& inexact) {
-  const fx192 x = {{ql[idx], qh[idx], 0ull}};
-  const fx192 sum = fx_shl(x, a.shift);
   const uint64_t m = qm[idx];
-  const double prod = __dmul_rn(fx_to_double(sum), __ldg(a.rt + (uint32_t)m));
-  fx192 t;
-  inexact |= !fx_from_double(prod, t);
-  inexact |= fx_any_below(t, a.shift);
-  const fx192 tx = fx_shr(t, a.shift);
-  inexact |= tx.w[2] != 0ull;
-  X128 term = {tx.w[0], tx.w[1]};
+  const double prod = __dmul_rn(x128_to_double(ql[idx], qh[idx], a.shift), __ldg(a.rt + (uint32_t)m));
+  X128 term;
+  inexact |= !x128_from_double(prod, a.shift, term.lo, term.hi);
   x_add(term, a.eps);
   const int owner = (int)(m >> 32);
   unsigned long long* w0 = reinterpret_cast<unsigned long long*>(tlo + owner);

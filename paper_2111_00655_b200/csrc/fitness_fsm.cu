@@ -49,15 +49,10 @@ __device__ __forceinline__ void fadd2(uint64_t& lo, uint64_t& hi, uint64_t blo, 
 // Price queue entry `idx` and add its term to the owner lane's accumulator.
 __device__ __forceinline__ void fsm_price(const uint64_t* ql, const uint64_t* qh, const uint64_t* qm, int idx,
                                           const FsmArgs& a, uint64_t* tlo, uint64_t* thi, bool& inexact) {
-  const fx192 sum = fx_shl(fx192{{ql[idx], qh[idx], 0ull}}, a.shift);
   const uint64_t m = qm[idx];
-  const double prod = __dmul_rn(fx_to_double(sum), __ldg(a.rt + (uint32_t)m));
-  fx192 t;
-  inexact |= !fx_from_double(prod, t);
-  inexact |= fx_any_below(t, a.shift);
-  const fx192 tx = fx_shr(t, a.shift);
-  inexact |= tx.w[2] != 0ull;
-  uint64_t lo = tx.w[0], hi = tx.w[1];
+  const double prod = __dmul_rn(x128_to_double(ql[idx], qh[idx], a.shift), __ldg(a.rt + (uint32_t)m));
+  uint64_t lo, hi;
+  inexact |= !x128_from_double(prod, a.shift, lo, hi);
   fadd2(lo, hi, a.eps_lo, a.eps_hi);
   const int owner = (int)(m >> 32);
   const unsigned long long o0 = atomicAdd(reinterpret_cast<unsigned long long*>(tlo + owner), lo);

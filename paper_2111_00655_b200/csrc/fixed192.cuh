@@ -261,3 +261,87 @@ FXI int fx_highest_bit(const fx192& a) {
     if (a.w[l]) return l * 64 + 63 - fx_clz64(a.w[l]);
   return -1;
 }
+
+// ------------------------------------------------------ 128-bit window
+// A value carried in a plan's 128-bit window is X * 2^(s-128) with X a
+// non-negative integer below 2^126 (region sums and terms).  These convert
+// it to and from double directly, without the 192-bit detour: round to
+// nearest, ties to even (as fx_to_double); the reverse conversion reports
+// bits that would be lost.
+
+FXI double fx_pow2(int k) {  // 2^k for -1022 <= k <= 1023
+  return fx_double_of((uint64_t)(k + 1023) << 52);
+}
+
+// low 64 bits of (hi:lo) >> k, 0 <= k < 128
+FXI uint64_t x128_shr64(uint64_t lo, uint64_t hi, int k) {
+  if (k == 0) return lo;
+  if (k < 64) return (lo >> k) | (hi << (64 - k));
+  if (k == 64) return hi;
+  return hi >> (k - 64);
+}
+
+// any of the low k bits of hi:lo set, 0 <= k <= 128
+FXI bool x128_low_nonzero(uint64_t lo, uint64_t hi, int k) {
+  if (k == 0) return false;
+  if (k < 64) return (lo & ((1ull << k) - 1ull)) != 0ull;
+  if (k == 64) return lo != 0ull;
+  if (k < 128) return lo != 0ull || (hi & ((1ull << (k - 64)) - 1ull)) != 0ull;
+  return (lo | hi) != 0ull;
+}
+
+// X = hi:lo (X < 2^126), value X * 2^(s-128), rounded to the nearest double
+FXI double x128_to_double(uint64_t lo, uint64_t hi, int s) {
+  if ((lo | hi) == 0ull) return 0.0;
+  const int msb = hi ? 127 - fx_clz64(hi) : 63 - fx_clz64(lo);
+  if (msb <= 52) return (double)lo * fx_pow2(s - 128);  // exact: X < 2^53
+  const int sh = msb - 52;                                // 1 .. 73 bits dropped
+  uint64_t m = x128_shr64(lo, hi, sh) & ((1ull << 53) - 1ull);
+  const bool round_bit = (x128_shr64(lo, hi, sh - 1) & 1ull) != 0ull;
+  const bool sticky = x128_low_nonzero(lo, hi, sh - 1);
+  int e = sh;
+  if (round_bit && (sticky || (m & 1ull))) {
+    m += 1ull;
+    if (m == (1ull << 53)) {
+      m >>= 1;
+      e += 1;
+    }
+  }
+  return (double)m * fx_pow2(e + s - 128);
+}
+
+// d (non-negative, finite) as X with value X * 2^(s-128); false when bits
+// below 2^(s-128) would be lost or X would reach 2^126
+FXI bool x128_from_double(double d, int s, uint64_t& lo, uint64_t& hi) {
+  lo = hi = 0ull;
+  const uint64_t bits = fx_bits_of(d);
+  if ((bits << 1) == 0ull) return true;  // +0.0 / -0.0
+  if (bits >> 63) return false;
+  const int ex = (int)((bits >> 52) & 0x7ff);
+  if (ex == 0x7ff) return false;
+  uint64_t m = bits & ((1ull << 52) - 1ull);
+  int e;
+  if (ex == 0) {
+    e = -1074;
+  } else {
+    m |= 1ull << 52;
+    e = ex - 1075;
+  }
+  const int t = e + 128 - s;  // X = m * 2^t
+  if (t < 0) {
+    if (t <= -64) return false;  // m != 0: all bits would be lost
+    if (m & ((1ull << -t) - 1ull)) return false;
+    lo = m >> -t;
+    return true;
+  }
+  if (t + 53 > 126) return false;
+  if (t == 0) {
+    lo = m;
+  } else if (t < 64) {
+    lo = m << t;
+    hi = m >> (64 - t);
+  } else {
+    hi = m << (t - 64);
+  }
+  return true;
+}
