@@ -113,7 +113,8 @@ fitness_fsm_kernel(FsmArgs a, const uint64_t* __restrict__ pop, int64_t n, doubl
     int32_t cached_word = -1;
     uint64_t word = 0ull, next_word = W == 0 && a.words > 0 ? __ldg(gen) : 0ull;
     for (int32_t p = 0; p < a.M; ++p) {
-      const uint4 h = __ldg(a.hdr + p);  // x = table offset, y = bit, z = slot | nend << 8
+      // x = table offset, y = bit, z = slot | nend << 8, w = step's max merges | max emits << 8
+      const uint4 h = __ldg(a.hdr + p);
       const int32_t bit = (int32_t)h.y;
       bool on = !dead;
       if (bit >= 0) {
@@ -145,7 +146,7 @@ fitness_fsm_kernel(FsmArgs a, const uint64_t* __restrict__ pop, int64_t n, doubl
         sh[S][t] = rep.y;
         sc[S][t] = (uint32_t)__ldg(a.cnt + p);
       }
-      const int nm = (e.x >> 17) & 7;
+      const int nm = (h.w & 0xFF) ? (e.x >> 17) & 7 : 0;
       for (int k = 0; k < nm; ++k) {  // component sums into the surviving anchor
         const int src = (e.y >> (6 * k)) & 7, dst = (e.y >> (6 * k + 3)) & 7;
         uint64_t lo = sl[dst][t], hi = sh[dst][t];
@@ -155,7 +156,7 @@ fitness_fsm_kernel(FsmArgs a, const uint64_t* __restrict__ pop, int64_t n, doubl
         sc[dst][t] += sc[src][t];
       }
       const int ne = (e.x >> 20) & 7;
-      const int nemax = __reduce_max_sync(0xffffffffu, (unsigned)ne);
+      const int nemax = (h.w >> 8) ? __reduce_max_sync(0xffffffffu, (unsigned)ne) : 0;
       for (int k = 0; k < nemax; ++k) {  // multi-unit regions close: queued for pricing
         const bool emit = k < ne;
         const int slot = (e.z >> (3 * k)) & 7;
@@ -426,6 +427,14 @@ int build_fsm_plan(cb_es_plan* P) {
                                    (uint32_t)(dx.w[1] >> 32)));
       }
     }
+    // step-level maxima: the kernel skips the emit / merge loops when no
+    // transition of the step has any (warp-uniform)
+    uint32_t max_emit = 0, max_merge = 0;
+    for (size_t k = hdr[p].x * 2; k < table.size(); k += 2) {
+      max_merge = std::max(max_merge, (table[k].x >> 17) & 7u);
+      max_emit = std::max(max_emit, (table[k].x >> 20) & 7u);
+    }
+    hdr[p].w = max_merge | (max_emit << 8);
     cur.swap(nxt);
   }
   cudaError_t e;
