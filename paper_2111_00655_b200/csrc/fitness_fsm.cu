@@ -134,9 +134,9 @@ fitness_fsm_kernel(FsmArgs a, const uint64_t* __restrict__ pop, int64_t n, doubl
         }
         on = (word >> (bit & 63)) & 1ull;
       }
-      const uint4* ent = a.table + 2 * ((size_t)h.x + 2 * state + (on ? 1u : 0u));
-      const uint4 e = __ldg(ent);
-      const uint4 dv = __ldg(ent + 1);  // exact delta: closed one-unit regions' terms - removed term
+      const uint32_t ent = 2u * (h.x + 2u * state + (on ? 1u : 0u));  // 32-bit index math
+      const uint4 e = __ldg(a.table + ent);
+      const uint4 dv = __ldg(a.table + ent + 1u);  // exact delta: closed one-unit regions' terms - removed term
       state = e.x & 0xFFFFu;
       const int S = h.z & 0xFF;
       fadd2(tot_lo, tot_hi, ((uint64_t)dv.y << 32) | dv.x, ((uint64_t)dv.w << 32) | dv.z);
