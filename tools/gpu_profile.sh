@@ -5,7 +5,7 @@ ARGS="--steps 3 --warmup 3 --no-cpu-baseline --e2e-steps 1 --search-generations 
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 2000 --csv \
   --log-file gpurun_out/launches.csv python bench.py $ARGS > gpurun_out/ncu_launch_run.log 2>&1
 tail -2 gpurun_out/ncu_launch_run.log
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:"fitness_pa_kernel" -s 8 -c 1 \
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:"fitness_fsm_kernel" -s 8 -c 1 \
   -o gpurun_out/fitness_full python bench.py $ARGS > gpurun_out/ncu_full_run.log 2>&1
 tail -2 gpurun_out/ncu_full_run.log
 timeout 900 ncu --set full --clock-control none -k regex:"dp_narrow|match_count|match_fill|breed_thread|price_kernel" -c 6 \
