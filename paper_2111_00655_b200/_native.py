@@ -72,6 +72,7 @@ class ESPlanInfo(ctypes.Structure):
         ("window_shift", c_int32),
         ("packed_labels", c_int32),
         ("fsm_transitions", c_int32),
+        ("fsm_entry_bytes", c_int32),
     ]
 
 

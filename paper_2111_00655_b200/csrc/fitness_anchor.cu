@@ -404,6 +404,7 @@ int build_anchor_plan(cb_es_plan* P) {
   const int hb = fx_highest_bit(bound);
   if (hb - lo > 125) return CB_OK;  // partial sums need more than 127 bits
   P->anchor_shift = lo;
+  P->anchor_span = hb - lo;
   std::vector<AHot> hot(M);
   std::vector<uint64_t> cold((size_t)M * 6);
   std::vector<int32_t> cnt(M);

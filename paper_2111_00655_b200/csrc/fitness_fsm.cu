@@ -19,7 +19,10 @@
 // one 128-bit add, and only the listed sum moves.  Components keep their data at their anchor (the
 // member whose unit ends last), as in fitness_pa_kernel.
 #include <algorithm>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
+#include <string>
 #include <unordered_map>
 
 #include "fitness_plan.cuh"
@@ -34,7 +37,10 @@ struct FsmArgs {
   fx192 base_const;
   uint64_t eps_lo, eps_hi;
   const uint4* __restrict__ hdr;       // [M]: table offset, bit, slot | nend << 8
-  const uint4* __restrict__ table;     // transitions
+  const uint4* __restrict__ table;     // transitions (32-byte layout)
+  const uint2* __restrict__ ctable;    // transitions (8-byte layout)
+  const uint4* __restrict__ dtab;      // distinct deltas of the 8-byte layout
+  int32_t n_delta;
   const uint64_t* __restrict__ cold;   // [M][6] rep, off, term1 (128-bit X)
   const int32_t* __restrict__ cnt;     // [M]
   const uint64_t* __restrict__ infeas;
@@ -63,11 +69,29 @@ __device__ __forceinline__ void fsm_price(const uint64_t* ql, const uint64_t* qh
 // y = merges (src 3 bits | dst 3 bits) x 5, z = emit anchor slots (3 bits) x 5;
 // then the transition's exact 128-bit delta: the terms of the one-unit
 // regions it closes minus the removed op-kernel term of an offloaded unit.
-template <int F, int W>
+template <int F>
+struct FsmSmemBase {  // sums, queues, per-lane totals, counts
+  static constexpr size_t bytes = (size_t)2 * F * FSM_THREADS * 8 + (size_t)(FSM_THREADS / 32) * (3 * FSM_QCAP + 64) * 8 +
+                                  (size_t)F * FSM_THREADS * 4;
+};
+
+//
+// Compact layout (8 bytes, C = true): x = next (12 bits) | open << 12 |
+// n_merge (2 bits) << 13 | n_emit (2 bits) << 15 | delta index (8 bits) << 17,
+// y = merges (6 bits) x 3 | emit slots (3 bits) x 3 << 18; the deltas (at
+// most 256 distinct values; BERT-base has 22) sit in shared memory.  Used
+// when every transition fits: a quarter of the table's cache footprint.
+template <int F, int W, bool C>
 __global__ void __launch_bounds__(FSM_THREADS)
 fitness_fsm_kernel(FsmArgs a, const uint64_t* __restrict__ pop, int64_t n, double* __restrict__ fit) {
   constexpr int T = FSM_THREADS;
   extern __shared__ __align__(16) unsigned char fsm_smem[];
+  // deltas after the per-thread arrays (dynamic size: n_delta entries)
+  uint4* sdelta = reinterpret_cast<uint4*>(fsm_smem + FsmSmemBase<F>::bytes);
+  if (C) {
+    for (int k = threadIdx.x; k < a.n_delta; k += T) sdelta[k] = __ldg(a.dtab + k);
+    __syncthreads();
+  }
   uint64_t(*sl)[T] = reinterpret_cast<uint64_t(*)[T]>(fsm_smem);  // [F][T] anchor sums, low word
   uint64_t(*sh)[T] = sl + F;                                         // high word
   uint64_t* ql0 = reinterpret_cast<uint64_t*>(sh + F);
@@ -134,32 +158,50 @@ fitness_fsm_kernel(FsmArgs a, const uint64_t* __restrict__ pop, int64_t n, doubl
         }
         on = (word >> (bit & 63)) & 1ull;
       }
-      const uint32_t ent = 2u * (h.x + 2u * state + (on ? 1u : 0u));  // 32-bit index math
-      const uint4 e = __ldg(a.table + ent);
-      const uint4 dv = __ldg(a.table + ent + 1u);  // exact delta: closed one-unit regions' terms - removed term
-      state = e.x & 0xFFFFu;
+      const uint32_t idx = h.x + 2u * state + (on ? 1u : 0u);  // 32-bit index math
+      uint32_t open, nmerge, nemit, merges, emits;
+      uint4 dv;  // exact delta: closed one-unit regions' terms - removed term
+      if (C) {
+        const uint2 e = __ldg(a.ctable + idx);
+        state = e.x & 0xFFFu;
+        open = (e.x >> 12) & 1u;
+        nmerge = (e.x >> 13) & 3u;
+        nemit = (e.x >> 15) & 3u;
+        dv = sdelta[(e.x >> 17) & 0xFFu];
+        merges = e.y;
+        emits = e.y >> 18;
+      } else {
+        const uint4 e = __ldg(a.table + 2u * idx);
+        dv = __ldg(a.table + 2u * idx + 1u);
+        state = e.x & 0xFFFFu;
+        open = (e.x >> 16) & 1u;
+        nmerge = (e.x >> 17) & 7u;
+        nemit = (e.x >> 20) & 7u;
+        merges = e.y;
+        emits = e.z;
+      }
       const int S = h.z & 0xFF;
       fadd2(tot_lo, tot_hi, ((uint64_t)dv.y << 32) | dv.x, ((uint64_t)dv.w << 32) | dv.z);
-      if ((e.x >> 16) & 1u) {  // the unit opens its slot
+      if (open) {  // the unit opens its slot
         const ulonglong2 rep = __ldg(reinterpret_cast<const ulonglong2*>(a.cold + (size_t)p * 6));
         sl[S][t] = rep.x;
         sh[S][t] = rep.y;
         sc[S][t] = (uint32_t)__ldg(a.cnt + p);
       }
-      const int nm = (h.w & 0xFF) ? (e.x >> 17) & 7 : 0;
+      const int nm = (h.w & 0xFF) ? (int)nmerge : 0;
       for (int k = 0; k < nm; ++k) {  // component sums into the surviving anchor
-        const int src = (e.y >> (6 * k)) & 7, dst = (e.y >> (6 * k + 3)) & 7;
+        const int src = (merges >> (6 * k)) & 7, dst = (merges >> (6 * k + 3)) & 7;
         uint64_t lo = sl[dst][t], hi = sh[dst][t];
         fadd2(lo, hi, sl[src][t], sh[src][t]);
         sl[dst][t] = lo;
         sh[dst][t] = hi;
         sc[dst][t] += sc[src][t];
       }
-      const int ne = (e.x >> 20) & 7;
+      const int ne = (int)nemit;
       const int nemax = (h.w >> 8) ? __reduce_max_sync(0xffffffffu, (unsigned)ne) : 0;
       for (int k = 0; k < nemax; ++k) {  // multi-unit regions close: queued for pricing
         const bool emit = k < ne;
-        const int slot = (e.z >> (3 * k)) & 7;
+        const int slot = (emits >> (3 * k)) & 7;
         const unsigned closing = __ballot_sync(0xffffffffu, emit);
         if (closing) {
           if (emit) {
@@ -205,19 +247,25 @@ fitness_fsm_kernel(FsmArgs a, const uint64_t* __restrict__ pop, int64_t n, doubl
   if (inexact) atomicAdd(a.flags, 1ull);
 }
 
-template <int F, int W>
+template <int F, int W, bool C>
 int launch_fsm_t(cb_es_plan* p, const uint64_t* d_pop, int64_t n, double* d_fit, cudaStream_t stream) {
-  const size_t smem = (size_t)2 * F * FSM_THREADS * 8 + (size_t)(FSM_THREADS / 32) * (3 * FSM_QCAP + 64) * 8 +
-                      (size_t)F * FSM_THREADS * 4;
-  static bool configured = false;
-  if (!configured) {
-    CB_CUDA_TRY(cudaFuncSetAttribute(fitness_fsm_kernel<F, W>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  const size_t smem = FsmSmemBase<F>::bytes + (C ? (size_t)p->fsm_deltas * sizeof(uint4) : 0);
+  static size_t configured = 0;
+  if (configured < smem) {
+    CB_CUDA_TRY(cudaFuncSetAttribute(fitness_fsm_kernel<F, W, C>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      (int)smem));
-    configured = true;
+    // a 164 KB shared-memory carveout (6 blocks of the F = 6 kernel) leaves
+    // ~90 KB of L1 for the transition table: +5% over the maximal carveout
+    // (9 blocks, ~30 KB of L1) on BERT-base
+    const char* cv = getenv("CB_FSM_CARVEOUT");
+    CB_CUDA_TRY(cudaFuncSetAttribute(fitness_fsm_kernel<F, W, C>, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                     cv ? atoi(cv) : 72));
+    configured = smem;
   }
   int per_sm = 0;
-  CB_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fitness_fsm_kernel<F, W>, FSM_THREADS, smem));
+  CB_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fitness_fsm_kernel<F, W, C>, FSM_THREADS, smem));
   if (per_sm < 1) per_sm = 1;
+  if (const char* cb = getenv("CB_FSM_BLOCKS")) per_sm = std::min(per_sm, std::max(1, atoi(cb)));
   FsmArgs a;
   a.M = p->M;
   a.words = p->words;
@@ -228,6 +276,9 @@ int launch_fsm_t(cb_es_plan* p, const uint64_t* d_pop, int64_t n, double* d_fit,
   a.eps_hi = ex.w[1];
   a.hdr = reinterpret_cast<const uint4*>(p->d_fsm_hdr.p);
   a.table = reinterpret_cast<const uint4*>(p->d_fsm_table.p);
+  a.ctable = reinterpret_cast<const uint2*>(p->d_fsm_ctable.p);
+  a.dtab = reinterpret_cast<const uint4*>(p->d_fsm_dtab.p);
+  a.n_delta = p->fsm_deltas;
   a.cold = p->d_acold.p;
   a.cnt = p->d_acnt.p;
   a.infeas = p->d_infeas.p;
@@ -235,19 +286,28 @@ int launch_fsm_t(cb_es_plan* p, const uint64_t* d_pop, int64_t n, double* d_fit,
   a.flags = p->d_flags.p;
   const int64_t want = (n + FSM_THREADS - 1) / FSM_THREADS;
   const int64_t grid = std::min<int64_t>(want, (int64_t)per_sm * cb_sm_count());
-  fitness_fsm_kernel<F, W><<<(unsigned)grid, FSM_THREADS, smem, stream>>>(a, d_pop, n, d_fit);
+  fitness_fsm_kernel<F, W, C><<<(unsigned)grid, FSM_THREADS, smem, stream>>>(a, d_pop, n, d_fit);
   CB_CUDA_TRY(cudaGetLastError());
   return CB_OK;
 }
 
 template <int F>
 int launch_fsm_w(cb_es_plan* p, const uint64_t* d_pop, int64_t n, double* d_fit, cudaStream_t stream) {
+  if (p->fsm_compact) {
+    switch (p->words) {
+      case 1: return launch_fsm_t<F, 1, true>(p, d_pop, n, d_fit, stream);
+      case 2: return launch_fsm_t<F, 2, true>(p, d_pop, n, d_fit, stream);
+      case 3: return launch_fsm_t<F, 3, true>(p, d_pop, n, d_fit, stream);
+      case 4: return launch_fsm_t<F, 4, true>(p, d_pop, n, d_fit, stream);
+      default: return launch_fsm_t<F, 0, true>(p, d_pop, n, d_fit, stream);
+    }
+  }
   switch (p->words) {
-    case 1: return launch_fsm_t<F, 1>(p, d_pop, n, d_fit, stream);
-    case 2: return launch_fsm_t<F, 2>(p, d_pop, n, d_fit, stream);
-    case 3: return launch_fsm_t<F, 3>(p, d_pop, n, d_fit, stream);
-    case 4: return launch_fsm_t<F, 4>(p, d_pop, n, d_fit, stream);
-    default: return launch_fsm_t<F, 0>(p, d_pop, n, d_fit, stream);
+    case 1: return launch_fsm_t<F, 1, false>(p, d_pop, n, d_fit, stream);
+    case 2: return launch_fsm_t<F, 2, false>(p, d_pop, n, d_fit, stream);
+    case 3: return launch_fsm_t<F, 3, false>(p, d_pop, n, d_fit, stream);
+    case 4: return launch_fsm_t<F, 4, false>(p, d_pop, n, d_fit, stream);
+    default: return launch_fsm_t<F, 0, false>(p, d_pop, n, d_fit, stream);
   }
 }
 
@@ -437,7 +497,81 @@ int build_fsm_plan(cb_es_plan* P) {
     hdr[p].w = max_merge | (max_emit << 8);
     cur.swap(nxt);
   }
+  if (getenv("CB_FSM_STATS")) {
+    int smax = 0, mm = 0, me = 0, dbits = 0, zero = 0;
+    std::unordered_map<uint64_t, int> dd;
+    for (int32_t q = 0; q < M; ++q) {
+      const size_t b = hdr[q].x * 2, e = q + 1 < M ? hdr[q + 1].x * 2 : table.size();
+      smax = std::max<int>(smax, (int)((e - b) / 4));
+      for (size_t k = b; k < e; k += 2) {
+        mm = std::max<int>(mm, (table[k].x >> 17) & 7);
+        me = std::max<int>(me, (table[k].x >> 20) & 7);
+        const uint64_t lo = ((uint64_t)table[k + 1].y << 32) | table[k + 1].x;
+        const uint64_t hi = ((uint64_t)table[k + 1].w << 32) | table[k + 1].z;
+        const bool neg = hi >> 63;
+        uint64_t ml = lo, mh = hi;
+        if (neg) { ml = ~lo + 1; mh = ~hi + (ml == 0); }
+        const int bits = mh ? 128 - __builtin_clzll(mh) : (ml ? 64 - __builtin_clzll(ml) : 0);
+        dbits = std::max(dbits, bits);
+        zero += !lo && !hi;
+        dd[lo * 1000003ull ^ hi] = 1;
+      }
+    }
+    fprintf(stderr, "fsm stats: M %d F %d entries %zu states/step max %d merges max %d emits max %d delta bits max %d zero %d distinct %zu window span %d\n",
+            M, F, table.size() / 2, smax, mm, me, dbits, zero, dd.size(), P->anchor_span);
+  }
+  const size_t n_entries = table.size() / 2;
+  // the 8-byte layout when every transition fits it
+  std::vector<uint2> ctab;
+  std::vector<uint4> dtab;
+  {
+    bool fits = !getenv("CB_FSM_WIDE_ENTRIES");
+    std::unordered_map<std::string, uint32_t> didx;
+    for (int32_t q = 0; fits && q < M; ++q) {
+      const size_t b = hdr[q].x, e = q + 1 < M ? hdr[q + 1].x : table.size() / 2;
+      if (e - b > 2 * 4096) fits = false;  // next-state ids take 12 bits
+    }
+    for (size_t k = 0; fits && k < table.size(); k += 2) {
+      const uint4 t0 = table[k], dv = table[k + 1];
+      const uint32_t nxt = t0.x & 0xFFFFu, open = (t0.x >> 16) & 1u, nm = (t0.x >> 17) & 7u, ne = (t0.x >> 20) & 7u;
+      if (nxt > 0xFFFu || nm > 3 || ne > 3) {
+        fits = false;
+        break;
+      }
+      const std::string key(reinterpret_cast<const char*>(&dv), sizeof(dv));
+      auto it = didx.find(key);
+      uint32_t d;
+      if (it == didx.end()) {
+        if (dtab.size() >= 256) {
+          fits = false;
+          break;
+        }
+        d = (uint32_t)dtab.size();
+        didx.emplace(key, d);
+        dtab.push_back(dv);
+      } else {
+        d = it->second;
+      }
+      ctab.push_back(make_uint2(nxt | (open << 12) | (nm << 13) | (ne << 15) | (d << 17),
+                                (t0.y & 0x3FFFFu) | ((t0.z & 0x1FFu) << 18)));
+    }
+    P->fsm_compact = fits;
+    if (!fits) {
+      ctab.clear();
+      dtab.clear();
+    }
+  }
   cudaError_t e;
+  if (P->fsm_compact) {
+    if ((e = P->d_fsm_ctable.upload(reinterpret_cast<const uint32_t*>(ctab.data()), ctab.size() * 2)) !=
+            cudaSuccess ||
+        (e = P->d_fsm_dtab.upload(reinterpret_cast<const uint32_t*>(dtab.data()), dtab.size() * 4)) != cudaSuccess) {
+      cb_set_error(std::string("CUDA error in plan upload: ") + cudaGetErrorString(e));
+      return CB_ERR_CUDA;
+    }
+    P->fsm_deltas = (int32_t)dtab.size();
+    table.resize(2);  // only the 8-byte copy is kept on the device
+  }
   if ((e = P->d_fsm_hdr.upload(reinterpret_cast<const uint32_t*>(hdr.data()), hdr.size() * 4)) != cudaSuccess ||
       (e = P->d_fsm_table.upload(reinterpret_cast<const uint32_t*>(table.data()), table.size() * 4)) !=
           cudaSuccess) {
@@ -445,12 +579,12 @@ int build_fsm_plan(cb_es_plan* P) {
     return CB_ERR_CUDA;
   }
   P->fsm_states_max = 0;
-  P->fsm_entries = (int64_t)table.size() / 2;
+  P->fsm_entries = (int64_t)n_entries;
   P->fsm_ok = true;
   // automatic selection only while the table stays cache-resident (NasNet-A's
   // 13.8 MB table makes every step an L2 round trip: slower than the
   // packed-label walk); `set_path("fsm")` still forces it
-  P->fsm_auto = table.size() * sizeof(uint4) <= ((size_t)1 << 20);
+  P->fsm_auto = n_entries * (P->fsm_compact ? sizeof(uint2) : 2 * sizeof(uint4)) <= ((size_t)1 << 20);
   return CB_OK;
 }
 

@@ -72,6 +72,7 @@ struct cb_es_plan {
   // overflowed it
   bool anchor_ok = false;
   int32_t anchor_shift = 0;
+  int32_t anchor_span = 0;  // highest bit of the partial-sum bound minus anchor_shift
   DBuf<uint8_t> d_ahot;     // AHot[M]
   DBuf<uint64_t> d_acold;   // [M][6]: rep, off, term1 as 128-bit X
   DBuf<int32_t> d_acnt;     // [M]
@@ -92,6 +93,9 @@ struct cb_es_plan {
   bool fsm_ok = false;
   bool fsm_auto = false;  // chosen by the automatic path (table <= 1 MB)
   DBuf<uint32_t> d_fsm_hdr, d_fsm_table;
+  bool fsm_compact = false;  // 8-byte transitions + shared delta table
+  DBuf<uint32_t> d_fsm_ctable, d_fsm_dtab;
+  int32_t fsm_deltas = 0;
   int32_t fsm_states_max = 0;
   int64_t fsm_entries = 0;
   // tournament order keys of the parent population (es.cu)

@@ -169,3 +169,27 @@ def test_edge_plans_every_path(gpu, n_rows):
             plan.set_path(path)
             assert np.array_equal(plan.evaluate(genomes), want), (name, path)
         plan.set_path("auto")
+
+
+@pytest.mark.parametrize("name", ["bert_base", "nasrnn"])
+def test_fsm_entry_layouts_agree(gpu, name, monkeypatch):
+    """The 8-byte transition layout (shared delta table) and the 32-byte one
+    (forced by CB_FSM_WIDE_ENTRIES at plan build) give identical fitness."""
+    g = workloads.CONFIGS[name]()
+    bs = workloads.paper_backends(g)
+    res = tp.optimize(g, bs.registry, bs.measurer, 0.01)
+    args = (g, bs.registry, bs.measurer, res.placement, 0.01, bs.graph_backend, res.kernel_matches)
+    compact = tp.FitnessPlan(*args)
+    monkeypatch.setenv("CB_FSM_WIDE_ENTRIES", "1")
+    wide = tp.FitnessPlan(*args)
+    monkeypatch.delenv("CB_FSM_WIDE_ENTRIES")
+    assert compact.has_fsm() and wide.has_fsm()
+    assert compact.info.fsm_entry_bytes == 8 and wide.info.fsm_entry_bytes == 32
+    assert compact.info.fsm_transitions == wide.info.fsm_transitions
+    genomes = _genomes(compact, np.random.default_rng(11), 4000)
+    compact.set_path("fsm")
+    wide.set_path("fsm")
+    got = compact.evaluate(genomes)
+    assert np.array_equal(got, wide.evaluate(genomes))
+    wide.set_path("unionfind")
+    assert np.array_equal(got, wide.evaluate(genomes))
