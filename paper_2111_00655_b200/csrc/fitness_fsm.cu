@@ -36,45 +36,57 @@ struct FsmArgs {
   int32_t M, words, shift;
   fx192 base_const;
   uint64_t eps_lo, eps_hi;
-  const uint4* __restrict__ hdr;       // [M]: table offset, bit, slot | nend << 8
+  // [M][2]: {table offset, bit info, slot | nend << 8, max merges | max emits << 8},
+  // then the unit's packed sum (128-bit X, kernel count in bits 112..127)
+  const uint4* __restrict__ hdr;
   const uint4* __restrict__ table;     // transitions (32-byte layout)
   const uint2* __restrict__ ctable;    // transitions (8-byte layout)
   const uint4* __restrict__ dtab;      // distinct deltas of the 8-byte layout
   int32_t n_delta;
-  const uint64_t* __restrict__ cold;   // [M][6] rep, off, term1 (128-bit X)
-  const int32_t* __restrict__ cnt;     // [M]
   const uint64_t* __restrict__ infeas;
   const double* __restrict__ rt;
   unsigned long long* flags;
 };
 
-__device__ __forceinline__ void fadd2(uint64_t& lo, uint64_t& hi, uint64_t blo, uint64_t bhi) {
+// Packed sums: a component's 128-bit sum X (non-negative, < 2^101 by the
+// plan's window check) with its kernel count in the top 16 bits, so one
+// 128-bit add merges both; queued entries carry the owner lane in bits 104..111.
+#define FSM_LANE_SHIFT 40
+#define FSM_CNT_SHIFT 48
+#define FSM_BIT_FORCED 0x80u  // bit info: the unit has no genome bit (always on)
+
+template <typename U>
+__device__ __forceinline__ void fadd2(U& lo, U& hi, uint64_t blo, uint64_t bhi) {
+  static_assert(sizeof(U) == 8, "64-bit words");
   asm("add.cc.u64 %0, %0, %2;\n\taddc.u64 %1, %1, %3;" : "+l"(lo), "+l"(hi) : "l"(blo), "l"(bhi));
 }
 
 // Price queue entry `idx` and add its term to the owner lane's accumulator.
-__device__ __forceinline__ void fsm_price(const uint64_t* ql, const uint64_t* qh, const uint64_t* qm, int idx,
-                                          const FsmArgs& a, uint64_t* tlo, uint64_t* thi, bool& inexact) {
-  const uint64_t m = qm[idx];
-  const double prod = __dmul_rn(x128_to_double(ql[idx], qh[idx], a.shift), __ldg(a.rt + (uint32_t)m));
+__device__ __forceinline__ void fsm_price(const ulonglong2* q, int idx, const FsmArgs& a, uint64_t* tlo,
+                                          uint64_t* thi, bool& inexact) {
+  const ulonglong2 v = q[idx];
+  const uint32_t cnt = (uint32_t)(v.y >> FSM_CNT_SHIFT);
+  const int owner = (int)((v.y >> FSM_LANE_SHIFT) & 0xFFu);
+  const uint64_t xhi = v.y & ((1ull << FSM_LANE_SHIFT) - 1ull);
+  const double prod = __dmul_rn(x128_to_double(v.x, xhi, a.shift), __ldg(a.rt + cnt));
   uint64_t lo, hi;
   inexact |= !x128_from_double(prod, a.shift, lo, hi);
   fadd2(lo, hi, a.eps_lo, a.eps_hi);
-  const int owner = (int)(m >> 32);
   const unsigned long long o0 = atomicAdd(reinterpret_cast<unsigned long long*>(tlo + owner), lo);
   atomicAdd(reinterpret_cast<unsigned long long*>(thi + owner), hi + ((o0 + lo) < o0));
 }
 
-// Transition entry (32 bytes): x = next | open << 16 | n_merge << 17 | n_emit << 20,
-// y = merges (src 3 bits | dst 3 bits) x 5, z = emit anchor slots (3 bits) x 5;
-// then the transition's exact 128-bit delta: the terms of the one-unit
-// regions it closes minus the removed op-kernel term of an offloaded unit.
 template <int F>
-struct FsmSmemBase {  // sums, queues, per-lane totals, counts
-  static constexpr size_t bytes = (size_t)2 * F * FSM_THREADS * 8 + (size_t)(FSM_THREADS / 32) * (3 * FSM_QCAP + 64) * 8 +
-                                  (size_t)F * FSM_THREADS * 4;
+struct FsmSmemBase {  // packed sums [F][T], per-warp queues and lane totals
+  static constexpr size_t bytes =
+      (size_t)F * FSM_THREADS * 16 + (size_t)(FSM_THREADS / 32) * (FSM_QCAP * 16 + 64 * 8);
 };
 
+// Transition entry (32 bytes, C = false): x = next | open << 16 | n_merge << 17 |
+// n_emit << 20, y = merges (src 3 bits | dst 3 bits) x 5, z = emit anchor
+// slots (3 bits) x 5; then the transition's exact 128-bit delta: the terms of
+// the one-unit regions it closes minus the removed op-kernel term of an
+// offloaded unit.
 //
 // Compact layout (8 bytes, C = true): x = next (12 bits) | open << 12 |
 // n_merge (2 bits) << 13 | n_emit (2 bits) << 15 | delta index (8 bits) << 17,
@@ -92,16 +104,12 @@ fitness_fsm_kernel(FsmArgs a, const uint64_t* __restrict__ pop, int64_t n, doubl
     for (int k = threadIdx.x; k < a.n_delta; k += T) sdelta[k] = __ldg(a.dtab + k);
     __syncthreads();
   }
-  uint64_t(*sl)[T] = reinterpret_cast<uint64_t(*)[T]>(fsm_smem);  // [F][T] anchor sums, low word
-  uint64_t(*sh)[T] = sl + F;                                         // high word
-  uint64_t* ql0 = reinterpret_cast<uint64_t*>(sh + F);
   const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
-  uint64_t* ql = ql0 + (size_t)warp * 3 * FSM_QCAP;
-  uint64_t* qh = ql + FSM_QCAP;
-  uint64_t* qm = qh + FSM_QCAP;  // low 32: kernel count, high 32: owner lane
-  uint64_t* tlo = ql0 + (size_t)(T / 32) * 3 * FSM_QCAP + (size_t)warp * 64;
+  ulonglong2* sv = reinterpret_cast<ulonglong2*>(fsm_smem);  // [F][T] packed anchor sums
+  ulonglong2* mine = sv + t;                                  // slot s at mine[s * T]
+  ulonglong2* q = sv + F * T + warp * FSM_QCAP;               // pricing queue of this warp
+  uint64_t* tlo = reinterpret_cast<uint64_t*>(sv + F * T + (T / 32) * FSM_QCAP) + warp * 64;
   uint64_t* thi = tlo + 32;
-  uint32_t(*sc)[T] = reinterpret_cast<uint32_t(*)[T]>(ql0 + (size_t)(T / 32) * (3 * FSM_QCAP + 64));
   tlo[lane] = thi[lane] = 0ull;
   __syncwarp();
   int qn = 0;
@@ -136,28 +144,30 @@ fitness_fsm_kernel(FsmArgs a, const uint64_t* __restrict__ pop, int64_t n, doubl
     uint64_t tot_lo = 0ull, tot_hi = 0ull;
     int32_t cached_word = -1;
     uint64_t word = 0ull, next_word = W == 0 && a.words > 0 ? __ldg(gen) : 0ull;
+    uint4 hn = __ldg(a.hdr);  // step headers are warp uniform: prefetched one step ahead
     for (int32_t p = 0; p < a.M; ++p) {
-      // x = table offset, y = bit, z = slot | nend << 8, w = step's max merges | max emits << 8
-      const uint4 h = __ldg(a.hdr + p);
-      const int32_t bit = (int32_t)h.y;
-      bool on = !dead;
-      if (bit >= 0) {
-        const int32_t wi = bit >> 6;
-        if (wi != cached_word) {  // warp uniform
-          if (W > 0) {
-            word = cur[0];
+      const uint4 h = hn;
+      if (p + 1 < a.M) hn = __ldg(a.hdr + 2 * (p + 1));
+      bool on;
+      if (W > 0) {
+        const uint32_t wi = h.y >> 8;
+        uint64_t wd = cur[0];
 #pragma unroll
-            for (int w = 1; w < WR; ++w)
-              if (wi == w) word = cur[w];
-          } else {
+        for (int w = 1; w < WR; ++w) wd = wi == (uint32_t)w ? cur[w] : wd;
+        on = ((wd >> (h.y & 63u)) & 1ull) != 0ull || (h.y & FSM_BIT_FORCED);
+      } else {
+        on = true;
+        if (!(h.y & FSM_BIT_FORCED)) {
+          const int32_t wi = (int32_t)(h.y >> 8);
+          if (wi != cached_word) {  // warp uniform
             word = wi == cached_word + 1 ? next_word : __ldg(gen + wi);
             next_word = wi + 1 < a.words ? __ldg(gen + wi + 1) : 0ull;
+            cached_word = wi;
           }
-          if (dead) word = 0ull;
-          cached_word = wi;
+          on = (word >> (h.y & 63u)) & 1ull;
         }
-        on = (word >> (bit & 63)) & 1ull;
       }
+      on = on && !dead;
       const uint32_t idx = h.x + 2u * state + (on ? 1u : 0u);  // 32-bit index math
       uint32_t open, nmerge, nemit, merges, emits;
       uint4 dv;  // exact delta: closed one-unit regions' terms - removed term
@@ -180,46 +190,36 @@ fitness_fsm_kernel(FsmArgs a, const uint64_t* __restrict__ pop, int64_t n, doubl
         merges = e.y;
         emits = e.z;
       }
-      const int S = h.z & 0xFF;
       fadd2(tot_lo, tot_hi, ((uint64_t)dv.y << 32) | dv.x, ((uint64_t)dv.w << 32) | dv.z);
-      if (open) {  // the unit opens its slot
-        const ulonglong2 rep = __ldg(reinterpret_cast<const ulonglong2*>(a.cold + (size_t)p * 6));
-        sl[S][t] = rep.x;
-        sh[S][t] = rep.y;
-        sc[S][t] = (uint32_t)__ldg(a.cnt + p);
+      if (open) {  // the unit opens its slot with its packed sum
+        const uint4 r = __ldg(a.hdr + 2 * p + 1);
+        mine[(h.z & 0xFFu) * T] = make_ulonglong2(((uint64_t)r.y << 32) | r.x, ((uint64_t)r.w << 32) | r.z);
       }
       const int nm = (h.w & 0xFF) ? (int)nmerge : 0;
       for (int k = 0; k < nm; ++k) {  // component sums into the surviving anchor
-        const int src = (merges >> (6 * k)) & 7, dst = (merges >> (6 * k + 3)) & 7;
-        uint64_t lo = sl[dst][t], hi = sh[dst][t];
-        fadd2(lo, hi, sl[src][t], sh[src][t]);
-        sl[dst][t] = lo;
-        sh[dst][t] = hi;
-        sc[dst][t] += sc[src][t];
+        const uint32_t src = (merges >> (6 * k)) & 7u, dst = (merges >> (6 * k + 3)) & 7u;
+        ulonglong2 d = mine[dst * T];
+        const ulonglong2 v = mine[src * T];
+        fadd2(d.x, d.y, v.x, v.y);
+        mine[dst * T] = d;
       }
       const int ne = (int)nemit;
       const int nemax = (h.w >> 8) ? __reduce_max_sync(0xffffffffu, (unsigned)ne) : 0;
       for (int k = 0; k < nemax; ++k) {  // multi-unit regions close: queued for pricing
         const bool emit = k < ne;
-        const int slot = (emits >> (3 * k)) & 7;
         const unsigned closing = __ballot_sync(0xffffffffu, emit);
         if (closing) {
           if (emit) {
-            const int at = qn + __popc(closing & ((1u << lane) - 1u));
-            ql[at] = sl[slot][t];
-            qh[at] = sh[slot][t];
-            qm[at] = ((uint64_t)lane << 32) | sc[slot][t];
+            ulonglong2 v = mine[((emits >> (3 * k)) & 7u) * T];
+            v.y |= (uint64_t)lane << FSM_LANE_SHIFT;
+            q[qn + __popc(closing & ((1u << lane) - 1u))] = v;
           }
           qn += __popc(closing);
           if (qn >= 32) {
             __syncwarp();
-            fsm_price(ql, qh, qm, lane, a, tlo, thi, inexact);
+            fsm_price(q, lane, a, tlo, thi, inexact);
             __syncwarp();
-            if (lane < qn - 32) {
-              ql[lane] = ql[32 + lane];
-              qh[lane] = qh[32 + lane];
-              qm[lane] = qm[32 + lane];
-            }
+            if (lane < qn - 32) q[lane] = q[32 + lane];
             __syncwarp();
             qn -= 32;
           }
@@ -227,7 +227,7 @@ fitness_fsm_kernel(FsmArgs a, const uint64_t* __restrict__ pop, int64_t n, doubl
       }
     }
     __syncwarp();
-    if (lane < qn) fsm_price(ql, qh, qm, lane, a, tlo, thi, inexact);
+    if (lane < qn) fsm_price(q, lane, a, tlo, thi, inexact);
     qn = 0;
     __syncwarp();
     fadd2(tot_lo, tot_hi, tlo[lane], thi[lane]);
@@ -279,8 +279,6 @@ int launch_fsm_t(cb_es_plan* p, const uint64_t* d_pop, int64_t n, double* d_fit,
   a.ctable = reinterpret_cast<const uint2*>(p->d_fsm_ctable.p);
   a.dtab = reinterpret_cast<const uint4*>(p->d_fsm_dtab.p);
   a.n_delta = p->fsm_deltas;
-  a.cold = p->d_acold.p;
-  a.cnt = p->d_acnt.p;
   a.infeas = p->d_infeas.p;
   a.rt = p->d_rt.p;
   a.flags = p->d_flags.p;
@@ -347,6 +345,15 @@ int build_fsm_plan(cb_es_plan* P) {
   P->fsm_ok = false;
   if (!P->anchor_ok || P->F <= 0 || P->F > 8 || P->M == 0) return CB_OK;
   const int32_t M = P->M, F = P->F;
+  // packed sums: non-negative unit sums below 2^101 (window span <= 100) and
+  // kernel counts that fit 16 bits
+  if (P->anchor_span > 100) return CB_OK;
+  int64_t cnt_total = 0;
+  for (int32_t q = 0; q < M; ++q) {
+    if ((P->prog[q].rep.w[2] >> 63) != 0 || P->prog[q].cnt < 0) return CB_OK;
+    cnt_total += P->prog[q].cnt;
+  }
+  if (cnt_total > 0xFFFF) return CB_OK;
   std::vector<std::vector<int32_t>> ends(M);
   for (int32_t q = 0; q < M; ++q) ends[P->prog_last[q]].push_back(q);
   std::vector<uint4> table;
@@ -361,7 +368,8 @@ int build_fsm_plan(cb_es_plan* P) {
     const int S = r.slot;
     occ_end[S] = P->prog_last[p];
     if ((int)ends[p].size() != r.nend) return CB_OK;  // program / end lists disagree
-    hdr[p] = make_uint4((uint32_t)(table.size() / 2), (uint32_t)r.bit, (uint32_t)S | ((uint32_t)r.nend << 8), 0u);
+    const uint32_t bitinfo = r.bit >= 0 ? ((uint32_t)r.bit & 63u) | ((uint32_t)(r.bit >> 6) << 8) : FSM_BIT_FORCED;
+    hdr[p] = make_uint4((uint32_t)(table.size() / 2), bitinfo, (uint32_t)S | ((uint32_t)r.nend << 8), 0u);
     if ((table.size() + 4 * cur.size()) * sizeof(uint4) > cap) return CB_OK;
     next_ids.clear();
     nxt.clear();
@@ -561,6 +569,14 @@ int build_fsm_plan(cb_es_plan* P) {
       dtab.clear();
     }
   }
+  // step headers interleaved with the units' packed sums
+  std::vector<uint4> hdr2((size_t)2 * M);
+  for (int32_t q = 0; q < M; ++q) {
+    const fx192 x = fx_shr(P->prog[q].rep, P->anchor_shift);
+    const uint64_t hi = x.w[1] | ((uint64_t)P->prog[q].cnt << FSM_CNT_SHIFT);
+    hdr2[2 * q] = hdr[q];
+    hdr2[2 * q + 1] = make_uint4((uint32_t)x.w[0], (uint32_t)(x.w[0] >> 32), (uint32_t)hi, (uint32_t)(hi >> 32));
+  }
   cudaError_t e;
   if (P->fsm_compact) {
     if ((e = P->d_fsm_ctable.upload(reinterpret_cast<const uint32_t*>(ctab.data()), ctab.size() * 2)) !=
@@ -572,7 +588,7 @@ int build_fsm_plan(cb_es_plan* P) {
     P->fsm_deltas = (int32_t)dtab.size();
     table.resize(2);  // only the 8-byte copy is kept on the device
   }
-  if ((e = P->d_fsm_hdr.upload(reinterpret_cast<const uint32_t*>(hdr.data()), hdr.size() * 4)) != cudaSuccess ||
+  if ((e = P->d_fsm_hdr.upload(reinterpret_cast<const uint32_t*>(hdr2.data()), hdr2.size() * 4)) != cudaSuccess ||
       (e = P->d_fsm_table.upload(reinterpret_cast<const uint32_t*>(table.data()), table.size() * 4)) !=
           cudaSuccess) {
     cb_set_error(std::string("CUDA error in plan upload: ") + cudaGetErrorString(e));
