@@ -100,6 +100,7 @@ fitness_fsm_kernel(FsmArgs a, const uint64_t* __restrict__ pop, int64_t n, doubl
   extern __shared__ __align__(16) unsigned char fsm_smem[];
   // deltas after the per-thread arrays (dynamic size: n_delta entries)
   uint4* sdelta = reinterpret_cast<uint4*>(fsm_smem + FsmSmemBase<F>::bytes);
+  const uint32_t sdelta_base = (uint32_t)__cvta_generic_to_shared(sdelta);
   if (C) {
     for (int k = threadIdx.x; k < a.n_delta; k += T) sdelta[k] = __ldg(a.dtab + k);
     __syncthreads();
@@ -177,7 +178,9 @@ fitness_fsm_kernel(FsmArgs a, const uint64_t* __restrict__ pop, int64_t n, doubl
         open = (e.x >> 12) & 1u;
         nmerge = (e.x >> 13) & 3u;
         nemit = (e.x >> 15) & 3u;
-        dv = sdelta[(e.x >> 17) & 0xFFu];
+        // one 16-byte shared load (the compiler splits a uint4 read in two)
+        const uint32_t da = sdelta_base + ((e.x >> 13) & 0xFF0u);
+        asm("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(dv.x), "=r"(dv.y), "=r"(dv.z), "=r"(dv.w) : "r"(da));
         merges = e.y;
         emits = e.y >> 18;
       } else {
@@ -195,17 +198,24 @@ fitness_fsm_kernel(FsmArgs a, const uint64_t* __restrict__ pop, int64_t n, doubl
         const uint4 r = __ldg(a.hdr + 2 * p + 1);
         mine[(h.z & 0xFFu) * T] = make_ulonglong2(((uint64_t)r.y << 32) | r.x, ((uint64_t)r.w << 32) | r.z);
       }
-      const int nm = (h.w & 0xFF) ? (int)nmerge : 0;
-      for (int k = 0; k < nm; ++k) {  // component sums into the surviving anchor
-        const uint32_t src = (merges >> (6 * k)) & 7u, dst = (merges >> (6 * k + 3)) & 7u;
-        ulonglong2 d = mine[dst * T];
-        const ulonglong2 v = mine[src * T];
-        fadd2(d.x, d.y, v.x, v.y);
-        mine[dst * T] = d;
+      if (h.w & 0xFF) {
+        constexpr int MAXM = C ? 3 : 5;
+#pragma unroll
+        for (int k = 0; k < MAXM; ++k) {  // component sums into the surviving anchor
+          if (k >= (int)nmerge) break;
+          const uint32_t src = (merges >> (6 * k)) & 7u, dst = (merges >> (6 * k + 3)) & 7u;
+          ulonglong2 d = mine[dst * T];
+          const ulonglong2 v = mine[src * T];
+          fadd2(d.x, d.y, v.x, v.y);
+          mine[dst * T] = d;
+        }
       }
       const int ne = (int)nemit;
       const int nemax = (h.w >> 8) ? __reduce_max_sync(0xffffffffu, (unsigned)ne) : 0;
-      for (int k = 0; k < nemax; ++k) {  // multi-unit regions close: queued for pricing
+      constexpr int MAXE = C ? 3 : 5;
+#pragma unroll
+      for (int k = 0; k < MAXE; ++k) {  // multi-unit regions close: queued for pricing
+        if (k >= nemax) break;
         const bool emit = k < ne;
         const unsigned closing = __ballot_sync(0xffffffffu, emit);
         if (closing) {
@@ -254,12 +264,19 @@ int launch_fsm_t(cb_es_plan* p, const uint64_t* d_pop, int64_t n, double* d_fit,
   if (configured < smem) {
     CB_CUDA_TRY(cudaFuncSetAttribute(fitness_fsm_kernel<F, W, C>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      (int)smem));
-    // a 164 KB shared-memory carveout (6 blocks of the F = 6 kernel) leaves
-    // ~90 KB of L1 for the transition table: +5% over the maximal carveout
-    // (9 blocks, ~30 KB of L1) on BERT-base
+    // the smallest shared-memory configuration holding 8 blocks (the
+    // register limit); the rest of the 256 KB stays L1 for the transition
+    // table (BERT-base, F = 6: 164 KB, +4% over the maximal carveout).  The
+    // percentage is rounded down so it maps back onto that configuration.
     const char* cv = getenv("CB_FSM_CARVEOUT");
+    int pct = 100;
+    for (int kb : {100, 132, 164, 196})
+      if ((size_t)kb * 1024 >= 8 * (smem + 1024)) {
+        pct = kb * 100 / 228;
+        break;
+      }
     CB_CUDA_TRY(cudaFuncSetAttribute(fitness_fsm_kernel<F, W, C>, cudaFuncAttributePreferredSharedMemoryCarveout,
-                                     cv ? atoi(cv) : 72));
+                                     cv ? atoi(cv) : pct));
     configured = smem;
   }
   int per_sm = 0;
