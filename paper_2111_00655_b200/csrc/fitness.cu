@@ -550,8 +550,9 @@ extern "C" const char* cb_es_plan_kernel(const cb_es_plan* p) {
   if (frontier && p->force_path == 3) return "fitness_wide_kernel";
   if (frontier && p->fsm_ok && (p->force_path == 7 || (p->force_path == -1 && p->fsm_auto))) {
     static thread_local char fbuf[48];
-    std::snprintf(fbuf, sizeof(fbuf), "fitness_fsm_kernel<%d, %d>", p->F <= 4 ? 4 : p->F <= 6 ? 6 : 8,
-                  p->words <= 4 ? p->words : 0);
+    // fitness_fsm_kernel<F, W, C>: C = 1 for the 8-byte transition layout
+    std::snprintf(fbuf, sizeof(fbuf), "fitness_fsm_kernel<%d, %d, %d>", p->F <= 4 ? 4 : p->F <= 6 ? 6 : 8,
+                  p->words <= 4 ? p->words : 0, p->fsm_compact ? 1 : 0);
     return fbuf;
   }
   if (frontier && p->pa_ok && p->anchor_ok && (p->force_path == 6 || p->force_path == -1)) {
