@@ -193,3 +193,27 @@ def test_fsm_entry_layouts_agree(gpu, name, monkeypatch):
     assert np.array_equal(got, wide.evaluate(genomes))
     wide.set_path("unionfind")
     assert np.array_equal(got, wide.evaluate(genomes))
+
+
+@pytest.mark.parametrize("seed,n,window", [(7, 1200, 4), (8, 2500, 3), (9, 700, 6), (10, 400, 8)])
+def test_fsm_long_narrow_programs_match_oracle(gpu, seed, n, window):
+    """Long, narrow random DAGs: many genome words (the FSM kernel's W = 0
+    path, words loaded on demand) with few frontier slots, every transition
+    layout, against the oracle."""
+    g = workloads.random_dag(n, seed=seed, ops=workloads.RANDOM_OPS, window=window)
+    bs = workloads.random_backends(g, n_backends=6, n_graph=1, seed=seed)
+    res = tp.optimize(g, bs.registry, bs.measurer, 0.01)
+    plan = tp.FitnessPlan(g, bs.registry, bs.measurer, res.placement, 0.01, bs.graph_backend,
+                          res.kernel_matches)
+    if not plan.has_fsm():
+        pytest.skip(f"no FSM program ({plan.info.frontier_slots} slots)")
+    genomes = _genomes(plan, np.random.default_rng(seed), 200)
+    oc = OracleCase(_case(g, bs, 0.01))
+    oc.price()
+    kernels = [[a.backend_pattern.order, a.root, sorted(a.nodes)]
+               for a in res.placement.assignments]
+    want = oc.fitness(kernels, bs.graph_backend, genomes, threads=8)
+    plan.set_path("fsm")
+    assert np.array_equal(plan.evaluate(genomes), want), (plan.words, plan.info.fsm_entry_bytes)
+    plan.set_path("auto")
+    assert np.array_equal(plan.evaluate(genomes), want)
