@@ -525,7 +525,7 @@ extern "C" int cb_es_plan_query(const cb_es_plan* p, cb_es_plan_info* info) {
   info->window_shift = p->anchor_ok ? p->anchor_shift : -1;
   info->packed_labels = p->F > 0 && p->packed_ok ? (p->pa_ok && p->anchor_ok ? 2 : 1) : 0;
   info->fsm_transitions = p->fsm_ok ? (int32_t)std::min<int64_t>(p->fsm_entries, INT32_MAX) : 0;
-  info->fsm_entry_bytes = p->fsm_ok ? (p->fsm_compact ? 8 : 32) : 0;
+  info->fsm_entry_bytes = p->fsm_ok ? (p->fsm_layout == 1 ? 8 : p->fsm_layout == 2 ? 16 : 32) : 0;
   return CB_OK;
 }
 
@@ -550,9 +550,9 @@ extern "C" const char* cb_es_plan_kernel(const cb_es_plan* p) {
   if (frontier && p->force_path == 3) return "fitness_wide_kernel";
   if (frontier && p->fsm_ok && (p->force_path == 7 || (p->force_path == -1 && p->fsm_auto))) {
     static thread_local char fbuf[48];
-    // fitness_fsm_kernel<F, W, C>: C = 1 for the 8-byte transition layout
+    // fitness_fsm_kernel<F, W, L>: L = transition layout (1: 8 bytes, 2: 16, 0: 32)
     std::snprintf(fbuf, sizeof(fbuf), "fitness_fsm_kernel<%d, %d, %d>", p->F <= 4 ? 4 : p->F <= 6 ? 6 : 8,
-                  p->words <= 4 ? p->words : 0, p->fsm_compact ? 1 : 0);
+                  p->words <= 4 ? p->words : 0, p->fsm_layout);
     return fbuf;
   }
   if (frontier && p->pa_ok && p->anchor_ok && (p->force_path == 6 || p->force_path == -1)) {

@@ -41,7 +41,8 @@ struct FsmArgs {
   const uint4* __restrict__ hdr;
   const uint4* __restrict__ table;     // transitions (32-byte layout)
   const uint2* __restrict__ ctable;    // transitions (8-byte layout)
-  const uint4* __restrict__ dtab;      // distinct deltas of the 8-byte layout
+  const uint4* __restrict__ mtable;    // transitions (16-byte layout)
+  const uint4* __restrict__ dtab;      // distinct deltas of the 8- / 16-byte layouts
   int32_t n_delta;
   const uint64_t* __restrict__ infeas;
   const double* __restrict__ rt;
@@ -93,7 +94,7 @@ struct FsmSmemBase {  // packed sums [F][T], per-warp queues and lane totals
 // y = merges (6 bits) x 3 | emit slots (3 bits) x 3 << 18; the deltas (at
 // most 256 distinct values; BERT-base has 22) sit in shared memory.  Used
 // when every transition fits: a quarter of the table's cache footprint.
-template <int F, int W, bool C>
+template <int F, int W, int L>
 __global__ void __launch_bounds__(FSM_THREADS)
 fitness_fsm_kernel(FsmArgs a, const uint64_t* __restrict__ pop, int64_t n, double* __restrict__ fit) {
   constexpr int T = FSM_THREADS;
@@ -101,7 +102,7 @@ fitness_fsm_kernel(FsmArgs a, const uint64_t* __restrict__ pop, int64_t n, doubl
   // deltas after the per-thread arrays (dynamic size: n_delta entries)
   uint4* sdelta = reinterpret_cast<uint4*>(fsm_smem + FsmSmemBase<F>::bytes);
   const uint32_t sdelta_base = (uint32_t)__cvta_generic_to_shared(sdelta);
-  if (C) {
+  if (L != 0) {
     for (int k = threadIdx.x; k < a.n_delta; k += T) sdelta[k] = __ldg(a.dtab + k);
     __syncthreads();
   }
@@ -172,7 +173,7 @@ fitness_fsm_kernel(FsmArgs a, const uint64_t* __restrict__ pop, int64_t n, doubl
       const uint32_t idx = h.x + 2u * state + (on ? 1u : 0u);  // 32-bit index math
       uint32_t open, nmerge, nemit, merges, emits;
       uint4 dv;  // exact delta: closed one-unit regions' terms - removed term
-      if (C) {
+      if (L == 1) {
         const uint2 e = __ldg(a.ctable + idx);
         state = e.x & 0xFFFu;
         open = (e.x >> 12) & 1u;
@@ -183,6 +184,16 @@ fitness_fsm_kernel(FsmArgs a, const uint64_t* __restrict__ pop, int64_t n, doubl
         asm("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(dv.x), "=r"(dv.y), "=r"(dv.z), "=r"(dv.w) : "r"(da));
         merges = e.y;
         emits = e.y >> 18;
+      } else if (L == 2) {
+        const uint4 e = __ldg(a.mtable + idx);
+        state = e.x & 0xFFFFu;
+        open = (e.x >> 16) & 1u;
+        nmerge = (e.x >> 17) & 7u;
+        nemit = (e.x >> 20) & 7u;
+        const uint32_t da = sdelta_base + ((e.x >> 20) & 0xFF0u);
+        asm("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(dv.x), "=r"(dv.y), "=r"(dv.z), "=r"(dv.w) : "r"(da));
+        merges = e.y;
+        emits = e.z;
       } else {
         const uint4 e = __ldg(a.table + 2u * idx);
         dv = __ldg(a.table + 2u * idx + 1u);
@@ -199,7 +210,7 @@ fitness_fsm_kernel(FsmArgs a, const uint64_t* __restrict__ pop, int64_t n, doubl
         mine[(h.z & 0xFFu) * T] = make_ulonglong2(((uint64_t)r.y << 32) | r.x, ((uint64_t)r.w << 32) | r.z);
       }
       if (h.w & 0xFF) {
-        constexpr int MAXM = C ? 3 : 5;
+        constexpr int MAXM = L == 1 ? 3 : 5;
 #pragma unroll
         for (int k = 0; k < MAXM; ++k) {  // component sums into the surviving anchor
           if (k >= (int)nmerge) break;
@@ -212,7 +223,7 @@ fitness_fsm_kernel(FsmArgs a, const uint64_t* __restrict__ pop, int64_t n, doubl
       }
       const int ne = (int)nemit;
       const int nemax = (h.w >> 8) ? __reduce_max_sync(0xffffffffu, (unsigned)ne) : 0;
-      constexpr int MAXE = C ? 3 : 5;
+      constexpr int MAXE = L == 1 ? 3 : 5;
 #pragma unroll
       for (int k = 0; k < MAXE; ++k) {  // multi-unit regions close: queued for pricing
         if (k >= nemax) break;
@@ -257,12 +268,12 @@ fitness_fsm_kernel(FsmArgs a, const uint64_t* __restrict__ pop, int64_t n, doubl
   if (inexact) atomicAdd(a.flags, 1ull);
 }
 
-template <int F, int W, bool C>
+template <int F, int W, int L>
 int launch_fsm_t(cb_es_plan* p, const uint64_t* d_pop, int64_t n, double* d_fit, cudaStream_t stream) {
-  const size_t smem = FsmSmemBase<F>::bytes + (C ? (size_t)p->fsm_deltas * sizeof(uint4) : 0);
+  const size_t smem = FsmSmemBase<F>::bytes + (L != 0 ? (size_t)p->fsm_deltas * sizeof(uint4) : 0);
   static size_t configured = 0;
   if (configured < smem) {
-    CB_CUDA_TRY(cudaFuncSetAttribute(fitness_fsm_kernel<F, W, C>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    CB_CUDA_TRY(cudaFuncSetAttribute(fitness_fsm_kernel<F, W, L>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      (int)smem));
     // the smallest shared-memory configuration holding 8 blocks (the
     // register limit); the rest of the 256 KB stays L1 for the transition
@@ -275,12 +286,12 @@ int launch_fsm_t(cb_es_plan* p, const uint64_t* d_pop, int64_t n, double* d_fit,
         pct = kb * 100 / 228;
         break;
       }
-    CB_CUDA_TRY(cudaFuncSetAttribute(fitness_fsm_kernel<F, W, C>, cudaFuncAttributePreferredSharedMemoryCarveout,
+    CB_CUDA_TRY(cudaFuncSetAttribute(fitness_fsm_kernel<F, W, L>, cudaFuncAttributePreferredSharedMemoryCarveout,
                                      cv ? atoi(cv) : pct));
     configured = smem;
   }
   int per_sm = 0;
-  CB_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fitness_fsm_kernel<F, W, C>, FSM_THREADS, smem));
+  CB_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fitness_fsm_kernel<F, W, L>, FSM_THREADS, smem));
   if (per_sm < 1) per_sm = 1;
   if (const char* cb = getenv("CB_FSM_BLOCKS")) per_sm = std::min(per_sm, std::max(1, atoi(cb)));
   FsmArgs a;
@@ -294,6 +305,7 @@ int launch_fsm_t(cb_es_plan* p, const uint64_t* d_pop, int64_t n, double* d_fit,
   a.hdr = reinterpret_cast<const uint4*>(p->d_fsm_hdr.p);
   a.table = reinterpret_cast<const uint4*>(p->d_fsm_table.p);
   a.ctable = reinterpret_cast<const uint2*>(p->d_fsm_ctable.p);
+  a.mtable = reinterpret_cast<const uint4*>(p->d_fsm_ctable.p);
   a.dtab = reinterpret_cast<const uint4*>(p->d_fsm_dtab.p);
   a.n_delta = p->fsm_deltas;
   a.infeas = p->d_infeas.p;
@@ -301,29 +313,31 @@ int launch_fsm_t(cb_es_plan* p, const uint64_t* d_pop, int64_t n, double* d_fit,
   a.flags = p->d_flags.p;
   const int64_t want = (n + FSM_THREADS - 1) / FSM_THREADS;
   const int64_t grid = std::min<int64_t>(want, (int64_t)per_sm * cb_sm_count());
-  fitness_fsm_kernel<F, W, C><<<(unsigned)grid, FSM_THREADS, smem, stream>>>(a, d_pop, n, d_fit);
+  fitness_fsm_kernel<F, W, L><<<(unsigned)grid, FSM_THREADS, smem, stream>>>(a, d_pop, n, d_fit);
   CB_CUDA_TRY(cudaGetLastError());
   return CB_OK;
 }
 
 template <int F>
 int launch_fsm_w(cb_es_plan* p, const uint64_t* d_pop, int64_t n, double* d_fit, cudaStream_t stream) {
-  if (p->fsm_compact) {
-    switch (p->words) {
-      case 1: return launch_fsm_t<F, 1, true>(p, d_pop, n, d_fit, stream);
-      case 2: return launch_fsm_t<F, 2, true>(p, d_pop, n, d_fit, stream);
-      case 3: return launch_fsm_t<F, 3, true>(p, d_pop, n, d_fit, stream);
-      case 4: return launch_fsm_t<F, 4, true>(p, d_pop, n, d_fit, stream);
-      default: return launch_fsm_t<F, 0, true>(p, d_pop, n, d_fit, stream);
-    }
+  switch (p->fsm_layout * 8 + (p->words <= 4 ? p->words : 0)) {
+    case 8 + 1: return launch_fsm_t<F, 1, 1>(p, d_pop, n, d_fit, stream);
+    case 8 + 2: return launch_fsm_t<F, 2, 1>(p, d_pop, n, d_fit, stream);
+    case 8 + 3: return launch_fsm_t<F, 3, 1>(p, d_pop, n, d_fit, stream);
+    case 8 + 4: return launch_fsm_t<F, 4, 1>(p, d_pop, n, d_fit, stream);
+    case 8 + 0: return launch_fsm_t<F, 0, 1>(p, d_pop, n, d_fit, stream);
+    case 16 + 1: return launch_fsm_t<F, 1, 2>(p, d_pop, n, d_fit, stream);
+    case 16 + 2: return launch_fsm_t<F, 2, 2>(p, d_pop, n, d_fit, stream);
+    case 16 + 3: return launch_fsm_t<F, 3, 2>(p, d_pop, n, d_fit, stream);
+    case 16 + 4: return launch_fsm_t<F, 4, 2>(p, d_pop, n, d_fit, stream);
+    case 16 + 0: return launch_fsm_t<F, 0, 2>(p, d_pop, n, d_fit, stream);
+    case 1: return launch_fsm_t<F, 1, 0>(p, d_pop, n, d_fit, stream);
+    case 2: return launch_fsm_t<F, 2, 0>(p, d_pop, n, d_fit, stream);
+    case 3: return launch_fsm_t<F, 3, 0>(p, d_pop, n, d_fit, stream);
+    case 4: return launch_fsm_t<F, 4, 0>(p, d_pop, n, d_fit, stream);
+    default: return launch_fsm_t<F, 0, 0>(p, d_pop, n, d_fit, stream);
   }
-  switch (p->words) {
-    case 1: return launch_fsm_t<F, 1, false>(p, d_pop, n, d_fit, stream);
-    case 2: return launch_fsm_t<F, 2, false>(p, d_pop, n, d_fit, stream);
-    case 3: return launch_fsm_t<F, 3, false>(p, d_pop, n, d_fit, stream);
-    case 4: return launch_fsm_t<F, 4, false>(p, d_pop, n, d_fit, stream);
-    default: return launch_fsm_t<F, 0, false>(p, d_pop, n, d_fit, stream);
-  }
+
 }
 
 // ------------------------------------------------------------ plan time
@@ -353,6 +367,8 @@ FsmState canonical(const int* lab, const bool* multi_of_label, int F) {
 }
 
 }  // namespace
+
+static int fsm_entry_bytes(const cb_es_plan* P) { return P->fsm_layout == 1 ? 8 : P->fsm_layout == 2 ? 16 : 32; }
 
 // Enumerate the reachable frontier states step by step and tabulate every
 // (state, bit) transition.  Leaves fsm_ok false when the program is wider
@@ -546,43 +562,62 @@ int build_fsm_plan(cb_es_plan* P) {
             M, F, table.size() / 2, smax, mm, me, dbits, zero, dd.size(), P->anchor_span);
   }
   const size_t n_entries = table.size() / 2;
-  // the 8-byte layout when every transition fits it
-  std::vector<uint2> ctab;
+  // the smallest layout every transition fits: 8 bytes (12-bit next state,
+  // <= 3 merges / emits), 16 bytes (<= 5), else 32; both short layouts index
+  // <= 256 distinct deltas.  CB_FSM_ENTRY_BYTES (8 / 16 / 32) sets the
+  // smallest layout tried (tests), CB_FSM_WIDE_ENTRIES forces 32.
+  std::vector<uint32_t> stab;
   std::vector<uint4> dtab;
+  P->fsm_layout = 0;
   {
-    bool fits = !getenv("CB_FSM_WIDE_ENTRIES");
+    int min_bytes = getenv("CB_FSM_ENTRY_BYTES") ? atoi(getenv("CB_FSM_ENTRY_BYTES")) : 8;
+    if (getenv("CB_FSM_WIDE_ENTRIES")) min_bytes = 32;
     std::unordered_map<std::string, uint32_t> didx;
-    for (int32_t q = 0; fits && q < M; ++q) {
-      const size_t b = hdr[q].x, e = q + 1 < M ? hdr[q + 1].x : table.size() / 2;
-      if (e - b > 2 * 4096) fits = false;  // next-state ids take 12 bits
-    }
-    for (size_t k = 0; fits && k < table.size(); k += 2) {
-      const uint4 t0 = table[k], dv = table[k + 1];
-      const uint32_t nxt = t0.x & 0xFFFFu, open = (t0.x >> 16) & 1u, nm = (t0.x >> 17) & 7u, ne = (t0.x >> 20) & 7u;
-      if (nxt > 0xFFFu || nm > 3 || ne > 3) {
-        fits = false;
-        break;
-      }
+    bool deltas_fit = true;
+    std::vector<uint32_t> dref(n_entries);
+    for (size_t k = 0; k < n_entries && deltas_fit; ++k) {
+      const uint4 dv = table[2 * k + 1];
       const std::string key(reinterpret_cast<const char*>(&dv), sizeof(dv));
       auto it = didx.find(key);
-      uint32_t d;
       if (it == didx.end()) {
         if (dtab.size() >= 256) {
-          fits = false;
+          deltas_fit = false;
           break;
         }
-        d = (uint32_t)dtab.size();
-        didx.emplace(key, d);
+        it = didx.emplace(key, (uint32_t)dtab.size()).first;
         dtab.push_back(dv);
-      } else {
-        d = it->second;
       }
-      ctab.push_back(make_uint2(nxt | (open << 12) | (nm << 13) | (ne << 15) | (d << 17),
-                                (t0.y & 0x3FFFFu) | ((t0.z & 0x1FFu) << 18)));
+      dref[k] = it->second;
     }
-    P->fsm_compact = fits;
-    if (!fits) {
-      ctab.clear();
+    bool fits8 = deltas_fit && min_bytes <= 8, fits16 = deltas_fit && min_bytes <= 16;
+    for (int32_t q = 0; fits8 && q < M; ++q) {
+      const size_t b = hdr[q].x, e = q + 1 < M ? hdr[q + 1].x : n_entries;
+      if (e - b > 2 * 4096) fits8 = false;  // next-state ids take 12 bits
+    }
+    for (size_t k = 0; fits8 && k < n_entries; ++k) {
+      const uint32_t x = table[2 * k].x;
+      if ((x & 0xFFFFu) > 0xFFFu || ((x >> 17) & 7u) > 3 || ((x >> 20) & 7u) > 3) fits8 = false;
+    }
+    if (fits8) {
+      P->fsm_layout = 1;
+      stab.resize(2 * n_entries);
+      for (size_t k = 0; k < n_entries; ++k) {
+        const uint4 t0 = table[2 * k];
+        const uint32_t nxt = t0.x & 0xFFFFu, open = (t0.x >> 16) & 1u, nm = (t0.x >> 17) & 7u, ne = (t0.x >> 20) & 7u;
+        stab[2 * k] = nxt | (open << 12) | (nm << 13) | (ne << 15) | (dref[k] << 17);
+        stab[2 * k + 1] = (t0.y & 0x3FFFFu) | ((t0.z & 0x1FFu) << 18);
+      }
+    } else if (fits16) {
+      P->fsm_layout = 2;
+      stab.resize(4 * n_entries);
+      for (size_t k = 0; k < n_entries; ++k) {
+        const uint4 t0 = table[2 * k];
+        stab[4 * k] = (t0.x & 0xFFFFFFu) | (dref[k] << 24);
+        stab[4 * k + 1] = t0.y;
+        stab[4 * k + 2] = t0.z;
+        stab[4 * k + 3] = 0u;
+      }
+    } else {
       dtab.clear();
     }
   }
@@ -595,15 +630,14 @@ int build_fsm_plan(cb_es_plan* P) {
     hdr2[2 * q + 1] = make_uint4((uint32_t)x.w[0], (uint32_t)(x.w[0] >> 32), (uint32_t)hi, (uint32_t)(hi >> 32));
   }
   cudaError_t e;
-  if (P->fsm_compact) {
-    if ((e = P->d_fsm_ctable.upload(reinterpret_cast<const uint32_t*>(ctab.data()), ctab.size() * 2)) !=
-            cudaSuccess ||
+  if (P->fsm_layout != 0) {
+    if ((e = P->d_fsm_ctable.upload(stab.data(), stab.size())) != cudaSuccess ||
         (e = P->d_fsm_dtab.upload(reinterpret_cast<const uint32_t*>(dtab.data()), dtab.size() * 4)) != cudaSuccess) {
       cb_set_error(std::string("CUDA error in plan upload: ") + cudaGetErrorString(e));
       return CB_ERR_CUDA;
     }
     P->fsm_deltas = (int32_t)dtab.size();
-    table.resize(2);  // only the 8-byte copy is kept on the device
+    table.resize(2);  // only the short copy is kept on the device
   }
   if ((e = P->d_fsm_hdr.upload(reinterpret_cast<const uint32_t*>(hdr2.data()), hdr2.size() * 4)) != cudaSuccess ||
       (e = P->d_fsm_table.upload(reinterpret_cast<const uint32_t*>(table.data()), table.size() * 4)) !=
@@ -614,10 +648,10 @@ int build_fsm_plan(cb_es_plan* P) {
   P->fsm_states_max = 0;
   P->fsm_entries = (int64_t)n_entries;
   P->fsm_ok = true;
-  // automatic selection only while the table stays cache-resident (NasNet-A's
-  // 13.8 MB table makes every step an L2 round trip: slower than the
-  // packed-label walk); `set_path("fsm")` still forces it
-  P->fsm_auto = n_entries * (P->fsm_compact ? sizeof(uint2) : 2 * sizeof(uint4)) <= ((size_t)1 << 20);
+  // automatic selection while the table stays cache-resident: in L1 for
+  // BERT-base (46 KB), in L2 for NasNet-A (13.8 MB at 16 bytes, still faster
+  // than the packed-label walk); `set_path("fsm")` forces it beyond
+  P->fsm_auto = n_entries * (size_t)fsm_entry_bytes(P) <= ((size_t)32 << 20);
   return CB_OK;
 }
 

@@ -93,7 +93,7 @@ struct cb_es_plan {
   bool fsm_ok = false;
   bool fsm_auto = false;  // chosen by the automatic path (table <= 1 MB)
   DBuf<uint32_t> d_fsm_hdr, d_fsm_table;
-  bool fsm_compact = false;  // 8-byte transitions + shared delta table
+  int32_t fsm_layout = 0;  // transitions: 1 = 8 bytes, 2 = 16 bytes (+ shared delta table), 0 = 32 bytes
   DBuf<uint32_t> d_fsm_ctable, d_fsm_dtab;
   int32_t fsm_deltas = 0;
   int32_t fsm_states_max = 0;

@@ -171,28 +171,34 @@ def test_edge_plans_every_path(gpu, n_rows):
         plan.set_path("auto")
 
 
-@pytest.mark.parametrize("name", ["bert_base", "nasrnn"])
+@pytest.mark.parametrize("name", ["bert_base", "nasrnn", "nasnet_a"])
 def test_fsm_entry_layouts_agree(gpu, name, monkeypatch):
-    """The 8-byte transition layout (shared delta table) and the 32-byte one
-    (forced by CB_FSM_WIDE_ENTRIES at plan build) give identical fitness."""
+    """The 8-byte and 16-byte transition layouts (shared delta table) and the
+    32-byte one (chosen by CB_FSM_ENTRY_BYTES at plan build) give identical
+    fitness; NasNet-A (up to 5 merges per transition) has no 8-byte form."""
     g = workloads.CONFIGS[name]()
     bs = workloads.paper_backends(g)
     res = tp.optimize(g, bs.registry, bs.measurer, 0.01)
     args = (g, bs.registry, bs.measurer, res.placement, 0.01, bs.graph_backend, res.kernel_matches)
-    compact = tp.FitnessPlan(*args)
-    monkeypatch.setenv("CB_FSM_WIDE_ENTRIES", "1")
-    wide = tp.FitnessPlan(*args)
-    monkeypatch.delenv("CB_FSM_WIDE_ENTRIES")
-    assert compact.has_fsm() and wide.has_fsm()
-    assert compact.info.fsm_entry_bytes == 8 and wide.info.fsm_entry_bytes == 32
-    assert compact.info.fsm_transitions == wide.info.fsm_transitions
-    genomes = _genomes(compact, np.random.default_rng(11), 4000)
-    compact.set_path("fsm")
-    wide.set_path("fsm")
-    got = compact.evaluate(genomes)
-    assert np.array_equal(got, wide.evaluate(genomes))
-    wide.set_path("unionfind")
-    assert np.array_equal(got, wide.evaluate(genomes))
+    plans = {}
+    for nbytes in (8, 16, 32):
+        monkeypatch.setenv("CB_FSM_ENTRY_BYTES", str(nbytes))
+        plans[nbytes] = tp.FitnessPlan(*args)
+    monkeypatch.delenv("CB_FSM_ENTRY_BYTES")
+    default = tp.FitnessPlan(*args)
+    assert all(p.has_fsm() for p in plans.values())
+    want_small = 16 if name == "nasnet_a" else 8
+    assert default.info.fsm_entry_bytes == want_small
+    assert plans[8].info.fsm_entry_bytes == want_small
+    assert plans[16].info.fsm_entry_bytes == 16 and plans[32].info.fsm_entry_bytes == 32
+    assert len({p.info.fsm_transitions for p in plans.values()}) == 1
+    genomes = _genomes(plans[8], np.random.default_rng(11), 1000 if name == "nasnet_a" else 4000)
+    plans[32].set_path("unionfind")
+    want = plans[32].evaluate(genomes)
+    for nbytes, plan in plans.items():
+        plan.set_path("fsm")
+        assert np.array_equal(plan.evaluate(genomes), want), nbytes
+    assert default.kernel_name().startswith("fitness_fsm_kernel")  # automatic choice
 
 
 @pytest.mark.parametrize("seed,n,window", [(7, 1200, 4), (8, 2500, 3), (9, 700, 6), (10, 400, 8)])
