@@ -77,10 +77,11 @@ __device__ __forceinline__ void fsm_price(const ulonglong2* q, int idx, const Fs
   atomicAdd(reinterpret_cast<unsigned long long*>(thi + owner), hi + ((o0 + lo) < o0));
 }
 
-template <int F>
-struct FsmSmemBase {  // packed sums [F][T], per-warp queues and lane totals
-  static constexpr size_t bytes =
+template <int F, int W>
+struct FsmSmemBase {  // packed sums [F][T], per-warp queues and lane totals, genome words [W + 1][T]
+  static constexpr size_t words_off =
       (size_t)F * FSM_THREADS * 16 + (size_t)(FSM_THREADS / 32) * (FSM_QCAP * 16 + 64 * 8);
+  static constexpr size_t bytes = words_off + (W > 0 ? (size_t)(W + 1) * FSM_THREADS * 8 : 0);
 };
 
 // Transition entry (32 bytes, C = false): x = next | open << 16 | n_merge << 17 |
@@ -100,7 +101,7 @@ fitness_fsm_kernel(FsmArgs a, const uint64_t* __restrict__ pop, int64_t n, doubl
   constexpr int T = FSM_THREADS;
   extern __shared__ __align__(16) unsigned char fsm_smem[];
   // deltas after the per-thread arrays (dynamic size: n_delta entries)
-  uint4* sdelta = reinterpret_cast<uint4*>(fsm_smem + FsmSmemBase<F>::bytes);
+  uint4* sdelta = reinterpret_cast<uint4*>(fsm_smem + FsmSmemBase<F, W>::bytes);
   const uint32_t sdelta_base = (uint32_t)__cvta_generic_to_shared(sdelta);
   if (L != 0) {
     for (int k = threadIdx.x; k < a.n_delta; k += T) sdelta[k] = __ldg(a.dtab + k);
@@ -113,6 +114,11 @@ fitness_fsm_kernel(FsmArgs a, const uint64_t* __restrict__ pop, int64_t n, doubl
   uint64_t* tlo = reinterpret_cast<uint64_t*>(sv + F * T + (T / 32) * FSM_QCAP) + warp * 64;
   uint64_t* thi = tlo + 32;
   tlo[lane] = thi[lane] = 0ull;
+  // W > 0: the genome's words, then an all-ones word for units without a
+  // genome bit; a step's header holds its word's byte offset and bit, so the
+  // bit is one shared load + shift (no per-step word select)
+  uint64_t* swd = reinterpret_cast<uint64_t*>(fsm_smem + FsmSmemBase<F, W>::words_off) + t;
+  if (W > 0) swd[W * T] = ~0ull;
   __syncwarp();
   int qn = 0;
   bool inexact = false;
@@ -139,6 +145,9 @@ fitness_fsm_kernel(FsmArgs a, const uint64_t* __restrict__ pop, int64_t n, doubl
       const int64_t inext = i + stride;  // prefetch the next genome of this thread
 #pragma unroll
       for (int w = 0; w < WR; ++w) pre[w] = inext < n ? __ldcs(pop + inext * W + w) : 0ull;
+      // an infeasible genome walks all-zero bits (its result is discarded)
+#pragma unroll
+      for (int w = 0; w < WR; ++w) swd[w * T] = dead ? 0ull : cur[w];
     } else if (in_range) {
       for (int32_t w = 0; w < a.words; ++w) dead |= (__ldg(gen + w) & __ldg(a.infeas + w)) != 0ull;
     }
@@ -147,16 +156,17 @@ fitness_fsm_kernel(FsmArgs a, const uint64_t* __restrict__ pop, int64_t n, doubl
     int32_t cached_word = -1;
     uint64_t word = 0ull, next_word = W == 0 && a.words > 0 ? __ldg(gen) : 0ull;
     uint4 hn = __ldg(a.hdr);  // step headers are warp uniform: prefetched one step ahead
+    auto bit_of = [&](uint32_t hy) {  // W > 0: the step's genome bit from shared memory
+      const uint64_t wd = swd[(hy >> 8) * T];
+      return (uint32_t)(wd >> (hy & 63u)) & 1u;
+    };
+    uint32_t on_next = W > 0 ? bit_of(hn.y) : 0u;
     for (int32_t p = 0; p < a.M; ++p) {
       const uint4 h = hn;
       if (p + 1 < a.M) hn = __ldg(a.hdr + 2 * (p + 1));
       bool on;
       if (W > 0) {
-        const uint32_t wi = h.y >> 8;
-        uint64_t wd = cur[0];
-#pragma unroll
-        for (int w = 1; w < WR; ++w) wd = wi == (uint32_t)w ? cur[w] : wd;
-        on = ((wd >> (h.y & 63u)) & 1ull) != 0ull || (h.y & FSM_BIT_FORCED);
+        on = on_next != 0u;
       } else {
         on = true;
         if (!(h.y & FSM_BIT_FORCED)) {
@@ -169,7 +179,7 @@ fitness_fsm_kernel(FsmArgs a, const uint64_t* __restrict__ pop, int64_t n, doubl
           on = (word >> (h.y & 63u)) & 1ull;
         }
       }
-      on = on && !dead;
+      if (W == 0) on = on && !dead;
       const uint32_t idx = h.x + 2u * state + (on ? 1u : 0u);  // 32-bit index math
       uint32_t open, nmerge, nemit, merges, emits;
       uint4 dv;  // exact delta: closed one-unit regions' terms - removed term
@@ -246,6 +256,7 @@ fitness_fsm_kernel(FsmArgs a, const uint64_t* __restrict__ pop, int64_t n, doubl
           }
         }
       }
+      if (W > 0) on_next = bit_of(hn.y);  // next step's bit, off the state chain
     }
     __syncwarp();
     if (lane < qn) fsm_price(q, lane, a, tlo, thi, inexact);
@@ -270,7 +281,7 @@ fitness_fsm_kernel(FsmArgs a, const uint64_t* __restrict__ pop, int64_t n, doubl
 
 template <int F, int W, int L>
 int launch_fsm_t(cb_es_plan* p, const uint64_t* d_pop, int64_t n, double* d_fit, cudaStream_t stream) {
-  const size_t smem = FsmSmemBase<F>::bytes + (L != 0 ? (size_t)p->fsm_deltas * sizeof(uint4) : 0);
+  const size_t smem = FsmSmemBase<F, W>::bytes + (L != 0 ? (size_t)p->fsm_deltas * sizeof(uint4) : 0);
   static size_t configured = 0;
   if (configured < smem) {
     CB_CUDA_TRY(cudaFuncSetAttribute(fitness_fsm_kernel<F, W, L>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -401,7 +412,10 @@ int build_fsm_plan(cb_es_plan* P) {
     const int S = r.slot;
     occ_end[S] = P->prog_last[p];
     if ((int)ends[p].size() != r.nend) return CB_OK;  // program / end lists disagree
-    const uint32_t bitinfo = r.bit >= 0 ? ((uint32_t)r.bit & 63u) | ((uint32_t)(r.bit >> 6) << 8) : FSM_BIT_FORCED;
+    // bit | word << 8; a unit without a genome bit reads bit 0 of word
+    // `words` (the kernel's all-ones word when W > 0) and is flagged for W = 0
+    const uint32_t bitinfo = r.bit >= 0 ? ((uint32_t)r.bit & 63u) | ((uint32_t)(r.bit >> 6) << 8)
+                                        : FSM_BIT_FORCED | ((uint32_t)P->words << 8);
     hdr[p] = make_uint4((uint32_t)(table.size() / 2), bitinfo, (uint32_t)S | ((uint32_t)r.nend << 8), 0u);
     if ((table.size() + 4 * cur.size()) * sizeof(uint4) > cap) return CB_OK;
     next_ids.clear();
