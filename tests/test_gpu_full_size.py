@@ -107,3 +107,36 @@ def test_nasrnn_cell_matches_oracle_beyond_reference_cap(gpu):
         want = case["oracle_dp"]
         assert res.cost_ms == want["cost"], case["name"]
         assert kernels_of(res.placement) == want["kernels"], case["name"]
+
+
+@pytest.mark.parametrize("name", CONFIGS)
+def test_fitness_matches_oracle_at_full_size(gpu, name):
+    """Every BASELINE model config at full size: the automatically chosen
+    fitness kernel (the FSM walk for all four) against the CPU oracle's
+    restatement of the reference's graph-level pricing, bit for bit, on
+    sparse, random and dense genomes."""
+    import json
+    from oracle import OracleCase
+    from paper_2111_00655_b200.cost import profile_to_json
+    from paper_2111_00655_b200.graph import graph_to_json
+    g, bs = _setup(name)
+    res = tp.optimize(g, bs.registry, bs.measurer, 0.01)
+    plan = tp.FitnessPlan(g, bs.registry, bs.measurer, res.placement, 0.01, bs.graph_backend,
+                          res.kernel_matches)
+    rng = np.random.default_rng(21)
+    feasible = np.array([k != 0 for k in plan.rep_kind], dtype=np.uint8)
+    rows = [(rng.random((700, plan.k)) < d).astype(np.uint8) & feasible for d in (0.05, 0.5, 0.95)]
+    rows.append((rng.random((100, plan.k)) < 0.5).astype(np.uint8))  # infeasible bits allowed
+    genomes = np.concatenate(rows)
+    case = json.loads(json.dumps({
+        "graph": graph_to_json(g),
+        "backends": [[b.id, b.kind.value] for b in bs.registry.backends.values()],
+        "patterns": [[bp.backend, bp.text(), bp.source.value] for bp in bs.registry.patterns],
+        "profiles": {b: profile_to_json(p) for b, p in bs.measurer.profiles.items()},
+        "epsilon": 0.01}))
+    oc = OracleCase(case)
+    oc.price()
+    kernels = [[a.backend_pattern.order, a.root, sorted(a.nodes)] for a in res.placement.assignments]
+    want = oc.fitness(kernels, bs.graph_backend, genomes, threads=8)
+    assert plan.kernel_name().startswith("fitness_fsm_kernel")
+    assert np.array_equal(plan.evaluate(genomes), want)
