@@ -211,13 +211,16 @@ typedef struct {
   int32_t packed_labels; /* 1: frontier fits the packed-label kernels (<= 16 slots),
                             2: also the packed anchor kernel (<= 8 slots) */
   int32_t fsm_transitions; /* transitions of the finite-state program (0 = none) */
-  int32_t fsm_entry_bytes; /* 8 (compact entries + shared delta table) or 32 */
+  int32_t fsm_entry_bytes; /* transition layout: 8 or 16 (+ shared delta table), or 32 */
 } cb_es_plan_info;
 int cb_es_plan_query(const cb_es_plan* p, cb_es_plan_info* info);
-/* Evaluation path: -1 automatic (frontier program when available), 0 the
- * union-find kernels, 1 the frontier program (packed-label form when it has
- * <= 16 slots), 2 the frontier program in its shared-memory-label form.
- * For tests and profiling; all paths return identical results. */
+/* Evaluation path: -1 automatic (the finite-state walk when its table is
+ * <= 32 MB, else the frontier program when available), 0 the union-find
+ * kernels, 1 the frontier program (packed-label form when it has <= 16
+ * slots), 2 the frontier program in its shared-memory-label form, 3 the
+ * warp-per-genome walk, 4 the anchor walk, 5 the packed-label walk, 6 the
+ * packed anchor walk, 7 the finite-state walk.  For tests and profiling; all
+ * paths return identical results. */
 int cb_es_plan_set_path(cb_es_plan* p, int32_t path);
 /* Merged-component pool entries per genome of the anchor kernel (1..24,
  * default min(frontier slots, 16)); genomes that need more are priced by
