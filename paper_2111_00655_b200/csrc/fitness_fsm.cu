@@ -19,6 +19,7 @@
 // one 128-bit add, and only the listed sum moves.  Components keep their data at their anchor (the
 // member whose unit ends last), as in fitness_pa_kernel.
 #include <algorithm>
+#include <chrono>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -377,6 +378,14 @@ FsmState canonical(const int* lab, const bool* multi_of_label, int F) {
   return s;
 }
 
+struct FsmTrans {  // one computed transition before its next-state id is assigned
+  FsmState ns;
+  uint32_t open = 0, merges = 0, emits = 0;
+  int n_merge = 0, n_emit = 0;
+  fx192 dx;
+  bool ok = false;
+};
+
 }  // namespace
 
 static int fsm_entry_bytes(const cb_es_plan* P) { return P->fsm_layout == 1 ? 8 : P->fsm_layout == 2 ? 16 : 32; }
@@ -388,6 +397,7 @@ static int fsm_entry_bytes(const cb_es_plan* P) { return P->fsm_layout == 1 ? 8 
 int build_fsm_plan(cb_es_plan* P) {
   P->fsm_ok = false;
   if (!P->anchor_ok || P->F <= 0 || P->F > 8 || P->M == 0) return CB_OK;
+  const auto t_build0 = std::chrono::steady_clock::now();
   const int32_t M = P->M, F = P->F;
   // packed sums: non-negative unit sums below 2^101 (window span <= 100) and
   // kernel counts that fit 16 bits
@@ -404,8 +414,10 @@ int build_fsm_plan(cb_es_plan* P) {
   std::vector<uint4> hdr(M);
   std::vector<int32_t> occ_end(F, -1);
   std::vector<FsmState> cur(1);  // the empty frontier
-  std::unordered_map<uint64_t, int32_t> next_ids;
+  std::vector<uint64_t> hkey;
+  std::vector<int32_t> hval;
   std::vector<FsmState> nxt;
+  std::vector<FsmTrans> tr;
   const size_t cap = (size_t)64 << 20;
   for (int32_t p = 0; p < M; ++p) {
     const UnitRec& r = P->prog[p];
@@ -418,129 +430,162 @@ int build_fsm_plan(cb_es_plan* P) {
                                         : FSM_BIT_FORCED | ((uint32_t)P->words << 8);
     hdr[p] = make_uint4((uint32_t)(table.size() / 2), bitinfo, (uint32_t)S | ((uint32_t)r.nend << 8), 0u);
     if ((table.size() + 4 * cur.size()) * sizeof(uint4) > cap) return CB_OK;
-    next_ids.clear();
+    // next-state ids: open addressing on key + 1 (0 = empty), sized for
+    // every transition of the step
+    size_t hsize = 16;
+    int hbits = 4;
+    while (hsize < 4 * cur.size()) {
+      hsize <<= 1;
+      ++hbits;
+    }
+    hkey.assign(hsize, 0ull);
+    hval.resize(hsize);
     nxt.clear();
-    for (const FsmState& st : cur) {
-      for (int on = 0; on < 2; ++on) {
-        int lab[8];
-        bool multi[17];
-        for (int i = 0; i < 17; ++i) multi[i] = false;
-        for (int s = 0; s < F; ++s) {
-          lab[s] = (st.lab >> (4 * s)) & 0xF;
-          if (lab[s]) multi[lab[s]] = (st.multi >> (lab[s] - 1)) & 1u;
-        }
-        uint32_t open = 0, merges = 0, emits = 0;
-        int n_merge = 0, n_emit = 0;
-        fx192 delta = fx_zero();  // terms of the one-unit regions closed by this transition
-        auto anchor_of = [&](int label) {  // member whose unit ends last (ties: larger slot)
-          int best = -1;
-          for (int s = 0; s < F; ++s)
-            if (lab[s] == label && (best < 0 || occ_end[s] > occ_end[best] || (occ_end[s] == occ_end[best] && s > best)))
-              best = s;
-          return best;
-        };
-        if (on) {
-          int join[8], nj = 0;
-          for (int j = 0; j < r.nback; ++j) {
-            const int b = P->prog_slots[r.back_off + j];
-            const int l = lab[b];
-            if (!l) continue;
-            bool seen = false;
-            for (int k = 0; k < nj; ++k) seen |= join[k] == l;
-            if (!seen) join[nj++] = l;
-          }
-          int anchors[8];
-          for (int k = 0; k < nj; ++k) anchors[k] = anchor_of(join[k]);
-          const int L = 16;  // temporary label of the new component
-          lab[S] = L;
-          multi[L] = nj > 0;
-          for (int k = 0; k < nj; ++k)
-            for (int s = 0; s < F; ++s)
-              if (lab[s] == join[k]) lab[s] = L;
-          const int Wn = anchor_of(L);
-          open = 1;
-          auto add_merge = [&](int src) {
-            if (n_merge >= 5) return false;
-            merges |= ((uint32_t)src | ((uint32_t)Wn << 3)) << (6 * n_merge);
-            ++n_merge;
-            return true;
-          };
-          for (int k = 0; k < nj; ++k)
-            if (anchors[k] != Wn && !add_merge(anchors[k])) return CB_OK;
-          if (S != Wn && !add_merge(S)) return CB_OK;
-        }
-        // releases: a component closes when its last member leaves; its data
-        // is at the anchor it had when the step's releases began (the anchor
-        // ends last, so members still present then end at this step too)
-        int anchor_at[17];
-        for (int l = 0; l < 17; ++l) anchor_at[l] = -1;
-        for (int s = 0; s < F; ++s)
-          if (lab[s] && anchor_at[lab[s]] < 0) anchor_at[lab[s]] = anchor_of(lab[s]);
-        for (int j = 0; j < r.nend; ++j) {
-          const int e = P->prog_slots[r.end_off + j];
-          const int l = lab[e];
-          if (!l) continue;
-          const int A = anchor_at[l];
-          lab[e] = 0;
-          bool left = false;
-          for (int s = 0; s < F; ++s) left |= lab[s] == l;
-          if (left) continue;
-          if (multi[l]) {
-            if (n_emit >= 5) return CB_OK;
-            emits |= (uint32_t)A << (3 * n_emit);
-            ++n_emit;
-          } else {
-            fx_add(delta, P->prog[ends[p][j]].term1);  // its unit: end-list entry j
-          }
-        }
-        // the new component's label may be 16: remap before canonicalising
-        int lab2[8];
-        bool multi2[17];
-        for (int i = 0; i < 17; ++i) multi2[i] = multi[i];
-        for (int s = 0; s < F; ++s) lab2[s] = lab[s];
-        if (on) {
-          int freel = 1;
-          bool used[17] = {false};
-          for (int s = 0; s < F; ++s) used[lab2[s]] = true;
-          while (used[freel]) ++freel;
-          for (int s = 0; s < F; ++s)
-            if (lab2[s] == 16) lab2[s] = freel;
-          multi2[freel] = multi[16];
-        }
-        const FsmState ns = canonical(lab2, multi2, F);
-        auto it = next_ids.find(ns.key());
-        int32_t nid;
-        if (it == next_ids.end()) {
-          nid = (int32_t)nxt.size();
-          if (nid > 0xFFFF) return CB_OK;
-          next_ids.emplace(ns.key(), nid);
-          nxt.push_back(ns);
-        } else {
-          nid = it->second;
-        }
-        // exact delta of the transition: terms of the one-unit regions it
-        // closes minus the removed op-kernel term of an offloaded unit
-        if (on && r.bit >= 0) fx_sub(delta, r.off);
-        // to the 128-bit window: shift the magnitude, then restore the sign
-        const bool neg = (delta.w[2] >> 63) != 0;
-        fx192 mag = delta;
-        if (neg) {
-          mag = fx_zero();
-          fx_sub(mag, delta);
-        }
-        fx192 dx = fx_shr(mag, P->anchor_shift);
-        if (dx.w[2] != 0 || (dx.w[1] >> 62) != 0) return CB_OK;  // outside the window
-        if (neg) {
-          const fx192 m2 = dx;
-          dx = fx_zero();
-          fx_sub(dx, m2);
-        }
-        table.push_back(make_uint4((uint32_t)nid | (open << 16) | ((uint32_t)n_merge << 17) |
-                                       ((uint32_t)n_emit << 20),
-                                   merges, emits, 0u));
-        table.push_back(make_uint4((uint32_t)dx.w[0], (uint32_t)(dx.w[0] >> 32), (uint32_t)dx.w[1],
-                                   (uint32_t)(dx.w[1] >> 32)));
+    // every (state, bit) transition of the step, in parallel over states;
+    // next-state ids are then assigned in order, so the table is the same
+    // for every thread count
+    tr.resize(2 * cur.size());
+    auto compute = [&](const FsmState& st, int on, FsmTrans& out) -> bool {
+      int lab[8];
+      bool multi[17];
+      for (int i = 0; i < 17; ++i) multi[i] = false;
+      for (int s = 0; s < F; ++s) {
+        lab[s] = (st.lab >> (4 * s)) & 0xF;
+        if (lab[s]) multi[lab[s]] = (st.multi >> (lab[s] - 1)) & 1u;
       }
+      uint32_t open = 0, merges = 0, emits = 0;
+      int n_merge = 0, n_emit = 0;
+      fx192 delta = fx_zero();  // terms of the one-unit regions closed by this transition
+      auto anchor_of = [&](int label) {  // member whose unit ends last (ties: larger slot)
+        int best = -1;
+        for (int s = 0; s < F; ++s)
+          if (lab[s] == label && (best < 0 || occ_end[s] > occ_end[best] || (occ_end[s] == occ_end[best] && s > best)))
+            best = s;
+        return best;
+      };
+      if (on) {
+        int join[8], nj = 0;
+        for (int j = 0; j < r.nback; ++j) {
+          const int b = P->prog_slots[r.back_off + j];
+          const int l = lab[b];
+          if (!l) continue;
+          bool seen = false;
+          for (int k = 0; k < nj; ++k) seen |= join[k] == l;
+          if (!seen) join[nj++] = l;
+        }
+        int anchors[8];
+        for (int k = 0; k < nj; ++k) anchors[k] = anchor_of(join[k]);
+        const int L = 16;  // temporary label of the new component
+        lab[S] = L;
+        multi[L] = nj > 0;
+        for (int k = 0; k < nj; ++k)
+          for (int s = 0; s < F; ++s)
+            if (lab[s] == join[k]) lab[s] = L;
+        const int Wn = anchor_of(L);
+        open = 1;
+        auto add_merge = [&](int src) {
+          if (n_merge >= 5) return false;
+          merges |= ((uint32_t)src | ((uint32_t)Wn << 3)) << (6 * n_merge);
+          ++n_merge;
+          return true;
+        };
+        for (int k = 0; k < nj; ++k)
+          if (anchors[k] != Wn && !add_merge(anchors[k])) return false;
+        if (S != Wn && !add_merge(S)) return false;
+      }
+      // releases: a component closes when its last member leaves; its data
+      // is at the anchor it had when the step's releases began (the anchor
+      // ends last, so members still present then end at this step too)
+      int anchor_at[17];
+      for (int l = 0; l < 17; ++l) anchor_at[l] = -1;
+      for (int s = 0; s < F; ++s)
+        if (lab[s] && anchor_at[lab[s]] < 0) anchor_at[lab[s]] = anchor_of(lab[s]);
+      for (int j = 0; j < r.nend; ++j) {
+        const int e = P->prog_slots[r.end_off + j];
+        const int l = lab[e];
+        if (!l) continue;
+        const int A = anchor_at[l];
+        lab[e] = 0;
+        bool left = false;
+        for (int s = 0; s < F; ++s) left |= lab[s] == l;
+        if (left) continue;
+        if (multi[l]) {
+          if (n_emit >= 5) return false;
+          emits |= (uint32_t)A << (3 * n_emit);
+          ++n_emit;
+        } else {
+          fx_add(delta, P->prog[ends[p][j]].term1);  // its unit: end-list entry j
+        }
+      }
+      // the new component's label may be 16: remap before canonicalising
+      int lab2[8];
+      bool multi2[17];
+      for (int i = 0; i < 17; ++i) multi2[i] = multi[i];
+      for (int s = 0; s < F; ++s) lab2[s] = lab[s];
+      if (on) {
+        int freel = 1;
+        bool used[17] = {false};
+        for (int s = 0; s < F; ++s) used[lab2[s]] = true;
+        while (used[freel]) ++freel;
+        for (int s = 0; s < F; ++s)
+          if (lab2[s] == 16) lab2[s] = freel;
+        multi2[freel] = multi[16];
+      }
+      const FsmState ns = canonical(lab2, multi2, F);
+      // exact delta of the transition: terms of the one-unit regions it
+      // closes minus the removed op-kernel term of an offloaded unit
+      if (on && r.bit >= 0) fx_sub(delta, r.off);
+      // to the 128-bit window: shift the magnitude, then restore the sign
+      const bool neg = (delta.w[2] >> 63) != 0;
+      fx192 mag = delta;
+      if (neg) {
+        mag = fx_zero();
+        fx_sub(mag, delta);
+      }
+      fx192 dx = fx_shr(mag, P->anchor_shift);
+      if (dx.w[2] != 0 || (dx.w[1] >> 62) != 0) return false;  // outside the window
+      if (neg) {
+        const fx192 m2 = dx;
+        dx = fx_zero();
+        fx_sub(dx, m2);
+      }
+      out.ns = ns;
+      out.open = open;
+      out.merges = merges;
+      out.emits = emits;
+      out.n_merge = n_merge;
+      out.n_emit = n_emit;
+      out.dx = dx;
+      return true;
+    };
+    const int64_t n_states = (int64_t)cur.size();
+#pragma omp parallel for schedule(static) if (n_states >= 64)
+    for (int64_t si = 0; si < n_states; ++si)
+      for (int on = 0; on < 2; ++on) tr[2 * si + on].ok = compute(cur[si], on, tr[2 * si + on]);
+    for (const FsmTrans& t_ : tr) {
+      if (!t_.ok) return CB_OK;
+      const FsmState& ns = t_.ns;
+      const uint32_t open = t_.open, merges = t_.merges, emits = t_.emits;
+      const int n_merge = t_.n_merge, n_emit = t_.n_emit;
+      const fx192& dx = t_.dx;
+      const uint64_t hk = ns.key() + 1ull;
+      size_t h = (size_t)((hk * 0x9E3779B97F4A7C15ull) >> (64 - hbits));  // Fibonacci hashing: top bits
+      while (hkey[h] != 0ull && hkey[h] != hk) h = (h + 1) & (hsize - 1);
+      int32_t nid;
+      if (hkey[h] == 0ull) {
+        nid = (int32_t)nxt.size();
+        if (nid > 0xFFFF) return CB_OK;
+        hkey[h] = hk;
+        hval[h] = nid;
+        nxt.push_back(ns);
+      } else {
+        nid = hval[h];
+      }
+      table.push_back(make_uint4((uint32_t)nid | (open << 16) | ((uint32_t)n_merge << 17) |
+                                     ((uint32_t)n_emit << 20),
+                                 merges, emits, 0u));
+      table.push_back(make_uint4((uint32_t)dx.w[0], (uint32_t)(dx.w[0] >> 32), (uint32_t)dx.w[1],
+                                 (uint32_t)(dx.w[1] >> 32)));
     }
     // step-level maxima: the kernel skips the emit / merge loops when no
     // transition of the step has any (warp-uniform)
@@ -572,8 +617,9 @@ int build_fsm_plan(cb_es_plan* P) {
         dd[lo * 1000003ull ^ hi] = 1;
       }
     }
-    fprintf(stderr, "fsm stats: M %d F %d entries %zu states/step max %d merges max %d emits max %d delta bits max %d zero %d distinct %zu window span %d\n",
-            M, F, table.size() / 2, smax, mm, me, dbits, zero, dd.size(), P->anchor_span);
+    fprintf(stderr, "fsm stats: M %d F %d entries %zu states/step max %d merges max %d emits max %d delta bits max %d zero %d distinct %zu window span %d enumeration %.1f ms\n",
+            M, F, table.size() / 2, smax, mm, me, dbits, zero, dd.size(), P->anchor_span,
+            std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_build0).count());
   }
   const size_t n_entries = table.size() / 2;
   // the smallest layout every transition fits: 8 bytes (12-bit next state,
