@@ -20,6 +20,8 @@
 // Evaluation (device).  The plan orders the units into a "frontier
 // program" (each unit holds a slot from its position to its last
 // neighbour's) and launch_fitness picks the kernel by the program's width F:
+//   F <= 8   fitness_fsm_kernel         (fitness_fsm.cu) tabulated state machine,
+//            while its transition table stays <= 32 MB (all model configs)
 //   F <= 8   fitness_pa_kernel          (fitness_packed128.cu) packed anchor labels
 //   F <= 16  fitness_packed128_kernel / fitness_frontier2_kernel (this file)
 //   F <= 64  fitness_anchor_kernel      (fitness_anchor.cu) union-find anchors
