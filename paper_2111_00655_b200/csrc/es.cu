@@ -116,7 +116,7 @@ breed_kernel(int32_t k, int32_t words, const uint64_t* __restrict__ parents,
 template <int W>
 __global__ void __launch_bounds__(256)
 breed_thread_kernel(int32_t k, const uint64_t* __restrict__ parents, const double* __restrict__ fit,
-                    const uint32_t* __restrict__ keys, int64_t n_parents, uint64_t* __restrict__ children, int64_t n_children,
+                    const cb_key_t* __restrict__ keys, int64_t n_parents, uint64_t* __restrict__ children, int64_t n_children,
                     const uint64_t* __restrict__ keep, int64_t n_keep, uint64_t seed,
                     uint32_t generation, uint32_t stream_id, int32_t tournament, double rate,
                     double log1m_rate) {
@@ -135,15 +135,62 @@ breed_thread_kernel(int32_t k, const uint64_t* __restrict__ parents, const doubl
 // Tournament order keys: the high word of each fitness (non-negative doubles
 // and +inf order like their bit patterns), half the bytes of the fitness
 // array so that a large population's keys stay in L2 for the random gathers.
-__global__ void fitness_keys_kernel(const double* __restrict__ fit, int64_t n, uint32_t* __restrict__ keys) {
+// Finite [min, max] of the (non-negative) fitness as ordered bit patterns:
+// mm[0] = min, mm[1] = max (preset to ~0 / 0).
+__global__ void fitness_minmax_kernel(const double* __restrict__ fit, int64_t n, unsigned long long* mm) {
+  unsigned long long lo = ~0ull, hi = 0ull;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride)
-    keys[i] = (uint32_t)((unsigned long long)__double_as_longlong(__ldg(fit + i)) >> 32);
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+    const double f = __ldcs(fit + i);
+    if (isfinite(f)) {
+      const unsigned long long u = (unsigned long long)__double_as_longlong(f);
+      lo = u < lo ? u : lo;
+      hi = u > hi ? u : hi;
+    }
+  }
+#pragma unroll
+  for (int d = 16; d > 0; d >>= 1) {
+    const unsigned long long l2 = __shfl_xor_sync(0xffffffffu, lo, d), h2 = __shfl_xor_sync(0xffffffffu, hi, d);
+    lo = l2 < lo ? l2 : lo;
+    hi = h2 > hi ? h2 : hi;
+  }
+  if ((threadIdx.x & 31) == 0) {
+    if (lo != ~0ull) atomicMin(mm, lo);
+    if (hi != 0ull) atomicMax(mm + 1, hi);
+  }
+}
+
+// 16-bit order keys (es_ops.cuh): floor((f - min) * 65534 / (max - min)),
+// 65535 for infinite fitness.  Fitness streams through evict-first so the
+// keys the tournaments gather next stay in L2.
+__global__ void fitness_keys_kernel(const double* __restrict__ fit, int64_t n, const unsigned long long* mm,
+                                    cb_key_t* __restrict__ keys) {
+  const unsigned long long ulo = mm[0], uhi = mm[1];
+  const double lo = __longlong_as_double((long long)ulo), hi = __longlong_as_double((long long)uhi);
+  const double scale = (ulo < uhi && hi > lo) ? 65534.0 / (hi - lo) : 0.0;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+    const double f = __ldcs(fit + i);
+    keys[i] = isfinite(f) ? (cb_key_t)fmin(65534.0, floor((f - lo) * scale)) : (cb_key_t)65535;
+  }
+}
+
+// Order keys of the parents into p->d_keys (two small passes over the fitness).
+static int launch_keys(cb_es_plan* p, const double* d_fit, int64_t n, cudaStream_t s) {
+  if (p->d_keys.n < (size_t)n) CB_CUDA_TRY(p->d_keys.alloc((size_t)n));
+  if (p->d_fminmax.n < 2) CB_CUDA_TRY(p->d_fminmax.alloc(2));
+  CB_CUDA_TRY(cudaMemsetAsync(p->d_fminmax.p, 0xFF, sizeof(unsigned long long), s));
+  CB_CUDA_TRY(cudaMemsetAsync(p->d_fminmax.p + 1, 0, sizeof(unsigned long long), s));
+  const int64_t kb = std::min<int64_t>((n + 255) / 256, (int64_t)cb_sm_count() * 16);
+  fitness_minmax_kernel<<<(unsigned)kb, 256, 0, s>>>(d_fit, n, p->d_fminmax.p);
+  fitness_keys_kernel<<<(unsigned)kb, 256, 0, s>>>(d_fit, n, p->d_fminmax.p, p->d_keys.p);
+  CB_CUDA_TRY(cudaGetLastError());
+  return CB_OK;
 }
 
 template <int W>
 static void launch_breed_thread(int32_t k, const uint64_t* parents, const double* fit,
-                                const uint32_t* keys, int64_t n_parents, uint64_t* children, int64_t n_children,
+                                const cb_key_t* keys, int64_t n_parents, uint64_t* children, int64_t n_children,
                                 const uint64_t* keep, int64_t n_keep, uint64_t seed, uint32_t gen,
                                 uint32_t sid, int32_t tournament, double rate, double log1m,
                                 cudaStream_t s) {
@@ -169,12 +216,11 @@ extern "C" int cb_es_breed(cb_es_plan* p, const uint64_t* d_parents, const doubl
   double log1m = (mutation_rate > 0.0 && mutation_rate < 1.0) ? log1p(-mutation_rate) : -1.0;
   cudaStream_t s = (cudaStream_t)stream;
   const uint32_t gen = (uint32_t)generation, sid = (uint32_t)stream_id;
-  uint32_t* keys = nullptr;
+  const cb_key_t* keys = nullptr;
   if (info.words <= 8) {
-    if (p->d_keys.n < (size_t)n_parents) CB_CUDA_TRY(p->d_keys.alloc((size_t)n_parents));
+    const int rc = launch_keys(p, d_parent_fit, n_parents, s);
+    if (rc != CB_OK) return rc;
     keys = p->d_keys.p;
-    const int64_t kb = std::min<int64_t>((n_parents + 255) / 256, (int64_t)cb_sm_count() * 16);
-    fitness_keys_kernel<<<(unsigned)kb, 256, 0, s>>>(d_parent_fit, n_parents, keys);
   }
   switch (info.words) {
 #define CB_BREED_CASE(Wn)                                                                   \
@@ -228,10 +274,8 @@ extern "C" int cb_es_generation(cb_es_plan* p, const uint64_t* d_parents, const 
     if (rc != CB_OK) return rc;
     return cb_fitness_device(p, d_children, n_children, d_child_fit, stream);
   }
-  if (p->d_keys.n < (size_t)n_parents) CB_CUDA_TRY(p->d_keys.alloc((size_t)n_parents));
-  const int64_t kb = std::min<int64_t>((n_parents + 255) / 256, (int64_t)cb_sm_count() * 16);
-  fitness_keys_kernel<<<(unsigned)kb, 256, 0, s>>>(d_parent_fit, n_parents, p->d_keys.p);
-  CB_CUDA_TRY(cudaGetLastError());
+  const int rc = launch_keys(p, d_parent_fit, n_parents, s);
+  if (rc != CB_OK) return rc;
   BreedArgs br;
   br.k = p->k;
   br.parents = d_parents;

@@ -99,7 +99,8 @@ struct cb_es_plan {
   int32_t fsm_states_max = 0;
   int64_t fsm_entries = 0;
   // tournament order keys of the parent population (es.cu)
-  DBuf<uint32_t> d_keys;
+  DBuf<uint16_t> d_keys;                // 16-bit tournament order keys (es_ops.cuh)
+  DBuf<unsigned long long> d_fminmax;  // finite fitness [min, max] bit patterns for the keys
   // packed anchor walk (fitness_packed128.cu, <= 8 slots): 16-byte step headers
   bool pa_ok = false;
   DBuf<uint32_t> d_pahdr;

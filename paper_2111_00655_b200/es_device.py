@@ -90,11 +90,12 @@ class DeviceEvolution:
         # -- the walk is issue bound and the in-kernel breed adds to its issue
         # load more than it hides of the breed's memory latency.
         self.fused = bool(fused) and plan.fused_generation()
-        # kernels of libcollage_b200.so per generation: tournament order keys,
-        # (fused | breed + fitness), the two CUB argmin kernels and their unpack
+        # kernels of libcollage_b200.so per generation: fitness min/max and the
+        # tournament order keys, (fused | breed + fitness), the two CUB argmin
+        # kernels and their unpack
         # (+ the overflow list kernel when the anchor walk prices the plan);
         # torch's index_select / copies of the elite row are not counted
-        self.launches_per_generation = (5 if self.fused else 6) + \
+        self.launches_per_generation = (6 if self.fused else 7) + \
             (1 if plan.kernel_name() == "fitness_anchor_kernel" else 0)
 
     # -- helpers -----------------------------------------------------------------------
