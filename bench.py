@@ -261,7 +261,8 @@ def run_mine(args) -> None:
         "higher_is_better": True,
         "scaling": "weak",
         "vs_baseline": None,
-        "dtype": "u64 bit-genomes, exact fixed-point costs (128-bit plan window)",
+        "dtype": "int128",
+        "arithmetic": "u64 bit-genomes; exact 128-bit fixed-point cost sums (plan window), f64 region pricing",
         "data": "synthetic (BERT-base graph built op by op; simulated backend cost tables)",
         "config": {"workload": f"{args.workload}: op-level DP + evolutionary search",
                    "nodes": len(g.nodes), "dp_kernels": len(res.placement),
@@ -509,7 +510,8 @@ def run_reference(args) -> None:
         "higher_is_better": True,
         "scaling": "weak",
         "vs_baseline": None,
-        "dtype": "f64 (fsum-exact), CPU",
+        "dtype": "f64",
+        "arithmetic": "f64 with exact sums (Kulisch accumulator, fsum-equivalent rounding), CPU",
         "data": "synthetic (BERT-base graph; simulated backend cost tables)",
         "config": {"workload": f"{args.workload}: op-level DP + evolutionary search",
                    "nodes": len(g.nodes), "genome_bits": k, "dp_status": status,
