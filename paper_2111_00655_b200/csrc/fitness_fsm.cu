@@ -28,7 +28,7 @@
 
 #include "fitness_plan.cuh"
 
-#define FSM_THREADS 128
+#define FSM_THREADS 256
 #define FSM_QCAP 64
 
 namespace {
@@ -287,14 +287,14 @@ int launch_fsm_t(cb_es_plan* p, const uint64_t* d_pop, int64_t n, double* d_fit,
   if (configured < smem) {
     CB_CUDA_TRY(cudaFuncSetAttribute(fitness_fsm_kernel<F, W, L>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      (int)smem));
-    // the smallest shared-memory configuration holding 8 blocks (the
-    // register limit); the rest of the 256 KB stays L1 for the transition
+    // the smallest shared-memory configuration holding 1024 threads (8
+    // blocks: the register limit); the rest of the 256 KB stays L1 for the transition
     // table (BERT-base, F = 6: 164 KB, +4% over the maximal carveout).  The
     // percentage is rounded down so it maps back onto that configuration.
     const char* cv = getenv("CB_FSM_CARVEOUT");
     int pct = 100;
     for (int kb : {100, 132, 164, 196})
-      if ((size_t)kb * 1024 >= 8 * (smem + 1024)) {
+      if ((size_t)kb * 1024 >= (1024 / FSM_THREADS) * (smem + 1024)) {
         pct = kb * 100 / 228;
         break;
       }
