@@ -8,11 +8,15 @@ import paper_2111_00655_b200 as tp
 from paper_2111_00655_b200 import workloads
 from paper_2111_00655_b200.es_device import DeviceEvolution
 
+# CB_FSM_ENTRY_BYTES=16 / 32 in the environment selects the FSM walk's
+# wider transition layouts; "narrow" (a long DAG with few slots) runs the
+# FSM walk with genome words loaded on demand (W = 0)
 for name, g, bs in (
         ("bert", workloads.bert_base(layers=1), None),
-        ("rand", workloads.random_dag(400, seed=2, ops=workloads.RANDOM_OPS, window=48), None)):
+        ("rand", workloads.random_dag(400, seed=2, ops=workloads.RANDOM_OPS, window=48), None),
+        ("narrow", workloads.random_dag(700, seed=9, ops=workloads.RANDOM_OPS, window=6), None)):
     bs = workloads.paper_backends(g, verify=False) if name == "bert" else \
-        workloads.random_backends(g, n_backends=6, n_graph=1, seed=2)
+        workloads.random_backends(g, n_backends=6, n_graph=1, seed=2 if name == "rand" else 9)
     res = tp.optimize(g, bs.registry, bs.measurer, 0.01)
     plan = tp.FitnessPlan(g, bs.registry, bs.measurer, res.placement, 0.01, bs.graph_backend,
                           res.kernel_matches)
@@ -47,4 +51,5 @@ for name, g, bs in (
         for _ in range(3):
             es.step()
         es.best()
-    print(name, plan.info.frontier_slots, paths, "ok", flush=True)
+    print(name, plan.info.frontier_slots, "words", plan.words, "fsm entry bytes", plan.info.fsm_entry_bytes,
+          paths, "ok", flush=True)
