@@ -136,7 +136,7 @@ breed_thread_kernel(int32_t k, const uint64_t* __restrict__ parents, const doubl
 // and +inf order like their bit patterns), half the bytes of the fitness
 // array so that a large population's keys stay in L2 for the random gathers.
 // Finite [min, max] of the (non-negative) fitness as ordered bit patterns:
-// mm[0] = min, mm[1] = max (preset to ~0 / 0).
+// mm[0] = ~min, mm[1] = max (both preset to 0, one memset).
 __global__ void fitness_minmax_kernel(const double* __restrict__ fit, int64_t n, unsigned long long* mm) {
   unsigned long long lo = ~0ull, hi = 0ull;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
@@ -155,7 +155,7 @@ __global__ void fitness_minmax_kernel(const double* __restrict__ fit, int64_t n,
     hi = h2 > hi ? h2 : hi;
   }
   if ((threadIdx.x & 31) == 0) {
-    if (lo != ~0ull) atomicMin(mm, lo);
+    if (lo != ~0ull) atomicMax(mm, ~lo);
     if (hi != 0ull) atomicMax(mm + 1, hi);
   }
 }
@@ -165,7 +165,7 @@ __global__ void fitness_minmax_kernel(const double* __restrict__ fit, int64_t n,
 // keys the tournaments gather next stay in L2.
 __global__ void fitness_keys_kernel(const double* __restrict__ fit, int64_t n, const unsigned long long* mm,
                                     cb_key_t* __restrict__ keys) {
-  const unsigned long long ulo = mm[0], uhi = mm[1];
+  const unsigned long long ulo = ~mm[0], uhi = mm[1];
   const double lo = __longlong_as_double((long long)ulo), hi = __longlong_as_double((long long)uhi);
   const double scale = (ulo < uhi && hi > lo) ? 65534.0 / (hi - lo) : 0.0;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
@@ -179,8 +179,7 @@ __global__ void fitness_keys_kernel(const double* __restrict__ fit, int64_t n, c
 static int launch_keys(cb_es_plan* p, const double* d_fit, int64_t n, cudaStream_t s) {
   if (p->d_keys.n < (size_t)n) CB_CUDA_TRY(p->d_keys.alloc((size_t)n));
   if (p->d_fminmax.n < 2) CB_CUDA_TRY(p->d_fminmax.alloc(2));
-  CB_CUDA_TRY(cudaMemsetAsync(p->d_fminmax.p, 0xFF, sizeof(unsigned long long), s));
-  CB_CUDA_TRY(cudaMemsetAsync(p->d_fminmax.p + 1, 0, sizeof(unsigned long long), s));
+  CB_CUDA_TRY(cudaMemsetAsync(p->d_fminmax.p, 0, 2 * sizeof(unsigned long long), s));
   const int64_t kb = std::min<int64_t>((n + 255) / 256, (int64_t)cb_sm_count() * 16);
   fitness_minmax_kernel<<<(unsigned)kb, 256, 0, s>>>(d_fit, n, p->d_fminmax.p);
   fitness_keys_kernel<<<(unsigned)kb, 256, 0, s>>>(d_fit, n, p->d_fminmax.p, p->d_keys.p);

@@ -126,19 +126,32 @@ class DeviceEvolution:
         self._evaluate(self.cur)
         self._record_best()
 
-    def _evaluate(self, which: int) -> None:
+    def _evaluate(self, which: int, stream: int | None = None) -> None:
         self.plan.evaluate_device(self.pop[which].data_ptr(), self.P, self.fit[which].data_ptr(),
-                                  self._stream())
+                                  self._stream() if stream is None else stream)
 
-    def _record_best(self) -> None:
+    def _ptrs(self):
+        # device pointers of the fixed buffers, as ctypes values (built once;
+        # the tensors are never reallocated)
+        p = getattr(self, "_ptr_cache", None)
+        if p is None:
+            p = self._ptr_cache = {
+                "pop": [self._ptr(t) for t in self.pop], "fit": [self._ptr(t) for t in self.fit],
+                "elite": self._ptr(self.elite), "best_idx": self._ptr(self.best_idx),
+                "best_val": self._ptr(self.best_val), "history": self.history.data_ptr(),
+                "hist_stride": self.history.element_size()}
+        return p
+
+    def _record_best(self, stream: int | None = None) -> None:
         if self.world == 1:
             # argmin, elite row and history entry in one native call
-            hist = (ctypes.c_void_p(self.history[self.generation:].data_ptr())
+            p = self._ptrs()
+            hist = (ctypes.c_void_p(p["history"] + self.generation * p["hist_stride"])
                     if self.generation < self.history.numel() else ctypes.c_void_p())
             nat.check(nat.lib().cb_argmin_elite(
-                self._ptr(self.fit[self.cur]), self.P, self._ptr(self.pop[self.cur]), self.W,
-                self._ptr(self.best_idx), self._ptr(self.best_val), self._ptr(self.elite), hist,
-                ctypes.c_void_p(self._stream())))
+                p["fit"][self.cur], self.P, p["pop"][self.cur], self.W, p["best_idx"],
+                p["best_val"], p["elite"], hist,
+                ctypes.c_void_p(self._stream() if stream is None else stream)))
             return
         nat.check(nat.lib().cb_argmin(self._ptr(self.fit[self.cur]), self.P,
                                       self._ptr(self.best_idx), self._ptr(self.best_val),
@@ -182,27 +195,26 @@ class DeviceEvolution:
             torch = _torch()
             ev = [torch.cuda.Event(enable_timing=True) for _ in range(2 if self.fused else 3)]
             ev[0].record()
-        args = (self.plan.handle.raw, self._ptr(self.pop[self.cur]), self._ptr(self.fit[self.cur]),
-                self.P)
+        p = self._ptrs()
+        stream = self._stream()
+        args = (self.plan.handle.raw, p["pop"][self.cur], p["fit"][self.cur], self.P)
         rng = (ctypes.c_uint64(self.seed), ctypes.c_uint64(self.generation),
                ctypes.c_uint64(self.rank), self.tournament, float(self.rate),
-               ctypes.c_void_p(self._stream()))
+               ctypes.c_void_p(stream))
         if self.fused:
-            nat.check(nat.lib().cb_es_generation(*args, self._ptr(self.pop[nxt]),
-                                                 self._ptr(self.fit[nxt]), self.P,
-                                                 self._ptr(self.elite), 1, *rng))
+            nat.check(nat.lib().cb_es_generation(*args, p["pop"][nxt], p["fit"][nxt], self.P,
+                                                 p["elite"], 1, *rng))
             self.cur = nxt
         else:
-            nat.check(nat.lib().cb_es_breed(*args, self._ptr(self.pop[nxt]), self.P,
-                                            self._ptr(self.elite), 1, *rng))
+            nat.check(nat.lib().cb_es_breed(*args, p["pop"][nxt], self.P, p["elite"], 1, *rng))
             if timing:
                 ev[1].record()
             self.cur = nxt
-            self._evaluate(self.cur)
+            self._evaluate(self.cur, stream)
         if timing:
             ev[-1].record()
             self.kernel_events.append(tuple(ev))
-        self._record_best()
+        self._record_best(stream)
 
     def best(self) -> tuple[float, np.ndarray]:
         """(cost, genome bits) of the global best; synchronises."""
