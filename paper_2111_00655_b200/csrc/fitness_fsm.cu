@@ -233,7 +233,9 @@ fitness_fsm_kernel(FsmArgs a, const uint64_t* __restrict__ pop, int64_t n, doubl
         }
       }
       const int ne = (int)nemit;
-      const int nemax = (h.w >> 8) ? __reduce_max_sync(0xffffffffu, (unsigned)ne) : 0;
+      // the step's largest emit count (uniform, from its header): later
+      // iterations of lanes with fewer emits see an empty ballot
+      const int nemax = (int)((h.w >> 8) & 0xFFu);
       constexpr int MAXE = L == 1 ? 3 : 5;
 #pragma unroll
       for (int k = 0; k < MAXE; ++k) {  // multi-unit regions close: queued for pricing
