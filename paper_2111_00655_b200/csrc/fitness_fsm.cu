@@ -157,14 +157,21 @@ fitness_fsm_kernel(FsmArgs a, const uint64_t* __restrict__ pop, int64_t n, doubl
     int32_t cached_word = -1;
     uint64_t word = 0ull, next_word = W == 0 && a.words > 0 ? __ldg(gen) : 0ull;
     uint4 hn = __ldg(a.hdr);  // step headers are warp uniform: prefetched one step ahead
+    // the 16-byte layout (an L2-resident table) also prefetches the unit's
+    // packed sum (NasNet-A +3 %; the L1-resident walks lose ~0.5 % to it)
+    constexpr bool PRE_REP = L == 2;
+    uint4 rn = PRE_REP ? __ldg(a.hdr + 1) : make_uint4(0u, 0u, 0u, 0u);
     auto bit_of = [&](uint32_t hy) {  // W > 0: the step's genome bit from shared memory
       const uint64_t wd = swd[(hy >> 8) * T];
       return (uint32_t)(wd >> (hy & 63u)) & 1u;
     };
     uint32_t on_next = W > 0 ? bit_of(hn.y) : 0u;
     for (int32_t p = 0; p < a.M; ++p) {
-      const uint4 h = hn;
-      if (p + 1 < a.M) hn = __ldg(a.hdr + 2 * (p + 1));
+      const uint4 h = hn, rp = rn;
+      if (p + 1 < a.M) {
+        hn = __ldg(a.hdr + 2 * (p + 1));
+        if (PRE_REP) rn = __ldg(a.hdr + 2 * (p + 1) + 1);
+      }
       bool on;
       if (W > 0) {
         on = on_next != 0u;
@@ -217,7 +224,7 @@ fitness_fsm_kernel(FsmArgs a, const uint64_t* __restrict__ pop, int64_t n, doubl
       }
       fadd2(tot_lo, tot_hi, ((uint64_t)dv.y << 32) | dv.x, ((uint64_t)dv.w << 32) | dv.z);
       if (open) {  // the unit opens its slot with its packed sum
-        const uint4 r = __ldg(a.hdr + 2 * p + 1);
+        const uint4 r = PRE_REP ? rp : __ldg(a.hdr + 2 * p + 1);
         mine[(h.z & 0xFFu) * T] = make_ulonglong2(((uint64_t)r.y << 32) | r.x, ((uint64_t)r.w << 32) | r.z);
       }
       if (h.w & 0xFF) {
