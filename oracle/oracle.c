@@ -810,3 +810,335 @@ int or_fitness(int n, const int32_t* in_ptr, const int32_t* in_src, const int32_
   free(slot_kernel); free(rep_ptr); free(rep); free(rep_ok);
   return k;
 }
+
+/* ------------------------------------------------- independent exact DP */
+/*
+ * or_dp_subtree -- a second, independent solver for the reference optimum,
+ * for graphs whose covered-set state space is out of reach (NasNet-A,
+ * 10-step NasRNN, the 100k-node random DAG).
+ *
+ * What it computes is the reference's result (tensorplace/dp.py:71-179):
+ * the partition of the graph into registered matches with the smallest
+ * fsum of (kernel cost + epsilon), ties broken by the canonical key
+ * (placement.py:78-82: sorted (registration index, node tuple) pairs).
+ * The covered-set DP reaches exactly these partitions (dp.py:10-14), and a
+ * match may only expose its root (matching.py:104-110), so every non-root
+ * member of a kernel is post-dominated by the kernel's root.  Hence the
+ * kernels of any partition nest along the post-dominator tree and
+ *
+ *   OPT(r) = min over matches m rooted at r of
+ *            cost(m) + eps + sum of OPT(x) for x not in m with ipdom(x) in m
+ *
+ * with the answer the sum of OPT(x) over the tree's roots.  Written apart
+ * from the device solver on purpose:
+ *   - post-dominator SETS are built literally as graph.py:224-237 does
+ *     (intersection of the successors' sets, plus the node), as sorted
+ *     arrays of topological indices; ipdom is the set's member with the
+ *     smallest topological index (graph.py:239-251);
+ *   - sums are exact Kulisch accumulators (ksum), not 192-bit fixed point;
+ *   - ties are settled by materialising both candidate kernel lists,
+ *     sorting them and comparing them as the reference compares keys
+ *     (key_cmp above), not by a symmetric-difference walk.
+ * It also reports the smallest positive exact regret of any (node,
+ * candidate) decision, from which the caller decides whether rounded
+ * comparisons (the reference compares rounded state costs) could pick a
+ * different partition: every pair of same-cover states differs by a sum of
+ * such regrets.
+ *
+ * Returns 0 ok, 1 uncoverable, 3 cycle, 4 memory cap for the literal
+ * post-dominator sets exceeded.
+ */
+static int ks_cmp(const ksum* a, const ksum* b) {
+  for (int i = KL - 1; i >= 0; --i)
+    if (a->w[i] != b->w[i]) return a->w[i] < b->w[i] ? -1 : 1;
+  return 0;
+}
+
+/* a - b for a >= b */
+static void ks_sub(ksum* out, const ksum* a, const ksum* b) {
+  uint64_t br = 0;
+  for (int i = 0; i < KL; ++i) {
+    uint64_t x = a->w[i], y = b->w[i];
+    uint64_t d = x - y - br;
+    br = (x < y) || (x == y && br) || (x - y < br);
+    out->w[i] = d;
+  }
+  out->bad = a->bad | b->bad;
+}
+
+static int elem_cmp_q(const void* a, const void* b, void* ctx) {
+  return elem_cmp((const mt_t*)ctx, *(const int32_t*)a, *(const int32_t*)b);
+}
+
+static const mt_t* g_mt_ctx;
+static int elem_cmp_qs(const void* a, const void* b) {
+  return elem_cmp(g_mt_ctx, *(const int32_t*)a, *(const int32_t*)b);
+}
+
+typedef struct {
+  int n;
+  const int32_t *mem_ptr, *members;
+  const int32_t *ch_ptr, *ch; /* post-dominator children */
+  const int32_t* choice;
+  int32_t* mark; /* stamp per node */
+  int32_t* stack;
+} sol_ctx;
+
+/* kernels of the subtree solution of option (m at r), appended to out */
+static int collect(sol_ctx* c, int m, int32_t* out, int nout, int* stamp) {
+  /* members of m, then for each member its pdom children outside m */
+  int sp = 0;
+  ++*stamp;
+  int st = *stamp;
+  out[nout++] = m;
+  for (int i = c->mem_ptr[m]; i < c->mem_ptr[m + 1]; ++i) c->mark[c->members[i]] = st;
+  for (int i = c->mem_ptr[m]; i < c->mem_ptr[m + 1]; ++i) {
+    int y = c->members[i];
+    for (int j = c->ch_ptr[y]; j < c->ch_ptr[y + 1]; ++j)
+      if (c->mark[c->ch[j]] != st) c->stack[sp++] = c->ch[j];
+  }
+  while (sp) {
+    int x = c->stack[--sp];
+    int mx = c->choice[x];
+    out[nout++] = mx;
+    /* children of mx's members outside mx: members of mx are exactly the
+       nodes whose chain reaches x inside mx */
+    ++*stamp;
+    int s2 = *stamp;
+    for (int i = c->mem_ptr[mx]; i < c->mem_ptr[mx + 1]; ++i) c->mark[c->members[i]] = s2;
+    for (int i = c->mem_ptr[mx]; i < c->mem_ptr[mx + 1]; ++i) {
+      int y = c->members[i];
+      for (int j = c->ch_ptr[y]; j < c->ch_ptr[y + 1]; ++j)
+        if (c->mark[c->ch[j]] != s2) c->stack[sp++] = c->ch[j];
+    }
+  }
+  return nout;
+}
+
+int or_dp_subtree(int n, const int32_t* kind, const int32_t* in_ptr, const int32_t* in_src,
+                  const uint8_t* is_output, int n_match, const int32_t* group_ptr,
+                  const int32_t* pat, const int32_t* mem_ptr, const int32_t* members,
+                  const double* cost, double eps, int64_t max_set_entries,
+                  int32_t* kernels_out, int32_t* n_kernels, double* cost_out,
+                  double* min_regret_out, int32_t* ipdom_out, int64_t* ties_out) {
+  og_t g;
+  memset(&g, 0, sizeof(g));
+  g.n = n; g.kind = kind; g.in_ptr = in_ptr; g.in_src = in_src; g.is_output = is_output;
+  if (og_prepare(&g) != 0) { og_free(&g); return 3; }
+  /* topological order: Kahn, smallest index first (graph.py:156-176) */
+  int32_t* topo = malloc(sizeof(int32_t) * (n + 1));
+  int32_t* tix = malloc(sizeof(int32_t) * (n + 1));
+  {
+    int* pend = calloc(n + 1, sizeof(int));
+    for (int v = 0; v < n; ++v)
+      for (int j = g.out_ptr[v]; j < g.out_ptr[v + 1]; ++j) pend[g.out_dst[j]]++;
+    /* min-heap of ready indices */
+    int* heap = malloc(sizeof(int) * (n + 1));
+    int hn = 0, done = 0;
+    for (int v = 0; v < n; ++v)
+      if (!pend[v]) {
+        int i = hn++;
+        heap[i] = v;
+        while (i && heap[(i - 1) / 2] > heap[i]) { int t = heap[i]; heap[i] = heap[(i - 1) / 2]; heap[(i - 1) / 2] = t; i = (i - 1) / 2; }
+      }
+    while (hn) {
+      int v = heap[0];
+      heap[0] = heap[--hn];
+      for (int i = 0;;) {
+        int l = 2 * i + 1, r = l + 1, m = i;
+        if (l < hn && heap[l] < heap[m]) m = l;
+        if (r < hn && heap[r] < heap[m]) m = r;
+        if (m == i) break;
+        int t = heap[i]; heap[i] = heap[m]; heap[m] = t;
+        i = m;
+      }
+      tix[v] = done;
+      topo[done++] = v;
+      for (int j = g.out_ptr[v]; j < g.out_ptr[v + 1]; ++j)
+        if (--pend[g.out_dst[j]] == 0) {
+          int i = hn++;
+          heap[i] = g.out_dst[j];
+          while (i && heap[(i - 1) / 2] > heap[i]) { int t = heap[i]; heap[i] = heap[(i - 1) / 2]; heap[(i - 1) / 2] = t; i = (i - 1) / 2; }
+        }
+    }
+    free(heap);
+    free(pend);
+  }
+  /* literal post-dominator sets (graph.py:224-237), without the virtual
+     sink (it post-dominates every node): sorted topological indices */
+  int32_t** pset = calloc(n + 1, sizeof(int32_t*));
+  int32_t* plen = calloc(n + 1, sizeof(int32_t));
+  int64_t entries = 0;
+  int rc = 0;
+  int32_t* tmp = malloc(sizeof(int32_t) * (n + 1));
+  int32_t* tmp2 = malloc(sizeof(int32_t) * (n + 1));
+  for (int t = n - 1; t >= 0 && rc == 0; --t) {
+    int v = topo[t];
+    int nc = 0;
+    if (!is_output[v]) {
+      int first = 1;
+      for (int j = g.out_ptr[v]; j < g.out_ptr[v + 1]; ++j) {
+        int s = g.out_dst[j];
+        if (first) {
+          memcpy(tmp, pset[s], sizeof(int32_t) * plen[s]);
+          nc = plen[s];
+          first = 0;
+        } else {
+          int a = 0, b = 0, k = 0;
+          while (a < nc && b < plen[s]) {
+            if (tmp[a] < pset[s][b]) ++a;
+            else if (tmp[a] > pset[s][b]) ++b;
+            else { tmp2[k++] = tmp[a]; ++a; ++b; }
+          }
+          memcpy(tmp, tmp2, sizeof(int32_t) * k);
+          nc = k;
+        }
+      }
+    } /* an output's successors include the sink, whose set is {sink} */
+    pset[v] = malloc(sizeof(int32_t) * (nc + 1));
+    pset[v][0] = t;
+    memcpy(pset[v] + 1, tmp, sizeof(int32_t) * nc);
+    plen[v] = nc + 1;
+    entries += nc + 1;
+    if (max_set_entries > 0 && entries > max_set_entries) rc = 4;
+  }
+  free(tmp2);
+  int32_t* ipdom = malloc(sizeof(int32_t) * (n + 1));
+  if (rc == 0)
+    for (int v = 0; v < n; ++v) {
+      /* strict post-dominators: the set without v itself; the nearest one has
+         the smallest topological index (graph.py:239-251) */
+      int best = -1;
+      for (int i = 0; i < plen[v]; ++i)
+        if (pset[v][i] != tix[v] && (best < 0 || pset[v][i] < best)) best = pset[v][i];
+      ipdom[v] = best < 0 ? -1 : topo[best];
+      if (ipdom_out) ipdom_out[v] = ipdom[v];
+    }
+  for (int v = 0; v < n; ++v) free(pset[v]);
+  free(pset);
+  free(plen);
+  if (rc) {
+    free(tmp); free(ipdom); free(topo); free(tix); og_free(&g);
+    return rc;
+  }
+  /* children lists of the post-dominator tree */
+  int32_t* ch_ptr = calloc(n + 2, sizeof(int32_t));
+  int32_t* ch = malloc(sizeof(int32_t) * (n + 1));
+  for (int v = 0; v < n; ++v) ch_ptr[(ipdom[v] < 0 ? n : ipdom[v]) + 1]++;
+  for (int v = 0; v <= n; ++v) ch_ptr[v + 1] += ch_ptr[v];
+  {
+    int32_t* fill = calloc(n + 1, sizeof(int32_t));
+    for (int v = 0; v < n; ++v) {
+      int p = ipdom[v] < 0 ? n : ipdom[v];
+      ch[ch_ptr[p] + fill[p]++] = v;
+    }
+    free(fill);
+  }
+  ksum* opt = malloc(sizeof(ksum) * (size_t)(n + 1));
+  uint8_t* feas = calloc(n + 1, 1);
+  int32_t* choice = malloc(sizeof(int32_t) * (n + 1));
+  int32_t* mark = calloc(n + 1, sizeof(int32_t));
+  int stamp = 0;
+  int32_t* stack = malloc(sizeof(int32_t) * (n + 1));
+  int32_t* la = malloc(sizeof(int32_t) * (n + 1));
+  int32_t* lb = malloc(sizeof(int32_t) * (n + 1));
+  sol_ctx sc = {n, mem_ptr, members, ch_ptr, ch, choice, mark, stack};
+  ksum minreg;
+  int have_reg = 0;
+  int64_t ties = 0;
+  memset(&minreg, 0, sizeof(minreg));
+  g_mt_ctx = NULL;
+  mt_t mt;
+  memset(&mt, 0, sizeof(mt));
+  mt.pat = (int32_t*)pat; mt.mem_ptr = (int32_t*)mem_ptr; mt.members = (int32_t*)members;
+  g_mt_ctx = &mt;
+  ksum* vals = malloc(sizeof(ksum) * 64);
+  int vcap = 64;
+  for (int t = 0; t < n; ++t) {
+    int r = topo[t];
+    int c0 = group_ptr[r], c1 = group_ptr[r + 1];
+    if (c1 - c0 > vcap) { vcap = c1 - c0; vals = realloc(vals, sizeof(ksum) * vcap); }
+    uint8_t* ok = calloc(c1 - c0 + 1, 1);
+    int best = -1;
+    for (int m = c0; m < c1; ++m) {
+      ksum* s = &vals[m - c0];
+      ks_zero(s);
+      ks_add(s, cost[m]);
+      ks_add(s, eps);
+      ++stamp;
+      for (int i = mem_ptr[m]; i < mem_ptr[m + 1]; ++i) mark[members[i]] = stamp;
+      int good = 1;
+      /* every member other than r must hang below r inside m (true for any
+         valid match); checked, not assumed */
+      for (int i = mem_ptr[m]; i < mem_ptr[m + 1] && good; ++i) {
+        int y = members[i];
+        if (y != r && (ipdom[y] < 0 || mark[ipdom[y]] != stamp)) good = 0;
+      }
+      for (int i = mem_ptr[m]; i < mem_ptr[m + 1] && good; ++i) {
+        int y = members[i];
+        for (int j = ch_ptr[y]; j < ch_ptr[y + 1] && good; ++j) {
+          int x = ch[j];
+          if (mark[x] == stamp) continue;
+          if (!feas[x]) good = 0;
+          else ks_merge(s, &opt[x]);
+        }
+      }
+      ok[m - c0] = (uint8_t)good;
+      if (!good) continue;
+      if (best < 0) { best = m; continue; }
+      int c = ks_cmp(s, &vals[best - c0]);
+      if (c < 0) best = m;
+      else if (c == 0) {
+        ++ties;
+        int na = collect(&sc, m, la, 0, &stamp);
+        /* collect() for `best` needs choice[] of the children only */
+        int nb = collect(&sc, best, lb, 0, &stamp);
+        qsort(la, na, sizeof(int32_t), elem_cmp_qs);
+        qsort(lb, nb, sizeof(int32_t), elem_cmp_qs);
+        if (key_cmp(&mt, la, na, lb, nb) < 0) best = m;
+      }
+    }
+    if (best >= 0) {
+      feas[r] = 1;
+      choice[r] = best;
+      opt[r] = vals[best - c0];
+      for (int m = c0; m < c1; ++m) {
+        if (!ok[m - c0] || m == best) continue;
+        int c = ks_cmp(&vals[m - c0], &opt[r]);
+        if (c <= 0) continue;
+        ksum d;
+        ks_sub(&d, &vals[m - c0], &opt[r]);
+        if (!have_reg || ks_cmp(&d, &minreg) < 0) { minreg = d; have_reg = 1; }
+      }
+    } else {
+      feas[r] = 0;
+      choice[r] = -1;
+    }
+    free(ok);
+  }
+  /* the answer: the tree roots' subtree solutions */
+  ksum total;
+  ks_zero(&total);
+  int feasible = 1, nk = 0;
+  for (int j = ch_ptr[n]; j < ch_ptr[n + 1]; ++j) {
+    int x = ch[j];
+    if (!feas[x]) { feasible = 0; break; }
+    ks_merge(&total, &opt[x]);
+    /* kernels of x's solution */
+    int start = nk;
+    nk = collect(&sc, choice[x], kernels_out, nk, &stamp);
+    (void)start;
+  }
+  if (!feasible) rc = 1;
+  else {
+    *n_kernels = nk;
+    *cost_out = ks_round(&total);
+    *min_regret_out = have_reg ? ks_round(&minreg) : INFINITY;
+    if (have_reg && ks_round(&minreg) == 0.0) *min_regret_out = 5e-324; /* below any double */
+  }
+  if (ties_out) *ties_out = ties;
+  free(vals); free(la); free(lb); free(stack); free(mark); free(choice); free(feas); free(opt);
+  free(ch); free(ch_ptr); free(tmp); free(ipdom); free(topo); free(tix);
+  og_free(&g);
+  return rc;
+}

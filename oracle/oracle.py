@@ -52,12 +52,28 @@ def lib():
         _lib.or_dp.argtypes = [c_int, P32, P32, P32, POINTER(c_uint8), c_int, P32, P32, P32, P32,
                                POINTER(c_double), c_double, c_int, P32, P32, POINTER(c_double),
                                POINTER(c_int64), P32, P32]
+        _lib.or_dp_subtree.restype = c_int
+        _lib.or_dp_subtree.argtypes = [c_int, P32, P32, P32, POINTER(c_uint8), c_int, P32, P32, P32,
+                                       P32, POINTER(c_double), c_double, c_int64, P32, P32,
+                                       POINTER(c_double), POINTER(c_double), P32, POINTER(c_int64)]
         _lib.or_fitness.restype = c_int
         _lib.or_fitness.argtypes = [c_int, P32, P32, P32, P32, P32, P32, POINTER(c_double), c_int,
                                     P32, c_int, POINTER(c_uint8), POINTER(c_double),
                                     POINTER(c_double), c_int, c_double, POINTER(c_uint64),
                                     c_int64, c_int, c_int, POINTER(c_double)]
     return _lib
+
+
+def window_safe(cost: float, min_regret: float | None) -> bool:
+    """True when no rounded comparison of the reference can disagree with the
+    exact one: any two states of one cover differ by a sum of decision
+    regrets, so a difference of at least 4 ulp(cost) (states cost at most
+    twice the total before they differ by more than the total) keeps their
+    rounded costs apart."""
+    import math
+    if min_regret is None or math.isinf(min_regret):
+        return True
+    return min_regret >= 4 * math.ulp(cost)
 
 
 def _p(a, t):
@@ -234,6 +250,34 @@ class OracleCase:
             return "limit", None, None
         ks = kern[:nk.value]
         return "ok", cost.value, self.kernels_json(ks)
+
+    def dp_subtree(self, max_set_entries: int = 2_000_000_000):
+        """The independent exact solver (or_dp_subtree): (status, cost,
+        kernels, min_regret) with status 'ok' | 'uncoverable' | 'memory'.
+        `window_safe(cost, min_regret)` tells whether the reference's rounded
+        comparisons provably pick the same partition."""
+        mt = self._mt or self.match_all()
+        if not hasattr(self, "cost"):
+            self.price()
+        kern = np.empty(self.n + 1, np.int32)
+        ipdom = np.empty(self.n + 1, np.int32)
+        nk = c_int32(); cost = c_double(); reg = c_double(); ties = c_int64()
+        rc = lib().or_dp_subtree(self.n, _p(self.kind, c_int32), _p(self.in_ptr, c_int32),
+                                 _p(self.in_src, c_int32), _p(self.is_output, c_uint8), mt["n"],
+                                 _p(mt["group_ptr"], c_int32), _p(mt["pat"], c_int32),
+                                 _p(mt["mem_ptr"], c_int32), _p(mt["members"], c_int32),
+                                 _p(self.cost, c_double), float(self.epsilon),
+                                 int(max_set_entries), _p(kern, c_int32), ctypes.byref(nk),
+                                 ctypes.byref(cost), ctypes.byref(reg), _p(ipdom, c_int32),
+                                 ctypes.byref(ties))
+        self.subtree_ties = ties.value
+        if rc == 1:
+            return "uncoverable", None, None, None
+        if rc == 4:
+            return "memory", None, None, None
+        assert rc == 0, rc
+        self.ipdom = ipdom[:self.n].copy()
+        return "ok", cost.value, self.kernels_json(kern[:nk.value]), reg.value
 
     def kernels_json(self, matches) -> list:
         mt = self._mt

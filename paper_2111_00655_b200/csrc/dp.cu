@@ -26,6 +26,8 @@
 #include <climits>
 #include <cstring>
 
+#include <cmath>
+
 #include "cb_internal.cuh"
 
 #define DP_NARROW_WARPS 16
@@ -384,13 +386,22 @@ __global__ void dp_total_kernel(int32_t n, const int32_t* __restrict__ ipdom, co
   }
 }
 
-// Half-width of the interval of reals that round to `d` (ties to even):
-// true when every x in (T, T + delta] with delta = `gap` rounds to d.
+// True when the reference's rounded comparisons cannot choose differently
+// from the exact ones.  The reference keeps one state per covered set and
+// compares states by their rounded costs (dp.py:128-147, cost.py:300-305).
+// Any two states of one cover differ by a sum of decision regrets (the
+// cover is a union of post-dominator subtrees, solved independently), so
+// a state that is exactly worse is worse by at least the minimum positive
+// regret `gap`.  States that matter cost at most the total T (costs are
+// non-negative); an exactly-worse one can share T's rounded value only if
+// it is within about one ulp of the binade above T.  gap >= 4 ulp(T) rules
+// that out (the same test as oracle/oracle.py window_safe).
 static bool rounding_window_safe(const fx192& total, const fx192& gap) {
-  // Cover with cost T* + g for g >= gap: unsafe if T* + gap rounds like T*.
-  fx192 t2 = total;
-  fx_add(t2, gap);
-  return fx_to_double(t2) != fx_to_double(total);
+  const double t = fx_to_double(total);
+  const double ulp = std::nextafter(t, INFINITY) - t;
+  fx192 lim;
+  if (!fx_from_double(4.0 * ulp, lim)) return false;
+  return fx_cmp(gap, lim) >= 0;
 }
 
 extern "C" int cb_dp_solve(cb_graph* g, cb_matches* m, double epsilon, int32_t* kernel_match,

@@ -25,7 +25,7 @@ import numpy as np
 
 from . import _native as nat
 from .cost import Measurer, price_matches
-from .errors import SearchLimitError, UncoverableGraphError
+from .errors import RoundingWindowError, SearchLimitError, UncoverableGraphError
 from .graph import ComputationGraph
 from .placement import Assignment, PlacementStrategy, validate_placement
 from .registry import PatternRegistry
@@ -87,12 +87,19 @@ def _new_frontiers(g: ComputationGraph) -> int:
 
 def optimize(g: ComputationGraph, registry: PatternRegistry, measurer: Measurer,
              epsilon: float, max_states: int | None = DEFAULT_MAX_STATES,
-             validate: bool | None = None) -> DPResult:
+             validate: bool | None = None, rounding: str = "raise") -> DPResult:
     """Cheapest full placement of `g` (exact, reference tie-breaking).
 
     Raises UncoverableGraphError when no full cover exists and
     SearchLimitError when `max_states` is given and the n + 1 subtree states
-    exceed it."""
+    exceed it.  The device compares exact sums; the reference compares
+    rounded ones.  When the solver cannot certify that both choose the same
+    partition (an alternative within 4 ulp of the total, see csrc/dp.cu
+    rounding_window_safe), `rounding="raise"` (default) raises
+    RoundingWindowError carrying the exact result, `rounding="exact"`
+    returns the exact optimum (`device["rounding_window_safe"]` False)."""
+    if rounding not in ("raise", "exact"):
+        raise ValueError("rounding must be 'raise' or 'exact'")
     stats = DPStats(nodes=len(g.nodes))
     c0, h0, p0 = measurer.calls, measurer.cache_hits, measurer.computations
     if not g.nodes:
@@ -149,5 +156,12 @@ def optimize(g: ComputationGraph, registry: PatternRegistry, measurer: Measurer,
     if validate or (validate is None and len(g.nodes) <= VALIDATE_MAX_NODES):
         validate_placement(g, placement)
     canon = np.asarray([chosen[i] for i in order], dtype=np.int32)
-    return DPResult(placement, res.cost_ms, stats,
-                    {frozenset(g.nodes): res.cost_ms, frozenset(): 0.0}, device, canon)
+    out = DPResult(placement, res.cost_ms, stats,
+                   {frozenset(g.nodes): res.cost_ms, frozenset(): 0.0}, device, canon)
+    if not device["rounding_window_safe"] and rounding == "raise":
+        raise RoundingWindowError(
+            f"an alternative placement differs from the exact optimum ({res.cost_ms!r} ms) by "
+            f"less than the rounding resolution of the total; the reference's rounded "
+            f"comparisons may pick either (pass rounding='exact' to accept the exact optimum)",
+            out)
+    return out

@@ -4,7 +4,7 @@ import numpy as np
 import pytest
 
 from conftest import golden
-from oracle import OracleCase
+from oracle import OracleCase, window_safe
 
 SUITES = ["fixtures", "dp_random", "dp_ties", "dp_large", "es_random", "models"]
 
@@ -32,6 +32,12 @@ def test_oracle_reproduces_reference(case):
     assert cost == exp["cost"]
     assert kernels == exp["kernels"]
     assert oc.dp_relaxations == exp["relaxations"]
+    # the independent solver (post-dominator subtrees) pins the configs the
+    # reference cannot solve (tests/test_dp_pins.py); here it must return the
+    # reference's own result on every case the reference solved
+    s2, cost2, kernels2, regret = oc.dp_subtree()
+    assert (s2, cost2, kernels2) == ("ok", exp["cost"], exp["kernels"])
+    assert window_safe(cost2, regret)
     if "es" in case:
         es = case["es"]
         fit = oc.fitness(exp["kernels"], es["graph_backend"], es["genomes"])
