@@ -1,31 +1,41 @@
 """Benchmark of the placement-search hot path (BASELINE.json metric:
-placement-search wall time and fitness evals/sec).
+placement-search wall time and fitness evals/sec at 1/2/4/8 B200).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl mine|reference]
     python -m torch.distributed.run --nproc-per-node N ... bench.py --gpus N
 
-Workload (N=1, BASELINE.json configs[1]): BERT-base (seq 128) inference
-graph, paper backend set (cuDNN / cuBLAS / TVM with rule-generated patterns
-/ TensorRT as the graph inference library), op-level DP then evolutionary
-search.  A step is one ES generation of the rank's population shard on the
-GPU: tournament selection + two-point crossover + mutation (cb_es_breed)
-and batched graph-level fitness of every genome (cb_fitness_device), plus
-for N>1 the NCCL all-gather of the per-rank elites.  `value` is genomes
-evaluated per second over all ranks (weak scaling: the shard per GPU is
-fixed).  The shard is sized so the population exceeds L2 (inputs larger
-than L2; no flush).  `e2e` prices a host-resident population through the
-public API (FitnessPlan.evaluate_packed -> cb_fitness_host: pinned H2D,
-fitness, D2H).  `search` reports the wall time of one full placement search
-(match + price + DP + plan + ES generations).
+Headline workload (BASELINE.json configs[4], the config the metric is
+quoted on at 1/2/4/8 GPUs): a synthetic random DAG of 100 000 ops, 8
+simulated backends (one graph inference library), the op-level DP placement
+(99 446 kernels, so 99 446-bit genomes) and an evolutionary search with a
+population of 1 048 576 genomes per GPU.  A step is one ES generation of
+the rank's shard on the GPU: tournament selection + two-point crossover +
+mutation (cb_es_breed) and the graph-level fitness of every child
+(cb_fitness_device), plus for N>1 the NCCL all-gather of the rank elites.
+`value` = genomes priced per second over all ranks (weak scaling: the shard
+per GPU is fixed); the population (13 GB per GPU) is far larger than L2, so
+no flush is needed.  `e2e` prices host-resident genomes through the public
+API (FitnessPlan.evaluate_packed -> cb_fitness_host: pinned H2D, fitness,
+D2H) -- the same genome distribution the reference arm prices (uniform
+random bits, as `evolve` seeds its population).  `search` reports the wall
+time of one complete placement search (match, price, DP, plan, ES
+generations) with its phases.  `configs` (N=1) sweeps all five BASELINE
+configs.
 
---impl reference times the reference algorithm (the CPU oracle restating
-tensorplace, oracle/oracle.c) on the host cores for the same workload.
+--impl reference runs the reference algorithm on the host cores: the
+reference's ES generation (tournament 4, two-point crossover, mutation
+1/k, elitism 1; evolution.py:195-250) on a bounded population, every child
+priced by oracle/oracle.c (the reference's graph-level pricing restated in
+C, OpenMP over all host threads).  Its input is the committed case file
+tests/golden/cases/<workload>.json.gz, so that arm never loads the product
+library.
 """
 
 from __future__ import annotations
 
 import argparse
 import gc
+import gzip
 import json
 import os
 import statistics
@@ -41,14 +51,31 @@ sys.path.insert(0, ROOT)
 os.environ.setdefault("OMP_WAIT_POLICY", "PASSIVE")
 
 L2_BYTES = 126 * 1024 * 1024
+CASES = os.path.join(ROOT, "tests", "golden", "cases")
+
+# per workload: GPU population per rank, e2e population, CPU-baseline sample
+# (fitness only) and reference-arm ES population (all bounded so the whole
+# default run stays within a few minutes)
+WORKLOADS = {
+    "random100k": dict(population=1 << 20, e2e=1 << 18, cpu=3000, ref=256,
+                       data="synthetic random DAG, 100 000 ops, 8 simulated backends"),
+    "bert_base": dict(population=None, e2e=1 << 24, cpu=2_000_000, ref=400_000,
+                      data="synthetic BERT-base (seq 128) graph, paper backend set"),
+    "resnet50": dict(population=None, e2e=1 << 24, cpu=2_000_000, ref=400_000,
+                     data="synthetic ResNet-50 graph, paper backend set"),
+    "nasnet_a": dict(population=None, e2e=1 << 22, cpu=200_000, ref=50_000,
+                     data="synthetic NasNet-A graph, paper backend set"),
+    "nasrnn": dict(population=None, e2e=1 << 23, cpu=500_000, ref=100_000,
+                   data="synthetic NasRNN (10 steps) graph, paper backend set"),
+}
 
 
 def _peaks() -> tuple[float, str]:
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
-            return float(json.load(fh)["hbm_gbs"]), "measured"
+            return float(json.load(fh)["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
     except Exception:
-        return 6650.0, "fallback"
+        return 6650.0, "fallback (B200_PROFILING.md)"
 
 
 class ClockSampler:
@@ -97,13 +124,34 @@ class ClockSampler:
                 "samples": len(self.samples)}
 
 
+# ---------------------------------------------------------------- shared inputs
+
+def uniform_rows(n: int, k: int, seed: int):
+    """n genomes of k uniformly random bits as packed uint64 rows (padding
+    bits clear) -- the distribution `evolve` seeds its population with
+    (tensorplace/evolution.py:201-203).  The first m rows of a draw equal an
+    m-row draw, so both arms can price prefixes of one stream."""
+    import numpy as np
+    words = max(1, (k + 63) // 64)
+    rows = np.random.default_rng(seed).integers(0, 1 << 64, size=(n, words), dtype=np.uint64,
+                                                endpoint=False) if k else \
+        np.zeros((n, words), np.uint64)
+    if k % 64:
+        rows[:, -1] &= np.uint64((1 << (k % 64)) - 1)
+    return rows
+
+
+def load_case(name: str) -> dict:
+    with gzip.open(os.path.join(CASES, f"{name}.json.gz"), "rt") as fh:
+        return json.load(fh)
+
+
 def build_workload(name: str):
     import paper_2111_00655_b200 as tp
     from paper_2111_00655_b200 import workloads
     g = workloads.CONFIGS[name]()
-    from paper_2111_00655_b200 import _native
-    bs = workloads.paper_backends(g, verify=_native.device_available()) if name != "random100k" else \
-        workloads.random_backends(g, n_backends=8, n_graph=1, seed=0)
+    bs = workloads.random_backends(g, n_backends=8, n_graph=1, seed=0) if name == "random100k" \
+        else workloads.paper_backends(g, verify=False)
     return tp, g, bs
 
 
@@ -115,6 +163,22 @@ def shard_size(words: int, requested: int | None) -> int:
         p <<= 1
     return p
 
+
+def _oracle(case: dict):
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    from oracle import OracleCase  # checker / baseline only
+    oc = OracleCase(case)
+    oc.price()
+    return oc
+
+
+def _genome_bits(oc, case, kernels) -> int:
+    graph = {b for b, kind in case["backends"] if kind == "graph_inference_library"}
+    backend_of = [b for b, _, _ in case["patterns"]]
+    return sum(1 for order, _, _ in kernels if backend_of[order] not in graph)
+
+
+# --------------------------------------------------------------------- my arm
 
 def run_mine(args) -> None:
     import numpy as np
@@ -146,30 +210,34 @@ def run_mine(args) -> None:
 
     from paper_2111_00655_b200.es_device import DeviceEvolution
 
+    wl = WORKLOADS[args.workload]
     tp, g, bs = build_workload(args.workload)
 
-    def search(P: int, gens: int, timed: bool):
+    def search(P: int, gens: int):
         t = {}
         t0 = time.perf_counter()
         res = tp.optimize(g, bs.registry, bs.measurer, 0.01)
-        t["dp_s"] = time.perf_counter() - t0
+        t1 = time.perf_counter()
         plan = tp.FitnessPlan(g, bs.registry, bs.measurer, res.placement, 0.01, bs.graph_backend,
                               res.kernel_matches)
+        t2 = time.perf_counter()
         es = DeviceEvolution(plan, P, seed=args.seed, device=dev, process_group=group)
         es.initialize()
         for _ in range(gens):
             es.step()
         torch.cuda.synchronize(dev)
-        t["total_s"] = time.perf_counter() - t0
-        t["es_s"] = t["total_s"] - t["dp_s"]
-        return res, plan, es, t
+        t3 = time.perf_counter()
+        t.update(wall_s=t3 - t0, optimize_s=t1 - t0, plan_s=t2 - t1, es_s=t3 - t2,
+                 optimize_phases_s=res.device["phases_s"], dp_device_ms=res.device["device_ms"])
+        return res, plan, t
 
     # warm search (module load, first launches), then the timed one on fresh objects
     bs.registry._tables.clear()
-    search(4096, 2, False)
+    search(4096, 2)
     bs.registry._tables.clear()
-    res, plan, es0, search_t = search(args.search_population, args.search_generations, True)
-    P = shard_size(plan.words, args.population)
+    gc.collect()
+    res, plan, search_t = search(args.search_population, args.search_generations)
+    P = shard_size(plan.words, args.population or wl["population"])
     es = DeviceEvolution(plan, P, seed=args.seed, device=dev, process_group=group)
     es.initialize()
     for _ in range(args.warmup):
@@ -190,23 +258,26 @@ def run_mine(args) -> None:
     mean = lambda xs: sum(xs) / len(xs) if xs else 0.0
     gen_ms, fit_ms, breed_ms = mean(kt["generation"]), mean(kt["fitness"]), mean(kt["breed"])
     best_cost, _ = es.best()
+    del es
+    torch.cuda.empty_cache()
 
-    # e2e through the public API with host buffers (pinned)
-    rng = np.random.default_rng(rank)
-    # the population the timed ES steps produced, now host-resident (pinned)
-    host = torch.empty((P, plan.words), dtype=torch.int64, pin_memory=True)
-    host.copy_(es.pop[es.cur])
+    # e2e through the public API with host buffers (pinned): uniform random
+    # genomes, the distribution the reference arm prices
+    E = args.e2e_population or wl["e2e"]
+    host = torch.empty((E, plan.words), dtype=torch.int64, pin_memory=True)
     host_np = host.numpy().view(np.uint64)
-    host_fit = torch.empty(P, dtype=torch.float64, pin_memory=True).numpy()
+    host_np[:] = uniform_rows(E, plan.k, 1000 + rank)
+    host_fit = torch.empty(E, dtype=torch.float64, pin_memory=True).numpy()
     plan.evaluate_packed(host_np, host_fit)  # warm
     barrier()
     t0 = time.perf_counter()
     for _ in range(args.e2e_steps):
-        fit = plan.evaluate_packed(host_np, host_fit)
+        plan.evaluate_packed(host_np, host_fit)
     e2e_s = time.perf_counter() - t0
     barrier()
+    del host
 
-    vals = torch.tensor([ms, e2e_s, gen_ms, fit_ms, breed_ms, search_t["total_s"]],
+    vals = torch.tensor([ms, e2e_s, gen_ms, fit_ms, breed_ms, search_t["wall_s"]],
                         dtype=torch.float64, device=dev)
     if world > 1:
         import torch.distributed as dist
@@ -219,37 +290,30 @@ def run_mine(args) -> None:
         return
     step_ms = ms / args.steps
     evals_per_s = world * P * args.steps / (ms / 1e3)
-    if es.fused:
-        # fused breed + fitness: child row out, fitness out, two parent rows and
-        # 2 x tournament 4-byte order keys gathered, per genome
-        per_genome = 8 * plan.words + 8 + 2 * 8 * plan.words + 2 * es.tournament * 4
-        dom_ms = gen_ms
-    else:
-        per_genome = plan.words * 8 + 8  # genome row in, fitness out
-        dom_ms = fit_ms
+    per_genome = plan.words * 8 + 8  # genome row in, fitness out
     bytes_per_launch = P * per_genome
     peak, peak_src = _peaks()
-    achieved = bytes_per_launch / (dom_ms / 1e3) / 1e9
-    kernel_name = plan.generation_kernel_name() if es.fused else plan.kernel_name()
+    achieved = bytes_per_launch / (fit_ms / 1e3) / 1e9
+    kernel_name = plan.kernel_name()
     traffic = None
-    inst_per_genome = None
+    issue = None
     prof = os.path.join(ROOT, "profiles", "fitness_ncu_summary.json")
     if os.path.exists(prof):
         try:
             with open(prof) as fh:
-                d = json.load(fh)
-            if d.get("workload") == args.workload and \
-                    kernel_name.replace(" ", "") in d.get("kernel", "").replace(" ", ""):
-                traffic = d.get("dram_bytes_per_launch_per_genome", 0) * P or None
-                inst_per_genome = d.get("warp_instructions_per_genome")
-        except (OSError, ValueError, KeyError):
+                summaries = json.load(fh)
+            d = summaries.get(args.workload, {}) if isinstance(summaries, dict) else {}
+            if d and kernel_name.replace(" ", "") in d.get("kernel", "").replace(" ", ""):
+                traffic = d.get("dram_bytes_per_genome", 0) * P or None
+                issue = d
+        except (OSError, ValueError, KeyError, AttributeError):
             traffic = None
     sweep = None
     if world == 1 and not args.no_configs:
-        sweep = config_sweep(dev)
+        sweep = config_sweep(dev, args)
     cpu = None  # last: its OpenMP pool must not compete with the sweep's host-side timings
     if world == 1 and not args.no_cpu_baseline:
-        cpu = cpu_baseline(g, bs, res, plan, args)
+        cpu = cpu_baseline(args, args.cpu_sample or wl["cpu"])
     line = {
         "metric": "fitness_evals_per_sec",
         "value": evals_per_s,
@@ -262,44 +326,45 @@ def run_mine(args) -> None:
         "scaling": "weak",
         "vs_baseline": None,
         "dtype": "int128",
-        "arithmetic": "u64 bit-genomes; exact 128-bit fixed-point cost sums (plan window), f64 region pricing",
-        "data": "synthetic (BERT-base graph built op by op; simulated backend cost tables)",
+        "arithmetic": "u64 bit-genomes; exact 128-bit fixed-point cost sums (plan window), "
+                      "f64 region pricing; identical to the reference's fsum results",
+        "data": f"synthetic ({wl['data']}; random-init ES population; simulated cost tables)",
         "config": {"workload": f"{args.workload}: op-level DP + evolutionary search",
                    "nodes": len(g.nodes), "dp_kernels": len(res.placement),
                    "genome_bits": plan.k, "genome_words": plan.words,
                    "population_per_gpu": P, "global_population": P * world,
                    "parallelism": f"population sharded over {world} GPU(s), "
                                   f"{'NCCL' if backend == 'nccl' else backend} all-gather of elites",
-                   "l2": "population > L2 (no flush)"},
-        "search": {"wall_s": search_s, "dp_s": search_t["dp_s"], "es_s": search_t["es_s"],
+                   "l2": f"population {P * plan.words * 8 / 1e9:.1f} GB per GPU > L2 (no flush)"},
+        "search": {"wall_s": search_s, **{k: v for k, v in search_t.items() if k != "wall_s"},
                    "es_population_per_gpu": args.search_population,
                    "es_generations": args.search_generations, "dp_cost_ms": res.cost_ms,
+                   "rounding_window_safe": res.device["rounding_window_safe"],
                    "best_cost_ms_after_timed_steps": best_cost},
-        "kernels_ms": ({"generation_fused": gen_ms} if es.fused else
-                       {"generation": gen_ms, "fitness": fit_ms, "breed": breed_ms}),
+        "kernels_ms": {"generation": gen_ms, "fitness": fit_ms, "breed": breed_ms},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic, "kernel": kernel_name,
                      "peak_source": peak_src,
                      "algorithmic_bytes_per_launch": bytes_per_launch,
                      "algorithmic_bytes_per_genome": per_genome},
-        "e2e": {"value": world * P * args.e2e_steps / e2e_s, "unit": "genomes/s",
-                "h2d_bytes_per_step": P * plan.words * 8, "d2h_bytes_per_step": P * 8},
-        "gpu_launches": args.steps * es.launches_per_generation,
+        "e2e": {"value": world * E * args.e2e_steps / e2e_s, "unit": "genomes/s",
+                "h2d_bytes_per_step": E * plan.words * 8, "d2h_bytes_per_step": E * 8,
+                "population": E, "genomes": "uniform random bits (as the reference arm)"},
+        "gpu_launches": args.steps * es_launches(plan),
         "clocks": clocks.summary(),
     }
     if cpu is not None:
         line["cpu_baseline"] = cpu
-    if inst_per_genome:
+    if issue and issue.get("warp_instructions_per_genome"):
         # the bound that binds: warp-instruction issue (4 schedulers per SM, one
         # instruction per cycle each), instructions per genome from the ncu capture
-        # of the same kernel (profiles/fitness_ncu_summary.json)
         sms = torch.cuda.get_device_properties(dev).multi_processor_count
         mhz = line["clocks"].get("sm_mhz") or 1965.0
         peak_issue = sms * 4 * mhz * 1e6
-        achieved_issue = inst_per_genome * P / (dom_ms / 1e3)
+        achieved_issue = issue["warp_instructions_per_genome"] * P / (fit_ms / 1e3)
         line["issue_roofline"] = {"bound": "issue", "achieved": achieved_issue, "peak": peak_issue,
                                   "unit": "warp instructions/s", "frac": achieved_issue / peak_issue,
-                                  "warp_instructions_per_genome": inst_per_genome,
+                                  "warp_instructions_per_genome": issue["warp_instructions_per_genome"],
                                   "source": "profiles/fitness_ncu_summary.json"}
     if sweep is not None:
         line["configs"] = sweep
@@ -309,68 +374,54 @@ def run_mine(args) -> None:
         dist.destroy_process_group()
 
 
-def _oracle_case(g, bs):
-    from paper_2111_00655_b200.cost import profile_to_json
-    from paper_2111_00655_b200.graph import graph_to_json
-    sys.path.insert(0, os.path.join(ROOT, "oracle"))
-    from oracle import OracleCase  # checker / baseline only
-    case = {"graph": graph_to_json(g),
-            "backends": [[b.id, b.kind.value] for b in bs.registry.backends.values()],
-            "patterns": [[bp.backend, bp.text(), bp.source.value] for bp in bs.registry.patterns],
-            "profiles": {b: profile_to_json(p) for b, p in bs.measurer.profiles.items()},
-            "epsilon": 0.01}
-    return OracleCase(json.loads(json.dumps(case)))
+def es_launches(plan) -> int:
+    from paper_2111_00655_b200.es_device import DeviceEvolution
+    return DeviceEvolution.launches_for(plan)
 
 
-def _random_packed(n: int, k: int, seed: int):
-    """n random genomes of k bits as packed uint64 rows (padding bits clear)."""
-    import numpy as np
-    words = max(1, (k + 63) // 64)
-    rows = np.random.default_rng(seed).integers(0, 1 << 63, size=(n, words), dtype=np.uint64)
-    rows ^= np.random.default_rng(seed + 1).integers(0, 2, size=(n, words), dtype=np.uint64) << np.uint64(63)
-    if k % 64:
-        rows[:, -1] &= np.uint64((1 << (k % 64)) - 1)
-    return rows
-
-
-def cpu_baseline(g, bs, res, plan, args) -> dict:
-    """The reference algorithm restated in C (oracle) on the host cores,
-    bounded sample: fitness of `sample` random genomes."""
-    import numpy as np
-    oc = _oracle_case(g, bs)
-    oc.price()
-    kernels = [[a.backend_pattern.order, a.root, sorted(a.nodes)] for a in res.placement.assignments]
+def cpu_baseline(args, sample: int) -> dict:
+    """The reference's graph-level pricing restated in C (oracle), all host
+    threads, on a bounded sample of the e2e genome stream."""
+    case = load_case(args.workload)
+    oc = _oracle(case)
+    status, _, kernels, _ = oc.dp_subtree()
+    assert status == "ok"
+    k = _genome_bits(oc, case, kernels)
     threads = os.cpu_count() or 1
-    sample = args.cpu_sample
-    pop = _random_packed(sample, plan.k, 1)
-    oc.fitness(kernels, bs.graph_backend, pop[:64], threads=threads)
+    pop = uniform_rows(sample, k, 1000)
+    oc.fitness(kernels, case["graph_backend"], pop[:32], threads=threads)
     t0 = time.perf_counter()
-    oc.fitness(kernels, bs.graph_backend, pop, threads=threads)
+    oc.fitness(kernels, case["graph_backend"], pop, threads=threads)
     dt = time.perf_counter() - t0
     return {"value": sample / dt, "unit": "genomes/s", "cores": threads, "kind": "port",
-            "sample": f"{sample} random packed genomes of the {args.workload} DP placement "
-                      f"({plan.k} bits), oracle/oracle.c or_fitness with {threads} OpenMP threads"}
+            "sample": f"{sample} uniform random genomes of the {args.workload} DP placement "
+                      f"({k} bits, the e2e stream's first rows), oracle/oracle.c or_fitness "
+                      f"with {threads} OpenMP threads"}
 
 
 # per-config sweep (BASELINE.json's five configs), one GPU: population for
 # the search wall time, generations, population for the fitness rate, CPU
-# sample for the oracle rate, and whether the oracle's covered-set DP (the
-# reference's algorithm) is run for a parity check
+# sample for the oracle rate
 SWEEP = {
-    "resnet50": dict(search_pop=65536, gens=50, fit_pop=1 << 22, cpu=200_000, ref_dp=True),
-    "bert_base": dict(search_pop=65536, gens=50, fit_pop=1 << 22, cpu=100_000, ref_dp=True),
-    "nasnet_a": dict(search_pop=65536, gens=50, fit_pop=1 << 20, cpu=20_000, ref_dp=True),
-    "nasrnn": dict(search_pop=65536, gens=50, fit_pop=65536, cpu=50_000, ref_dp=True),
-    "random100k": dict(search_pop=65536, gens=10, fit_pop=1 << 20, cpu=200, ref_dp=False),
+    "resnet50": dict(search_pop=65536, gens=50, fit_pop=1 << 22, cpu=200_000),
+    "bert_base": dict(search_pop=65536, gens=50, fit_pop=1 << 22, cpu=100_000),
+    "nasnet_a": dict(search_pop=65536, gens=50, fit_pop=1 << 20, cpu=20_000),
+    "nasrnn": dict(search_pop=65536, gens=50, fit_pop=1 << 22, cpu=50_000),
+    "random100k": dict(search_pop=65536, gens=10, fit_pop=1 << 18, cpu=300),
 }
 
 
-def config_sweep(dev) -> dict:
-    """Search wall time, DP time, fitness rate and CPU-oracle rate for each
-    BASELINE.json config (supplementary to the headline line)."""
+def config_sweep(dev, args) -> dict:
+    """Search wall time (with phases), DP time, fitness rate and CPU-oracle
+    rate for each BASELINE.json config, and the DP placement checked against
+    its pin (tests/golden/dp_pins.json, oracle-derived)."""
+    import hashlib
+
     import numpy as np
     import torch
     from paper_2111_00655_b200.es_device import DeviceEvolution
+    with open(os.path.join(ROOT, "tests", "golden", "dp_pins.json")) as fh:
+        pins = json.load(fh)
     out = {}
     for name, cfg in SWEEP.items():
         tp, g, bs = build_workload(name)
@@ -384,50 +435,32 @@ def config_sweep(dev) -> dict:
             t1 = time.perf_counter()
             plan = tp.FitnessPlan(g, bs.registry, bs.measurer, res.placement, 0.01, bs.graph_backend,
                                   res.kernel_matches)
+            t2 = time.perf_counter()
             es = DeviceEvolution(plan, cfg["search_pop"], seed=0, device=dev)
             es.initialize()
             for _ in range(cfg["gens"] if rep else 2):
                 es.step()
             torch.cuda.synchronize(dev)
-            t2 = time.perf_counter()
+            t3 = time.perf_counter()
         best, _ = es.best()
-        # the matcher and pricing on their own (table cache cleared), host wall with syncs
-        from paper_2111_00655_b200.cost import price_matches
-        tm, tpr = [], []
-        for _ in range(3):  # best of 3 (the first pays buffer allocation)
-            bs.registry._tables.clear()
-            torch.cuda.synchronize(dev)
-            m0 = time.perf_counter()
-            table = bs.registry.match_table(g)
-            torch.cuda.synchronize(dev)
-            m1 = time.perf_counter()
-            price_matches(bs.measurer, bs.registry, table)
-            torch.cuda.synchronize(dev)
-            m2 = time.perf_counter()
-            tm.append(m1 - m0)
-            tpr.append(m2 - m1)
-        row.update(matcher={"anchors": len(g.nodes), "patterns": len(bs.registry.patterns),
-                            "matches": int(table.n_matches), "wall_ms": 1e3 * min(tm),
-                            "anchors_per_s": len(g.nodes) / min(tm),
-                            "note": "host wall incl. download of the match table"},
-                   pricing={"matches": int(table.n_matches), "wall_ms": 1e3 * min(tpr)},
-                   dp={"nodes": len(g.nodes), "device_ms": res.device["device_ms"],
-                       "levels": res.device["levels"], "launches": res.device["launches"],
-                       "nodes_per_s": len(g.nodes) / (res.device["device_ms"] / 1e3)})
-        row.update(search_wall_s=t2 - t0, dp_s=t1 - t0, dp_device_ms=res.device["device_ms"],
+        kernels = [[a.backend_pattern.order, a.root, sorted(a.nodes)] for a in res.placement.assignments]
+        digest = hashlib.sha256(json.dumps(kernels, separators=(",", ":")).encode()).hexdigest()
+        pin = pins[name]
+        row.update(search_wall_s=t3 - t0, optimize_s=t1 - t0, plan_s=t2 - t1, es_s=t3 - t2,
+                   optimize_phases_s=res.device["phases_s"], dp_device_ms=res.device["device_ms"],
+                   dp_levels=res.device["levels"], dp_launches=res.device["launches"],
                    es_population=cfg["search_pop"], es_generations=cfg["gens"],
                    dp_kernels=len(res.placement), dp_cost_ms=res.cost_ms, es_best_cost_ms=best,
                    rounding_window_safe=res.device["rounding_window_safe"],
+                   dp_matches_pin=res.cost_ms == pin["cost"] and digest == pin["kernels_sha256"],
                    genome_bits=plan.k, frontier_slots=plan.info.frontier_slots,
-                   window_shift=plan.info.window_shift,
                    fitness_kernel=plan.kernel_name())
         P = cfg["fit_pop"]
-        es = DeviceEvolution(plan, P, seed=1, device=dev, fused=False)  # the fitness kernel alone
+        es = DeviceEvolution(plan, P, seed=1, device=dev)  # the fitness kernel alone
         es.initialize()
         es.step()
         es.enable_kernel_timing(True)
-        gens = 3
-        for _ in range(gens):
+        for _ in range(3):
             es.step()
         torch.cuda.synchronize(dev)
         kt = es.kernel_times_ms()
@@ -437,67 +470,90 @@ def config_sweep(dev) -> dict:
         del es
         torch.cuda.empty_cache()
         # CPU oracle (reference algorithm in C), bounded sample, all host threads
-        oc = _oracle_case(g, bs)
-        oc.price()
-        kernels = [[a.backend_pattern.order, a.root, sorted(a.nodes)] for a in res.placement.assignments]
+        case = load_case(name)
+        oc = _oracle(case)
         threads = os.cpu_count() or 1
-        pop = np.random.default_rng(3).integers(0, 2, size=(cfg["cpu"], plan.k), dtype=np.uint8)
+        pop = uniform_rows(cfg["cpu"], plan.k, 3)
         t0 = time.perf_counter()
         oc.fitness(kernels, bs.graph_backend, pop, threads=threads)
         row["cpu_oracle_fitness_per_s"] = cfg["cpu"] / (time.perf_counter() - t0)
         row["cpu_threads"] = threads
-        if name in ("resnet50", "bert_base"):
-            # the reference's own search API, drop-in: tp.evolve with the default
-            # ESConfig (population 32, 200 generations; reference draws replayed
-            # exactly, each generation priced in one GPU batch)
-            t0 = time.perf_counter()
-            r2 = tp.optimize(g, bs.registry, bs.measurer, 0.01)
-            ev = tp.evolve(g, bs.registry, bs.measurer, r2.placement, 0.01, tp.ESConfig(),
-                           graph_backend=bs.graph_backend, kernel_matches=r2.kernel_matches)
-            row["evolve_default"] = {"s": time.perf_counter() - t0, "cost_ms": ev.cost_ms,
-                                     "evaluations": ev.evaluations,
-                                     "note": "optimize + evolve(ESConfig()) through the public API"}
-        if cfg["ref_dp"]:
-            t0 = time.perf_counter()
-            status, cost, ref_kernels = oc.dp(max_states=200_000)
-            row["reference_dp"] = {"status": status, "s": time.perf_counter() - t0,
-                                   "placement_identical": status == "ok" and ref_kernels == kernels
-                                   and cost == res.cost_ms}
-        else:
-            row["reference_dp"] = {"status": "not run (covered-set state space of a 100k-node graph)"}
         out[name] = row
     return out
 
 
+# ----------------------------------------------------------------- reference arm
+
+def _breed(rng, pop, fits, k, tournament: int = 4):
+    """One generation of the reference's ES (tensorplace/evolution.py:
+    222-250): the best genome survives (elitism 1), every other child is a
+    two-point crossover of two size-4 tournament winners, each bit flipped
+    with probability 1/k.  Genomes are rows of bits (uint8)."""
+    import numpy as np
+    P = len(pop)
+    best = int(np.argmin(fits))
+    out = np.empty_like(pop)
+    out[0] = pop[best]
+    n = P - 1
+    idx = rng.integers(0, P, size=(2, n, tournament))
+    f = fits[idx]
+    win = np.take_along_axis(idx, np.argmin(f, axis=2)[..., None], axis=2)[..., 0]
+    cut = np.sort(rng.integers(0, k + 1, size=(n, 2)), axis=1)
+    col = np.arange(k)
+    mid = (col >= cut[:, :1]) & (col < cut[:, 1:])
+    out[1:] = np.where(mid, pop[win[1]], pop[win[0]])
+    # independent flips with probability 1/k: Binomial(k, 1/k) distinct
+    # positions per child
+    nflip = rng.binomial(k, 1.0 / k, size=n)
+    for c in np.nonzero(nflip)[0]:
+        pos = rng.choice(k, size=nflip[c], replace=False)
+        out[1 + c, pos] ^= 1
+    return out
+
+
+def _pack(bits):
+    import numpy as np
+    n, k = bits.shape
+    words = max(1, (k + 63) // 64)
+    buf = np.zeros((n, words * 8), np.uint8)
+    if k:
+        pk = np.packbits(bits, axis=1, bitorder="little")
+        buf[:, :pk.shape[1]] = pk
+    return buf.view(np.uint64)
+
+
 def run_reference(args) -> None:
-    world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
     if rank != 0:
         return
     import numpy as np
-    tp, g, bs = build_workload(args.workload)
-    oc = _oracle_case(g, bs)
+    wl = WORKLOADS[args.workload]
+    case = load_case(args.workload)
     t0 = time.perf_counter()
-    oc.price()
-    status, cost, kernels = oc.dp(max_states=2_000_000)
+    oc = _oracle(case)
+    status, cost, kernels, _ = oc.dp_subtree()
     dp_s = time.perf_counter() - t0
+    assert status == "ok"
+    k = _genome_bits(oc, case, kernels)
+    target = case["graph_backend"]
     threads = os.cpu_count() or 1
-    k = sum(1 for _, _, _ in kernels) if kernels else 0
-    # genome length: kernels not on graph backends
-    gb = {b for b, kind in [[b.id, b.kind.value] for b in bs.registry.backends.values()]
-          if kind == "graph_inference_library"}
-    order_backend = [bp.backend for bp in bs.registry.patterns]
-    k = sum(1 for o, _, _ in kernels if order_backend[o] not in gb)
-    sample = args.ref_sample
-    for _ in range(args.warmup):
-        oc.fitness(kernels, bs.graph_backend, _random_packed(256, k, 2), threads=threads)
+    S = args.ref_sample or wl["ref"]
+    # the reference's initial population: all-zero seed + uniform random rows
+    bits = np.unpackbits(uniform_rows(S, k, 1000).view(np.uint8), axis=1,
+                         bitorder="little")[:, :k].copy()
+    bits[0] = 0
+    rng = np.random.default_rng(args.seed)
+    fits = oc.fitness(kernels, target, _pack(bits), threads=threads)
     times = []
-    for step in range(args.steps):
-        pop = _random_packed(sample, k, 100 + step)  # packed rows, as the GPU arm reads them
+    for step in range(args.warmup + args.steps):
         t0 = time.perf_counter()
-        oc.fitness(kernels, bs.graph_backend, pop, threads=threads)
-        times.append(time.perf_counter() - t0)
-    value = sample * len(times) / sum(times)
+        bits = _breed(rng, bits, fits, k)
+        fits = oc.fitness(kernels, target, _pack(bits), threads=threads)
+        if step >= args.warmup:
+            times.append(time.perf_counter() - t0)
+    value = S * len(times) / sum(times)
+    maps = open("/proc/self/maps").read() if os.path.exists("/proc/self/maps") else ""
     line = {
         "impl": "reference",
         "metric": "fitness_evals_per_sec",
@@ -512,15 +568,21 @@ def run_reference(args) -> None:
         "vs_baseline": None,
         "dtype": "f64",
         "arithmetic": "f64 with exact sums (Kulisch accumulator, fsum-equivalent rounding), CPU",
-        "data": "synthetic (BERT-base graph; simulated backend cost tables)",
+        "data": f"synthetic ({wl['data']}; random-init ES population; simulated cost tables)",
         "config": {"workload": f"{args.workload}: op-level DP + evolutionary search",
-                   "nodes": len(g.nodes), "genome_bits": k, "dp_status": status,
-                   "dp_cost_ms": cost, "dp_s": dp_s},
+                   "nodes": len(case["graph"]["nodes"]), "genome_bits": k,
+                   "dp_kernels": len(kernels), "dp_cost_ms": cost,
+                   "dp": "oracle/oracle.c or_dp_subtree (the reference DP exceeds its state cap)"
+                         if args.workload in ("random100k", "nasnet_a", "nasrnn") else
+                         "oracle/oracle.c or_dp_subtree (equal to the reference DP)",
+                   "dp_s": dp_s, "population": S,
+                   "input": f"tests/golden/cases/{args.workload}.json.gz"},
         "cpu_baseline": {"value": value, "unit": "genomes/s", "cores": threads, "kind": "port",
-                         "sample": f"{sample} random packed genomes per step, oracle/oracle.c "
-                                   f"(reference algorithm restated in C), {threads} threads"},
+                         "sample": f"ES generations of {S} genomes (the reference's breed, numpy; "
+                                   f"every child priced by oracle/oracle.c with {threads} threads)"},
         "e2e": {"value": value, "unit": "genomes/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
+        "product_library_loaded": "libcollage_b200" in maps,
     }
     print(json.dumps(line), flush=True)
 
@@ -531,15 +593,16 @@ def main() -> None:
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=("mine", "reference"), default="mine")
-    ap.add_argument("--workload", default="bert_base")
+    ap.add_argument("--workload", default="random100k", choices=sorted(WORKLOADS))
     ap.add_argument("--population", type=int, default=None, help="genomes per GPU")
+    ap.add_argument("--e2e-population", type=int, default=None)
     ap.add_argument("--search-population", type=int, default=65536)
-    ap.add_argument("--search-generations", type=int, default=50)
-    ap.add_argument("--e2e-steps", type=int, default=5)
-    ap.add_argument("--cpu-sample", type=int, default=2_000_000,
-                    help="genomes in the CPU-baseline sample (~10 s of CPU work on BERT)")
-    ap.add_argument("--ref-sample", type=int, default=400_000,
-                    help="genomes per step of the --impl reference arm")
+    ap.add_argument("--search-generations", type=int, default=10)
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--cpu-sample", type=int, default=None,
+                    help="genomes in the CPU-baseline sample (default per workload)")
+    ap.add_argument("--ref-sample", type=int, default=None,
+                    help="ES population of the --impl reference arm (default per workload)")
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-configs", action="store_true", help="skip the five-config sweep")

@@ -88,12 +88,21 @@ static double ks_round(const ksum* k) {
   /* value = sum bit_i 2^(i-1152); take 53 bits from `top` down */
   int low = top - 52;
   if (low < 0) low = 0; /* subnormal territory: never reached for costs */
-  uint64_t m = 0;
-  for (int i = top; i >= low; --i) m = (m << 1) | (uint64_t)ks_bit(k, i);
+  /* bits [low, top] (at most 53) from the two limbs they span */
+  int lb = low >> 6, lo = low & 63;
+  unsigned __int128 win = (unsigned __int128)k->w[lb];
+  if (lb + 1 < KL) win |= (unsigned __int128)k->w[lb + 1] << 64;
+  uint64_t m = (uint64_t)(win >> lo) & ((top - low == 63) ? ~0ull : ((1ull << (top - low + 1)) - 1ull));
   if (low > 0) {
     int rb = ks_bit(k, low - 1);
-    int sticky = 0;
-    for (int i = low - 2; i >= 0 && !sticky; --i) sticky = ks_bit(k, i);
+    /* sticky: any bit below low - 1, limb by limb */
+    int sticky = 0, b = low - 2;
+    if (b >= 0) {
+      int limb = b >> 6, off = b & 63;
+      uint64_t mask = off == 63 ? ~0ull : ((1ull << (off + 1)) - 1ull);
+      sticky = (k->w[limb] & mask) != 0;
+      for (int i = limb - 1; i >= 0 && !sticky; --i) sticky = k->w[i] != 0;
+    }
     if (rb && (sticky || (m & 1))) m += 1;
   }
   return ldexp((double)m, low - 1152);
@@ -746,66 +755,89 @@ int or_fitness(int n, const int32_t* in_ptr, const int32_t* in_src, const int32_
   }
   rep_ptr[k] = nr;
   int maxk = n_kernels + n + 1;
-#pragma omp parallel for num_threads(threads) schedule(dynamic, 16)
-  for (int64_t gi = 0; gi < n_genomes; ++gi) {
-    const uint64_t* bits = genomes + gi * words;
-    int infeasible = 0;
-    for (int s = 0; s < k && !infeasible; ++s)
-      if (((bits[s >> 6] >> (s & 63)) & 1) && !rep_ok[s]) infeasible = 1;
-    if (infeasible) { out[gi] = INFINITY; continue; }
-    /* decoded placement as a list of matches */
+  /* per-thread scratch, allocated once: the decoded kernel list, the kernel
+     of every node, union-find parents and the region buckets */
+#pragma omp parallel num_threads(threads)
+  {
     int* dk = malloc(sizeof(int) * maxk);
-    int nd = 0, s = 0;
-    for (int i = 0; i < n_kernels; ++i) {
-      int flip = 0;
-      if (s < k && slot_kernel[s] == i) {
-        flip = (bits[s >> 6] >> (s & 63)) & 1;
-        if (flip) for (int j = rep_ptr[s]; j < rep_ptr[s + 1]; ++j) dk[nd++] = rep[j];
-        ++s;
-      }
-      if (!flip) dk[nd++] = kernel_match[i];
-    }
     int* kernel_of = malloc(sizeof(int) * (n + 1));
-    for (int i = 0; i < nd; ++i)
-      for (int j = mem_ptr[dk[i]]; j < mem_ptr[dk[i] + 1]; ++j) kernel_of[members[j]] = i;
-    int* par = malloc(sizeof(int) * (nd + 1));
-    for (int i = 0; i < nd; ++i) par[i] = i;
-    for (int v = 0; v < n; ++v) {
-      int ki = kernel_of[v], b = mbackend[dk[ki]];
-      if (!is_graph[b]) continue;
-      for (int j = in_ptr[v]; j < in_ptr[v + 1]; ++j) {
-        int p = in_src[j];
-        if (p < 0) continue;
-        int pk = kernel_of[p];
-        if (pk != ki && mbackend[dk[pk]] == b) {
-          int ra = uf_find(par, pk), rb = uf_find(par, ki);
-          if (ra != rb) { if (ra < rb) par[rb] = ra; else par[ra] = rb; }
+    int* par = malloc(sizeof(int) * (maxk + 1));
+    int* rid = malloc(sizeof(int) * (maxk + 1));
+    int* rcnt = malloc(sizeof(int) * (maxk + 2));
+    int* rmem = malloc(sizeof(int) * (maxk + 1));
+    int* rb = malloc(sizeof(int) * (maxk + 1));
+#pragma omp for schedule(dynamic, 4)
+    for (int64_t gi = 0; gi < n_genomes; ++gi) {
+      const uint64_t* bits = genomes + gi * words;
+      int infeasible = 0;
+      for (int s = 0; s < k && !infeasible; ++s)
+        if (((bits[s >> 6] >> (s & 63)) & 1) && !rep_ok[s]) infeasible = 1;
+      if (infeasible) { out[gi] = INFINITY; continue; }
+      /* decoded placement as a list of matches (evolution.py decode) */
+      int nd = 0, s = 0;
+      for (int i = 0; i < n_kernels; ++i) {
+        int flip = 0;
+        if (s < k && slot_kernel[s] == i) {
+          flip = (bits[s >> 6] >> (s & 63)) & 1;
+          if (flip) for (int j = rep_ptr[s]; j < rep_ptr[s + 1]; ++j) dk[nd++] = rep[j];
+          ++s;
+        }
+        if (!flip) dk[nd++] = kernel_match[i];
+      }
+      for (int i = 0; i < nd; ++i)
+        for (int j = mem_ptr[dk[i]]; j < mem_ptr[dk[i] + 1]; ++j) kernel_of[members[j]] = i;
+      /* union-find over same-backend graph kernels that touch (cost.py:339-357) */
+      for (int i = 0; i < nd; ++i) par[i] = i;
+      for (int v = 0; v < n; ++v) {
+        int ki = kernel_of[v], b = mbackend[dk[ki]];
+        if (!is_graph[b]) continue;
+        for (int j = in_ptr[v]; j < in_ptr[v + 1]; ++j) {
+          int p = in_src[j];
+          if (p < 0) continue;
+          int pk = kernel_of[p];
+          if (pk != ki && mbackend[dk[pk]] == b) {
+            int ra = uf_find(par, pk), rb2 = uf_find(par, ki);
+            if (ra != rb2) { if (ra < rb2) par[rb2] = ra; else par[ra] = rb2; }
+          }
         }
       }
+      /* terms: every other kernel's cost + eps; every region's
+         round(fsum(members)) * r(n) + eps (cost.py:359-373) */
+      ksum total, rs;
+      ks_zero(&total);
+      int nr = 0;
+      for (int i = 0; i < nd; ++i) rid[i] = -1;
+      for (int i = 0; i < nd; ++i) {
+        int b = mbackend[dk[i]];
+        if (!is_graph[b]) { ks_add(&total, mcost[dk[i]]); ks_add(&total, eps); continue; }
+        int r = uf_find(par, i);
+        if (rid[r] < 0) { rid[r] = nr; rcnt[nr] = 0; rb[nr] = b; ++nr; }
+        rcnt[rid[r]]++;
+      }
+      /* bucket the members of every region (counting sort by region) */
+      int acc = 0;
+      for (int r = 0; r < nr; ++r) { int c = rcnt[r]; rcnt[r] = acc; acc += c; }
+      rcnt[nr] = acc;
+      for (int i = 0; i < nd; ++i) {
+        if (!is_graph[mbackend[dk[i]]]) continue;
+        rmem[rcnt[rid[uf_find(par, i)]]++] = i;
+      }
+      for (int r = nr; r > 0; --r) rcnt[r] = rcnt[r - 1];
+      rcnt[0] = 0;
+      for (int r = 0; r < nr; ++r) {
+        ks_zero(&rs);
+        for (int q = rcnt[r]; q < rcnt[r + 1]; ++q) ks_add(&rs, mcost[dk[rmem[q]]]);
+        int b = rb[r], cnt = rcnt[r + 1] - rcnt[r];
+        volatile double prod = alpha[b] * (double)(cnt - 1);
+        volatile double t = 1.0 - prod;
+        double rr = t > floor_[b] ? t : floor_[b];
+        volatile double term = ks_round(&rs) * rr;
+        ks_add(&total, term);
+        ks_add(&total, eps);
+      }
+      out[gi] = ks_round(&total);
     }
-    ksum total;
-    ks_zero(&total);
-    ksum* rs = calloc(nd + 1, sizeof(ksum));
-    int* rn = calloc(nd + 1, sizeof(int));
-    for (int i = 0; i < nd; ++i) {
-      int b = mbackend[dk[i]];
-      if (!is_graph[b]) { ks_add(&total, mcost[dk[i]]); ks_add(&total, eps); continue; }
-      int r = uf_find(par, i);
-      ks_add(&rs[r], mcost[dk[i]]);
-      rn[r]++;
-    }
-    for (int i = 0; i < nd; ++i) {
-      if (!rn[i]) continue;
-      int b = mbackend[dk[i]];
-      volatile double prod = alpha[b] * (double)(rn[i] - 1);
-      volatile double t = 1.0 - prod;
-      double r = t > floor_[b] ? t : floor_[b];
-      volatile double term = ks_round(&rs[i]) * r;
-      ks_add(&total, term);
-      ks_add(&total, eps);
-    }
-    out[gi] = ks_round(&total);
-    free(rs); free(rn); free(par); free(kernel_of); free(dk);
+    free(dk); free(kernel_of); free(par); free(rid); free(rcnt); free(rmem); free(rb);
   }
   free(slot_kernel); free(rep_ptr); free(rep); free(rep_ok);
   return k;

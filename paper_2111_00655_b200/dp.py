@@ -18,6 +18,7 @@ the node count + 1).
 from __future__ import annotations
 
 import ctypes
+import time
 from dataclasses import dataclass, field
 from typing import Any, Mapping
 
@@ -111,12 +112,16 @@ def optimize(g: ComputationGraph, registry: PatternRegistry, measurer: Measurer,
     if max_states is not None and len(g.nodes) + 1 > max_states:
         raise SearchLimitError(f"operator-level search needs {len(g.nodes) + 1} live states on "
                                f"a {len(g.nodes)}-node graph, above the cap of {max_states}")
+    t0 = time.perf_counter()
     table = registry.match_table(g)
+    t1 = time.perf_counter()
     price_matches(measurer, registry, table)
+    t2 = time.perf_counter()
     kernels = np.empty(len(g.nodes), dtype=np.int32)
     res = nat.DPResultStruct()
     nat.check(nat.lib().cb_dp_solve(g.native, table.handle.raw, float(epsilon),
                                     nat.ptr(kernels, nat.c_int32), ctypes.byref(res)))
+    t3 = time.perf_counter()
     sizes = np.diff(table.group_ptr)
     stats.pops = len(g.nodes)
     stats.candidates_total = int(table.n_matches)
@@ -130,7 +135,8 @@ def optimize(g: ComputationGraph, registry: PatternRegistry, measurer: Measurer,
     stats.computations = measurer.computations - p0
     device = {"device_ms": res.device_ms, "levels": res.n_levels, "launches": res.n_launches,
               "ties": res.ties, "walk_steps": res.walk_steps,
-              "rounding_window_safe": bool(res.window_safe)}
+              "rounding_window_safe": bool(res.window_safe),
+              "phases_s": {"match": t1 - t0, "price": t2 - t1, "dp_call": t3 - t2}}
     if not res.feasible:
         z = res.first_zero_candidate
         if z >= 0:
@@ -153,8 +159,10 @@ def optimize(g: ComputationGraph, registry: PatternRegistry, measurer: Measurer,
     assignments = [Assignment.fast(sets[i], patterns[pats[i]], roots[i]) for i in order]
     stats.improvements = len(assignments)
     placement = PlacementStrategy.from_canonical(assignments)
+    t4 = time.perf_counter()
     if validate or (validate is None and len(g.nodes) <= VALIDATE_MAX_NODES):
         validate_placement(g, placement)
+    device["phases_s"].update(result=t4 - t3, validate=time.perf_counter() - t4)
     canon = np.asarray([chosen[i] for i in order], dtype=np.int32)
     out = DPResult(placement, res.cost_ms, stats,
                    {frozenset(g.nodes): res.cost_ms, frozenset(): 0.0}, device, canon)

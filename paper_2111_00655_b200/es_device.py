@@ -95,8 +95,15 @@ class DeviceEvolution:
         # kernels and their unpack
         # (+ the overflow list kernel when the anchor walk prices the plan);
         # torch's index_select / copies of the elite row are not counted
-        self.launches_per_generation = (6 if self.fused else 7) + \
-            (1 if plan.kernel_name() == "fitness_anchor_kernel" else 0)
+        self.launches_per_generation = self.launches_for(plan, self.fused)
+
+    @staticmethod
+    def launches_for(plan: FitnessPlan, fused: bool = False) -> int:
+        """Kernels of libcollage_b200.so per generation: fitness min/max and the
+        tournament order keys, (fused | breed + fitness), the two CUB argmin
+        kernels and their unpack (+ the overflow list kernel when the anchor
+        walk prices the plan); torch's copies of the elite row are not counted."""
+        return (6 if fused else 7) + (1 if plan.kernel_name() == "fitness_anchor_kernel" else 0)
 
     # -- helpers -----------------------------------------------------------------------
     def _stream(self) -> int:

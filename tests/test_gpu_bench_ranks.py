@@ -24,7 +24,7 @@ def test_two_rank_bench_line(gpu):
     env = dict(os.environ, CB_BENCH_DIST_BACKEND="gloo")
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
            "--master-addr", "127.0.0.1", "--master-port", str(_port()), "bench.py", "--gpus", "2",
-           "--steps", "3", "--warmup", "3", "--population", "262144", "--search-generations", "3",
+           "--workload", "bert_base", "--steps", "3", "--warmup", "3", "--population", "262144", "--search-generations", "3",
            "--e2e-steps", "1"]
     out = subprocess.run(cmd, cwd=ROOT, env=env, capture_output=True, text=True, timeout=600)
     assert out.returncode == 0, out.stderr[-2000:]
