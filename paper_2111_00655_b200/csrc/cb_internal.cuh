@@ -149,3 +149,10 @@ struct LevelSegment {
   bool narrow;
 };
 std::vector<LevelSegment> cb_plan_levels(const cb_graph* g, int32_t narrow_max);
+
+// True when `func` on the current device has not yet been given a dynamic
+// shared-memory limit of at least `bytes` (and records it): the attribute
+// is per device, so a process driving several GPUs sets it on each.
+// Thread-safe.
+bool cb_smem_claim(const void* func, size_t bytes);
+

@@ -481,12 +481,9 @@ extern "C" int cb_dp_solve(cb_graph* g, cb_matches* m, double epsilon, int32_t* 
   cudaEventCreate(&ev1);
   cudaEventRecord(ev0);
   std::vector<LevelSegment> segs = cb_plan_levels(g, 2 * DP_NARROW_WARPS);
-  static bool smem_configured = false;
-  if (!smem_configured) {
+  if (cb_smem_claim((const void*)dp_narrow_kernel, DP_STAGE_MAX))
     CB_CUDA_TRY(cudaFuncSetAttribute(dp_narrow_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      (int)DP_STAGE_MAX));
-    smem_configured = true;
-  }
   for (const LevelSegment& s : segs) {
     if (s.narrow) {
       auto al = [](size_t b) { return (b + 15) & ~(size_t)15; };

@@ -571,7 +571,7 @@ extern "C" const char* cb_es_plan_kernel(const cb_es_plan* p) {
     return pk[p->F <= 4 ? 0 : p->F <= 6 ? 1 : p->F <= 8 ? 2 : p->F <= 12 ? 3 : 4];
   }
   if (frontier && (p->force_path == 4 || (p->force_path == -1 && !p->packed_ok)))
-    return p->anchor_ok ? "fitness_anchor_kernel" : "fitness_wide_kernel";
+    return p->anchor_ok && p->anchor_wide_ok ? "fitness_anchor_kernel" : "fitness_wide_kernel";
   if (frontier) {
     if (p->force_path != 2 && p->packed_ok) return "fitness_frontier2_kernel";
     return "fitness_frontier_kernel";
@@ -1248,12 +1248,9 @@ template <int F>
 static int launch_frontier_t(cb_es_plan* p, const uint64_t* d_pop, int64_t n, double* d_fit,
                              cudaStream_t stream) {
   const size_t smem = sizeof(FrontierSmem<F>);
-  static bool configured = false;
-  if (!configured) {
+  if (cb_smem_claim((const void*)fitness_frontier_kernel<F>, smem))
     CB_CUDA_TRY(cudaFuncSetAttribute(fitness_frontier_kernel<F>,
                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    configured = true;
-  }
   int per_sm = 0;
   CB_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fitness_frontier_kernel<F>,
                                                             FR_THREADS, smem));
@@ -1272,12 +1269,9 @@ static int launch_frontier2_t(cb_es_plan* p, const uint64_t* d_pop, int64_t n, d
                               cudaStream_t stream) {
   const size_t smem = ((size_t)4 * F * FR_THREADS + (size_t)(FR_THREADS / 32) * (4 * FR_QCAP + 96)) *
                       sizeof(uint64_t);
-  static bool configured = false;
-  if (!configured) {
+  if (cb_smem_claim((const void*)fitness_frontier2_kernel<LT, F>, smem))
     CB_CUDA_TRY(cudaFuncSetAttribute(fitness_frontier2_kernel<LT, F>,
                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    configured = true;
-  }
   int per_sm = 0;
   CB_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fitness_frontier2_kernel<LT, F>,
                                                             FR_THREADS, smem));
@@ -1321,12 +1315,9 @@ static int launch_fitness(cb_es_plan* p, const uint64_t* d_pop, int64_t n, doubl
   FitArgs a = make_args(p);
   if (p->smem_path) {
     const size_t smem = (size_t)FIT_WARPS * p->M * (sizeof(fx192) + 8);
-    static size_t configured = 0;
-    if (smem > 48 * 1024 && configured < smem) {
+    if (smem > 48 * 1024 && cb_smem_claim((const void*)fitness_smem_kernel, smem))
       CB_CUDA_TRY(cudaFuncSetAttribute(fitness_smem_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)std::max<size_t>(smem, 48 * 1024)));
-      configured = smem;
-    }
     int per_sm = 0;
     CB_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fitness_smem_kernel,
                                                               FIT_WARPS * 32, smem));

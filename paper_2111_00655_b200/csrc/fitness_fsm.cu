@@ -292,8 +292,7 @@ fitness_fsm_kernel(FsmArgs a, const uint64_t* __restrict__ pop, int64_t n, doubl
 template <int F, int W, int L>
 int launch_fsm_t(cb_es_plan* p, const uint64_t* d_pop, int64_t n, double* d_fit, cudaStream_t stream) {
   const size_t smem = FsmSmemBase<F, W>::bytes + (L != 0 ? (size_t)p->fsm_deltas * sizeof(uint4) : 0);
-  static size_t configured = 0;
-  if (configured < smem) {
+  if (cb_smem_claim((const void*)fitness_fsm_kernel<F, W, L>, smem)) {
     CB_CUDA_TRY(cudaFuncSetAttribute(fitness_fsm_kernel<F, W, L>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      (int)smem));
     // the smallest shared-memory configuration holding 1024 threads (8
@@ -309,7 +308,6 @@ int launch_fsm_t(cb_es_plan* p, const uint64_t* d_pop, int64_t n, double* d_fit,
       }
     CB_CUDA_TRY(cudaFuncSetAttribute(fitness_fsm_kernel<F, W, L>, cudaFuncAttributePreferredSharedMemoryCarveout,
                                      cv ? atoi(cv) : pct));
-    configured = smem;
   }
   int per_sm = 0;
   CB_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fitness_fsm_kernel<F, W, L>, FSM_THREADS, smem));

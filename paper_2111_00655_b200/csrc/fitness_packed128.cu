@@ -600,12 +600,9 @@ template <typename LT, int F>
 int launch_pk_t(cb_es_plan* p, const uint64_t* d_pop, int64_t n, double* d_fit, cudaStream_t stream) {
   const size_t smem = ((size_t)3 * F * PK_THREADS + (size_t)(PK_THREADS / 32) * (3 * PK_QCAP + 64)) *
                       sizeof(uint64_t);
-  static bool configured = false;
-  if (!configured) {
+  if (cb_smem_claim((const void*)fitness_packed128_kernel<LT, F>, smem))
     CB_CUDA_TRY(cudaFuncSetAttribute(fitness_packed128_kernel<LT, F>,
                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    configured = true;
-  }
   int per_sm = 0;
   CB_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fitness_packed128_kernel<LT, F>,
                                                             PK_THREADS, smem));
@@ -622,12 +619,9 @@ template <int F, int W>
 int launch_pa_t(cb_es_plan* p, const uint64_t* d_pop, int64_t n, double* d_fit, cudaStream_t stream) {
   const size_t smem = ((size_t)3 * F * PK_THREADS + (size_t)(PK_THREADS / 32) * (3 * PK_QCAP + 64)) *
                       sizeof(uint64_t);
-  static bool configured = false;
-  if (!configured) {
+  if (cb_smem_claim((const void*)fitness_pa_kernel<F, W>, smem))
     CB_CUDA_TRY(cudaFuncSetAttribute(fitness_pa_kernel<F, W>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      (int)smem));
-    configured = true;
-  }
   int per_sm = 0;
   CB_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fitness_pa_kernel<F, W>, PK_THREADS, smem));
   if (per_sm < 1) per_sm = 1;
@@ -656,12 +650,9 @@ int launch_pab_t(cb_es_plan* p, const BreedArgs& br, uint64_t* d_children, int64
                  cudaStream_t stream) {
   const size_t smem = ((size_t)3 * F * PK_THREADS + (size_t)(PK_THREADS / 32) * (3 * PK_QCAP + 64)) *
                       sizeof(uint64_t);
-  static bool configured = false;
-  if (!configured) {
+  if (cb_smem_claim((const void*)fitness_pa_breed_kernel<F, W>, smem))
     CB_CUDA_TRY(cudaFuncSetAttribute(fitness_pa_breed_kernel<F, W>,
                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    configured = true;
-  }
   int per_sm = 0;
   CB_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fitness_pa_breed_kernel<F, W>,
                                                             PK_THREADS, smem));

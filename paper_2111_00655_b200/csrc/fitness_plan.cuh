@@ -73,16 +73,21 @@ struct cb_es_plan {
   bool anchor_ok = false;
   int32_t anchor_shift = 0;
   int32_t anchor_span = 0;  // highest bit of the partial-sum bound minus anchor_shift
-  DBuf<uint8_t> d_ahot;     // AHot[M]
-  DBuf<uint64_t> d_acold;   // [M][6]: rep, off, term1 as 128-bit X
+  DBuf<uint64_t> d_acold;   // [M][6]: rep, off, term1 as 128-bit X (packed-label walks)
   DBuf<int32_t> d_acnt;     // [M]
+  bool anchor_wide_ok = false;  // packed-sum anchor walk usable (span and counts fit)
+  DBuf<uint8_t> d_astep;        // AStep[M] 16-byte step records
+  DBuf<uint64_t> d_aoff, d_arepc, d_aterm;  // [M][2]: off, rep | cnt << 108, one-unit term (X)
+  DBuf<uint8_t> d_alists;       // long back / end slot lists
+  DBuf<int32_t> d_an_infeas_word;  // genome words holding infeasible bits, and their masks
+  DBuf<uint64_t> d_an_infeas_mask;
   int32_t pool_entries = 16;
   // pool_auto: the pool size follows the overflow rate of earlier launches,
   // read back asynchronously into pinned memory (never synchronised on)
   bool pool_auto = true;
   int32_t* h_ovf = nullptr;       // pinned: overflow count of the last finished launch
   int64_t last_anchor_n = 0;
-  int32_t auto_pool = 14;
+  int32_t auto_pool = 8;
   cudaStream_t host_stream = nullptr;  // single-chunk cb_fitness_host calls
   ~cb_es_plan() {
     if (h_ovf) cudaFreeHost(h_ovf);

@@ -147,23 +147,28 @@ def optimize(g: ComputationGraph, registry: PatternRegistry, measurer: Measurer,
                 f"candidate matches", op_kinds=(kind,), node_ids=(nid,))
         raise UncoverableGraphError("no full placement found; some nodes cannot be covered "
                                     "compatibly by the registered patterns")
-    chosen = kernels[:res.n_kernels].tolist()
+    chosen = kernels[:res.n_kernels]
+    # canonical order (sorted node tuple): the kernels are disjoint, so it is
+    # the order of their smallest members (member lists are sorted, node
+    # indices follow node ids) -- vectorised; the Assignment objects are
+    # built only when the placement's assignments are first read
+    first = table.members[table.mem_ptr[chosen]] if len(chosen) else np.zeros(0, np.int64)
+    canon = np.ascontiguousarray(chosen[np.argsort(first, kind="stable")], dtype=np.int32)
     patterns = registry.patterns
-    # canonical order (sorted node tuple) computed once for the placement and
-    # for the match indices the fitness plan takes
-    sets = table.node_sets(chosen)
-    keys = [tuple(sorted(x)) for x in sets]
-    order = sorted(range(len(chosen)), key=keys.__getitem__)
-    pats = table.pat[chosen].tolist() if chosen else []
-    roots = np.asarray(g._ids)[table.root[chosen]].tolist() if chosen else []
-    assignments = [Assignment.fast(sets[i], patterns[pats[i]], roots[i]) for i in order]
-    stats.improvements = len(assignments)
-    placement = PlacementStrategy.from_canonical(assignments)
+
+    def build() -> list[Assignment]:
+        ms = canon.tolist()
+        sets = table.node_sets(ms)
+        pats = table.pat[canon].tolist()
+        roots = np.asarray(g._ids)[table.root[canon]].tolist()
+        return [Assignment.fast(sets[i], patterns[pats[i]], roots[i]) for i in range(len(ms))]
+
+    stats.improvements = len(canon)
+    placement = PlacementStrategy.lazy(len(canon), build)
     t4 = time.perf_counter()
     if validate or (validate is None and len(g.nodes) <= VALIDATE_MAX_NODES):
         validate_placement(g, placement)
     device["phases_s"].update(result=t4 - t3, validate=time.perf_counter() - t4)
-    canon = np.asarray([chosen[i] for i in order], dtype=np.int32)
     out = DPResult(placement, res.cost_ms, stats,
                    {frozenset(g.nodes): res.cost_ms, frozenset(): 0.0}, device, canon)
     if not device["rounding_window_safe"] and rounding == "raise":

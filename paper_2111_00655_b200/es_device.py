@@ -78,6 +78,7 @@ class DeviceEvolution:
         self.cur = 0
         self.best_idx = torch.zeros(1, dtype=torch.int64, device=self.device)
         self.best_val = torch.zeros(1, dtype=torch.float64, device=self.device)
+        self.elite_val = torch.full((1,), float("inf"), dtype=torch.float64, device=self.device)
         self.elite = torch.zeros((1, self.W), **opts)
         self.gather_fit = torch.empty(self.world, dtype=torch.float64, device=self.device)
         self.gather_rows = torch.empty((self.world, self.W), **opts)
@@ -116,6 +117,10 @@ class DeviceEvolution:
     def initialize(self) -> None:
         """Row 0 of rank 0 is the all-zero genome (the DP placement itself);
         every other row is uniformly random."""
+        with _torch().cuda.device(self.device):  # native launches use the current device
+            self._initialize()
+
+    def _initialize(self) -> None:
         torch = _torch()
         gen = torch.Generator(device=self.device)
         gen.manual_seed(self.seed * 1_000_003 + self.rank)
@@ -159,6 +164,7 @@ class DeviceEvolution:
                 p["fit"][self.cur], self.P, p["pop"][self.cur], self.W, p["best_idx"],
                 p["best_val"], p["elite"], hist,
                 ctypes.c_void_p(self._stream() if stream is None else stream)))
+            self.elite_val = self.best_val
             return
         nat.check(nat.lib().cb_argmin(self._ptr(self.fit[self.cur]), self.P,
                                       self._ptr(self.best_idx), self._ptr(self.best_val),
@@ -168,9 +174,11 @@ class DeviceEvolution:
             elite, best = exchange_elites(self.best_val, row, self.group, self.gather_fit,
                                           self.gather_rows)
             self.elite.copy_(elite)
+            self.elite_val.copy_(best)
         else:
             self.elite.copy_(row)
             best = self.best_val
+            self.elite_val.copy_(best)
         if self.generation < self.history.numel():
             self.history[self.generation:self.generation + 1].copy_(best)
 
@@ -195,6 +203,10 @@ class DeviceEvolution:
 
     def step(self) -> None:
         """One generation (no host synchronisation)."""
+        with _torch().cuda.device(self.device):  # native launches use the current device
+            self._step()
+
+    def _step(self) -> None:
         self.generation += 1
         nxt = 1 - self.cur
         timing = getattr(self, "timing", False)
@@ -227,8 +239,8 @@ class DeviceEvolution:
         """(cost, genome bits) of the global best; synchronises."""
         bits = self.elite[0].cpu().numpy().view(np.uint8)
         unpacked = np.unpackbits(bits, bitorder="little")[:self.k]
-        vals = self.history[:min(self.generation + 1, self.history.numel())].cpu().numpy()
-        return float(vals.min()), unpacked
+        # the elite's own fitness (the history stops at its capacity)
+        return float(self.elite_val.item()), unpacked
 
     def history_values(self) -> np.ndarray:
         return self.history[:min(self.generation + 1, self.history.numel())].cpu().numpy()

@@ -99,7 +99,7 @@ def test_plan_outside_the_128_bit_window_uses_192_bit_kernels(gpu):
                                    fusion_discount=p.fusion_discount, region_alpha=p.region_alpha,
                                    region_floor=p.region_floor)
     meas = SimMeasurer(profiles)
-    res = tp.optimize(g, bs.registry, meas, 0.01)
+    res = tp.optimize(g, bs.registry, meas, 0.01, rounding="exact")
     plan = tp.FitnessPlan(g, bs.registry, meas, res.placement, 0.01, bs.graph_backend,
                           res.kernel_matches)
     assert plan.k > 0
@@ -140,7 +140,7 @@ def test_edge_plans_every_path(gpu, n_rows):
                         ("cheap-graph", lambda b: 0.5 if b == bs.graph_backend else 1.0),
                         ("no-graph", lambda b: 1e3 if b == bs.graph_backend else 1.0)):
         meas = _scaled(bs, scale)
-        res = tp.optimize(g, bs.registry, meas, 0.01)
+        res = tp.optimize(g, bs.registry, meas, 0.01, rounding="exact")
         plan = tp.FitnessPlan(g, bs.registry, meas, res.placement, 0.01, bs.graph_backend,
                               res.kernel_matches)
         assert (plan.k == 0) == (name == "all-graph"), (name, plan.k)

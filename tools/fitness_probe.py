@@ -14,11 +14,13 @@ plan = tp.FitnessPlan(g, bs.registry, bs.measurer, res.placement, 0.01, bs.graph
 i = plan.info
 print(name, 'k', plan.k, 'units', i.units, 'edges', i.edges, 'frontier', i.frontier_slots, 'dp', res.device)
 for label, fill in (('random', None), ('sparse', 0.1), ('dense', 0.9)):
+    rnd = lambda: torch.randint(-(1 << 63), (1 << 63) - 1, (P, plan.words), dtype=torch.int64, device='cuda')
     if fill is None:
-        pop = torch.randint(-(1 << 62), 1 << 62, (P, plan.words), dtype=torch.int64, device='cuda')
-    else:
-        bits = (torch.rand((P, plan.words, 64), device='cuda') < fill).to(torch.int64)
-        pop = (bits << torch.arange(64, device='cuda')).sum(-1)
+        pop = rnd()
+    elif fill < 0.5:  # density 1/8: AND of three random words
+        pop = rnd() & rnd() & rnd()
+    else:  # density 7/8
+        pop = rnd() | rnd() | rnd()
     feas = np.zeros(plan.words, np.uint64)  # keep genomes feasible, as an ES population is
     for s_ in range(plan.k):
         if plan.rep_kind[s_] != 0:
