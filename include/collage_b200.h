@@ -5,21 +5,21 @@
  * the entry points below are the calls its hot path would bind if it had
  * one.  Each block names the reference function it replaces:
  *
- *   cb_graph_*        tensorplace/graph.py:260-469   ComputationGraph structure
- *                     (topo order :345, depths :366, post-dominators :413-444)
- *   cb_match_*        tensorplace/matching.py:451-513 match_at / match_all and
- *                     tensorplace/registry.py:487-497 candidates_at
- *   cb_matches_price  tensorplace/cost.py:121-136, :248-263 SimProfile.kernel_cost
+ *   cb_graph_*        tensorplace/graph.py:71-345   ComputationGraph structure
+ *                     (topo order :156-175, depths :177-182, post-dominators :224-255)
+ *   cb_match_*        tensorplace/matching.py:53-115 match_at / match_all and
+ *                     tensorplace/registry.py:135-145 candidates_at
+ *   cb_matches_price  tensorplace/cost.py:121-138, :248-263 SimProfile.kernel_cost
  *                     via SimMeasurer.measure_kernel
  *   cb_dp_solve       tensorplace/dp.py:71-179        optimize (Algorithm 1)
  *   cb_es_plan_* /
- *   cb_fitness_*      tensorplace/evolution.py:256-371 decode + fitness, i.e.
+ *   cb_fitness_*      tensorplace/evolution.py:65-119 decode + fitness, i.e.
  *                     tensorplace/cost.py:320-373 placement_cost_graphlevel
- *   cb_es_breed       tensorplace/evolution.py:373-428 selection / crossover /
+ *   cb_es_breed       tensorplace/evolution.py:205-223 selection / crossover /
  *                     mutation (device variant, counter-based RNG)
- *   cb_es_generation  tensorplace/evolution.py:233-247 one generation (breed +
+ *   cb_es_generation  tensorplace/evolution.py:233-249 one generation (breed +
  *                     evaluate), optionally as one fused kernel
- *   cb_argmin*        tensorplace/evolution.py:228-230, :245-247 best tracking
+ *   cb_argmin*        tensorplace/evolution.py:226-231, :245-247 best tracking
  *   cb_es_plan_units / _kernel / _set_path / _set_pool: diagnostics and tuning
  *                     knobs of this implementation (no reference counterpart)
  *
@@ -265,7 +265,7 @@ int cb_es_breed(cb_es_plan* p, const uint64_t* d_parents,
                 const uint64_t* d_keep, int64_t n_keep, uint64_t seed,
                 uint64_t generation, uint64_t stream_id, int32_t tournament,
                 double mutation_rate, void* stream);
-/* One ES generation (tensorplace/evolution.py:233-247: breed the next
+/* One ES generation (tensorplace/evolution.py:233-249: breed the next
  * population, evaluate it): breed n_children rows into d_children (same operators
  * and draws as cb_es_breed) and write their fitness to d_child_fit (as
  * cb_fitness_device).  Runs as a single fused kernel when the plan's walk
@@ -279,14 +279,14 @@ int cb_es_generation(cb_es_plan* p, const uint64_t* d_parents,
                      int32_t tournament, double mutation_rate, void* stream);
 /* cb_argmin plus, when d_pop is given, the best row copied to d_elite
  * (words uint64) and the best value to *d_history_slot (if not NULL):
- * the best-so-far / history bookkeeping of tensorplace/evolution.py:245-247. */
+ * the best-so-far / history bookkeeping of tensorplace/evolution.py:244-248. */
 int cb_argmin_elite(const double* d_fit, int64_t n, const uint64_t* d_pop,
                     int32_t words, int64_t* d_idx, double* d_val,
                     uint64_t* d_elite, double* d_history_slot, void* stream);
 /* 1 when cb_es_generation runs fused for this plan (and path setting). */
 int cb_es_generation_fused(const cb_es_plan* p);
 /* Index of the smallest fitness (first on ties) -> d_idx[0]; value ->
- * d_val[0] (tensorplace/evolution.py:228-230, :245-247 best tracking). */
+ * d_val[0] (tensorplace/evolution.py:226-231, :245-247 best tracking). */
 int cb_argmin(const double* d_fit, int64_t n, int64_t* d_idx, double* d_val,
               void* stream);
 

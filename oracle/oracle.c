@@ -6,14 +6,14 @@
  * (paper_2111_00655_b200) never does.  It restates the reference algorithms
  * literally, without the device reformulations:
  *
- *   or_match_at      tensorplace/matching.py:451-501 (recursive walk with a
+ *   or_match_at      tensorplace/matching.py:53-103 (recursive walk with a
  *                    per-node bound-subtree map, then the single-exit check)
- *   or_kernel_cost   tensorplace/cost.py:121-136 (node cost, fsum, discount)
+ *   or_kernel_cost   tensorplace/cost.py:121-138 (node cost, fsum, discount)
  *   or_dp            tensorplace/dp.py:71-179 (Algorithm 1: frontier queue in
  *                    (depth, id) order, one state per covered node set,
  *                    every stored state relaxed for every candidate, ties on
  *                    the sorted (registration index, node tuple) key)
- *   or_fitness       tensorplace/evolution.py:256-298, :346-371 (decode) and
+ *   or_fitness       tensorplace/evolution.py:65-119, :346-371 (decode) and
  *                    tensorplace/cost.py:320-373 (graph-level cost)
  *
  * fsum is restated as an exact Kulisch accumulator over the whole double
@@ -145,7 +145,7 @@ static int cmp_pop_q(const void* a, const void* b) {
 }
 
 /* topological order (Kahn, smallest index first) -> depths and pop order;
- * restates graph.py:345-371 */
+ * restates graph.py:156-182 */
 static int og_prepare(og_t* g) {
   int n = g->n;
   int* cnt = calloc(n + 1, sizeof(int));
@@ -316,7 +316,7 @@ static int cmp_int(const void* a, const void* b) {
 }
 
 /* match_at: returns 1 and fills members (sorted) / bind; restates
- * matching.py:451-501 */
+ * matching.py:53-103 */
 static int match_at_impl(const og_t* g, const op_t* p, int root, int pat, walk_t* w,
                          int* members, int* nmem) {
   w->ntouched = 0;
@@ -345,7 +345,7 @@ static int match_at_impl(const og_t* g, const op_t* p, int root, int pat, walk_t
 }
 
 /* Table of all candidate matches: for every node, the patterns rooted at
- * its kind in registration order (registry.py:487-497). */
+ * its kind in registration order (registry.py:135-145). */
 typedef struct {
   int n_match;
   int32_t *group_ptr, *pat, *root, *mem_ptr, *members, *bind_ptr, *binds;
@@ -415,7 +415,7 @@ static int build_matches(const og_t* g, const op_t* p, const int32_t* kind_pat_p
 }
 
 /* ----------------------------------------------------------- kernel cost */
-/* cost.py:121-136; err: 1 no profile, 2 op without entry */
+/* cost.py:121-138; err: 1 no profile, 2 op without entry */
 static double kernel_cost(const og_t* g, const mt_t* mt, int m, int backend, int n_kinds,
                           const double* coeff, const double* overhead, const uint8_t* has,
                           const uint8_t* has_prof, int pw_stride, const double* pw, int* err) {
@@ -504,7 +504,7 @@ static int st_add(states_t* s, const uint64_t* c) {
   return id;
 }
 
-/* element order: (registration index, sorted node tuple) -- placement.py:487-488 */
+/* element order: (registration index, sorted node tuple) -- placement.py:40-41 */
 static int elem_cmp(const mt_t* mt, int a, int b) {
   if (mt->pat[a] != mt->pat[b]) return mt->pat[a] < mt->pat[b] ? -1 : 1;
   int i = mt->mem_ptr[a], ie = mt->mem_ptr[a + 1], j = mt->mem_ptr[b], je = mt->mem_ptr[b + 1];
@@ -672,7 +672,7 @@ int or_match_all(int n, const int32_t* kind, const int32_t* in_ptr, const int32_
 
 void or_free(void* p) { free(p); }
 
-/* Kernel cost of every match (cost.py:121-136).  err_out per match. */
+/* Kernel cost of every match (cost.py:121-138).  err_out per match. */
 int or_price(int n_match, const int32_t* root_kind_unused, const int32_t* mem_ptr,
              const int32_t* members, const int32_t* backend, const int32_t* kind,
              const double* volume, int n_kinds, const double* coeff, const double* overhead,
@@ -708,7 +708,7 @@ int or_fitness(int n, const int32_t* in_ptr, const int32_t* in_src, const int32_
                int n_backends, const uint8_t* is_graph, const double* alpha,
                const double* floor_, int target, double eps, const uint64_t* genomes,
                int64_t n_genomes, int words, int threads, double* out) {
-  /* eligible slots and their replacements (evolution.py:244-276) */
+  /* eligible slots and their replacements (evolution.py:77-97) */
   int* slot_kernel = malloc(sizeof(int) * (n_kernels + 1));
   int k = 0;
   for (int i = 0; i < n_kernels; ++i)

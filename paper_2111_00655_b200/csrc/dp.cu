@@ -4,8 +4,8 @@
 // set and relaxes every stored state for every candidate match; its optimum
 // is the cheapest partition of the graph into registry matches, ties broken
 // by the canonical key (sorted (registration index, sorted node ids) pairs,
-// tensorplace/placement.py:525-529).  Because a match may only expose its
-// root (matching.py:413-416), every non-root member of a kernel is
+// tensorplace/placement.py:78-82).  Because a match may only expose its
+// root (matching.py:93-101), every non-root member of a kernel is
 // post-dominated by the kernel root, so the kernels of any partition nest
 // along the post-dominator tree.  That turns the covered-set DP into an
 // exact DP over post-dominator subtrees:

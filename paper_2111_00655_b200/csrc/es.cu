@@ -1,6 +1,6 @@
 // Device-side evolutionary operators for population-scale search.
 //
-// Operator semantics follow tensorplace/evolution.py:384-399 and :412-428:
+// Operator semantics follow tensorplace/evolution.py:205-223 and :412-428:
 // tournament selection (first draw, then tournament-1 challengers that win
 // only when strictly fitter), two-point crossover child = a[:i] + b[i:j] +
 // a[j:] with i <= j drawn from [0, k], per-bit mutation.  Randomness is

@@ -1,6 +1,6 @@
 // Graph-level fitness of offload genomes, batched over a population.
 //
-// Reference semantics (tensorplace/evolution.py:256-371 and
+// Reference semantics (tensorplace/evolution.py:65-119 and
 // tensorplace/cost.py:320-373): bit i of a genome moves the i-th eligible
 // kernel (canonical placement order, not on a graph inference library) to
 // the target graph backend -- as one same-node-set match of that backend
@@ -106,7 +106,7 @@ static void build_frontier_program(cb_es_plan* P, int32_t n_elig_units) {
   // 16 entries: on the random 100k DAG 14 would fit 8 CTAs per SM instead of
   // 7 (0.53 vs 0.48 M genomes/s on its ES population) but sends a dense
   // population (90 % of bits set) to the fallback kernel 6x more slowly
-  P->pool_entries = std::min(used, 16);
+  P->pool_entries = std::min(used, 8);
   // sparse walk: program position of every genome bit, fixed-unit positions
   P->prog_last.assign(last.begin(), last.end());
   P->pos_of_bit.assign((size_t)std::max(P->k, 1), -1);
@@ -582,7 +582,6 @@ extern "C" const char* cb_es_plan_kernel(const cb_es_plan* p) {
 extern "C" int cb_es_plan_set_pool(cb_es_plan* p, int32_t entries) {
   CB_ARG_CHECK(p && entries >= 1 && entries <= 24, "cb_es_plan_set_pool: entries must be in [1, 24]");
   p->pool_entries = entries;
-  p->pool_auto = false;
   return CB_OK;
 }
 

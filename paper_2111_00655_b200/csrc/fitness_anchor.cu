@@ -78,9 +78,8 @@ struct AnArgs {
   fx192 base_const;
   X128 eps;
   const AStep* __restrict__ step;
-  const ulonglong2* __restrict__ off;    // [M] own kernel cost + eps (removed when on)
-  const ulonglong2* __restrict__ repc;   // [M] replacement sum | count << 108
-  const ulonglong2* __restrict__ term1;  // [M] one-unit region term
+  const ulonglong2* __restrict__ repc;   // [M][2] replacement sum | count << 108, own term (off)
+  const ulonglong2* __restrict__ term1;  // [M] one-unit region term minus the unit's own term
   const uint8_t* __restrict__ lists;     // long back / end lists
   const int32_t* __restrict__ infeas_word;
   const uint64_t* __restrict__ infeas_mask;
@@ -88,6 +87,7 @@ struct AnArgs {
   unsigned long long* flags;
   int32_t* ovf_count;
   int64_t* ovf_list;
+  ulonglong2* spill;  // [64 - C][resident threads]: pool entries beyond the shared ones
 };
 
 // Price the queued regions (one per lane) and add each term to its owner's
@@ -109,6 +109,151 @@ __device__ __forceinline__ void an_flush(const ulonglong2* qx, const uint8_t* qo
   __syncwarp();
 }
 
+// 32-bit shared-memory accesses (the addresses stay in registers instead of
+// being rebuilt from the generic window on every access)
+__device__ __forceinline__ uint32_t lds_u8(uint32_t a) {
+  uint32_t v;
+  asm volatile("ld.shared.u8 %0, [%1];" : "=r"(v) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ void sts_u8(uint32_t a, uint32_t v) {
+  asm volatile("st.shared.u8 [%0], %1;" ::"r"(a), "r"(v));
+}
+__device__ __forceinline__ int2 lds_s32x2(uint32_t a) {
+  int2 v;
+  asm volatile("ld.shared.v2.s32 {%0, %1}, [%2];" : "=r"(v.x), "=r"(v.y) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ X128 lds_x(uint32_t a) {
+  X128 v;
+  asm volatile("ld.shared.v2.u64 {%0, %1}, [%2];" : "=l"(v.lo), "=l"(v.hi) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ void sts_x(uint32_t a, const X128& v) {
+  asm volatile("st.shared.v2.u64 [%0], {%1, %2};" ::"r"(a), "l"(v.lo), "l"(v.hi));
+}
+
+// Per-lane walk state and the slot tables it reads.
+struct AnLane {
+  uint32_t lab;    // shared address of this lane's label for slot 0 (slot s at +4 s)
+  uint32_t pool;   // shared address of this lane's pool entry 0 (entry e < C at + e * 16 T)
+  ulonglong2* spill;  // this lane's global entries (entry e >= C at [(e - C) * stride])
+  int64_t spill_stride;
+  uint32_t wtab;   // shared address of the warp's slot table (slot s at + 8 s)
+  uint64_t act;    // occupied slots
+  uint64_t pfree;  // free pool entries (64: C in shared memory, the rest spilled)
+  bool ovf;
+  X128 total;      // genome-dependent part of the cost (two's complement)
+};
+
+template <int C>
+__device__ __forceinline__ X128 pool_ld(const AnLane& L, uint32_t e) {
+  if (e < (uint32_t)C) return lds_x(L.pool + e * (16 * AN_THREADS));
+  const ulonglong2 v = L.spill[(int64_t)(e - C) * L.spill_stride];
+  return {v.x, v.y};
+}
+template <int C>
+__device__ __forceinline__ void pool_st(const AnLane& L, uint32_t e, const X128& v) {
+  if (e < (uint32_t)C)
+    sts_x(L.pool + e * (16 * AN_THREADS), v);
+  else
+    L.spill[(int64_t)(e - C) * L.spill_stride] = make_ulonglong2(v.lo, v.hi);
+}
+
+// Back edge to slot b of the new unit whose component is anchored at A:
+// find b's anchor, merge the two components at the later-ending anchor.
+// Every lane runs the same predicated sequence.
+template <int C>
+__device__ __forceinline__ void an_merge(AnLane& L, const AnArgs& a, bool need, int b, int& A) {
+  int x = b;
+  uint32_t lx = need ? lds_u8(L.lab + 4 * b) : L_ANCHOR;
+  if (!(lx & L_ANCHOR)) {
+    x = (int)lx;
+    lx = lds_u8(L.lab + 4 * x);
+  }
+  if (!(lx & L_ANCHOR)) {
+    x = (int)lx;
+    lx = lds_u8(L.lab + 4 * x);
+  }
+  while (__any_sync(0xffffffffu, !(lx & L_ANCHOR))) {  // rare deeper chains
+    if (!(lx & L_ANCHOR)) {
+      x = (int)lx;
+      lx = lds_u8(L.lab + 4 * x);
+    }
+  }
+  if (x != b) sts_u8(L.lab + 4 * b, (uint32_t)x);  // path compression (x == b when !need)
+  const bool mrg = need && x != A;
+  const uint32_t lA = lds_u8(L.lab + 4 * A);
+  const int2 tA = lds_s32x2(L.wtab + 8 * A), tX = lds_s32x2(L.wtab + 8 * x);
+  const bool keepA = tA.y >= tX.y;  // the later-ending anchor survives
+  const int Wn = keepA ? A : x, Xn = keepA ? x : A;
+  const uint32_t lW = keepA ? lA : lx, lX = keepA ? lx : lA;
+  const int pW = keepA ? tA.x : tX.x, pX = keepA ? tX.x : tA.x;
+  const bool mW = (lW & L_MERGED) != 0u, mX = (lX & L_MERGED) != 0u;
+  const uint32_t eW = lW & 63u, eX = lX & 63u;
+  // merged components: their pool sums; one-unit components: the unit's
+  // replacement sum, and its own kernel term leaves the total now
+  X128 sW = {0ull, 0ull}, sX = {0ull, 0ull}, oW = {0ull, 0ull}, oX = {0ull, 0ull};
+  if (mrg && mW) sW = pool_ld<C>(L, eW);
+  if (mrg && !mW) {
+    sW = ld_x(a.repc + 2 * pW);
+    oW = ld_x(a.repc + 2 * pW + 1);
+  }
+  if (mrg && mX) sX = pool_ld<C>(L, eX);
+  if (mrg && !mX) {
+    sX = ld_x(a.repc + 2 * pX);
+    oX = ld_x(a.repc + 2 * pX + 1);
+  }
+  x_add(sW, sX);
+  x_add(oW, oX);
+  x_sub(L.total, oW);
+  const bool alloc = mrg && !mW && !mX;
+  const uint32_t e = mW ? eW : (mX ? eX : (L.pfree ? (uint32_t)(__ffsll((long long)L.pfree) - 1) : 0u));
+  L.ovf |= alloc && L.pfree == 0ull;  // all 64 entries live: the genome goes to the fallback kernel
+  if (alloc) L.pfree &= L.pfree - 1ull;
+  if (mrg && mW && mX) L.pfree |= 1ull << eX;
+  if (mrg) {
+    pool_st<C>(L, e, sW);
+    sts_u8(L.lab + 4 * Wn, L_ANCHOR | L_MERGED | e);
+    sts_u8(L.lab + 4 * Xn, (uint32_t)Wn);
+    A = Wn;
+  }
+}
+
+// Release of slot e (uniform): a leaving anchor closes its region -- a
+// one-unit region adds its precomputed term, a merged one is queued.
+template <int C>
+__device__ __forceinline__ void an_close(AnLane& L, const AnArgs& a, int e, int lane, ulonglong2* qx,
+                                         uint8_t* qown, int& qn, unsigned long long* tacc, bool& inexact) {
+  const bool was = (L.act >> e) & 1ull;
+  if (!__any_sync(0xffffffffu, was)) return;
+  L.act &= ~(1ull << e);
+  const uint32_t le = lds_u8(L.lab + 4 * e);
+  const bool anc = was && (le & L_ANCHOR);
+  const bool emit = anc && (le & L_MERGED);
+  if (anc && !emit) x_add(L.total, ld_x(a.term1 + lds_s32x2(L.wtab + 8 * e).x));
+  X128 ev = {0ull, 0ull};
+  if (emit) {
+    ev = pool_ld<C>(L, le & 63u);
+    L.pfree |= 1ull << (le & 63u);
+  }
+  // closed multi-unit regions of all lanes are priced 32 at a time
+  const unsigned closing = __ballot_sync(0xffffffffu, emit);
+  if (closing) {
+    const int cnt = __popc(closing);
+    if (qn + cnt > AN_QCAP) {
+      an_flush(qx, qown, qn, lane, a, tacc, inexact);
+      qn = 0;
+    }
+    if (emit) {
+      const int at = qn + __popc(closing & ((1u << lane) - 1u));
+      qx[at] = make_ulonglong2(ev.lo, ev.hi);
+      qown[at] = (uint8_t)lane;
+    }
+    qn += cnt;
+  }
+}
+
 template <int C>
 __global__ void __launch_bounds__(AN_THREADS, 8)
 fitness_anchor_kernel(AnArgs a, const uint64_t* __restrict__ pop, int64_t n, double* __restrict__ fit) {
@@ -121,12 +266,16 @@ fitness_anchor_kernel(AnArgs a, const uint64_t* __restrict__ pop, int64_t n, dou
   uint8_t* qown_all = reinterpret_cast<uint8_t*>(wtab_all + W * 64);  // [W][QCAP]
   uint8_t* LAB = qown_all + W * AN_QCAP;                             // [T / 4][Fp][4]
   const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
-  ulonglong2* pl = pool + t;                                   // pl[e * T]
-  uint8_t* lab = LAB + (t >> 2) * a.Fp * 4 + (t & 3);          // lab[s * 4]
   ulonglong2* qx = qx_all + warp * AN_QCAP;
   uint8_t* qown = qown_all + warp * AN_QCAP;
   unsigned long long* tacc = tacc_all + warp * 64;
   int2* wtab = wtab_all + warp * 64;
+  AnLane L;
+  L.lab = (uint32_t)__cvta_generic_to_shared(LAB + (t >> 2) * a.Fp * 4 + (t & 3));
+  L.pool = (uint32_t)__cvta_generic_to_shared(pool + t);
+  L.wtab = (uint32_t)__cvta_generic_to_shared(wtab);
+  L.spill_stride = (int64_t)gridDim.x * T;
+  L.spill = a.spill + (int64_t)blockIdx.x * T + t;
   tacc[2 * lane] = tacc[2 * lane + 1] = 0ull;
   __syncwarp();
   bool inexact = false;
@@ -138,119 +287,64 @@ fitness_anchor_kernel(AnArgs a, const uint64_t* __restrict__ pop, int64_t n, dou
     bool dead = !in_range;
     for (int32_t j = 0; j < a.n_infeas; ++j)
       dead |= (__ldg(gen + __ldg(a.infeas_word + j)) & __ldg(a.infeas_mask + j)) != 0ull;
-    uint64_t act = 0ull;
-    uint32_t pfree = C >= 32 ? 0xffffffffu : ((1u << C) - 1u);
-    bool ovf = false;
-    X128 total = {0ull, 0ull};
+    L.act = 0ull;
+    L.pfree = ~0ull;
+    L.ovf = false;
+    L.total = {0ull, 0ull};
     int qn = 0;
     int32_t cur_w = -1;
-    uint64_t word = 0ull, next_word = a.words > 0 ? __ldg(gen) : 0ull;
+    uint64_t word = 0ull;
     uint4 nh = __ldg(reinterpret_cast<const uint4*>(a.step));
-    X128 noff = ld_x(a.off);
     for (int32_t p = 0; p < a.M; ++p) {
       const uint4 h = nh;
-      const X128 off = noff;
-      if (p + 1 < a.M) {
-        nh = __ldg(reinterpret_cast<const uint4*>(a.step + p + 1));
-        noff = ld_x(a.off + p + 1);
-      }
+      if (p + 1 < a.M) nh = __ldg(reinterpret_cast<const uint4*>(a.step + p + 1));
       const uint32_t bitf = h.x & 0xFFFFFFu;
       const int S = (int)((h.x >> 24) & 63u);
-      const bool lng = (h.x >> 31) != 0u;
       if (lane == 0) wtab[S] = make_int2(p, (int32_t)h.y);
       bool on = !dead;
       if (bitf != 0xFFFFFFu) {
         const int32_t wi = (int32_t)(bitf >> 6);
-        if (wi != cur_w) {  // warp uniform; the next word is loaded one word ahead
-          word = wi == cur_w + 1 ? next_word : __ldg(gen + wi);
-          next_word = wi + 1 < a.words ? __ldg(gen + wi + 1) : 0ull;
+        if (wi != cur_w) {  // warp uniform
+          word = dead ? 0ull : __ldg(gen + wi);
           cur_w = wi;
         }
-        on = on && ((word >> (bitf & 63u)) & 1ull);
+        on = (word >> (bitf & 63u)) & 1ull;
       }
       __syncwarp();
       if (on) {
-        x_sub(total, off);
-        act |= 1ull << S;
-        lab[S * 4] = (uint8_t)L_ANCHOR;
+        L.act |= 1ull << S;
+        sts_u8(L.lab + 4 * S, L_ANCHOR);
       }
-      const int nb = lng ? (int)(h.z & 0xFFFFu) : (int)(h.z & 7u);
-      const int ne = lng ? (int)(h.z >> 16) : (int)((h.z >> 3) & 7u);
       int A = S;  // anchor of the new unit's component
-      for (int j = 0; j < nb; ++j) {
-        const int b = lng ? (int)__ldg(a.lists + h.w + j) : (int)((h.z >> (6 + 6 * j)) & 63u);
-        if (!on || !((act >> b) & 1ull)) continue;
-        int x = b;
-        uint32_t lx = lab[x * 4];
-        while (!(lx & L_ANCHOR)) {
-          x = (int)lx;
-          lx = lab[x * 4];
-        }
-        if (x != b) lab[b * 4] = (uint8_t)x;  // path compression
-        if (x == A) continue;
-        const uint32_t lA = lab[A * 4];
-        const int2 tA = wtab[A], tX = wtab[x];
-        const bool keepA = tA.y >= tX.y;  // the later-ending anchor survives
-        const int Wn = keepA ? A : x, Xn = keepA ? x : A;
-        const uint32_t lW = keepA ? lA : lx, lX = keepA ? lx : lA;
-        X128 sW = (lW & L_MERGED) ? X128{pl[(lW & 63u) * T].x, pl[(lW & 63u) * T].y}
-                                  : ld_x(a.repc + (keepA ? tA.x : tX.x));
-        const X128 sX = (lX & L_MERGED) ? X128{pl[(lX & 63u) * T].x, pl[(lX & 63u) * T].y}
-                                        : ld_x(a.repc + (keepA ? tX.x : tA.x));
-        x_add(sW, sX);
-        int e;
-        if (lW & L_MERGED) {
-          e = (int)(lW & 63u);
-          if (lX & L_MERGED) pfree |= 1u << (lX & 63u);
-        } else if (lX & L_MERGED) {
-          e = (int)(lX & 63u);
-        } else if (pfree) {
-          e = __ffs(pfree) - 1;
-          pfree &= pfree - 1u;
-        } else {
-          ovf = true;  // pool exhausted: the genome goes to the fallback kernel
-          e = 0;
-        }
-        pl[e * T] = make_ulonglong2(sW.lo, sW.hi);
-        lab[Wn * 4] = (uint8_t)(L_ANCHOR | L_MERGED | (uint32_t)e);
-        lab[Xn * 4] = (uint8_t)Wn;
-        A = Wn;
-      }
-      for (int j = 0; j < ne; ++j) {
-        const int e = lng ? (int)__ldg(a.lists + h.w + nb + j) : (int)((h.w >> (6 * j)) & 63u);
-        bool emit = false;
-        ulonglong2 ev = make_ulonglong2(0ull, 0ull);
-        if ((act >> e) & 1ull) {
-          act &= ~(1ull << e);
-          const uint32_t le = lab[e * 4];
-          if (le & L_ANCHOR) {  // the anchor leaves: its region is complete
-            if (le & L_MERGED) {
-              emit = true;
-              ev = pl[(le & 63u) * T];
-              pfree |= 1u << (le & 63u);
-            } else {
-              x_add(total, ld_x(a.term1 + wtab[e].x));
-            }
+      if (!(h.x >> 31)) {
+        // short lists (<= 4 back, <= 4 end slots) in the record: unrolled,
+        // every guard warp uniform
+        const int nb = (int)(h.z & 7u), ne = (int)((h.z >> 3) & 7u);
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          if (j < nb) {
+            const int b = (int)((h.z >> (6 + 6 * j)) & 63u);
+            const bool need = on && ((L.act >> b) & 1ull);
+            if (__any_sync(0xffffffffu, need)) an_merge<C>(L, a, need, b, A);
           }
         }
-        // closed multi-unit regions of all lanes are priced 32 at a time
-        const unsigned closing = __ballot_sync(0xffffffffu, emit);
-        if (closing) {
-          const int cnt = __popc(closing);
-          if (qn + cnt > AN_QCAP) {
-            an_flush(qx, qown, qn, lane, a, tacc, inexact);
-            qn = 0;
-          }
-          if (emit) {
-            const int at = qn + __popc(closing & ((1u << lane) - 1u));
-            qx[at] = ev;
-            qown[at] = (uint8_t)lane;
-          }
-          qn += cnt;
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+          if (j < ne) an_close<C>(L, a, (int)((h.w >> (6 * j)) & 63u), lane, qx, qown, qn, tacc, inexact);
+      } else {
+        const int nb = (int)(h.z & 0xFFFFu), ne = (int)(h.z >> 16);
+        for (int j = 0; j < nb; ++j) {
+          const int b = (int)__ldg(a.lists + h.w + j);
+          const bool need = on && ((L.act >> b) & 1ull);
+          if (__any_sync(0xffffffffu, need)) an_merge<C>(L, a, need, b, A);
         }
+        for (int j = 0; j < ne; ++j)
+          an_close<C>(L, a, (int)__ldg(a.lists + h.w + nb + j), lane, qx, qown, qn, tacc, inexact);
       }
     }
     an_flush(qx, qown, qn, lane, a, tacc, inexact);
+    X128 total = L.total;
+    const bool ovf = L.ovf;
     x_add(total, X128{tacc[2 * lane], tacc[2 * lane + 1]});
     tacc[2 * lane] = tacc[2 * lane + 1] = 0ull;
     __syncwarp();
@@ -302,7 +396,6 @@ int launch_anchor_t(cb_es_plan* p, const uint64_t* d_pop, int64_t n, double* d_f
   const fx192 ex = fx_shr(p->eps, p->anchor_shift);
   a.eps = {ex.w[0], ex.w[1]};
   a.step = reinterpret_cast<const AStep*>(p->d_astep.p);
-  a.off = reinterpret_cast<const ulonglong2*>(p->d_aoff.p);
   a.repc = reinterpret_cast<const ulonglong2*>(p->d_arepc.p);
   a.term1 = reinterpret_cast<const ulonglong2*>(p->d_aterm.p);
   a.lists = p->d_alists.p;
@@ -314,16 +407,18 @@ int launch_anchor_t(cb_es_plan* p, const uint64_t* d_pop, int64_t n, double* d_f
   a.ovf_list = p->d_ovf_list.p;
   const int64_t want = (n + AN_THREADS - 1) / AN_THREADS;
   const int64_t grid = std::min<int64_t>(want, (int64_t)per_sm * cb_sm_count());
+  const size_t spill = (size_t)(64 - C) * grid * AN_THREADS * 2;  // uint64 words
+  DBuf<uint64_t>* sp;
+  {
+    std::lock_guard<std::mutex> lock(p->aspill_mu);
+    auto& slot = p->aspill[stream];
+    if (!slot) slot.reset(new DBuf<uint64_t>());
+    sp = slot.get();
+  }
+  if (sp->n < spill) CB_CUDA_TRY(sp->alloc(spill));
+  a.spill = reinterpret_cast<ulonglong2*>(sp->p);
   fitness_anchor_kernel<C><<<(unsigned)grid, AN_THREADS, smem, stream>>>(a, d_pop, n, d_fit);
   CB_CUDA_TRY(cudaGetLastError());
-  if (p->pool_auto) {  // let the next launch see this one's overflow count
-    if (!p->h_ovf) {
-      CB_CUDA_TRY(cudaHostAlloc((void**)&p->h_ovf, sizeof(int32_t), cudaHostAllocDefault));
-      *p->h_ovf = 0;
-    }
-    CB_CUDA_TRY(cudaMemcpyAsync(p->h_ovf, p->d_ovf_count.p, sizeof(int32_t), cudaMemcpyDeviceToHost, stream));
-    p->last_anchor_n = n;
-  }
   // genomes that ran out of pool entries: warp-per-genome kernel over the list
   return launch_fitness_wide_list(p, d_pop, n, d_fit, p->d_ovf_list.p, p->d_ovf_count.p, stream);
 }
@@ -387,7 +482,10 @@ int build_anchor_plan(cb_es_plan* P) {
     cnt[p] = r.cnt;
   }
   std::vector<AStep> steps(M);
-  std::vector<uint64_t> off((size_t)M * 2), repc((size_t)M * 2), term((size_t)M * 2);
+  // per unit: [rep | cnt << 108, off] (read when it joins a merged region,
+  // whose members' own kernel terms leave the total then) and term1 - off
+  // (a one-unit region replaces the unit's own term by its region term)
+  std::vector<uint64_t> repc((size_t)M * 4), term((size_t)M * 2);
   std::vector<uint8_t> lists;
   for (int32_t p = 0; p < M && P->anchor_wide_ok; ++p) {
     const UnitRec& r = P->prog[p];
@@ -407,11 +505,13 @@ int build_anchor_plan(cb_es_plan* P) {
       for (int j = 0; j < r.nend; ++j) lists.push_back(P->prog_slots[r.end_off + j]);
     }
     steps[p] = h;
-    const fx192 xo = fx_shr(r.off, lo), xr = fx_shr(r.rep, lo), xt = fx_shr(r.term1, lo);
-    off[2 * p] = xo.w[0];
-    off[2 * p + 1] = xo.w[1];
-    repc[2 * p] = xr.w[0];
-    repc[2 * p + 1] = xr.w[1] | ((uint64_t)r.cnt << 44);
+    const fx192 xo = fx_shr(r.off, lo), xr = fx_shr(r.rep, lo);
+    fx192 xt = fx_shr(r.term1, lo);
+    fx_sub(xt, xo);  // two's complement in the low 128 bits
+    repc[4 * p] = xr.w[0];
+    repc[4 * p + 1] = xr.w[1] | ((uint64_t)r.cnt << 44);
+    repc[4 * p + 2] = xo.w[0];
+    repc[4 * p + 3] = xo.w[1];
     term[2 * p] = xt.w[0];
     term[2 * p + 1] = xt.w[1];
   }
@@ -467,7 +567,7 @@ int build_anchor_plan(cb_es_plan* P) {
   if (P->anchor_wide_ok &&
       ((e = P->d_astep.upload(reinterpret_cast<const uint8_t*>(steps.data()), steps.size() * sizeof(AStep))) !=
            cudaSuccess ||
-       (e = P->d_aoff.upload(off)) != cudaSuccess || (e = P->d_arepc.upload(repc)) != cudaSuccess ||
+       (e = P->d_arepc.upload(repc)) != cudaSuccess ||
        (e = P->d_aterm.upload(term)) != cudaSuccess || (e = P->d_alists.upload(lists)) != cudaSuccess ||
        (e = P->d_an_infeas_word.upload(iw)) != cudaSuccess ||
        (e = P->d_an_infeas_mask.upload(im)) != cudaSuccess)) {
@@ -481,22 +581,11 @@ int build_anchor_plan(cb_es_plan* P) {
 int launch_fitness_anchor(cb_es_plan* p, const uint64_t* d_pop, int64_t n, double* d_fit,
                           cudaStream_t stream) {
   if (!p->anchor_wide_ok) return launch_fitness_wide(p, d_pop, n, d_fit, stream);
-  int C = p->pool_entries;
-  if (p->pool_auto) {
-    // 8 entries fit 8 CTAs of 128 threads per SM on a 36-slot program; when
-    // more than 1 % of the previous launch's genomes overflowed (dense
-    // populations) use 12, above 5 % 16.  The count is read without
-    // synchronising: it is the last launch that finished, a hint only --
-    // results never depend on C.
-    const volatile int32_t* h = p->h_ovf;
-    if (h && p->last_anchor_n > 0) {
-      const int64_t pct = (int64_t)*h * 100 / p->last_anchor_n;
-      p->auto_pool = pct >= 5 ? 16 : (pct >= 1 ? 12 : 8);
-    }
-    C = std::min(p->pool_entries, p->auto_pool);
-  }
+  // C pool entries per lane live in shared memory, the other 64 - C in a
+  // global spill area (touched only by genomes with more live merged
+  // components): 8 keeps 32 warps resident per SM on a 36-slot program
+  const int C = p->pool_entries;
   if (C <= 8) return launch_anchor_t<8>(p, d_pop, n, d_fit, stream);
   if (C <= 12) return launch_anchor_t<12>(p, d_pop, n, d_fit, stream);
-  if (C <= 16) return launch_anchor_t<16>(p, d_pop, n, d_fit, stream);
-  return launch_anchor_t<24>(p, d_pop, n, d_fit, stream);
+  return launch_anchor_t<16>(p, d_pop, n, d_fit, stream);
 }

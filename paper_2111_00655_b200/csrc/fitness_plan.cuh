@@ -1,5 +1,9 @@
 // Fitness plan: the host-built, genome-independent part of graph-level pricing.
 #pragma once
+#include <map>
+#include <memory>
+#include <mutex>
+
 #include "cb_internal.cuh"
 
 // One record per dynamic unit of the frontier program (thread-per-genome
@@ -77,20 +81,17 @@ struct cb_es_plan {
   DBuf<int32_t> d_acnt;     // [M]
   bool anchor_wide_ok = false;  // packed-sum anchor walk usable (span and counts fit)
   DBuf<uint8_t> d_astep;        // AStep[M] 16-byte step records
-  DBuf<uint64_t> d_aoff, d_arepc, d_aterm;  // [M][2]: off, rep | cnt << 108, one-unit term (X)
+  DBuf<uint64_t> d_arepc, d_aterm;  // [M][4] rep | cnt << 108, off; [M][2] term1 - off (X)
   DBuf<uint8_t> d_alists;       // long back / end slot lists
   DBuf<int32_t> d_an_infeas_word;  // genome words holding infeasible bits, and their masks
   DBuf<uint64_t> d_an_infeas_mask;
+  // pool entries beyond the shared ones, per resident thread -- one area per
+  // stream, so launches on different streams (the host pipeline) never share
+  std::map<cudaStream_t, std::unique_ptr<DBuf<uint64_t>>> aspill;
+  std::mutex aspill_mu;
   int32_t pool_entries = 16;
-  // pool_auto: the pool size follows the overflow rate of earlier launches,
-  // read back asynchronously into pinned memory (never synchronised on)
-  bool pool_auto = true;
-  int32_t* h_ovf = nullptr;       // pinned: overflow count of the last finished launch
-  int64_t last_anchor_n = 0;
-  int32_t auto_pool = 8;
   cudaStream_t host_stream = nullptr;  // single-chunk cb_fitness_host calls
   ~cb_es_plan() {
-    if (h_ovf) cudaFreeHost(h_ovf);
     if (host_stream) cudaStreamDestroy(host_stream);
   }
   // finite-state walk (fitness_fsm.cu, <= 8 slots): per-step headers and

@@ -1,14 +1,14 @@
 // Graph container, host-side structural analysis and device upload.
 //
 // Mirrors the structural queries of tensorplace/graph.py: deterministic
-// topological order with smallest-id tie-break (:345-364), longest-path depth
-// (:366-371) and immediate post-dominators relative to a virtual sink that
-// joins all outputs (:413-444).  The reference materialises full
+// topological order with smallest-id tie-break (:156-175), longest-path depth
+// (:177-182) and immediate post-dominators relative to a virtual sink that
+// joins all outputs (:224-255).  The reference materialises full
 // post-dominator sets (quadratic); here the post-dominator tree is built
 // directly by intersecting successor paths in reverse topological order
 // (Cooper-Harvey-Kennedy on the reversed DAG), which yields the same
 // immediate post-dominator: the nearest strict post-dominator is exactly the
-// one with the smallest topological index (graph.py:441).
+// one with the smallest topological index (graph.py:249).
 #include <algorithm>
 #include <cstring>
 #include <map>

@@ -1,13 +1,13 @@
 // Backend pattern matcher: every (anchor node, candidate pattern) pair.
 //
-// Semantics follow tensorplace/matching.py:451-501 (match_at): the pattern
+// Semantics follow tensorplace/matching.py:53-103 (match_at): the pattern
 // root binds the anchor, pattern argument i descends to the producer of the
 // bound node's i-th input, wildcards bind edges only, a zero-argument op
 // pattern accepts any arity, two positions may bind one node only when their
 // sub-patterns are structurally equal, and every non-root bound node must be
 // neither a graph output nor consumed outside the match.  Candidate patterns
 // per anchor are the registry's root index in registration order
-// (tensorplace/registry.py:487-497).
+// (tensorplace/registry.py:135-145).
 //
 // Device layout: one warp per anchor (group), one lane per candidate
 // pattern.  Pass 1 decides every pair and counts members; warp ballots give

@@ -1,6 +1,6 @@
 // Kernel cost of every match under the simulated profiles.
 //
-// tensorplace/cost.py:121-136: node cost = coeff[op] * volume + overhead[op]
+// tensorplace/cost.py:121-138: node cost = coeff[op] * volume + overhead[op]
 // (two separately rounded IEEE operations -- no FMA contraction), kernel cost
 // = fsum(node costs) * fusion_discount ** (n - 1).  The power table is
 // computed by the host with Python's own float pow so the product is

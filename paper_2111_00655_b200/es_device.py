@@ -5,7 +5,7 @@ Each rank owns a population shard of packed genomes (uint64 rows, same bit
 layout as the reference's genome).  A generation is: the rank's best row
 (device argmin) -> all-gather of every rank's best fitness and genome over
 NCCL (NVLink) -> the global best becomes row 0 of every rank's next shard
-(elitism, as in tensorplace/evolution.py:416-418) -> tournament selection,
+(elitism, as in tensorplace/evolution.py:237-240) -> tournament selection,
 two-point crossover and mutation of the remaining rows from the rank's own
 shard (cb_es_breed) -> batched fitness of the new shard (cb_fitness_device).
 No host synchronisation happens inside a generation; the per-generation best
