@@ -257,6 +257,7 @@ def run_mine(args) -> None:
     kt = es.kernel_times_ms()
     mean = lambda xs: sum(xs) / len(xs) if xs else 0.0
     gen_ms, fit_ms, breed_ms = mean(kt["generation"]), mean(kt["fitness"]), mean(kt["breed"])
+    xchg_ms = mean(kt["exchange"])
     best_cost, _ = es.best()
     del es
     torch.cuda.empty_cache()
@@ -277,12 +278,12 @@ def run_mine(args) -> None:
     barrier()
     del host
 
-    vals = torch.tensor([ms, e2e_s, gen_ms, fit_ms, breed_ms, search_t["wall_s"]],
+    vals = torch.tensor([ms, e2e_s, gen_ms, fit_ms, breed_ms, search_t["wall_s"], xchg_ms],
                         dtype=torch.float64, device=dev)
     if world > 1:
         import torch.distributed as dist
         dist.all_reduce(vals, op=dist.ReduceOp.MAX)
-    ms, e2e_s, gen_ms, fit_ms, breed_ms, search_s = vals.tolist()
+    ms, e2e_s, gen_ms, fit_ms, breed_ms, search_s, xchg_ms = vals.tolist()
     if rank != 0:
         if world > 1:
             import torch.distributed as dist
@@ -341,7 +342,9 @@ def run_mine(args) -> None:
                    "es_generations": args.search_generations, "dp_cost_ms": res.cost_ms,
                    "rounding_window_safe": res.device["rounding_window_safe"],
                    "best_cost_ms_after_timed_steps": best_cost},
-        "kernels_ms": {"generation": gen_ms, "fitness": fit_ms, "breed": breed_ms},
+        "kernels_ms": {"generation": gen_ms, "fitness": fit_ms, "breed": breed_ms,
+                       **({"exchange": xchg_ms, "exchange_us_per_generation": 1e3 * xchg_ms}
+                          if world > 1 else {})},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic, "kernel": kernel_name,
                      "peak_source": peak_src,

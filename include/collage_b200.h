@@ -172,6 +172,10 @@ typedef struct {
  * kernel in pop order of its root. */
 int cb_dp_solve(cb_graph* g, cb_matches* m, double epsilon,
                 int32_t* kernel_match, cb_dp_result* res);
+/* cb_dp_solve with every launch, copy and event on `stream` (cudaStream_t
+ * as void*, NULL = legacy default stream); returns after the stream work. */
+int cb_dp_solve_stream(cb_graph* g, cb_matches* m, double epsilon, int32_t* kernel_match,
+                       cb_dp_result* res, void* stream);
 
 /* Graph-level cost of one arbitrary placement (host code of the native
  * runtime; populations go through cb_fitness_*).  Kernels are given as node
@@ -212,6 +216,7 @@ typedef struct {
                             2: also the packed anchor kernel (<= 8 slots) */
   int32_t fsm_transitions; /* transitions of the finite-state program (0 = none) */
   int32_t fsm_entry_bytes; /* transition layout: 8 or 16 (+ shared delta table), or 32 */
+  int32_t onwalk;        /* 1: the ON-unit walk applies (<= 64 slots, packed 128-bit sums) */
 } cb_es_plan_info;
 int cb_es_plan_query(const cb_es_plan* p, cb_es_plan_info* info);
 /* Evaluation path: -1 automatic (the finite-state walk when its table is
@@ -283,6 +288,17 @@ int cb_es_generation(cb_es_plan* p, const uint64_t* d_parents,
 int cb_argmin_elite(const double* d_fit, int64_t n, const uint64_t* d_pop,
                     int32_t words, int64_t* d_idx, double* d_val,
                     uint64_t* d_elite, double* d_history_slot, void* stream);
+
+/* Sharded search exchange (tensorplace/evolution.py:244-248 best tracking,
+ * across ranks).  cb_elite_record: argmin of the rank's fitness and its row
+ * as one record d_record[0 .. words] = [fitness bits, row].  After an
+ * all-gather of the records ([world][1 + words]), cb_elite_pick writes the
+ * lowest-fitness row (first rank on ties) to d_elite, its fitness to
+ * *d_elite_val and, if given, to *d_history_slot. */
+int cb_elite_record(const double* d_fit, int64_t n, const uint64_t* d_pop, int32_t words,
+                    int64_t* d_idx, double* d_val, uint64_t* d_record, void* stream);
+int cb_elite_pick(const uint64_t* d_records, int32_t world, int32_t words, uint64_t* d_elite,
+                  double* d_elite_val, double* d_history_slot, void* stream);
 /* 1 when cb_es_generation runs fused for this plan (and path setting). */
 int cb_es_generation_fused(const cb_es_plan* p);
 /* Index of the smallest fitness (first on ties) -> d_idx[0]; value ->

@@ -73,6 +73,7 @@ class ESPlanInfo(ctypes.Structure):
         ("packed_labels", c_int32),
         ("fsm_transitions", c_int32),
         ("fsm_entry_bytes", c_int32),
+        ("onwalk", c_int32),
     ]
 
 
@@ -108,6 +109,8 @@ _SIGNATURES = {
                                  _P_U8, c_int32, _P_F64, _P_F64, _P_I8]),
     "cb_matches_set_costs": (c_int, [c_void_p, _P_F64]),
     "cb_dp_solve": (c_int, [c_void_p, c_void_p, c_double, _P_I32, POINTER(DPResultStruct)]),
+    "cb_dp_solve_stream": (c_int, [c_void_p, c_void_p, c_double, _P_I32, POINTER(DPResultStruct),
+                                   c_void_p]),
     "cb_placement_cost_graphlevel": (c_int, [c_void_p, c_int32, _P_I32, _P_I32, _P_I32, _P_F64,
                                              c_int32, _P_U8, _P_F64, _P_F64, c_double, _P_F64]),
     "cb_es_plan_create": (c_int, [c_void_p, c_void_p, c_int32, _P_I32, c_int32, _P_U8, _P_F64,
@@ -128,6 +131,9 @@ _SIGNATURES = {
                                  c_void_p, c_int64, c_uint64, c_uint64, c_uint64, c_int32,
                                  c_double, c_void_p]),
     "cb_es_generation_fused": (c_int, [c_void_p]),
+    "cb_elite_record": (c_int, [c_void_p, c_int64, c_void_p, c_int32, c_void_p, c_void_p, c_void_p,
+                                 c_void_p]),
+    "cb_elite_pick": (c_int, [c_void_p, c_int32, c_int32, c_void_p, c_void_p, c_void_p, c_void_p]),
     "cb_argmin_elite": (c_int, [c_void_p, c_int64, c_void_p, c_int32, c_void_p, c_void_p, c_void_p,
                                 c_void_p, c_void_p]),
     "cb_argmin": (c_int, [c_void_p, c_int64, c_void_p, c_void_p, c_void_p]),

@@ -406,6 +406,12 @@ static bool rounding_window_safe(const fx192& total, const fx192& gap) {
 
 extern "C" int cb_dp_solve(cb_graph* g, cb_matches* m, double epsilon, int32_t* kernel_match,
                            cb_dp_result* res) {
+  return cb_dp_solve_stream(g, m, epsilon, kernel_match, res, nullptr);
+}
+
+extern "C" int cb_dp_solve_stream(cb_graph* g, cb_matches* m, double epsilon, int32_t* kernel_match,
+                                  cb_dp_result* res, void* stream) {
+  cudaStream_t strm = (cudaStream_t)stream;
   CB_ARG_CHECK(g && m && res, "cb_dp_solve: null argument");
   CB_ARG_CHECK(m->by_root && m->n_groups == g->n, "cb_dp_solve: matches must come from cb_match_all");
   if (!m->costs_set) {
@@ -454,9 +460,9 @@ extern "C" int cb_dp_solve(cb_graph* g, cb_matches* m, double epsilon, int32_t* 
   CB_CUDA_TRY(stack.alloc((size_t)n + 1));
   CB_CUDA_TRY(counters.alloc(4));
   CB_CUDA_TRY(d_level_ptr.upload(g->level_ptr));
-  CB_CUDA_TRY(cudaMemset(lock.p, 0, sizeof(int)));
-  CB_CUDA_TRY(cudaMemset(counters.p, 0, 4 * sizeof(unsigned long long)));
-  CB_CUDA_TRY(cudaMemset(feas.p, 0, n));
+  CB_CUDA_TRY(cudaMemsetAsync(lock.p, 0, sizeof(int), strm));
+  CB_CUDA_TRY(cudaMemsetAsync(counters.p, 0, 4 * sizeof(unsigned long long), strm));
+  CB_CUDA_TRY(cudaMemsetAsync(feas.p, 0, n, strm));
 
   DPArgs a;
   a.level_nodes = g->d_level_nodes.p;
@@ -479,7 +485,7 @@ extern "C" int cb_dp_solve(cb_graph* g, cb_matches* m, double epsilon, int32_t* 
   cudaEvent_t ev0, ev1;
   cudaEventCreate(&ev0);
   cudaEventCreate(&ev1);
-  cudaEventRecord(ev0);
+  cudaEventRecord(ev0, strm);
   std::vector<LevelSegment> segs = cb_plan_levels(g, 2 * DP_NARROW_WARPS);
   if (cb_smem_claim((const void*)dp_narrow_kernel, DP_STAGE_MAX))
     CB_CUDA_TRY(cudaFuncSetAttribute(dp_narrow_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -504,17 +510,17 @@ extern "C" int cb_dp_solve(cb_graph* g, cb_matches* m, double epsilon, int32_t* 
         st.n_pch = (int32_t)g->pch.size();
         bytes += tab_bytes;
       }
-      dp_narrow_kernel<<<1, DP_NARROW_WARPS * 32, bytes>>>(a, d_level_ptr.p, s.lvl_begin, s.lvl_end, st);
+      dp_narrow_kernel<<<1, DP_NARROW_WARPS * 32, bytes, strm>>>(a, d_level_ptr.p, s.lvl_begin, s.lvl_end, st);
     } else {
       int32_t i0 = g->level_ptr[s.lvl_begin], i1 = g->level_ptr[s.lvl_end];
       int32_t blocks = (i1 - i0 + DP_WIDE_WARPS - 1) / DP_WIDE_WARPS;
-      dp_wide_kernel<<<blocks, DP_WIDE_WARPS * 32>>>(a, i0, i1);
+      dp_wide_kernel<<<blocks, DP_WIDE_WARPS * 32, 0, strm>>>(a, i0, i1);
     }
     CB_CUDA_TRY(cudaGetLastError());
   }
-  dp_total_kernel<<<1, 256>>>(n, g->d_ipdom.p, opt.p, feas.p, regret.p, d_tot.p, d_reg.p,
+  dp_total_kernel<<<1, 256, 0, strm>>>(n, g->d_ipdom.p, opt.p, feas.p, regret.p, d_tot.p, d_reg.p,
                               d_feas_out.p);
-  cudaEventRecord(ev1);
+  cudaEventRecord(ev1, strm);
   CB_CUDA_TRY(cudaEventSynchronize(ev1));
   float ms = 0.f;
   cudaEventElapsedTime(&ms, ev0, ev1);

@@ -11,6 +11,7 @@
 //
 // One warp per child: lane 0 draws, every lane assembles whole uint64 words
 // of the child from the two parents with segment masks (coalesced rows).
+#include <map>
 #include <cub/cub.cuh>
 
 #include "fitness_plan.cuh"
@@ -296,8 +297,12 @@ extern "C" int cb_es_generation_fused(const cb_es_plan* p) { return p && fused_g
 
 // index of the smallest fitness (first on ties) -> *d_idx, value -> *d_val
 static int argmin_to(const double* d_fit, int64_t n, int64_t* d_idx, double* d_val, cudaStream_t s) {
-  static thread_local void* tmp = nullptr;
-  static thread_local size_t tmp_bytes = 0;
+  // CUB scratch per (host thread, device): a process may drive several GPUs
+  static thread_local std::map<int, std::pair<void*, size_t>> scratch;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  void*& tmp = scratch[dev].first;
+  size_t& tmp_bytes = scratch[dev].second;
   size_t bytes = 0;
   CB_CUDA_TRY(cub::DeviceReduce::ArgMin(nullptr, bytes, d_fit, d_val, d_idx, n, s));
   if (bytes > tmp_bytes) {
@@ -337,4 +342,59 @@ extern "C" int cb_argmin(const double* d_fit, int64_t n, int64_t* d_idx, double*
                          void* stream) {
   CB_ARG_CHECK(d_fit && d_idx && d_val && n > 0, "cb_argmin: bad arguments");
   return argmin_to(d_fit, n, d_idx, d_val, (cudaStream_t)stream);
+}
+
+// ---------------------------------------------------------------- elite exchange
+// The sharded search's only exchange step: every rank contributes one record
+// [best fitness bits, best row] (one all-gather), and every rank picks the
+// lowest fitness (first rank on ties) on the device.
+
+__global__ void elite_record_kernel(const int64_t* idx, const double* val, const uint64_t* __restrict__ pop,
+                                    int32_t words, uint64_t* rec) {
+  const int64_t i = *idx;
+  if (threadIdx.x == 0) rec[0] = (uint64_t)__double_as_longlong(*val);
+  for (int32_t w = threadIdx.x; w < words; w += blockDim.x) rec[1 + w] = pop[i * words + w];
+}
+
+__global__ void elite_pick_kernel(const uint64_t* __restrict__ recs, int32_t world, int32_t words,
+                                  uint64_t* elite, double* elite_val, double* hist) {
+  __shared__ int best;
+  if (threadIdx.x == 0) {
+    int b = 0;
+    double bv = __longlong_as_double((long long)recs[0]);
+    for (int r = 1; r < world; ++r) {
+      const double v = __longlong_as_double((long long)recs[(int64_t)r * (1 + words)]);
+      if (v < bv) {
+        b = r;
+        bv = v;
+      }
+    }
+    best = b;
+    *elite_val = bv;
+    if (hist) *hist = bv;
+  }
+  __syncthreads();
+  const uint64_t* row = recs + (int64_t)best * (1 + words) + 1;
+  for (int32_t w = threadIdx.x; w < words; w += blockDim.x) elite[w] = row[w];
+}
+
+extern "C" int cb_elite_record(const double* d_fit, int64_t n, const uint64_t* d_pop, int32_t words,
+                               int64_t* d_idx, double* d_val, uint64_t* d_record, void* stream) {
+  CB_ARG_CHECK(d_fit && d_pop && d_idx && d_val && d_record && n > 0 && words > 0,
+               "cb_elite_record: bad arguments");
+  cudaStream_t s = (cudaStream_t)stream;
+  int rc = argmin_to(d_fit, n, d_idx, d_val, s);
+  if (rc != CB_OK) return rc;
+  elite_record_kernel<<<1, 128, 0, s>>>(d_idx, d_val, d_pop, words, d_record);
+  CB_CUDA_TRY(cudaGetLastError());
+  return CB_OK;
+}
+
+extern "C" int cb_elite_pick(const uint64_t* d_records, int32_t world, int32_t words, uint64_t* d_elite,
+                             double* d_elite_val, double* d_history_slot, void* stream) {
+  CB_ARG_CHECK(d_records && world > 0 && words > 0 && d_elite && d_elite_val, "cb_elite_pick: bad arguments");
+  elite_pick_kernel<<<1, 128, 0, (cudaStream_t)stream>>>(d_records, world, words, d_elite, d_elite_val,
+                                                         d_history_slot);
+  CB_CUDA_TRY(cudaGetLastError());
+  return CB_OK;
 }

@@ -121,6 +121,7 @@ static void build_frontier_program(cb_es_plan* P, int32_t n_elig_units) {
   P->fixed_pos.push_back(M);  // sentinel
   P->prog.resize(M);
   P->prog_slots.clear();
+  P->prog_back_pos.clear();
   for (int32_t p = 0; p < M; ++p) {
     const int32_t u = order[p];
     UnitRec r;
@@ -134,10 +135,16 @@ static void build_frontier_program(cb_es_plan* P, int32_t n_elig_units) {
     r.slot = (uint8_t)slot[p];
     r.back_off = (int32_t)P->prog_slots.size();
     for (int32_t q : nbr[u])
-      if (pos[q] < p) P->prog_slots.push_back((uint8_t)slot[pos[q]]);
+      if (pos[q] < p) {
+        P->prog_slots.push_back((uint8_t)slot[pos[q]]);
+        P->prog_back_pos.push_back(pos[q]);
+      }
     r.nback = (uint8_t)(P->prog_slots.size() - r.back_off);
     r.end_off = (int32_t)P->prog_slots.size();
-    for (int32_t q : ends_at[p]) P->prog_slots.push_back((uint8_t)slot[q]);
+    for (int32_t q : ends_at[p]) {
+      P->prog_slots.push_back((uint8_t)slot[q]);
+      P->prog_back_pos.push_back(-1);
+    }
     r.nend = (uint8_t)(P->prog_slots.size() - r.end_off);
     r.hot.x = (uint32_t)r.bit;
     r.hot.y = (uint32_t)r.slot | ((uint32_t)r.nback << 8) | ((uint32_t)r.nend << 16);
@@ -501,7 +508,8 @@ extern "C" int cb_es_plan_create(cb_graph* g, cb_matches* m, int32_t n_kernels,
     if ((e = P->d_pos_of_bit.upload(P->pos_of_bit)) != cudaSuccess) return fail_cuda(e);
     if ((e = P->d_fixed_pos.upload(P->fixed_pos)) != cudaSuccess) return fail_cuda(e);
   }
-  if ((rc = build_anchor_plan(P)) != CB_OK || (rc = build_fsm_plan(P)) != CB_OK) {
+  if ((rc = build_anchor_plan(P)) != CB_OK || (rc = build_fsm_plan(P)) != CB_OK ||
+      (rc = build_onwalk_plan(P)) != CB_OK) {
     delete P;
     return rc;
   }
@@ -525,6 +533,7 @@ extern "C" int cb_es_plan_query(const cb_es_plan* p, cb_es_plan_info* info) {
   info->frontier_slots = p->F;
   info->seed_cost = p->seed_cost;
   info->window_shift = p->anchor_ok ? p->anchor_shift : -1;
+  info->onwalk = p->ow_ok ? 1 : 0;
   info->packed_labels = p->F > 0 && p->packed_ok ? (p->pa_ok && p->anchor_ok ? 2 : 1) : 0;
   info->fsm_transitions = p->fsm_ok ? (int32_t)std::min<int64_t>(p->fsm_entries, INT32_MAX) : 0;
   info->fsm_entry_bytes = p->fsm_ok ? (p->fsm_layout == 1 ? 8 : p->fsm_layout == 2 ? 16 : 32) : 0;
@@ -570,6 +579,8 @@ extern "C" const char* cb_es_plan_kernel(const cb_es_plan* p) {
                                "fitness_packed128_kernel<uint64_t, 16>"};
     return pk[p->F <= 4 ? 0 : p->F <= 6 ? 1 : p->F <= 8 ? 2 : p->F <= 12 ? 3 : 4];
   }
+  if (frontier && p->ow_ok && (p->force_path == 8 || (p->force_path == -1 && !p->packed_ok)))
+    return "fitness_onwalk_kernel";
   if (frontier && (p->force_path == 4 || (p->force_path == -1 && !p->packed_ok)))
     return p->anchor_ok && p->anchor_wide_ok ? "fitness_anchor_kernel" : "fitness_wide_kernel";
   if (frontier) {
@@ -586,7 +597,9 @@ extern "C" int cb_es_plan_set_pool(cb_es_plan* p, int32_t entries) {
 }
 
 extern "C" int cb_es_plan_set_path(cb_es_plan* p, int32_t path) {
-  CB_ARG_CHECK(p && path >= -1 && path <= 7, "cb_es_plan_set_path: bad arguments");
+  CB_ARG_CHECK(p && path >= -1 && path <= 8, "cb_es_plan_set_path: bad arguments");
+  CB_ARG_CHECK(path != 8 || p->ow_ok,
+               "cb_es_plan_set_path: no ON-unit walk program (> 64 slots or values outside a 128-bit window)");
   CB_ARG_CHECK(path != 7 || p->fsm_ok, "cb_es_plan_set_path: no finite-state program for this plan");
   CB_ARG_CHECK(path != 6 || (p->pa_ok && p->anchor_ok),
                "cb_es_plan_set_path: no packed anchor program (> 8 slots or values outside a 128-bit window)");
@@ -1295,6 +1308,8 @@ static int launch_fitness(cb_es_plan* p, const uint64_t* d_pop, int64_t n, doubl
     return launch_fitness_packed_anchor(p, d_pop, n, d_fit, stream);
   if (frontier && p->packed_ok && p->anchor_ok && (p->force_path == 5 || p->force_path == -1))
     return launch_fitness_packed128(p, d_pop, n, d_fit, stream);
+  if (frontier && p->ow_ok && (p->force_path == 8 || (p->force_path == -1 && !p->packed_ok)))
+    return launch_fitness_onwalk(p, d_pop, n, d_fit, stream);
   if (frontier && (p->force_path == 4 || (p->force_path == -1 && !p->packed_ok)))
     return p->anchor_ok ? launch_fitness_anchor(p, d_pop, n, d_fit, stream)
                         : launch_fitness_wide(p, d_pop, n, d_fit, stream);

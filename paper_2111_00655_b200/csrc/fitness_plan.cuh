@@ -63,6 +63,7 @@ struct cb_es_plan {
   int32_t F_needed = 0;  // width of the program before the FRONTIER_MAX cap
   std::vector<UnitRec> prog;
   std::vector<uint8_t> prog_slots;
+  std::vector<int32_t> prog_back_pos;  // position of each back-list entry's unit (-1 for end entries)
   DBuf<UnitRec> d_prog;
   DBuf<uint8_t> d_prog_slots;
   // sparse walk (fitness_wide.cu): last neighbour position of each program
@@ -90,6 +91,12 @@ struct cb_es_plan {
   std::map<cudaStream_t, std::unique_ptr<DBuf<uint64_t>>> aspill;
   std::mutex aspill_mu;
   int32_t pool_entries = 16;
+  // ON-unit walk (fitness_onwalk.cu, <= 64 slots): per-position records
+  bool ow_ok = false;
+  bool ow_seq = false;            // genome bit b is program position b
+  DBuf<uint8_t> d_owrec;          // OwRec[M] (48 bytes)
+  DBuf<uint64_t> d_owmrec;        // [M][4]: rep | cnt << 108, term1 (X)
+  DBuf<uint32_t> d_owlists;       // long back lists
   cudaStream_t host_stream = nullptr;  // single-chunk cb_fitness_host calls
   ~cb_es_plan() {
     if (host_stream) cudaStreamDestroy(host_stream);
@@ -142,5 +149,9 @@ bool fused_generation_ok(const cb_es_plan* p);
 int launch_fused_generation(cb_es_plan* p, const BreedArgs& br, uint64_t* d_children, int64_t n,
                             double* d_fit, cudaStream_t stream);
 int launch_fitness_anchor(cb_es_plan* p, const uint64_t* d_pop, int64_t n, double* d_fit,
+                          cudaStream_t stream);
+// fitness_onwalk.cu: per-lane walk over the genome's ON units (F <= 64)
+int build_onwalk_plan(cb_es_plan* p);
+int launch_fitness_onwalk(cb_es_plan* p, const uint64_t* d_pop, int64_t n, double* d_fit,
                           cudaStream_t stream);
 

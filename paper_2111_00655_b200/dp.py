@@ -88,7 +88,8 @@ def _new_frontiers(g: ComputationGraph) -> int:
 
 def optimize(g: ComputationGraph, registry: PatternRegistry, measurer: Measurer,
              epsilon: float, max_states: int | None = DEFAULT_MAX_STATES,
-             validate: bool | None = None, rounding: str = "raise") -> DPResult:
+             validate: bool | None = None, rounding: str = "raise",
+             stream: int | None = None) -> DPResult:
     """Cheapest full placement of `g` (exact, reference tie-breaking).
 
     Raises UncoverableGraphError when no full cover exists and
@@ -98,7 +99,9 @@ def optimize(g: ComputationGraph, registry: PatternRegistry, measurer: Measurer,
     partition (an alternative within 4 ulp of the total, see csrc/dp.cu
     rounding_window_safe), `rounding="raise"` (default) raises
     RoundingWindowError carrying the exact result, `rounding="exact"`
-    returns the exact optimum (`device["rounding_window_safe"]` False)."""
+    returns the exact optimum (`device["rounding_window_safe"]` False).
+    `stream` (a cudaStream_t as int, e.g. torch's `cuda_stream`) runs the DP
+    launches there instead of the legacy default stream."""
     if rounding not in ("raise", "exact"):
         raise ValueError("rounding must be 'raise' or 'exact'")
     stats = DPStats(nodes=len(g.nodes))
@@ -119,8 +122,9 @@ def optimize(g: ComputationGraph, registry: PatternRegistry, measurer: Measurer,
     t2 = time.perf_counter()
     kernels = np.empty(len(g.nodes), dtype=np.int32)
     res = nat.DPResultStruct()
-    nat.check(nat.lib().cb_dp_solve(g.native, table.handle.raw, float(epsilon),
-                                    nat.ptr(kernels, nat.c_int32), ctypes.byref(res)))
+    nat.check(nat.lib().cb_dp_solve_stream(g.native, table.handle.raw, float(epsilon),
+                                           nat.ptr(kernels, nat.c_int32), ctypes.byref(res),
+                                           ctypes.c_void_p(stream or 0)))
     t3 = time.perf_counter()
     sizes = np.diff(table.group_ptr)
     stats.pops = len(g.nodes)

@@ -31,23 +31,24 @@ def _torch():
     return torch
 
 
-def exchange_elites(best_val, best_row, group, out_fit, out_rows):
-    """All-gather every rank's best (fitness, genome row) and return the
-    global best row and value as device tensors (ties: lowest rank).
-
-    `best_val` (1,), `best_row` (1, W); `out_fit` (world,), `out_rows`
-    (world, W) are caller-owned buffers.  NCCL uses the in-place tensor
+def gather_records(record, group, out) -> None:
+    """All-gather every rank's elite record ([fitness bits, genome row],
+    int64, shape (1, 1 + W)) into `out` (world, 1 + W): the search's only
+    collective, one call per generation.  NCCL uses the in-place tensor
     collective; other backends (gloo in the CPU tests) the list form."""
-    torch = _torch()
     import torch.distributed as dist
     if dist.get_backend(group) == "nccl":
-        dist.all_gather_into_tensor(out_fit, best_val, group=group)
-        dist.all_gather_into_tensor(out_rows, best_row, group=group)
+        dist.all_gather_into_tensor(out, record, group=group)
     else:
-        dist.all_gather(list(out_fit.view(-1, 1).unbind(0)), best_val, group=group)
-        dist.all_gather(list(out_rows.unbind(0)), best_row.view(-1), group=group)
-    who = torch.argmin(out_fit).view(1)
-    return out_rows.index_select(0, who), out_fit.index_select(0, who)
+        dist.all_gather(list(out.unbind(0)), record.view(-1), group=group)
+
+
+def pick_elite_host(records: np.ndarray) -> tuple[int, float]:
+    """The rule cb_elite_pick applies on the device, restated for host-side
+    checks: the lowest fitness, first rank on ties."""
+    fit = records[:, 0].astype(np.int64).view(np.float64)
+    best = int(np.argmin(fit))  # first occurrence of the minimum
+    return best, float(fit[best])
 
 
 class DeviceEvolution:
@@ -80,8 +81,8 @@ class DeviceEvolution:
         self.best_val = torch.zeros(1, dtype=torch.float64, device=self.device)
         self.elite_val = torch.full((1,), float("inf"), dtype=torch.float64, device=self.device)
         self.elite = torch.zeros((1, self.W), **opts)
-        self.gather_fit = torch.empty(self.world, dtype=torch.float64, device=self.device)
-        self.gather_rows = torch.empty((self.world, self.W), **opts)
+        self.record = torch.zeros((1, 1 + self.W), **opts)
+        self.gather_recs = torch.empty((self.world, 1 + self.W), **opts)
         self.history = torch.full((history_capacity,), float("inf"), dtype=torch.float64,
                                   device=self.device)
         self.generation = 0
@@ -104,7 +105,8 @@ class DeviceEvolution:
         tournament order keys, (fused | breed + fitness), the two CUB argmin
         kernels and their unpack (+ the overflow list kernel when the anchor
         walk prices the plan); torch's copies of the elite row are not counted."""
-        return (6 if fused else 7) + (1 if plan.kernel_name() == "fitness_anchor_kernel" else 0)
+        return (6 if fused else 7) + (1 if plan.kernel_name() in ("fitness_anchor_kernel",
+                                                                  "fitness_onwalk_kernel") else 0)
 
     # -- helpers -----------------------------------------------------------------------
     def _stream(self) -> int:
@@ -166,34 +168,41 @@ class DeviceEvolution:
                 ctypes.c_void_p(self._stream() if stream is None else stream)))
             self.elite_val = self.best_val
             return
-        nat.check(nat.lib().cb_argmin(self._ptr(self.fit[self.cur]), self.P,
-                                      self._ptr(self.best_idx), self._ptr(self.best_val),
-                                      ctypes.c_void_p(self._stream())))
-        row = self.pop[self.cur].index_select(0, self.best_idx)
-        if self.world > 1:
-            elite, best = exchange_elites(self.best_val, row, self.group, self.gather_fit,
-                                          self.gather_rows)
-            self.elite.copy_(elite)
-            self.elite_val.copy_(best)
-        else:
-            self.elite.copy_(row)
-            best = self.best_val
-            self.elite_val.copy_(best)
-        if self.generation < self.history.numel():
-            self.history[self.generation:self.generation + 1].copy_(best)
+        # N > 1: one record per rank, one all-gather, the pick on the device
+        p = self._ptrs()
+        stream = self._stream() if stream is None else stream
+        timing = getattr(self, "timing", False)
+        if timing:
+            torch = _torch()
+            ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+            ev[0].record()
+        nat.check(nat.lib().cb_elite_record(
+            p["fit"][self.cur], self.P, p["pop"][self.cur], self.W, p["best_idx"], p["best_val"],
+            self._ptr(self.record), ctypes.c_void_p(stream)))
+        gather_records(self.record, self.group, self.gather_recs)
+        hist = (ctypes.c_void_p(p["history"] + self.generation * p["hist_stride"])
+                if self.generation < self.history.numel() else ctypes.c_void_p())
+        nat.check(nat.lib().cb_elite_pick(
+            self._ptr(self.gather_recs), self.world, self.W, p["elite"],
+            self._ptr(self.elite_val), hist, ctypes.c_void_p(stream)))
+        if timing:
+            ev[1].record()
+            self.exchange_events.append(tuple(ev))
 
     def enable_kernel_timing(self, on: bool = True) -> None:
         """Record CUDA events around the breed and fitness launches of every
         step (on the launching stream) for per-kernel durations."""
         self.timing = on
         self.kernel_events: list[tuple] = []
+        self.exchange_events: list[tuple] = []
 
     def kernel_times_ms(self) -> dict[str, list[float]]:
         """Per-step device times: 'generation' (breed + fitness), and for the
         unfused path its 'breed' and 'fitness' parts."""
         torch = _torch()
         torch.cuda.synchronize(self.device)
-        out = {"generation": [], "breed": [], "fitness": []}
+        out = {"generation": [], "breed": [], "fitness": [],
+               "exchange": [a.elapsed_time(b) for a, b in getattr(self, "exchange_events", [])]}
         for ev in self.kernel_events:
             out["generation"].append(ev[0].elapsed_time(ev[-1]))
             if len(ev) == 3:

@@ -1,5 +1,7 @@
-"""Multi-process (world_size 2, gloo on CPU) coverage of the sharded search's
-only exchange step: the per-generation all-gather of rank elites."""
+"""Multi-process (world_size 2 and 3, gloo on CPU) coverage of the sharded
+search's only exchange step: the per-generation all-gather of one elite
+record per rank ([fitness bits, genome row]) and the pick rule the device
+applies to the gathered records (lowest fitness, first rank on ties)."""
 
 import os
 import socket
@@ -9,7 +11,9 @@ import torch
 import torch.distributed as dist
 import torch.multiprocessing as mp
 
-from paper_2111_00655_b200.es_device import exchange_elites
+import numpy as np
+
+from paper_2111_00655_b200.es_device import gather_records, pick_elite_host
 
 
 def _free_port() -> int:
@@ -26,12 +30,14 @@ def _worker(rank: int, world: int, port: int, results):
         W = 3
         # rank r's best fitness; rank 1 holds the global best, rank 2.. ties
         vals = [5.0, 2.5, 2.5, 9.0]
-        best = torch.tensor([vals[rank]], dtype=torch.float64)
-        row = torch.full((1, W), 100 + rank, dtype=torch.int64)
-        out_fit = torch.empty(world, dtype=torch.float64)
-        out_rows = torch.empty((world, W), dtype=torch.int64)
-        elite, val = exchange_elites(best, row, dist.group.WORLD, out_fit, out_rows)
-        results[rank] = (elite.tolist(), float(val))
+        record = torch.empty((1, 1 + W), dtype=torch.int64)
+        record[0, 0] = torch.tensor([vals[rank]], dtype=torch.float64).view(torch.int64)[0]
+        record[0, 1:] = 100 + rank
+        out = torch.empty((world, 1 + W), dtype=torch.int64)
+        gather_records(record, dist.group.WORLD, out)
+        recs = out.numpy()
+        best, val = pick_elite_host(recs)
+        results[rank] = ([recs[best, 1:].tolist()], val)
     finally:
         dist.destroy_process_group()
 

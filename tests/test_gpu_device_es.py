@@ -99,3 +99,32 @@ def test_evolve_device_public_api(gpu, name):
                                                        reg.graph_backend_ids())
     assert [c for _, c in out.history] == sorted((c for _, c in out.history), reverse=True)
     assert out.genome_length == plan.k and out.evaluations == 8192 * 31
+
+
+def test_elite_pick_kernel_follows_the_host_rule(gpu):
+    """cb_elite_pick over gathered records: lowest fitness, first rank on
+    ties, row copied, value (and history slot) written."""
+    import ctypes
+
+    import numpy as np
+    import torch
+
+    from paper_2111_00655_b200 import _native as nat
+    from paper_2111_00655_b200.es_device import pick_elite_host
+    rng = np.random.default_rng(0)
+    for world, W in ((2, 1), (3, 5), (8, 1554)):
+        fits = rng.choice([3.0, 1.5, 1.5, np.inf, 7.25], size=world)
+        recs = np.empty((world, 1 + W), np.int64)
+        recs[:, 0] = fits.view(np.int64)
+        recs[:, 1:] = rng.integers(-(1 << 62), 1 << 62, size=(world, W))
+        d = torch.from_numpy(recs).cuda()
+        elite = torch.zeros(W, dtype=torch.int64, device="cuda")
+        val = torch.zeros(1, dtype=torch.float64, device="cuda")
+        hist = torch.zeros(1, dtype=torch.float64, device="cuda")
+        nat.check(nat.lib().cb_elite_pick(ctypes.c_void_p(d.data_ptr()), world, W,
+                                          ctypes.c_void_p(elite.data_ptr()),
+                                          ctypes.c_void_p(val.data_ptr()),
+                                          ctypes.c_void_p(hist.data_ptr()), ctypes.c_void_p(0)))
+        best, want = pick_elite_host(recs)
+        assert val.item() == want == hist.item()
+        assert np.array_equal(elite.cpu().numpy(), recs[best, 1:])
