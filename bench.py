@@ -215,10 +215,12 @@ def run_mine(args) -> None:
 
     def search(P: int, gens: int):
         t = {}
+        # a fresh measurer (empty cost cache), as a single search run starts
+        meas = tp.SimMeasurer(bs.measurer.profiles)
         t0 = time.perf_counter()
-        res = tp.optimize(g, bs.registry, bs.measurer, 0.01)
+        res = tp.optimize(g, bs.registry, meas, 0.01)
         t1 = time.perf_counter()
-        plan = tp.FitnessPlan(g, bs.registry, bs.measurer, res.placement, 0.01, bs.graph_backend,
+        plan = tp.FitnessPlan(g, bs.registry, meas, res.placement, 0.01, bs.graph_backend,
                               res.kernel_matches)
         t2 = time.perf_counter()
         es = DeviceEvolution(plan, P, seed=args.seed, device=dev, process_group=group)
@@ -433,10 +435,11 @@ def config_sweep(dev, args) -> dict:
             bs.registry._tables.clear()
             gc.collect()
             torch.cuda.synchronize(dev)
+            meas = tp.SimMeasurer(bs.measurer.profiles)  # empty cost cache, as a single run
             t0 = time.perf_counter()
-            res = tp.optimize(g, bs.registry, bs.measurer, 0.01, validate=False)
+            res = tp.optimize(g, bs.registry, meas, 0.01, validate=False)
             t1 = time.perf_counter()
-            plan = tp.FitnessPlan(g, bs.registry, bs.measurer, res.placement, 0.01, bs.graph_backend,
+            plan = tp.FitnessPlan(g, bs.registry, meas, res.placement, 0.01, bs.graph_backend,
                                   res.kernel_matches)
             t2 = time.perf_counter()
             es = DeviceEvolution(plan, cfg["search_pop"], seed=0, device=dev)

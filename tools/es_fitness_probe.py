@@ -12,6 +12,8 @@ bs = workloads.paper_backends(g) if name != 'random100k' else workloads.random_b
 res = tp.optimize(g, bs.registry, bs.measurer, 0.01, validate=False)
 plan = tp.FitnessPlan(g, bs.registry, bs.measurer, res.placement, 0.01, bs.graph_backend, res.kernel_matches)
 import os
+if os.environ.get('CB_PATH'):
+    plan.set_path(os.environ['CB_PATH'])
 if os.environ.get('CB_POOL'):
     plan.set_pool(int(os.environ['CB_POOL']))
 es = DeviceEvolution(plan, P, seed=1, fused=False)
