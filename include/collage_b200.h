@@ -216,7 +216,6 @@ typedef struct {
                             2: also the packed anchor kernel (<= 8 slots) */
   int32_t fsm_transitions; /* transitions of the finite-state program (0 = none) */
   int32_t fsm_entry_bytes; /* transition layout: 8 or 16 (+ shared delta table), or 32 */
-  int32_t onwalk;        /* 1: the ON-unit walk applies (<= 64 slots, packed 128-bit sums) */
 } cb_es_plan_info;
 int cb_es_plan_query(const cb_es_plan* p, cb_es_plan_info* info);
 /* Evaluation path: -1 automatic (the finite-state walk when its table is

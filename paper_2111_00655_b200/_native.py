@@ -73,7 +73,6 @@ class ESPlanInfo(ctypes.Structure):
         ("packed_labels", c_int32),
         ("fsm_transitions", c_int32),
         ("fsm_entry_bytes", c_int32),
-        ("onwalk", c_int32),
     ]
 
 

@@ -508,8 +508,7 @@ extern "C" int cb_es_plan_create(cb_graph* g, cb_matches* m, int32_t n_kernels,
     if ((e = P->d_pos_of_bit.upload(P->pos_of_bit)) != cudaSuccess) return fail_cuda(e);
     if ((e = P->d_fixed_pos.upload(P->fixed_pos)) != cudaSuccess) return fail_cuda(e);
   }
-  if ((rc = build_anchor_plan(P)) != CB_OK || (rc = build_fsm_plan(P)) != CB_OK ||
-      (rc = build_onwalk_plan(P)) != CB_OK) {
+  if ((rc = build_anchor_plan(P)) != CB_OK || (rc = build_fsm_plan(P)) != CB_OK) {
     delete P;
     return rc;
   }
@@ -533,7 +532,6 @@ extern "C" int cb_es_plan_query(const cb_es_plan* p, cb_es_plan_info* info) {
   info->frontier_slots = p->F;
   info->seed_cost = p->seed_cost;
   info->window_shift = p->anchor_ok ? p->anchor_shift : -1;
-  info->onwalk = p->ow_ok ? 1 : 0;
   info->packed_labels = p->F > 0 && p->packed_ok ? (p->pa_ok && p->anchor_ok ? 2 : 1) : 0;
   info->fsm_transitions = p->fsm_ok ? (int32_t)std::min<int64_t>(p->fsm_entries, INT32_MAX) : 0;
   info->fsm_entry_bytes = p->fsm_ok ? (p->fsm_layout == 1 ? 8 : p->fsm_layout == 2 ? 16 : 32) : 0;
@@ -579,8 +577,6 @@ extern "C" const char* cb_es_plan_kernel(const cb_es_plan* p) {
                                "fitness_packed128_kernel<uint64_t, 16>"};
     return pk[p->F <= 4 ? 0 : p->F <= 6 ? 1 : p->F <= 8 ? 2 : p->F <= 12 ? 3 : 4];
   }
-  if (frontier && p->ow_ok && (p->force_path == 8 || (p->force_path == -1 && !p->packed_ok)))
-    return "fitness_onwalk_kernel";
   if (frontier && (p->force_path == 4 || (p->force_path == -1 && !p->packed_ok)))
     return p->anchor_ok && p->anchor_wide_ok ? "fitness_anchor_kernel" : "fitness_wide_kernel";
   if (frontier) {
@@ -597,9 +593,7 @@ extern "C" int cb_es_plan_set_pool(cb_es_plan* p, int32_t entries) {
 }
 
 extern "C" int cb_es_plan_set_path(cb_es_plan* p, int32_t path) {
-  CB_ARG_CHECK(p && path >= -1 && path <= 8, "cb_es_plan_set_path: bad arguments");
-  CB_ARG_CHECK(path != 8 || p->ow_ok,
-               "cb_es_plan_set_path: no ON-unit walk program (> 64 slots or values outside a 128-bit window)");
+  CB_ARG_CHECK(p && path >= -1 && path <= 7, "cb_es_plan_set_path: bad arguments");
   CB_ARG_CHECK(path != 7 || p->fsm_ok, "cb_es_plan_set_path: no finite-state program for this plan");
   CB_ARG_CHECK(path != 6 || (p->pa_ok && p->anchor_ok),
                "cb_es_plan_set_path: no packed anchor program (> 8 slots or values outside a 128-bit window)");
@@ -1308,8 +1302,6 @@ static int launch_fitness(cb_es_plan* p, const uint64_t* d_pop, int64_t n, doubl
     return launch_fitness_packed_anchor(p, d_pop, n, d_fit, stream);
   if (frontier && p->packed_ok && p->anchor_ok && (p->force_path == 5 || p->force_path == -1))
     return launch_fitness_packed128(p, d_pop, n, d_fit, stream);
-  if (frontier && p->ow_ok && (p->force_path == 8 || (p->force_path == -1 && !p->packed_ok)))
-    return launch_fitness_onwalk(p, d_pop, n, d_fit, stream);
   if (frontier && (p->force_path == 4 || (p->force_path == -1 && !p->packed_ok)))
     return p->anchor_ok ? launch_fitness_anchor(p, d_pop, n, d_fit, stream)
                         : launch_fitness_wide(p, d_pop, n, d_fit, stream);

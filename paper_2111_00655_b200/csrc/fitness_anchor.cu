@@ -3,35 +3,41 @@
 //
 // Semantics are those of every fitness kernel here (tensorplace/
 // evolution.py:65-135 decode, tensorplace/cost.py:320-373 graph-level
-// pricing).  Lanes walk the frontier program in lockstep, one genome each;
-// only the component structure of the occupied slots and the merged
-// components' sums are per-lane data, everything else is uniform:
+// pricing): the genome's ON units form regions = connected components of
+// the unit graph; a region of one unit costs its precomputed term1, a larger
+// one round(sum) * r(n) + eps, every OFF unit its own kernel term.
+//
+// Lanes walk the frontier program in lockstep, one genome each, so every
+// per-step record is a warp-uniform (broadcast) load; only the component
+// structure of the occupied slots and the merged components' sums are
+// per-lane data:
 //
 // * Anchors.  A component's data lives at its ANCHOR: the member slot whose
 //   unit has the latest end (last neighbour position).  Merging two
-//   components keeps the later-ending anchor, so no member ever outlives
-//   its anchor: releasing a non-anchor slot is a bit clear, releasing an
-//   anchor closes the region, and no data ever moves between slots.
+//   components keeps the later-ending anchor, so no member outlives its
+//   anchor and no data ever moves between slots.
 // * Byte labels.  A non-anchor slot holds a parent slot of its component
 //   (path-compressed on lookup; a pointer always targets a slot that ends no
-//   earlier).  An anchor holds a flag, plus a pool entry when the component
-//   has merged.  A one-unit component needs no data of its own: the unit in
-//   a slot, its end and its constants are the same for every lane, kept per
-//   warp in shared memory (program position, end) and read from the plan.
-// * Packed sums.  A merged component's exact sum is carried in the plan's
-//   128-bit window (X = v >> s, checked at plan time) with its kernel count
-//   in bits 108-127, so a merge is one 128-bit add; pool entries live in
-//   shared memory ([entry][thread], 16 bytes).  A genome needing more live
-//   merged components than the pool holds is listed for the warp-per-genome
-//   kernel (fitness_wide.cu) instead.
-// * Region pricing (round(sum) * r(n) + eps) happens in warp batches: a
-//   closing region is queued with its owner lane, and the queue (32 entries)
-//   is priced one entry per lane, adding into the owner's accumulator.
-// * Step records are 16 bytes (genome bit, slot, end position, up to four
-//   back and four end slots inline), prefetched one step ahead.
+//   earlier); an anchor holds a flag, plus a pool entry when merged.
+// * Visiting ON unit p adds term1(p) - off(p) to the lane's total (right
+//   while p stays alone); merging a one-unit component takes its term1 back
+//   and contributes its replacement sum to the merged component's pool
+//   entry (128-bit window sum with the kernel count in bits 108-127).
+// * Closing without end lists.  The plan hands a slot to a later unit only
+//   after its unit's last neighbour, and an anchor ends last in its
+//   component, so a merged component is complete exactly when its anchor
+//   slot is handed on: the step reading the slot's old label queues the
+//   sum for pricing (round, __dmul_rn by r(n), + eps: warp batches of 32).
+//   Every pool entry is named by one anchor label, so a lane never holds
+//   more than F entries (C in shared memory, the rest in a global spill).
+// * Per-warp slot table.  The unit currently in each slot is the same for
+//   all lanes: (end, replacement sum | count, term1) per slot, written by
+//   three lanes per step from the unit's 48-byte slot record, so merges
+//   read everything from shared memory.
+// * Genome words are read per lane one word ahead (rows are read once).
 //
-// Shared memory per thread: one byte per slot + 16 bytes per pool entry, and
-// per warp the slot tables, the region queue and the owner accumulators.
+// Shared memory per thread: one byte per slot + 16 bytes per pool entry; per
+// warp the slot table, the region queue and the owner accumulators.
 #include <algorithm>
 #include <cmath>
 #include <cstring>
@@ -46,10 +52,9 @@ namespace {
 // 16-byte step record
 struct __align__(16) AStep {
   uint32_t bs;     // genome bit (bits 0-23; 0xFFFFFF: always-on fixed unit) | slot << 24 | long << 31
-  int32_t last;    // program position of the unit's last neighbour
-  uint32_t lists;  // short: nback (3 bits) | nend << 3 | back slot j at 6 + 6 j (j < 4)
-                   // long:  nback (16 bits) | nend << 16
-  uint32_t ends;   // short: end slot j at 6 j (j < 4); long: offset of back + end lists
+  uint32_t lists;  // short: nback (3 bits) | back slot j at 3 + 6 j (j < 4); long: nback
+  uint32_t off;    // long: offset of the back list
+  uint32_t pad;
 };
 static_assert(sizeof(AStep) == 16, "AStep layout");
 
@@ -68,25 +73,19 @@ __device__ __forceinline__ void x_add(X128& a, const X128& b) {
 __device__ __forceinline__ void x_sub(X128& a, const X128& b) {
   asm("sub.cc.u64 %0, %0, %2;\n\tsubc.u64 %1, %1, %3;" : "+l"(a.lo), "+l"(a.hi) : "l"(b.lo), "l"(b.hi));
 }
-__device__ __forceinline__ X128 ld_x(const ulonglong2* p) {
-  const ulonglong2 v = __ldg(p);
-  return {v.x, v.y};
-}
 
 struct AnArgs {
-  int32_t M, words, shift, n_infeas, Fp;
+  int32_t M, words, shift, n_infeas, Fp, F;
   fx192 base_const;
   X128 eps;
   const AStep* __restrict__ step;
-  const ulonglong2* __restrict__ repc;   // [M][2] replacement sum | count << 108, own term (off)
-  const ulonglong2* __restrict__ term1;  // [M] one-unit region term minus the unit's own term
-  const uint8_t* __restrict__ lists;     // long back / end lists
+  const ulonglong2* __restrict__ t1m;   // [M] term1 - off (two's complement X)
+  const uint4* __restrict__ srec;       // [M][3] (end, -, -, -), rep | cnt << 108, term1
+  const uint8_t* __restrict__ lists;    // long back lists
   const int32_t* __restrict__ infeas_word;
   const uint64_t* __restrict__ infeas_mask;
   const double* __restrict__ rt;
   unsigned long long* flags;
-  int32_t* ovf_count;
-  int64_t* ovf_list;
   ulonglong2* spill;  // [64 - C][resident threads]: pool entries beyond the shared ones
 };
 
@@ -109,8 +108,7 @@ __device__ __forceinline__ void an_flush(const ulonglong2* qx, const uint8_t* qo
   __syncwarp();
 }
 
-// 32-bit shared-memory accesses (the addresses stay in registers instead of
-// being rebuilt from the generic window on every access)
+// 32-bit shared-memory addressing (addresses stay in registers)
 __device__ __forceinline__ uint32_t lds_u8(uint32_t a) {
   uint32_t v;
   asm volatile("ld.shared.u8 %0, [%1];" : "=r"(v) : "r"(a));
@@ -119,9 +117,9 @@ __device__ __forceinline__ uint32_t lds_u8(uint32_t a) {
 __device__ __forceinline__ void sts_u8(uint32_t a, uint32_t v) {
   asm volatile("st.shared.u8 [%0], %1;" ::"r"(a), "r"(v));
 }
-__device__ __forceinline__ int2 lds_s32x2(uint32_t a) {
-  int2 v;
-  asm volatile("ld.shared.v2.s32 {%0, %1}, [%2];" : "=r"(v.x), "=r"(v.y) : "r"(a));
+__device__ __forceinline__ int32_t lds_s32(uint32_t a) {
+  int32_t v;
+  asm volatile("ld.shared.s32 %0, [%1];" : "=r"(v) : "r"(a));
   return v;
 }
 __device__ __forceinline__ X128 lds_x(uint32_t a) {
@@ -132,17 +130,21 @@ __device__ __forceinline__ X128 lds_x(uint32_t a) {
 __device__ __forceinline__ void sts_x(uint32_t a, const X128& v) {
   asm volatile("st.shared.v2.u64 [%0], {%1, %2};" ::"r"(a), "l"(v.lo), "l"(v.hi));
 }
+__device__ __forceinline__ void sts_v4(uint32_t a, const uint4& v) {
+  asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(a), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w));
+}
 
-// Per-lane walk state and the slot tables it reads.
+constexpr uint32_t WT_BYTES = 48;  // slot table entry: end | rep, count | term1
+
+// Per-lane walk state.
 struct AnLane {
-  uint32_t lab;    // shared address of this lane's label for slot 0 (slot s at +4 s)
+  uint32_t lab;    // shared address of this lane's label for slot 0 (slot s at + 4 s)
   uint32_t pool;   // shared address of this lane's pool entry 0 (entry e < C at + e * 16 T)
   ulonglong2* spill;  // this lane's global entries (entry e >= C at [(e - C) * stride])
   int64_t spill_stride;
-  uint32_t wtab;   // shared address of the warp's slot table (slot s at + 8 s)
-  uint64_t act;    // occupied slots
-  uint64_t pfree;  // free pool entries (64: C in shared memory, the rest spilled)
-  bool ovf;
+  uint32_t wtab;   // shared address of the warp's slot table (slot s at + 48 s)
+  uint64_t act;    // slots holding an ON unit
+  uint64_t pfree;  // free pool entries
   X128 total;      // genome-dependent part of the cost (two's complement)
 };
 
@@ -162,15 +164,10 @@ __device__ __forceinline__ void pool_st(const AnLane& L, uint32_t e, const X128&
 
 // Back edge to slot b of the new unit whose component is anchored at A:
 // find b's anchor, merge the two components at the later-ending anchor.
-// Every lane runs the same predicated sequence.
 template <int C>
-__device__ __forceinline__ void an_merge(AnLane& L, const AnArgs& a, bool need, int b, int& A) {
+__device__ __forceinline__ void an_merge(AnLane& L, bool need, int b, int& A) {
   int x = b;
   uint32_t lx = need ? lds_u8(L.lab + 4 * b) : L_ANCHOR;
-  if (!(lx & L_ANCHOR)) {
-    x = (int)lx;
-    lx = lds_u8(L.lab + 4 * x);
-  }
   if (!(lx & L_ANCHOR)) {
     x = (int)lx;
     lx = lds_u8(L.lab + 4 * x);
@@ -182,76 +179,68 @@ __device__ __forceinline__ void an_merge(AnLane& L, const AnArgs& a, bool need, 
     }
   }
   if (x != b) sts_u8(L.lab + 4 * b, (uint32_t)x);  // path compression (x == b when !need)
-  const bool mrg = need && x != A;
+  if (!need || x == A) return;
   const uint32_t lA = lds_u8(L.lab + 4 * A);
-  const int2 tA = lds_s32x2(L.wtab + 8 * A), tX = lds_s32x2(L.wtab + 8 * x);
-  const bool keepA = tA.y >= tX.y;  // the later-ending anchor survives
+  const bool keepA = lds_s32(L.wtab + WT_BYTES * A) >= lds_s32(L.wtab + WT_BYTES * x);
   const int Wn = keepA ? A : x, Xn = keepA ? x : A;
   const uint32_t lW = keepA ? lA : lx, lX = keepA ? lx : lA;
-  const int pW = keepA ? tA.x : tX.x, pX = keepA ? tX.x : tA.x;
-  const bool mW = (lW & L_MERGED) != 0u, mX = (lX & L_MERGED) != 0u;
-  const uint32_t eW = lW & 63u, eX = lX & 63u;
+  X128 sW, sX;
   // merged components: their pool sums; one-unit components: the unit's
-  // replacement sum, and its own kernel term leaves the total now
-  X128 sW = {0ull, 0ull}, sX = {0ull, 0ull}, oW = {0ull, 0ull}, oX = {0ull, 0ull};
-  if (mrg && mW) sW = pool_ld<C>(L, eW);
-  if (mrg && !mW) {
-    sW = ld_x(a.repc + 2 * pW);
-    oW = ld_x(a.repc + 2 * pW + 1);
+  // replacement sum, and its one-unit term leaves the total
+  if (lW & L_MERGED) {
+    sW = pool_ld<C>(L, lW & 63u);
+  } else {
+    sW = lds_x(L.wtab + WT_BYTES * Wn + 16);
+    x_sub(L.total, lds_x(L.wtab + WT_BYTES * Wn + 32));
   }
-  if (mrg && mX) sX = pool_ld<C>(L, eX);
-  if (mrg && !mX) {
-    sX = ld_x(a.repc + 2 * pX);
-    oX = ld_x(a.repc + 2 * pX + 1);
+  if (lX & L_MERGED) {
+    sX = pool_ld<C>(L, lX & 63u);
+  } else {
+    sX = lds_x(L.wtab + WT_BYTES * Xn + 16);
+    x_sub(L.total, lds_x(L.wtab + WT_BYTES * Xn + 32));
   }
   x_add(sW, sX);
-  x_add(oW, oX);
-  x_sub(L.total, oW);
-  const bool alloc = mrg && !mW && !mX;
-  const uint32_t e = mW ? eW : (mX ? eX : (L.pfree ? (uint32_t)(__ffsll((long long)L.pfree) - 1) : 0u));
-  L.ovf |= alloc && L.pfree == 0ull;  // all 64 entries live: the genome goes to the fallback kernel
-  if (alloc) L.pfree &= L.pfree - 1ull;
-  if (mrg && mW && mX) L.pfree |= 1ull << eX;
-  if (mrg) {
-    pool_st<C>(L, e, sW);
-    sts_u8(L.lab + 4 * Wn, L_ANCHOR | L_MERGED | e);
-    sts_u8(L.lab + 4 * Xn, (uint32_t)Wn);
-    A = Wn;
+  uint32_t e;
+  if (lW & L_MERGED) {
+    e = lW & 63u;
+    if (lX & L_MERGED) L.pfree |= 1ull << (lX & 63u);
+  } else if (lX & L_MERGED) {
+    e = lX & 63u;
+  } else {
+    // at most F <= 64 entries are ever named by anchor labels
+    e = (uint32_t)(__ffsll((long long)L.pfree) - 1);
+    L.pfree &= L.pfree - 1ull;
   }
+  pool_st<C>(L, e, sW);
+  sts_u8(L.lab + 4 * Wn, L_ANCHOR | L_MERGED | e);
+  sts_u8(L.lab + 4 * Xn, (uint32_t)Wn);
+  A = Wn;
 }
 
-// Release of slot e (uniform): a leaving anchor closes its region -- a
-// one-unit region adds its precomputed term, a merged one is queued.
+// The label a slot held before it is handed on (or the program ends): a
+// merged anchor's region is complete -- queue it; all lanes take part.
 template <int C>
-__device__ __forceinline__ void an_close(AnLane& L, const AnArgs& a, int e, int lane, ulonglong2* qx,
-                                         uint8_t* qown, int& qn, unsigned long long* tacc, bool& inexact) {
-  const bool was = (L.act >> e) & 1ull;
-  if (!__any_sync(0xffffffffu, was)) return;
-  L.act &= ~(1ull << e);
-  const uint32_t le = lds_u8(L.lab + 4 * e);
-  const bool anc = was && (le & L_ANCHOR);
-  const bool emit = anc && (le & L_MERGED);
-  if (anc && !emit) x_add(L.total, ld_x(a.term1 + lds_s32x2(L.wtab + 8 * e).x));
+__device__ __forceinline__ void an_close(AnLane& L, uint32_t old, int lane, ulonglong2* qx, uint8_t* qown,
+                                         int& qn, const AnArgs& a, unsigned long long* tacc, bool& inexact) {
+  const bool emit = (old & (L_ANCHOR | L_MERGED)) == (L_ANCHOR | L_MERGED);
+  const unsigned closing = __ballot_sync(0xffffffffu, emit);
+  if (!closing) return;
   X128 ev = {0ull, 0ull};
   if (emit) {
-    ev = pool_ld<C>(L, le & 63u);
-    L.pfree |= 1ull << (le & 63u);
+    ev = pool_ld<C>(L, old & 63u);
+    L.pfree |= 1ull << (old & 63u);
   }
-  // closed multi-unit regions of all lanes are priced 32 at a time
-  const unsigned closing = __ballot_sync(0xffffffffu, emit);
-  if (closing) {
-    const int cnt = __popc(closing);
-    if (qn + cnt > AN_QCAP) {
-      an_flush(qx, qown, qn, lane, a, tacc, inexact);
-      qn = 0;
-    }
-    if (emit) {
-      const int at = qn + __popc(closing & ((1u << lane) - 1u));
-      qx[at] = make_ulonglong2(ev.lo, ev.hi);
-      qown[at] = (uint8_t)lane;
-    }
-    qn += cnt;
+  const int cnt = __popc(closing);
+  if (qn + cnt > AN_QCAP) {
+    an_flush(qx, qown, qn, lane, a, tacc, inexact);
+    qn = 0;
   }
+  if (emit) {
+    const int at = qn + __popc(closing & ((1u << lane) - 1u));
+    qx[at] = make_ulonglong2(ev.lo, ev.hi);
+    qown[at] = (uint8_t)lane;
+  }
+  qn += cnt;
 }
 
 template <int C>
@@ -259,24 +248,24 @@ __global__ void __launch_bounds__(AN_THREADS, 8)
 fitness_anchor_kernel(AnArgs a, const uint64_t* __restrict__ pop, int64_t n, double* __restrict__ fit) {
   constexpr int T = AN_THREADS, W = AN_THREADS / 32;
   extern __shared__ __align__(16) unsigned char an_smem[];
-  ulonglong2* pool = reinterpret_cast<ulonglong2*>(an_smem);         // [C][T]
-  ulonglong2* qx_all = pool + C * T;                                 // [W][QCAP]
+  ulonglong2* pool = reinterpret_cast<ulonglong2*>(an_smem);                  // [C][T]
+  ulonglong2* qx_all = pool + C * T;                                          // [W][QCAP]
   unsigned long long* tacc_all = reinterpret_cast<unsigned long long*>(qx_all + W * AN_QCAP);  // [W][32][2]
-  int2* wtab_all = reinterpret_cast<int2*>(tacc_all + W * 64);      // [W][64] (position, end) per slot
-  uint8_t* qown_all = reinterpret_cast<uint8_t*>(wtab_all + W * 64);  // [W][QCAP]
-  uint8_t* LAB = qown_all + W * AN_QCAP;                             // [T / 4][Fp][4]
+  unsigned char* wtab_all = reinterpret_cast<unsigned char*>(tacc_all + W * 64);  // [W][F][48]
+  uint8_t* qown_all = wtab_all + (size_t)W * a.F * WT_BYTES;                 // [W][QCAP]
+  uint8_t* LAB = qown_all + W * AN_QCAP;                                      // [T / 4][Fp][4]
   const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
   ulonglong2* qx = qx_all + warp * AN_QCAP;
   uint8_t* qown = qown_all + warp * AN_QCAP;
   unsigned long long* tacc = tacc_all + warp * 64;
-  int2* wtab = wtab_all + warp * 64;
   AnLane L;
   L.lab = (uint32_t)__cvta_generic_to_shared(LAB + (t >> 2) * a.Fp * 4 + (t & 3));
   L.pool = (uint32_t)__cvta_generic_to_shared(pool + t);
-  L.wtab = (uint32_t)__cvta_generic_to_shared(wtab);
+  L.wtab = (uint32_t)__cvta_generic_to_shared(wtab_all + (size_t)warp * a.F * WT_BYTES);
   L.spill_stride = (int64_t)gridDim.x * T;
   L.spill = a.spill + (int64_t)blockIdx.x * T + t;
   tacc[2 * lane] = tacc[2 * lane + 1] = 0ull;
+  for (int s = 0; s < a.F; ++s) sts_u8(L.lab + 4 * s, 0u);
   __syncwarp();
   bool inexact = false;
   const int64_t stride = (int64_t)gridDim.x * T;
@@ -289,71 +278,70 @@ fitness_anchor_kernel(AnArgs a, const uint64_t* __restrict__ pop, int64_t n, dou
       dead |= (__ldg(gen + __ldg(a.infeas_word + j)) & __ldg(a.infeas_mask + j)) != 0ull;
     L.act = 0ull;
     L.pfree = ~0ull;
-    L.ovf = false;
     L.total = {0ull, 0ull};
     int qn = 0;
-    int32_t cur_w = -1;
-    uint64_t word = 0ull;
-    uint4 nh = __ldg(reinterpret_cast<const uint4*>(a.step));
+    // genome words: w0 = word cur_w, w1 = word cur_w + 1 (loaded ahead)
+    int32_t cur_w = -2;
+    uint64_t w0 = 0ull, w1 = 0ull;
+    // step p + 1's records are loaded while step p runs
+    AStep nh = a.step[0];
+    ulonglong2 nt = __ldg(a.t1m);
+    const uint4* srl = a.srec + (lane < 3 ? lane : 0);
+    uint4 ns = __ldg(srl);
     for (int32_t p = 0; p < a.M; ++p) {
-      const uint4 h = nh;
-      if (p + 1 < a.M) nh = __ldg(reinterpret_cast<const uint4*>(a.step + p + 1));
-      const uint32_t bitf = h.x & 0xFFFFFFu;
-      const int S = (int)((h.x >> 24) & 63u);
-      if (lane == 0) wtab[S] = make_int2(p, (int32_t)h.y);
+      const AStep h = nh;
+      const ulonglong2 tm = nt;
+      const uint4 sr = ns;
+      if (p + 1 < a.M) {
+        nh = a.step[p + 1];
+        nt = __ldg(a.t1m + p + 1);
+        ns = __ldg(srl + 3 * (int64_t)(p + 1));
+      }
+      const uint32_t bitf = h.bs & 0xFFFFFFu;
+      const int S = (int)((h.bs >> 24) & 63u);
+      // the unit's slot-table entry (three lanes, 16 bytes each)
+      if (lane < 3) sts_v4(L.wtab + WT_BYTES * S + 16 * lane, sr);
       bool on = !dead;
       if (bitf != 0xFFFFFFu) {
         const int32_t wi = (int32_t)(bitf >> 6);
         if (wi != cur_w) {  // warp uniform
-          word = dead ? 0ull : __ldg(gen + wi);
+          w0 = (wi == cur_w + 1) ? w1 : (dead ? 0ull : __ldg(gen + wi));
+          w1 = (!dead && wi + 1 < a.words) ? __ldg(gen + wi + 1) : 0ull;
           cur_w = wi;
         }
-        on = (word >> (bitf & 63u)) & 1ull;
+        on = (w0 >> (bitf & 63u)) & 1ull;
       }
-      __syncwarp();
-      if (on) {
-        L.act |= 1ull << S;
-        sts_u8(L.lab + 4 * S, L_ANCHOR);
-      }
+      // the slot's previous owner is complete
+      const uint32_t labS = L.lab + 4 * S;
+      an_close<C>(L, lds_u8(labS), lane, qx, qown, qn, a, tacc, inexact);
+      sts_u8(labS, on ? L_ANCHOR : 0u);
+      L.act = on ? (L.act | (1ull << S)) : (L.act & ~(1ull << S));
+      if (on) x_add(L.total, X128{tm.x, tm.y});
+      __syncwarp();  // slot table entry visible to every lane
       int A = S;  // anchor of the new unit's component
-      if (!(h.x >> 31)) {
-        // short lists (<= 4 back, <= 4 end slots) in the record: unrolled,
-        // every guard warp uniform
-        const int nb = (int)(h.z & 7u), ne = (int)((h.z >> 3) & 7u);
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          if (j < nb) {
-            const int b = (int)((h.z >> (6 + 6 * j)) & 63u);
-            const bool need = on && ((L.act >> b) & 1ull);
-            if (__any_sync(0xffffffffu, need)) an_merge<C>(L, a, need, b, A);
-          }
-        }
-#pragma unroll
-        for (int j = 0; j < 4; ++j)
-          if (j < ne) an_close<C>(L, a, (int)((h.w >> (6 * j)) & 63u), lane, qx, qown, qn, tacc, inexact);
-      } else {
-        const int nb = (int)(h.z & 0xFFFFu), ne = (int)(h.z >> 16);
-        for (int j = 0; j < nb; ++j) {
-          const int b = (int)__ldg(a.lists + h.w + j);
-          const bool need = on && ((L.act >> b) & 1ull);
-          if (__any_sync(0xffffffffu, need)) an_merge<C>(L, a, need, b, A);
-        }
-        for (int j = 0; j < ne; ++j)
-          an_close<C>(L, a, (int)__ldg(a.lists + h.w + nb + j), lane, qx, qown, qn, tacc, inexact);
+      // back neighbours (warp uniform); one call site keeps the loop small
+      const bool lng = (h.bs >> 31) != 0u;
+      const int nb = lng ? (int)h.lists : (int)(h.lists & 7u);
+#pragma unroll 1
+      for (int j = 0; j < nb; ++j) {
+        const int b = lng ? (int)__ldg(a.lists + h.off + j) : (int)((h.lists >> (3 + 6 * j)) & 63u);
+        const bool need = on && ((L.act >> b) & 1ull);
+        if (__any_sync(0xffffffffu, need)) an_merge<C>(L, need, b, A);
       }
+    }
+    // regions open at the end of the program; labels cleared for the next genome
+    for (int s = 0; s < a.F; ++s) {
+      const uint32_t la = L.lab + 4 * s;
+      an_close<C>(L, lds_u8(la), lane, qx, qown, qn, a, tacc, inexact);
+      sts_u8(la, 0u);
     }
     an_flush(qx, qown, qn, lane, a, tacc, inexact);
     X128 total = L.total;
-    const bool ovf = L.ovf;
     x_add(total, X128{tacc[2 * lane], tacc[2 * lane + 1]});
     tacc[2 * lane] = tacc[2 * lane + 1] = 0ull;
     __syncwarp();
     if (in_range) {
-      if (ovf && !dead) {
-        fit[i] = __longlong_as_double(0x7ff8000000000000ll);
-        const int32_t at = atomicAdd(a.ovf_count, 1);
-        a.ovf_list[at] = i;
-      } else if (dead) {
+      if (dead) {
         fit[i] = __longlong_as_double(0x7ff0000000000000ll);
       } else {
         // sign-extend the 128-bit dynamic part, scale back, add the constant
@@ -367,47 +355,44 @@ fitness_anchor_kernel(AnArgs a, const uint64_t* __restrict__ pop, int64_t n, dou
   if (inexact) atomicAdd(a.flags, 1ull);
 }
 
-size_t anchor_smem(int C, int Fp) {
+size_t anchor_smem(int C, int F, int Fp) {
   constexpr int T = AN_THREADS, W = AN_THREADS / 32;
-  return (size_t)C * T * 16 + (size_t)W * (AN_QCAP * 16 + 64 * 8 + 64 * 8 + AN_QCAP) +
+  return (size_t)C * T * 16 + (size_t)W * (AN_QCAP * 16 + 64 * 8 + (size_t)F * WT_BYTES + AN_QCAP) +
          (size_t)(T / 4) * Fp * 4;
 }
 
 template <int C>
 int launch_anchor_t(cb_es_plan* p, const uint64_t* d_pop, int64_t n, double* d_fit, cudaStream_t stream) {
   const int Fp = p->F | 1;  // odd row stride: a uniform slot hits 8 distinct banks
-  const size_t smem = anchor_smem(C, Fp);
-  CB_CUDA_TRY(cudaFuncSetAttribute(fitness_anchor_kernel<C>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   (int)smem));
+  const size_t smem = anchor_smem(C, p->F, Fp);
+  if (cb_smem_claim((const void*)fitness_anchor_kernel<C>, smem))
+    CB_CUDA_TRY(cudaFuncSetAttribute(fitness_anchor_kernel<C>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)smem));
   int per_sm = 0;
   CB_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fitness_anchor_kernel<C>, AN_THREADS,
                                                             smem));
   if (per_sm < 1) per_sm = 1;
-  if (p->d_ovf_list.n < (size_t)std::max<int64_t>(n, 1)) CB_CUDA_TRY(p->d_ovf_list.alloc((size_t)n));
-  if (p->d_ovf_count.n < 1) CB_CUDA_TRY(p->d_ovf_count.alloc(1));
-  CB_CUDA_TRY(cudaMemsetAsync(p->d_ovf_count.p, 0, sizeof(int32_t), stream));
   AnArgs a;
   a.M = p->M;
   a.words = p->words;
   a.shift = p->anchor_shift;
   a.n_infeas = (int32_t)p->d_an_infeas_word.n;
   a.Fp = Fp;
+  a.F = p->F;
   a.base_const = p->base_const;
   const fx192 ex = fx_shr(p->eps, p->anchor_shift);
   a.eps = {ex.w[0], ex.w[1]};
   a.step = reinterpret_cast<const AStep*>(p->d_astep.p);
-  a.repc = reinterpret_cast<const ulonglong2*>(p->d_arepc.p);
-  a.term1 = reinterpret_cast<const ulonglong2*>(p->d_aterm.p);
+  a.t1m = reinterpret_cast<const ulonglong2*>(p->d_aterm.p);
+  a.srec = reinterpret_cast<const uint4*>(p->d_arepc.p);
   a.lists = p->d_alists.p;
   a.infeas_word = p->d_an_infeas_word.p;
   a.infeas_mask = p->d_an_infeas_mask.p;
   a.rt = p->d_rt.p;
   a.flags = p->d_flags.p;
-  a.ovf_count = p->d_ovf_count.p;
-  a.ovf_list = p->d_ovf_list.p;
   const int64_t want = (n + AN_THREADS - 1) / AN_THREADS;
   const int64_t grid = std::min<int64_t>(want, (int64_t)per_sm * cb_sm_count());
-  const size_t spill = (size_t)(64 - C) * grid * AN_THREADS * 2;  // uint64 words
+  const size_t spill = (size_t)std::max(p->F - C, 1) * grid * AN_THREADS * 2;  // uint64 words
   DBuf<uint64_t>* sp;
   {
     std::lock_guard<std::mutex> lock(p->aspill_mu);
@@ -419,8 +404,7 @@ int launch_anchor_t(cb_es_plan* p, const uint64_t* d_pop, int64_t n, double* d_f
   a.spill = reinterpret_cast<ulonglong2*>(sp->p);
   fitness_anchor_kernel<C><<<(unsigned)grid, AN_THREADS, smem, stream>>>(a, d_pop, n, d_fit);
   CB_CUDA_TRY(cudaGetLastError());
-  // genomes that ran out of pool entries: warp-per-genome kernel over the list
-  return launch_fitness_wide_list(p, d_pop, n, d_fit, p->d_ovf_list.p, p->d_ovf_count.p, stream);
+  return CB_OK;
 }
 
 }  // namespace
@@ -482,38 +466,36 @@ int build_anchor_plan(cb_es_plan* P) {
     cnt[p] = r.cnt;
   }
   std::vector<AStep> steps(M);
-  // per unit: [rep | cnt << 108, off] (read when it joins a merged region,
-  // whose members' own kernel terms leave the total then) and term1 - off
-  // (a one-unit region replaces the unit's own term by its region term)
-  std::vector<uint64_t> repc((size_t)M * 4), term((size_t)M * 2);
+  // per position: term1 - off (added when the unit is ON), and its slot
+  // record: end, replacement sum | count << 108, term1 (the slot table entry)
+  std::vector<uint64_t> srec((size_t)M * 6), term((size_t)M * 2);
   std::vector<uint8_t> lists;
   for (int32_t p = 0; p < M && P->anchor_wide_ok; ++p) {
     const UnitRec& r = P->prog[p];
     AStep h;
     std::memset(&h, 0, sizeof(h));
     h.bs = (r.bit >= 0 ? (uint32_t)r.bit : 0xFFFFFFu) | ((uint32_t)r.slot << 24);
-    h.last = P->prog_last[p];
-    if (r.nback <= 4 && r.nend <= 4) {
-      h.lists = (uint32_t)r.nback | ((uint32_t)r.nend << 3);
-      for (int j = 0; j < r.nback; ++j) h.lists |= (uint32_t)P->prog_slots[r.back_off + j] << (6 + 6 * j);
-      for (int j = 0; j < r.nend; ++j) h.ends |= (uint32_t)P->prog_slots[r.end_off + j] << (6 * j);
+    if (r.nback <= 4) {
+      h.lists = (uint32_t)r.nback;
+      for (int j = 0; j < r.nback; ++j) h.lists |= (uint32_t)P->prog_slots[r.back_off + j] << (3 + 6 * j);
     } else {
       h.bs |= 1u << 31;
-      h.lists = (uint32_t)r.nback | ((uint32_t)r.nend << 16);
-      h.ends = (uint32_t)lists.size();
+      h.lists = (uint32_t)r.nback;
+      h.off = (uint32_t)lists.size();
       for (int j = 0; j < r.nback; ++j) lists.push_back(P->prog_slots[r.back_off + j]);
-      for (int j = 0; j < r.nend; ++j) lists.push_back(P->prog_slots[r.end_off + j]);
     }
     steps[p] = h;
-    const fx192 xo = fx_shr(r.off, lo), xr = fx_shr(r.rep, lo);
-    fx192 xt = fx_shr(r.term1, lo);
-    fx_sub(xt, xo);  // two's complement in the low 128 bits
-    repc[4 * p] = xr.w[0];
-    repc[4 * p + 1] = xr.w[1] | ((uint64_t)r.cnt << 44);
-    repc[4 * p + 2] = xo.w[0];
-    repc[4 * p + 3] = xo.w[1];
-    term[2 * p] = xt.w[0];
-    term[2 * p + 1] = xt.w[1];
+    const fx192 xo = fx_shr(r.off, lo), xr = fx_shr(r.rep, lo), xt = fx_shr(r.term1, lo);
+    fx192 xtm = xt;
+    fx_sub(xtm, xo);  // two's complement in the low 128 bits
+    srec[6 * p] = (uint64_t)(uint32_t)P->prog_last[p];
+    srec[6 * p + 1] = 0;
+    srec[6 * p + 2] = xr.w[0];
+    srec[6 * p + 3] = xr.w[1] | ((uint64_t)r.cnt << 44);
+    srec[6 * p + 4] = xt.w[0];
+    srec[6 * p + 5] = xt.w[1];
+    term[2 * p] = xtm.w[0];
+    term[2 * p + 1] = xtm.w[1];
   }
   if (lists.empty()) lists.push_back(0);
   std::vector<int32_t> iw;
@@ -567,7 +549,7 @@ int build_anchor_plan(cb_es_plan* P) {
   if (P->anchor_wide_ok &&
       ((e = P->d_astep.upload(reinterpret_cast<const uint8_t*>(steps.data()), steps.size() * sizeof(AStep))) !=
            cudaSuccess ||
-       (e = P->d_arepc.upload(repc)) != cudaSuccess ||
+       (e = P->d_arepc.upload(srec)) != cudaSuccess ||
        (e = P->d_aterm.upload(term)) != cudaSuccess || (e = P->d_alists.upload(lists)) != cudaSuccess ||
        (e = P->d_an_infeas_word.upload(iw)) != cudaSuccess ||
        (e = P->d_an_infeas_mask.upload(im)) != cudaSuccess)) {
@@ -581,10 +563,10 @@ int build_anchor_plan(cb_es_plan* P) {
 int launch_fitness_anchor(cb_es_plan* p, const uint64_t* d_pop, int64_t n, double* d_fit,
                           cudaStream_t stream) {
   if (!p->anchor_wide_ok) return launch_fitness_wide(p, d_pop, n, d_fit, stream);
-  // C pool entries per lane live in shared memory, the other 64 - C in a
-  // global spill area (touched only by genomes with more live merged
-  // components): 8 keeps 32 warps resident per SM on a 36-slot program
+  // C pool entries per lane live in shared memory, the other F - C (at most
+  // F entries are ever held) in a global spill area
   const int C = p->pool_entries;
+  if (C <= 4) return launch_anchor_t<4>(p, d_pop, n, d_fit, stream);
   if (C <= 8) return launch_anchor_t<8>(p, d_pop, n, d_fit, stream);
   if (C <= 12) return launch_anchor_t<12>(p, d_pop, n, d_fit, stream);
   return launch_anchor_t<16>(p, d_pop, n, d_fit, stream);

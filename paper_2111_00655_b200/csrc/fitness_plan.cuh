@@ -91,12 +91,6 @@ struct cb_es_plan {
   std::map<cudaStream_t, std::unique_ptr<DBuf<uint64_t>>> aspill;
   std::mutex aspill_mu;
   int32_t pool_entries = 16;
-  // ON-unit walk (fitness_onwalk.cu, <= 64 slots): per-position records
-  bool ow_ok = false;
-  bool ow_seq = false;            // genome bit b is program position b
-  DBuf<uint8_t> d_owrec;          // OwRec[M] (48 bytes)
-  DBuf<uint64_t> d_owmrec;        // [M][4]: rep | cnt << 108, term1 (X)
-  DBuf<uint32_t> d_owlists;       // long back lists
   cudaStream_t host_stream = nullptr;  // single-chunk cb_fitness_host calls
   ~cb_es_plan() {
     if (host_stream) cudaStreamDestroy(host_stream);
@@ -117,8 +111,6 @@ struct cb_es_plan {
   // packed anchor walk (fitness_packed128.cu, <= 8 slots): 16-byte step headers
   bool pa_ok = false;
   DBuf<uint32_t> d_pahdr;
-  DBuf<int64_t> d_ovf_list;
-  DBuf<int32_t> d_ovf_count;
   bool packed_ok = true;     // every unit's back / end lists fit the packed header
   int32_t force_path = -1;  // -1 auto, 0 union-find, 1 frontier, 2 frontier (smem labels),
                             // 3 sparse warp-per-genome walk, 4 anchor walk (thread per genome),
@@ -129,11 +121,8 @@ struct cb_es_plan {
 // fitness_wide.cu: warp-per-genome sparse walk of the frontier program (F <= 128)
 int launch_fitness_wide(cb_es_plan* p, const uint64_t* d_pop, int64_t n, double* d_fit,
                         cudaStream_t stream);
-// the same over the genome indices list[0 .. *list_count) (count on the device)
-int launch_fitness_wide_list(cb_es_plan* p, const uint64_t* d_pop, int64_t n_max, double* d_fit,
-                             const int64_t* list, const int32_t* list_count, cudaStream_t stream);
 // fitness_anchor.cu: 128-bit window analysis + step headers (plan time);
-// thread-per-genome anchor walk (F <= 64), overflow to the wide kernel
+// thread-per-genome lockstep anchor walk (F <= 64)
 int build_anchor_plan(cb_es_plan* p);
 // fitness_packed128.cu: packed-label walk (<= 16 slots) in the 128-bit window
 int launch_fitness_packed128(cb_es_plan* p, const uint64_t* d_pop, int64_t n, double* d_fit,
@@ -150,8 +139,3 @@ int launch_fused_generation(cb_es_plan* p, const BreedArgs& br, uint64_t* d_chil
                             double* d_fit, cudaStream_t stream);
 int launch_fitness_anchor(cb_es_plan* p, const uint64_t* d_pop, int64_t n, double* d_fit,
                           cudaStream_t stream);
-// fitness_onwalk.cu: per-lane walk over the genome's ON units (F <= 64)
-int build_onwalk_plan(cb_es_plan* p);
-int launch_fitness_onwalk(cb_es_plan* p, const uint64_t* d_pop, int64_t n, double* d_fit,
-                          cudaStream_t stream);
-

@@ -328,13 +328,3 @@ int launch_fitness_wide(cb_es_plan* p, const uint64_t* d_pop, int64_t n, double*
   if (p->F <= 64) return launch_wide_t<2>(p, d_pop, n, d_fit, stream);
   return launch_wide_t<4>(p, d_pop, n, d_fit, stream);
 }
-
-int launch_fitness_wide_list(cb_es_plan* p, const uint64_t* d_pop, int64_t n_max, double* d_fit,
-                             const int64_t* list, const int32_t* list_count, cudaStream_t stream) {
-  // the count lives on the device: size the grid for the worst case, idle
-  // warps exit at once
-  const int64_t n = std::min<int64_t>(n_max, (int64_t)4 * cb_sm_count() * 16);
-  if (p->F <= 32) return launch_wide_t<1>(p, d_pop, n, d_fit, stream, list, list_count);
-  if (p->F <= 64) return launch_wide_t<2>(p, d_pop, n, d_fit, stream, list, list_count);
-  return launch_wide_t<4>(p, d_pop, n, d_fit, stream, list, list_count);
-}

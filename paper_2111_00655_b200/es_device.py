@@ -103,10 +103,8 @@ class DeviceEvolution:
     def launches_for(plan: FitnessPlan, fused: bool = False) -> int:
         """Kernels of libcollage_b200.so per generation: fitness min/max and the
         tournament order keys, (fused | breed + fitness), the two CUB argmin
-        kernels and their unpack (+ the overflow list kernel when the anchor
-        walk prices the plan); torch's copies of the elite row are not counted."""
-        return (6 if fused else 7) + (1 if plan.kernel_name() in ("fitness_anchor_kernel",
-                                                                  "fitness_onwalk_kernel") else 0)
+        kernels and their unpack; torch's copies of the elite row are not counted."""
+        return 6 if fused else 7
 
     # -- helpers -----------------------------------------------------------------------
     def _stream(self) -> int:

@@ -224,7 +224,7 @@ class FitnessPlan:
         frontier slots; 'packed128': the packed-label walk in the plan's
         128-bit window; 'packed_anchor': the same with anchor labels, <= 8
         slots) | 'anchor' (thread per genome, lockstep, <= 64 slots) |
-        'onwalk' (thread per genome, visiting only its ON units, <= 64 slots) | 'wide'
+        'wide'
         (warp per genome, sparse walk, <= 128 slots) | 'unionfind'
         (warp/CTA per genome, any plan).  All give identical results;
         `auto` picks the packed anchor kernel for <= 8 slots, the
@@ -232,7 +232,7 @@ class FitnessPlan:
         when the plan fits one), the
         anchor kernel up to 64, the wide kernel up to 128, else union-find."""
         code = {"auto": -1, "unionfind": 0, "frontier": 1, "frontier_smem": 2, "wide": 3,
-                "anchor": 4, "packed128": 5, "packed_anchor": 6, "fsm": 7, "onwalk": 8}[path]
+                "anchor": 4, "packed128": 5, "packed_anchor": 6, "fsm": 7}[path]
         nat.check(nat.lib().cb_es_plan_set_path(self.handle.raw, code))
 
     def kernel_name(self) -> str:
@@ -255,11 +255,6 @@ class FitnessPlan:
             f = name[name.index('<') + 1:].split(',')[0]
             return f"fitness_pa_breed_kernel<{f}, {self.words}>"
         return name
-
-    def has_onwalk(self) -> bool:
-        """Whether the 'onwalk' path applies (<= 64 frontier slots, packed
-        sums inside the 128-bit window)."""
-        return bool(self.info.onwalk)
 
     def has_fsm(self) -> bool:
         """Whether the 'fsm' path applies (finite-state program built)."""

@@ -211,5 +211,5 @@ def test_random100k_fitness_matches_oracle(gpu):
     kernels = [[a.backend_pattern.order, a.root, sorted(a.nodes)] for a in res.placement.assignments]
     assert _digest(kernels) == pin["kernels_sha256"]
     want = oc.fitness(kernels, bs.graph_backend, packed, threads=os.cpu_count() or 1)
-    assert plan.kernel_name() == "fitness_onwalk_kernel"
+    assert plan.kernel_name() == "fitness_anchor_kernel"
     assert np.array_equal(got, want)

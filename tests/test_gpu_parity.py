@@ -155,7 +155,7 @@ def test_fitness_paths_agree_with_oracle(gpu, case):
     plan.set_path("unionfind")
     assert np.array_equal(plan.evaluate(genomes), want)
     if plan.info.frontier_slots:
-        for path in ("wide", "anchor") + (("onwalk",) if plan.has_onwalk() else ()):
+        for path in ("wide", "anchor"):
             plan.set_path(path)
             assert np.array_equal(plan.evaluate(genomes), want), path
         plan.set_pool(1)

@@ -56,7 +56,7 @@ def test_wide_plan_matches_oracle(gpu, seed, n, window):
     want = oc.fitness(kernels, bs.graph_backend, genomes, threads=8)
     got = plan.evaluate(genomes)  # auto: wide kernel for > 16 slots
     assert np.array_equal(got, want)
-    for path in ("wide", "anchor") + (("onwalk",) if plan.has_onwalk() else ()):
+    for path in ("wide", "anchor"):
         plan.set_path(path)
         assert np.array_equal(plan.evaluate(genomes), want), path
     # tiny pools: most genomes overflow to the warp-per-genome kernel
@@ -79,7 +79,7 @@ def test_wide_kernel_agrees_on_models(gpu, name):
     genomes = _genomes(plan, np.random.default_rng(5), 2000)
     plan.set_path("auto")
     want = plan.evaluate(genomes)
-    for path in ("wide", "anchor", "frontier") + (("onwalk",) if plan.has_onwalk() else ()) + (("packed128",) if plan.has_packed128() else ()) + (("packed_anchor",) if plan.has_packed_anchor() else ()) + (("fsm",) if plan.has_fsm() else ()):
+    for path in ("wide", "anchor", "frontier") + (("packed128",) if plan.has_packed128() else ()) + (("packed_anchor",) if plan.has_packed_anchor() else ()) + (("fsm",) if plan.has_fsm() else ()):
         plan.set_path(path)
         assert np.array_equal(plan.evaluate(genomes), want), path
     plan.set_path("auto")
@@ -157,8 +157,6 @@ def test_edge_plans_every_path(gpu, n_rows):
         paths = ["auto", "unionfind"]
         if plan.info.frontier_slots:
             paths += ["wide", "anchor"] if plan.info.window_shift >= 0 else ["wide"]
-        if plan.has_onwalk():
-            paths.append("onwalk")
         if 0 < plan.info.frontier_slots <= 32:
             paths += ["frontier", "frontier_smem"]
         if plan.has_packed128():
