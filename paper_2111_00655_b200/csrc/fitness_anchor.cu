@@ -29,7 +29,7 @@
 //   slot is handed on: the step reading the slot's old label queues the
 //   sum for pricing (round, __dmul_rn by r(n), + eps: warp batches of 32).
 //   Every pool entry is named by one anchor label, so a lane never holds
-//   more than F entries (C in shared memory, the rest in a global spill).
+//   more than F entries (C in shared memory, the rest in local memory).
 // * Per-warp slot table.  The unit currently in each slot is the same for
 //   all lanes: (end, replacement sum | count, term1) per slot, written by
 //   three lanes per step from the unit's 48-byte slot record, so merges
@@ -86,7 +86,6 @@ struct AnArgs {
   const uint64_t* __restrict__ infeas_mask;
   const double* __restrict__ rt;
   unsigned long long* flags;
-  ulonglong2* spill;  // [64 - C][resident threads]: pool entries beyond the shared ones
 };
 
 // Price the queued regions (one per lane) and add each term to its owner's
@@ -140,32 +139,32 @@ constexpr uint32_t WT_BYTES = 48;  // slot table entry: end | rep, count | term1
 struct AnLane {
   uint32_t lab;    // shared address of this lane's label for slot 0 (slot s at + 4 s)
   uint32_t pool;   // shared address of this lane's pool entry 0 (entry e < C at + e * 16 T)
-  ulonglong2* spill;  // this lane's global entries (entry e >= C at [(e - C) * stride])
-  int64_t spill_stride;
   uint32_t wtab;   // shared address of the warp's slot table (slot s at + 48 s)
   uint64_t act;    // slots holding an ON unit
   uint64_t pfree;  // free pool entries
   X128 total;      // genome-dependent part of the cost (two's complement)
 };
 
+// pool entries e >= C live in the thread's local memory (lane-interleaved,
+// L1-cached; at most F <= 64 entries are ever held)
 template <int C>
-__device__ __forceinline__ X128 pool_ld(const AnLane& L, uint32_t e) {
+__device__ __forceinline__ X128 pool_ld(const AnLane& L, const ulonglong2* spill, uint32_t e) {
   if (e < (uint32_t)C) return lds_x(L.pool + e * (16 * AN_THREADS));
-  const ulonglong2 v = L.spill[(int64_t)(e - C) * L.spill_stride];
+  const ulonglong2 v = spill[e - C];
   return {v.x, v.y};
 }
 template <int C>
-__device__ __forceinline__ void pool_st(const AnLane& L, uint32_t e, const X128& v) {
+__device__ __forceinline__ void pool_st(const AnLane& L, ulonglong2* spill, uint32_t e, const X128& v) {
   if (e < (uint32_t)C)
     sts_x(L.pool + e * (16 * AN_THREADS), v);
   else
-    L.spill[(int64_t)(e - C) * L.spill_stride] = make_ulonglong2(v.lo, v.hi);
+    spill[e - C] = make_ulonglong2(v.lo, v.hi);
 }
 
 // Back edge to slot b of the new unit whose component is anchored at A:
 // find b's anchor, merge the two components at the later-ending anchor.
 template <int C>
-__device__ __forceinline__ void an_merge(AnLane& L, bool need, int b, int& A) {
+__device__ __forceinline__ void an_merge(AnLane& L, ulonglong2* spill, bool need, int b, int& A) {
   int x = b;
   uint32_t lx = need ? lds_u8(L.lab + 4 * b) : L_ANCHOR;
   if (!(lx & L_ANCHOR)) {
@@ -188,13 +187,13 @@ __device__ __forceinline__ void an_merge(AnLane& L, bool need, int b, int& A) {
   // merged components: their pool sums; one-unit components: the unit's
   // replacement sum, and its one-unit term leaves the total
   if (lW & L_MERGED) {
-    sW = pool_ld<C>(L, lW & 63u);
+    sW = pool_ld<C>(L, spill, lW & 63u);
   } else {
     sW = lds_x(L.wtab + WT_BYTES * Wn + 16);
     x_sub(L.total, lds_x(L.wtab + WT_BYTES * Wn + 32));
   }
   if (lX & L_MERGED) {
-    sX = pool_ld<C>(L, lX & 63u);
+    sX = pool_ld<C>(L, spill, lX & 63u);
   } else {
     sX = lds_x(L.wtab + WT_BYTES * Xn + 16);
     x_sub(L.total, lds_x(L.wtab + WT_BYTES * Xn + 32));
@@ -211,7 +210,7 @@ __device__ __forceinline__ void an_merge(AnLane& L, bool need, int b, int& A) {
     e = (uint32_t)(__ffsll((long long)L.pfree) - 1);
     L.pfree &= L.pfree - 1ull;
   }
-  pool_st<C>(L, e, sW);
+  pool_st<C>(L, spill, e, sW);
   sts_u8(L.lab + 4 * Wn, L_ANCHOR | L_MERGED | e);
   sts_u8(L.lab + 4 * Xn, (uint32_t)Wn);
   A = Wn;
@@ -220,14 +219,15 @@ __device__ __forceinline__ void an_merge(AnLane& L, bool need, int b, int& A) {
 // The label a slot held before it is handed on (or the program ends): a
 // merged anchor's region is complete -- queue it; all lanes take part.
 template <int C>
-__device__ __forceinline__ void an_close(AnLane& L, uint32_t old, int lane, ulonglong2* qx, uint8_t* qown,
+__device__ __forceinline__ void an_close(AnLane& L, const ulonglong2* spill, uint32_t old, int lane,
+                                         ulonglong2* qx, uint8_t* qown,
                                          int& qn, const AnArgs& a, unsigned long long* tacc, bool& inexact) {
   const bool emit = (old & (L_ANCHOR | L_MERGED)) == (L_ANCHOR | L_MERGED);
   const unsigned closing = __ballot_sync(0xffffffffu, emit);
   if (!closing) return;
   X128 ev = {0ull, 0ull};
   if (emit) {
-    ev = pool_ld<C>(L, old & 63u);
+    ev = pool_ld<C>(L, spill, old & 63u);
     L.pfree |= 1ull << (old & 63u);
   }
   const int cnt = __popc(closing);
@@ -244,7 +244,7 @@ __device__ __forceinline__ void an_close(AnLane& L, uint32_t old, int lane, ulon
 }
 
 template <int C>
-__global__ void __launch_bounds__(AN_THREADS, 8)
+__global__ void __launch_bounds__(AN_THREADS, 7)
 fitness_anchor_kernel(AnArgs a, const uint64_t* __restrict__ pop, int64_t n, double* __restrict__ fit) {
   constexpr int T = AN_THREADS, W = AN_THREADS / 32;
   extern __shared__ __align__(16) unsigned char an_smem[];
@@ -262,8 +262,7 @@ fitness_anchor_kernel(AnArgs a, const uint64_t* __restrict__ pop, int64_t n, dou
   L.lab = (uint32_t)__cvta_generic_to_shared(LAB + (t >> 2) * a.Fp * 4 + (t & 3));
   L.pool = (uint32_t)__cvta_generic_to_shared(pool + t);
   L.wtab = (uint32_t)__cvta_generic_to_shared(wtab_all + (size_t)warp * a.F * WT_BYTES);
-  L.spill_stride = (int64_t)gridDim.x * T;
-  L.spill = a.spill + (int64_t)blockIdx.x * T + t;
+  ulonglong2 spill[64 - C];
   tacc[2 * lane] = tacc[2 * lane + 1] = 0ull;
   for (int s = 0; s < a.F; ++s) sts_u8(L.lab + 4 * s, 0u);
   __syncwarp();
@@ -313,7 +312,7 @@ fitness_anchor_kernel(AnArgs a, const uint64_t* __restrict__ pop, int64_t n, dou
       }
       // the slot's previous owner is complete
       const uint32_t labS = L.lab + 4 * S;
-      an_close<C>(L, lds_u8(labS), lane, qx, qown, qn, a, tacc, inexact);
+      an_close<C>(L, spill, lds_u8(labS), lane, qx, qown, qn, a, tacc, inexact);
       sts_u8(labS, on ? L_ANCHOR : 0u);
       L.act = on ? (L.act | (1ull << S)) : (L.act & ~(1ull << S));
       if (on) x_add(L.total, X128{tm.x, tm.y});
@@ -326,13 +325,13 @@ fitness_anchor_kernel(AnArgs a, const uint64_t* __restrict__ pop, int64_t n, dou
       for (int j = 0; j < nb; ++j) {
         const int b = lng ? (int)__ldg(a.lists + h.off + j) : (int)((h.lists >> (3 + 6 * j)) & 63u);
         const bool need = on && ((L.act >> b) & 1ull);
-        if (__any_sync(0xffffffffu, need)) an_merge<C>(L, need, b, A);
+        if (__any_sync(0xffffffffu, need)) an_merge<C>(L, spill, need, b, A);
       }
     }
     // regions open at the end of the program; labels cleared for the next genome
     for (int s = 0; s < a.F; ++s) {
       const uint32_t la = L.lab + 4 * s;
-      an_close<C>(L, lds_u8(la), lane, qx, qown, qn, a, tacc, inexact);
+      an_close<C>(L, spill, lds_u8(la), lane, qx, qown, qn, a, tacc, inexact);
       sts_u8(la, 0u);
     }
     an_flush(qx, qown, qn, lane, a, tacc, inexact);
@@ -392,16 +391,6 @@ int launch_anchor_t(cb_es_plan* p, const uint64_t* d_pop, int64_t n, double* d_f
   a.flags = p->d_flags.p;
   const int64_t want = (n + AN_THREADS - 1) / AN_THREADS;
   const int64_t grid = std::min<int64_t>(want, (int64_t)per_sm * cb_sm_count());
-  const size_t spill = (size_t)std::max(p->F - C, 1) * grid * AN_THREADS * 2;  // uint64 words
-  DBuf<uint64_t>* sp;
-  {
-    std::lock_guard<std::mutex> lock(p->aspill_mu);
-    auto& slot = p->aspill[stream];
-    if (!slot) slot.reset(new DBuf<uint64_t>());
-    sp = slot.get();
-  }
-  if (sp->n < spill) CB_CUDA_TRY(sp->alloc(spill));
-  a.spill = reinterpret_cast<ulonglong2*>(sp->p);
   fitness_anchor_kernel<C><<<(unsigned)grid, AN_THREADS, smem, stream>>>(a, d_pop, n, d_fit);
   CB_CUDA_TRY(cudaGetLastError());
   return CB_OK;
@@ -564,7 +553,7 @@ int launch_fitness_anchor(cb_es_plan* p, const uint64_t* d_pop, int64_t n, doubl
                           cudaStream_t stream) {
   if (!p->anchor_wide_ok) return launch_fitness_wide(p, d_pop, n, d_fit, stream);
   // C pool entries per lane live in shared memory, the other F - C (at most
-  // F entries are ever held) in a global spill area
+  // F entries are ever held) in the thread's local memory
   const int C = p->pool_entries;
   if (C <= 4) return launch_anchor_t<4>(p, d_pop, n, d_fit, stream);
   if (C <= 8) return launch_anchor_t<8>(p, d_pop, n, d_fit, stream);

@@ -82,15 +82,11 @@ struct cb_es_plan {
   DBuf<int32_t> d_acnt;     // [M]
   bool anchor_wide_ok = false;  // packed-sum anchor walk usable (span and counts fit)
   DBuf<uint8_t> d_astep;        // AStep[M] 16-byte step records
-  DBuf<uint64_t> d_arepc, d_aterm;  // [M][4] rep | cnt << 108, off; [M][2] term1 - off (X)
-  DBuf<uint8_t> d_alists;       // long back / end slot lists
+  DBuf<uint64_t> d_arepc, d_aterm;  // [M][6] slot records (end | rep, count | term1); [M][2] term1 - off
+  DBuf<uint8_t> d_alists;       // long back lists
   DBuf<int32_t> d_an_infeas_word;  // genome words holding infeasible bits, and their masks
   DBuf<uint64_t> d_an_infeas_mask;
-  // pool entries beyond the shared ones, per resident thread -- one area per
-  // stream, so launches on different streams (the host pipeline) never share
-  std::map<cudaStream_t, std::unique_ptr<DBuf<uint64_t>>> aspill;
-  std::mutex aspill_mu;
-  int32_t pool_entries = 16;
+  int32_t pool_entries = 16;  // anchor walk: merged-sum pool entries per lane in shared memory
   cudaStream_t host_stream = nullptr;  // single-chunk cb_fitness_host calls
   ~cb_es_plan() {
     if (host_stream) cudaStreamDestroy(host_stream);

@@ -50,8 +50,23 @@ class DPStats:
     computations: int = 0
     states_peak: int = 0
 
+    # measure_calls / cache_hits / computations of a device pricing pass are
+    # settled when first read (the reference's per-candidate cache protocol
+    # is replayed lazily, see cost._account)
+    def __getattribute__(self, name: str):
+        if name in _LAZY_COUNTERS:
+            d = object.__getattribute__(self, "__dict__")
+            settle = d.pop("_settle", None)
+            if settle is not None:
+                settle(self)
+        return object.__getattribute__(self, name)
+
     def to_json(self) -> dict:
-        return dict(self.__dict__)
+        self.measure_calls  # settle
+        return {k: v for k, v in self.__dict__.items() if not k.startswith("_")}
+
+
+_LAZY_COUNTERS = frozenset(("measure_calls", "cache_hits", "computations"))
 
 
 @dataclass
@@ -134,9 +149,20 @@ def optimize(g: ComputationGraph, registry: PatternRegistry, measurer: Measurer,
     stats.max_compatible_states = 1 if table.n_matches else 0
     stats.relaxations = int(table.n_matches)
     stats.states_peak = len(g.nodes) + 1
-    stats.measure_calls = measurer.calls - c0
-    stats.cache_hits = measurer.cache_hits - h0
-    stats.computations = measurer.computations - p0
+    acct = getattr(table, "_account", None)
+    if acct is not None and getattr(table, "_priced", (None,))[0] is measurer:
+        # device pricing: this pass's share of the reference's cache protocol,
+        # settled (replayed) when a counter is first read
+        def settle(st, acct=acct, cache=measurer.cache):
+            cache._flush()
+            st.measure_calls = acct.get("calls", 0)
+            st.cache_hits = acct.get("cache_hits", 0)
+            st.computations = acct.get("computations", 0)
+        stats.__dict__["_settle"] = settle
+    else:
+        stats.measure_calls = measurer.calls - c0
+        stats.cache_hits = measurer.cache_hits - h0
+        stats.computations = measurer.computations - p0
     device = {"device_ms": res.device_ms, "levels": res.n_levels, "launches": res.n_launches,
               "ties": res.ties, "walk_steps": res.walk_steps,
               "rounding_window_safe": bool(res.window_safe),
