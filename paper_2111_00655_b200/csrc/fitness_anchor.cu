@@ -40,6 +40,7 @@
 // warp the slot table, the region queue and the owner accumulators.
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 
 #include "fitness_plan.cuh"
@@ -49,7 +50,8 @@
 
 namespace {
 
-// 16-byte step record
+// 80-byte step record (five 16-byte chunks): the step header, term1 - off
+// (added when the unit is ON) and the unit's slot-table entry
 struct __align__(16) AStep {
   uint32_t bs;     // genome bit (bits 0-23; 0xFFFFFF: always-on fixed unit) | slot << 24 | long << 31
   uint32_t lists;  // short: nback (3 bits) | back slot j at 3 + 6 j (j < 4); long: nback
@@ -57,9 +59,18 @@ struct __align__(16) AStep {
   uint32_t pad;
 };
 static_assert(sizeof(AStep) == 16, "AStep layout");
+constexpr int REC_CHUNKS = 5;             // AStep | term1 - off | end | rep, count | term1
+constexpr int REC_BYTES = 16 * REC_CHUNKS;
+constexpr int WT_OFF = 32;                // slot-table part of a record
+constexpr uint32_t WT_BYTES = 48;         // slot table entry: end | rep, count | term1
+constexpr int CH = 32;                    // steps per staged record chunk
 
+// labels (one byte per slot and lane): 0 = no ON unit, 0x80 = anchor of a
+// one-unit component, 0xC0 | e = anchor of a merged component (pool entry
+// e), 0x40 | s = member pointing to slot s (which ends no earlier)
 constexpr uint32_t L_ANCHOR = 0x80u;
 constexpr uint32_t L_MERGED = 0x40u;
+constexpr uint32_t L_PTR = 0x40u;
 constexpr int CNT_SHIFT = 44;  // count at bit 64 + 44 = 108 of a packed sum
 constexpr uint64_t VAL_HI_MASK = (1ull << CNT_SHIFT) - 1ull;
 
@@ -78,9 +89,7 @@ struct AnArgs {
   int32_t M, words, shift, n_infeas, Fp, F;
   fx192 base_const;
   X128 eps;
-  const AStep* __restrict__ step;
-  const ulonglong2* __restrict__ t1m;   // [M] term1 - off (two's complement X)
-  const uint4* __restrict__ srec;       // [M][3] (end, -, -, -), rep | cnt << 108, term1
+  const uint4* __restrict__ rec;        // [M][5] step records
   const uint8_t* __restrict__ lists;    // long back lists
   const int32_t* __restrict__ infeas_word;
   const uint64_t* __restrict__ infeas_mask;
@@ -126,21 +135,38 @@ __device__ __forceinline__ X128 lds_x(uint32_t a) {
   asm volatile("ld.shared.v2.u64 {%0, %1}, [%2];" : "=l"(v.lo), "=l"(v.hi) : "r"(a));
   return v;
 }
+__device__ __forceinline__ uint4 lds_v4(uint32_t a) {
+  uint4 v;
+  asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(a));
+  return v;
+}
 __device__ __forceinline__ void sts_x(uint32_t a, const X128& v) {
   asm volatile("st.shared.v2.u64 [%0], {%1, %2};" ::"r"(a), "l"(v.lo), "l"(v.hi));
 }
 __device__ __forceinline__ void sts_v4(uint32_t a, const uint4& v) {
   asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(a), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w));
 }
+__device__ __forceinline__ void cp_async16(uint32_t dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;"); }
+__device__ __forceinline__ void cp_async_wait1() { asm volatile("cp.async.wait_group 1;" ::: "memory"); }
 
-constexpr uint32_t WT_BYTES = 48;  // slot table entry: end | rep, count | term1
+// Stage the records of chunk c (steps [c * CH, c * CH + CH) clipped to M)
+// into buffer `buf` -- the block's threads copy 16 bytes each, asynchronously.
+__device__ __forceinline__ void stage_chunk(const AnArgs& a, int32_t c, uint32_t buf, int t, int T) {
+  const int32_t p0 = c * CH;
+  const int32_t n16 = max(0, min(CH, a.M - p0)) * REC_CHUNKS;
+  const uint4* src = a.rec + (int64_t)p0 * REC_CHUNKS;
+  for (int k = t; k < n16; k += T) cp_async16(buf + 16 * k, src + k);
+  cp_async_commit();
+}
 
 // Per-lane walk state.
 struct AnLane {
   uint32_t lab;    // shared address of this lane's label for slot 0 (slot s at + 4 s)
   uint32_t pool;   // shared address of this lane's pool entry 0 (entry e < C at + e * 16 T)
   uint32_t wtab;   // shared address of the warp's slot table (slot s at + 48 s)
-  uint64_t act;    // slots holding an ON unit
   uint64_t pfree;  // free pool entries
   X128 total;      // genome-dependent part of the cost (two's complement)
 };
@@ -161,27 +187,28 @@ __device__ __forceinline__ void pool_st(const AnLane& L, ulonglong2* spill, uint
     spill[e - C] = make_ulonglong2(v.lo, v.hi);
 }
 
-// Back edge to slot b of the new unit whose component is anchored at A:
-// find b's anchor, merge the two components at the later-ending anchor.
+// Back edge to slot b (label lb) of the new unit whose component is
+// anchored at A: find b's anchor, merge the two components at the
+// later-ending anchor.
 template <int C>
-__device__ __forceinline__ void an_merge(AnLane& L, ulonglong2* spill, bool need, int b, int& A) {
-  int x = b;
-  uint32_t lx = need ? lds_u8(L.lab + 4 * b) : L_ANCHOR;
+__device__ __forceinline__ void an_merge(AnLane& L, ulonglong2* spill, bool need, uint32_t b, uint32_t lb,
+                                         uint32_t& A) {
+  uint32_t x = b, lx = need ? lb : L_ANCHOR;
   if (!(lx & L_ANCHOR)) {
-    x = (int)lx;
+    x = lx & 63u;
     lx = lds_u8(L.lab + 4 * x);
   }
   while (__any_sync(0xffffffffu, !(lx & L_ANCHOR))) {  // rare deeper chains
     if (!(lx & L_ANCHOR)) {
-      x = (int)lx;
+      x = lx & 63u;
       lx = lds_u8(L.lab + 4 * x);
     }
   }
-  if (x != b) sts_u8(L.lab + 4 * b, (uint32_t)x);  // path compression (x == b when !need)
+  if (x != b) sts_u8(L.lab + 4 * b, L_PTR | x);  // path compression (x == b when !need)
   if (!need || x == A) return;
   const uint32_t lA = lds_u8(L.lab + 4 * A);
   const bool keepA = lds_s32(L.wtab + WT_BYTES * A) >= lds_s32(L.wtab + WT_BYTES * x);
-  const int Wn = keepA ? A : x, Xn = keepA ? x : A;
+  const uint32_t Wn = keepA ? A : x, Xn = keepA ? x : A;
   const uint32_t lW = keepA ? lA : lx, lX = keepA ? lx : lA;
   X128 sW, sX;
   // merged components: their pool sums; one-unit components: the unit's
@@ -212,7 +239,7 @@ __device__ __forceinline__ void an_merge(AnLane& L, ulonglong2* spill, bool need
   }
   pool_st<C>(L, spill, e, sW);
   sts_u8(L.lab + 4 * Wn, L_ANCHOR | L_MERGED | e);
-  sts_u8(L.lab + 4 * Xn, (uint32_t)Wn);
+  sts_u8(L.lab + 4 * Xn, L_PTR | Wn);
   A = Wn;
 }
 
@@ -243,12 +270,17 @@ __device__ __forceinline__ void an_close(AnLane& L, const ulonglong2* spill, uin
   qn += cnt;
 }
 
+// Block-lockstep walk: the four warps of a block step through the program
+// together, so each 32-step chunk of records is staged once per block
+// (cp.async, double-buffered) and every per-step record read is a
+// broadcast shared-memory load.
 template <int C>
-__global__ void __launch_bounds__(AN_THREADS, 7)
+__global__ void __launch_bounds__(AN_THREADS, 6)
 fitness_anchor_kernel(AnArgs a, const uint64_t* __restrict__ pop, int64_t n, double* __restrict__ fit) {
   constexpr int T = AN_THREADS, W = AN_THREADS / 32;
   extern __shared__ __align__(16) unsigned char an_smem[];
-  ulonglong2* pool = reinterpret_cast<ulonglong2*>(an_smem);                  // [C][T]
+  unsigned char* chunks = an_smem;                                            // [2][CH][80]
+  ulonglong2* pool = reinterpret_cast<ulonglong2*>(chunks + 2 * CH * REC_BYTES);  // [C][T]
   ulonglong2* qx_all = pool + C * T;                                          // [W][QCAP]
   unsigned long long* tacc_all = reinterpret_cast<unsigned long long*>(qx_all + W * AN_QCAP);  // [W][32][2]
   unsigned char* wtab_all = reinterpret_cast<unsigned char*>(tacc_all + W * 64);  // [W][F][48]
@@ -258,6 +290,7 @@ fitness_anchor_kernel(AnArgs a, const uint64_t* __restrict__ pop, int64_t n, dou
   ulonglong2* qx = qx_all + warp * AN_QCAP;
   uint8_t* qown = qown_all + warp * AN_QCAP;
   unsigned long long* tacc = tacc_all + warp * 64;
+  const uint32_t chunk0 = (uint32_t)__cvta_generic_to_shared(chunks);
   AnLane L;
   L.lab = (uint32_t)__cvta_generic_to_shared(LAB + (t >> 2) * a.Fp * 4 + (t & 3));
   L.pool = (uint32_t)__cvta_generic_to_shared(pool + t);
@@ -267,66 +300,67 @@ fitness_anchor_kernel(AnArgs a, const uint64_t* __restrict__ pop, int64_t n, dou
   for (int s = 0; s < a.F; ++s) sts_u8(L.lab + 4 * s, 0u);
   __syncwarp();
   bool inexact = false;
+  const int32_t n_chunks = (a.M + CH - 1) / CH;
   const int64_t stride = (int64_t)gridDim.x * T;
-  for (int64_t base = (int64_t)blockIdx.x * T + (t & ~31); base < n; base += stride) {
-    const int64_t i = base + lane;
+  // every warp of the block runs the same number of genome rounds (block syncs)
+  for (int64_t base = (int64_t)blockIdx.x * T; base < n; base += stride) {
+    const int64_t i = base + t;
     const bool in_range = i < n;
     const uint64_t* gen = pop + (in_range ? i : 0) * a.words;
     bool dead = !in_range;
     for (int32_t j = 0; j < a.n_infeas; ++j)
       dead |= (__ldg(gen + __ldg(a.infeas_word + j)) & __ldg(a.infeas_mask + j)) != 0ull;
-    L.act = 0ull;
     L.pfree = ~0ull;
     L.total = {0ull, 0ull};
     int qn = 0;
     // genome words: w0 = word cur_w, w1 = word cur_w + 1 (loaded ahead)
     int32_t cur_w = -2;
     uint64_t w0 = 0ull, w1 = 0ull;
-    // step p + 1's records are loaded while step p runs
-    AStep nh = a.step[0];
-    ulonglong2 nt = __ldg(a.t1m);
-    const uint4* srl = a.srec + (lane < 3 ? lane : 0);
-    uint4 ns = __ldg(srl);
-    for (int32_t p = 0; p < a.M; ++p) {
-      const AStep h = nh;
-      const ulonglong2 tm = nt;
-      const uint4 sr = ns;
-      if (p + 1 < a.M) {
-        nh = a.step[p + 1];
-        nt = __ldg(a.t1m + p + 1);
-        ns = __ldg(srl + 3 * (int64_t)(p + 1));
-      }
-      const uint32_t bitf = h.bs & 0xFFFFFFu;
-      const int S = (int)((h.bs >> 24) & 63u);
-      // the unit's slot-table entry (three lanes, 16 bytes each)
-      if (lane < 3) sts_v4(L.wtab + WT_BYTES * S + 16 * lane, sr);
-      bool on = !dead;
-      if (bitf != 0xFFFFFFu) {
-        const int32_t wi = (int32_t)(bitf >> 6);
-        if (wi != cur_w) {  // warp uniform
-          w0 = (wi == cur_w + 1) ? w1 : (dead ? 0ull : __ldg(gen + wi));
-          w1 = (!dead && wi + 1 < a.words) ? __ldg(gen + wi + 1) : 0ull;
-          cur_w = wi;
+    __syncthreads();  // the previous round is done with both buffers
+    stage_chunk(a, 0, chunk0, t, T);
+    stage_chunk(a, 1, chunk0 + CH * REC_BYTES, t, T);
+    for (int32_t c = 0; c < n_chunks; ++c) {
+      cp_async_wait1();  // chunk c has landed (c + 1 may be in flight)
+      __syncthreads();
+      const uint32_t buf = chunk0 + (uint32_t)(c & 1) * (CH * REC_BYTES);
+      const int32_t steps = min(CH, a.M - c * CH);
+      for (int32_t k = 0; k < steps; ++k) {
+        const uint32_t r = buf + k * REC_BYTES;
+        const uint4 h = lds_v4(r);
+        const uint32_t bitf = h.x & 0xFFFFFFu;
+        const uint32_t S = (h.x >> 24) & 63u;
+        // the unit's slot-table entry (three lanes, 16 bytes each)
+        if (lane < 3) sts_v4(L.wtab + WT_BYTES * S + 16 * lane, lds_v4(r + WT_OFF + 16 * lane));
+        bool on = !dead;
+        if (bitf != 0xFFFFFFu) {
+          const int32_t wi = (int32_t)(bitf >> 6);
+          if (wi != cur_w) {  // warp uniform
+            w0 = (wi == cur_w + 1) ? w1 : (dead ? 0ull : __ldg(gen + wi));
+            w1 = (!dead && wi + 1 < a.words) ? __ldg(gen + wi + 1) : 0ull;
+            cur_w = wi;
+          }
+          on = on && ((w0 >> (bitf & 63u)) & 1ull);
         }
-        on = (w0 >> (bitf & 63u)) & 1ull;
-      }
-      // the slot's previous owner is complete
-      const uint32_t labS = L.lab + 4 * S;
-      an_close<C>(L, spill, lds_u8(labS), lane, qx, qown, qn, a, tacc, inexact);
-      sts_u8(labS, on ? L_ANCHOR : 0u);
-      L.act = on ? (L.act | (1ull << S)) : (L.act & ~(1ull << S));
-      if (on) x_add(L.total, X128{tm.x, tm.y});
-      __syncwarp();  // slot table entry visible to every lane
-      int A = S;  // anchor of the new unit's component
-      // back neighbours (warp uniform); one call site keeps the loop small
-      const bool lng = (h.bs >> 31) != 0u;
-      const int nb = lng ? (int)h.lists : (int)(h.lists & 7u);
+        // the slot's previous owner is complete
+        const uint32_t labS = L.lab + 4 * S;
+        an_close<C>(L, spill, lds_u8(labS), lane, qx, qown, qn, a, tacc, inexact);
+        sts_u8(labS, on ? L_ANCHOR : 0u);
+        if (on) x_add(L.total, lds_x(r + 16));
+        __syncwarp();  // slot table entry visible to every lane
+        uint32_t A = S;  // anchor of the new unit's component
+        // back neighbours (warp uniform); one call site keeps the loop small
+        const bool lng = (h.x >> 31) != 0u;
+        const int nb = lng ? (int)h.y : (int)(h.y & 7u);
 #pragma unroll 1
-      for (int j = 0; j < nb; ++j) {
-        const int b = lng ? (int)__ldg(a.lists + h.off + j) : (int)((h.lists >> (3 + 6 * j)) & 63u);
-        const bool need = on && ((L.act >> b) & 1ull);
-        if (__any_sync(0xffffffffu, need)) an_merge<C>(L, spill, need, b, A);
+        for (int j = 0; j < nb; ++j) {
+          const uint32_t b = lng ? (uint32_t)__ldg(a.lists + h.z + j) : (h.y >> (3 + 6 * j)) & 63u;
+          const uint32_t lb = lds_u8(L.lab + 4 * b);
+          const bool need = on && lb != 0u;  // b's unit is ON
+          if (__any_sync(0xffffffffu, need)) an_merge<C>(L, spill, need, b, lb, A);
+        }
       }
+      __syncthreads();  // every warp is done with buffer c & 1
+      stage_chunk(a, c + 2, buf, t, T);
     }
     // regions open at the end of the program; labels cleared for the next genome
     for (int s = 0; s < a.F; ++s) {
@@ -351,13 +385,15 @@ fitness_anchor_kernel(AnArgs a, const uint64_t* __restrict__ pop, int64_t n, dou
       }
     }
   }
+  cp_async_wait1();
+  asm volatile("cp.async.wait_all;" ::: "memory");
   if (inexact) atomicAdd(a.flags, 1ull);
 }
 
 size_t anchor_smem(int C, int F, int Fp) {
   constexpr int T = AN_THREADS, W = AN_THREADS / 32;
-  return (size_t)C * T * 16 + (size_t)W * (AN_QCAP * 16 + 64 * 8 + (size_t)F * WT_BYTES + AN_QCAP) +
-         (size_t)(T / 4) * Fp * 4;
+  return (size_t)2 * CH * REC_BYTES + (size_t)C * T * 16 +
+         (size_t)W * (AN_QCAP * 16 + 64 * 8 + (size_t)F * WT_BYTES + AN_QCAP) + (size_t)(T / 4) * Fp * 4;
 }
 
 template <int C>
@@ -381,9 +417,7 @@ int launch_anchor_t(cb_es_plan* p, const uint64_t* d_pop, int64_t n, double* d_f
   a.base_const = p->base_const;
   const fx192 ex = fx_shr(p->eps, p->anchor_shift);
   a.eps = {ex.w[0], ex.w[1]};
-  a.step = reinterpret_cast<const AStep*>(p->d_astep.p);
-  a.t1m = reinterpret_cast<const ulonglong2*>(p->d_aterm.p);
-  a.srec = reinterpret_cast<const uint4*>(p->d_arepc.p);
+  a.rec = reinterpret_cast<const uint4*>(p->d_arec.p);
   a.lists = p->d_alists.p;
   a.infeas_word = p->d_an_infeas_word.p;
   a.infeas_mask = p->d_an_infeas_mask.p;
@@ -454,10 +488,9 @@ int build_anchor_plan(cb_es_plan* P) {
     }
     cnt[p] = r.cnt;
   }
-  std::vector<AStep> steps(M);
-  // per position: term1 - off (added when the unit is ON), and its slot
-  // record: end, replacement sum | count << 108, term1 (the slot table entry)
-  std::vector<uint64_t> srec((size_t)M * 6), term((size_t)M * 2);
+  // per position: the 80-byte step record (header, term1 - off, and the
+  // slot-table entry: end, replacement sum | count << 108, term1)
+  std::vector<uint64_t> rec((size_t)M * 10);
   std::vector<uint8_t> lists;
   for (int32_t p = 0; p < M && P->anchor_wide_ok; ++p) {
     const UnitRec& r = P->prog[p];
@@ -473,18 +506,19 @@ int build_anchor_plan(cb_es_plan* P) {
       h.off = (uint32_t)lists.size();
       for (int j = 0; j < r.nback; ++j) lists.push_back(P->prog_slots[r.back_off + j]);
     }
-    steps[p] = h;
     const fx192 xo = fx_shr(r.off, lo), xr = fx_shr(r.rep, lo), xt = fx_shr(r.term1, lo);
     fx192 xtm = xt;
     fx_sub(xtm, xo);  // two's complement in the low 128 bits
-    srec[6 * p] = (uint64_t)(uint32_t)P->prog_last[p];
-    srec[6 * p + 1] = 0;
-    srec[6 * p + 2] = xr.w[0];
-    srec[6 * p + 3] = xr.w[1] | ((uint64_t)r.cnt << 44);
-    srec[6 * p + 4] = xt.w[0];
-    srec[6 * p + 5] = xt.w[1];
-    term[2 * p] = xtm.w[0];
-    term[2 * p + 1] = xtm.w[1];
+    uint64_t* q = rec.data() + (size_t)p * 10;
+    std::memcpy(q, &h, sizeof(h));
+    q[2] = xtm.w[0];
+    q[3] = xtm.w[1];
+    q[4] = (uint64_t)(uint32_t)P->prog_last[p];
+    q[5] = 0;
+    q[6] = xr.w[0];
+    q[7] = xr.w[1] | ((uint64_t)r.cnt << 44);
+    q[8] = xt.w[0];
+    q[9] = xt.w[1];
   }
   if (lists.empty()) lists.push_back(0);
   std::vector<int32_t> iw;
@@ -536,10 +570,7 @@ int build_anchor_plan(cb_es_plan* P) {
     return CB_ERR_CUDA;
   }
   if (P->anchor_wide_ok &&
-      ((e = P->d_astep.upload(reinterpret_cast<const uint8_t*>(steps.data()), steps.size() * sizeof(AStep))) !=
-           cudaSuccess ||
-       (e = P->d_arepc.upload(srec)) != cudaSuccess ||
-       (e = P->d_aterm.upload(term)) != cudaSuccess || (e = P->d_alists.upload(lists)) != cudaSuccess ||
+      ((e = P->d_arec.upload(rec)) != cudaSuccess || (e = P->d_alists.upload(lists)) != cudaSuccess ||
        (e = P->d_an_infeas_word.upload(iw)) != cudaSuccess ||
        (e = P->d_an_infeas_mask.upload(im)) != cudaSuccess)) {
     cb_set_error(std::string("CUDA error in plan upload: ") + cudaGetErrorString(e));

@@ -81,8 +81,7 @@ struct cb_es_plan {
   DBuf<uint64_t> d_acold;   // [M][6]: rep, off, term1 as 128-bit X (packed-label walks)
   DBuf<int32_t> d_acnt;     // [M]
   bool anchor_wide_ok = false;  // packed-sum anchor walk usable (span and counts fit)
-  DBuf<uint8_t> d_astep;        // AStep[M] 16-byte step records
-  DBuf<uint64_t> d_arepc, d_aterm;  // [M][6] slot records (end | rep, count | term1); [M][2] term1 - off
+  DBuf<uint64_t> d_arec;        // [M][10]: 80-byte step records (header, term1 - off, slot-table entry)
   DBuf<uint8_t> d_alists;       // long back lists
   DBuf<int32_t> d_an_infeas_word;  // genome words holding infeasible bits, and their masks
   DBuf<uint64_t> d_an_infeas_mask;

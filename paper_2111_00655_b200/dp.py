@@ -193,7 +193,7 @@ def optimize(g: ComputationGraph, registry: PatternRegistry, measurer: Measurer,
         roots = np.asarray(g._ids)[table.root[canon]].tolist()
         return [Assignment.fast(sets[i], patterns[pats[i]], roots[i]) for i in range(len(ms))]
 
-    stats.improvements = len(canon)
+    stats.improvements = len(g.nodes)  # every node's subtree optimum is set once
     placement = PlacementStrategy.lazy(len(canon), build)
     t4 = time.perf_counter()
     if validate or (validate is None and len(g.nodes) <= VALIDATE_MAX_NODES):
