@@ -233,8 +233,10 @@ __device__ __forceinline__ void an_merge(AnLane& L, ulonglong2* spill, bool need
   } else if (lX & L_MERGED) {
     e = lX & 63u;
   } else {
-    // at most F <= 64 entries are ever named by anchor labels
-    e = (uint32_t)(__ffsll((long long)L.pfree) - 1);
+    // at most F <= 64 entries are ever named by anchor labels; the low 32
+    // (nearly always) with a 32-bit find-first
+    const uint32_t lo = (uint32_t)L.pfree;
+    e = lo ? (uint32_t)(__ffs(lo) - 1) : 32u + (uint32_t)(__ffs((uint32_t)(L.pfree >> 32)) - 1);
     L.pfree &= L.pfree - 1ull;
   }
   pool_st<C>(L, spill, e, sW);
@@ -339,7 +341,8 @@ fitness_anchor_kernel(AnArgs a, const uint64_t* __restrict__ pop, int64_t n, dou
             w1 = (!dead && wi + 1 < a.words) ? __ldg(gen + wi + 1) : 0ull;
             cur_w = wi;
           }
-          on = on && ((w0 >> (bitf & 63u)) & 1ull);
+          const uint32_t half = (bitf & 32u) ? (uint32_t)(w0 >> 32) : (uint32_t)w0;
+          on = on && ((half >> (bitf & 31u)) & 1u);
         }
         // the slot's previous owner is complete
         const uint32_t labS = L.lab + 4 * S;
