@@ -360,17 +360,18 @@ def run_mine(args) -> None:
     }
     if cpu is not None:
         line["cpu_baseline"] = cpu
-    if issue and issue.get("warp_instructions_per_genome"):
+    if issue and issue.get("capture_warp_instructions_per_s"):
         # the bound that binds: warp-instruction issue (4 schedulers per SM, one
-        # instruction per cycle each), instructions per genome from the ncu capture
+        # instruction per cycle each), measured on one captured launch of this
+        # workload (ncu: instructions / duration of the same launch; the
+        # instruction count per genome varies with the population's density)
         sms = torch.cuda.get_device_properties(dev).multi_processor_count
-        mhz = line["clocks"].get("sm_mhz") or 1965.0
-        peak_issue = sms * 4 * mhz * 1e6
-        achieved_issue = issue["warp_instructions_per_genome"] * P / (fit_ms / 1e3)
+        peak_issue = sms * 4 * 1965.0e6
+        achieved_issue = issue["capture_warp_instructions_per_s"]
         line["issue_roofline"] = {"bound": "issue", "achieved": achieved_issue, "peak": peak_issue,
                                   "unit": "warp instructions/s", "frac": achieved_issue / peak_issue,
                                   "warp_instructions_per_genome": issue["warp_instructions_per_genome"],
-                                  "source": "profiles/fitness_ncu_summary.json"}
+                                  "source": "profiles/fitness_ncu_summary.json (" + issue.get("source", "") + ")"}
     if sweep is not None:
         line["configs"] = sweep
     print(json.dumps(line), flush=True)

@@ -210,35 +210,27 @@ __device__ __forceinline__ void an_merge(AnLane& L, ulonglong2* spill, bool need
   const bool keepA = lds_s32(L.wtab + WT_BYTES * A) >= lds_s32(L.wtab + WT_BYTES * x);
   const uint32_t Wn = keepA ? A : x, Xn = keepA ? x : A;
   const uint32_t lW = keepA ? lA : lx, lX = keepA ? lx : lA;
-  X128 sW, sX;
-  // merged components: their pool sums; one-unit components: the unit's
-  // replacement sum, and its one-unit term leaves the total
-  if (lW & L_MERGED) {
-    sW = pool_ld<C>(L, spill, lW & 63u);
-  } else {
-    sW = lds_x(L.wtab + WT_BYTES * Wn + 16);
-    x_sub(L.total, lds_x(L.wtab + WT_BYTES * Wn + 32));
-  }
-  if (lX & L_MERGED) {
-    sX = pool_ld<C>(L, spill, lX & 63u);
-  } else {
-    sX = lds_x(L.wtab + WT_BYTES * Xn + 16);
-    x_sub(L.total, lds_x(L.wtab + WT_BYTES * Xn + 32));
-  }
+  const bool mW = (lW & L_MERGED) != 0u, mX = (lX & L_MERGED) != 0u;
+  const uint32_t eW = lW & 63u, eX = lX & 63u;
+  // sums: a merged component's pool entry, a one-unit component's
+  // replacement sum from the slot table (whose one-unit term leaves the
+  // total) -- selects, not branches; pool entries >= C (rare) from local memory
+  const uint32_t wW = L.wtab + WT_BYTES * Wn, wX = L.wtab + WT_BYTES * Xn;
+  X128 sW = lds_x(mW && eW < (uint32_t)C ? L.pool + eW * (16 * AN_THREADS) : wW + 16);
+  X128 sX = lds_x(mX && eX < (uint32_t)C ? L.pool + eX * (16 * AN_THREADS) : wX + 16);
+  if (mW && eW >= (uint32_t)C) sW = pool_ld<C>(L, spill, eW);
+  if (mX && eX >= (uint32_t)C) sX = pool_ld<C>(L, spill, eX);
+  const X128 tW = lds_x(wW + 32), tX = lds_x(wX + 32);
+  x_sub(L.total, X128{mW ? 0ull : tW.lo, mW ? 0ull : tW.hi});
+  x_sub(L.total, X128{mX ? 0ull : tX.lo, mX ? 0ull : tX.hi});
   x_add(sW, sX);
-  uint32_t e;
-  if (lW & L_MERGED) {
-    e = lW & 63u;
-    if (lX & L_MERGED) L.pfree |= 1ull << (lX & 63u);
-  } else if (lX & L_MERGED) {
-    e = lX & 63u;
-  } else {
-    // at most F <= 64 entries are ever named by anchor labels; the low 32
-    // (nearly always) with a 32-bit find-first
-    const uint32_t lo = (uint32_t)L.pfree;
-    e = lo ? (uint32_t)(__ffs(lo) - 1) : 32u + (uint32_t)(__ffs((uint32_t)(L.pfree >> 32)) - 1);
-    L.pfree &= L.pfree - 1ull;
-  }
+  // the surviving entry: W's, else X's, else a fresh one (at most F <= 64
+  // entries are ever named by anchor labels; the low 32 nearly always)
+  const uint32_t lo = (uint32_t)L.pfree;
+  const uint32_t fresh = lo ? (uint32_t)(__ffs(lo) - 1) : 32u + (uint32_t)(__ffs((uint32_t)(L.pfree >> 32)) - 1);
+  const uint32_t e = mW ? eW : (mX ? eX : fresh);
+  L.pfree = (!mW && !mX) ? (L.pfree & (L.pfree - 1ull)) : L.pfree;
+  L.pfree |= (mW && mX) ? (1ull << eX) : 0ull;
   pool_st<C>(L, spill, e, sW);
   sts_u8(L.lab + 4 * Wn, L_ANCHOR | L_MERGED | e);
   sts_u8(L.lab + 4 * Xn, L_PTR | Wn);

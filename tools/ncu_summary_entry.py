@@ -20,6 +20,7 @@ def val(name):
 
 
 dram = val("dram__bytes_read.sum") + val("dram__bytes_write.sum")
+dur_ns = float(vals[ix["gpu__time_duration.sum"]].replace(",", "")) * {"nsecond": 1, "usecond": 1e3, "msecond": 1e6, "second": 1e9}[units[ix["gpu__time_duration.sum"]]]
 inst = val("smsp__inst_executed.sum")
 kernel = vals[ix["Kernel Name"]]
 root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
@@ -27,6 +28,7 @@ path = os.path.join(root, "profiles", "fitness_ncu_summary.json")
 d = json.load(open(path)) if os.path.exists(path) else {}
 d[workload] = {"kernel": kernel.split("(")[0].replace("(anonymous namespace)::", ""), "tag": tag,
                "genomes_in_launch": genomes, "dram_bytes_per_genome": dram / genomes,
-               "warp_instructions_per_genome": inst / genomes, "source": src}
+               "warp_instructions_per_genome": inst / genomes, "capture_duration_s": dur_ns / 1e9,
+               "capture_warp_instructions_per_s": inst / (dur_ns / 1e9), "source": src}
 json.dump(d, open(path, "w"), indent=1)
 print(json.dumps(d[workload], indent=1))
