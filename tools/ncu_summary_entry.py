@@ -20,7 +20,7 @@ def val(name):
 
 
 dram = val("dram__bytes_read.sum") + val("dram__bytes_write.sum")
-dur_ns = float(vals[ix["gpu__time_duration.sum"]].replace(",", "")) * {"nsecond": 1, "usecond": 1e3, "msecond": 1e6, "second": 1e9}[units[ix["gpu__time_duration.sum"]]]
+dur_ns = float(vals[ix["gpu__time_duration.sum"]].replace(",", "")) * {"nsecond": 1, "ns": 1, "usecond": 1e3, "us": 1e3, "msecond": 1e6, "ms": 1e6, "second": 1e9, "s": 1e9}[units[ix["gpu__time_duration.sum"]]]
 inst = val("smsp__inst_executed.sum")
 kernel = vals[ix["Kernel Name"]]
 root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
