@@ -45,7 +45,6 @@
 
 #include "fitness_plan.cuh"
 
-#define AN_THREADS 128
 #define AN_QCAP 32
 
 namespace {
@@ -173,16 +172,16 @@ struct AnLane {
 
 // pool entries e >= C live in the thread's local memory (lane-interleaved,
 // L1-cached; at most F <= 64 entries are ever held)
-template <int C>
+template <int C, int T>
 __device__ __forceinline__ X128 pool_ld(const AnLane& L, const ulonglong2* spill, uint32_t e) {
-  if (e < (uint32_t)C) return lds_x(L.pool + e * (16 * AN_THREADS));
+  if (e < (uint32_t)C) return lds_x(L.pool + e * (16 * T));
   const ulonglong2 v = spill[e - C];
   return {v.x, v.y};
 }
-template <int C>
+template <int C, int T>
 __device__ __forceinline__ void pool_st(const AnLane& L, ulonglong2* spill, uint32_t e, const X128& v) {
   if (e < (uint32_t)C)
-    sts_x(L.pool + e * (16 * AN_THREADS), v);
+    sts_x(L.pool + e * (16 * T), v);
   else
     spill[e - C] = make_ulonglong2(v.lo, v.hi);
 }
@@ -190,7 +189,7 @@ __device__ __forceinline__ void pool_st(const AnLane& L, ulonglong2* spill, uint
 // Back edge to slot b (label lb) of the new unit whose component is
 // anchored at A: find b's anchor, merge the two components at the
 // later-ending anchor.
-template <int C>
+template <int C, int T>
 __device__ __forceinline__ void an_merge(AnLane& L, ulonglong2* spill, bool need, uint32_t b, uint32_t lb,
                                          uint32_t& A) {
   uint32_t x = b, lx = need ? lb : L_ANCHOR;
@@ -216,10 +215,10 @@ __device__ __forceinline__ void an_merge(AnLane& L, ulonglong2* spill, bool need
   // replacement sum from the slot table (whose one-unit term leaves the
   // total) -- selects, not branches; pool entries >= C (rare) from local memory
   const uint32_t wW = L.wtab + WT_BYTES * Wn, wX = L.wtab + WT_BYTES * Xn;
-  X128 sW = lds_x(mW && eW < (uint32_t)C ? L.pool + eW * (16 * AN_THREADS) : wW + 16);
-  X128 sX = lds_x(mX && eX < (uint32_t)C ? L.pool + eX * (16 * AN_THREADS) : wX + 16);
-  if (mW && eW >= (uint32_t)C) sW = pool_ld<C>(L, spill, eW);
-  if (mX && eX >= (uint32_t)C) sX = pool_ld<C>(L, spill, eX);
+  X128 sW = lds_x(mW && eW < (uint32_t)C ? L.pool + eW * (16 * T) : wW + 16);
+  X128 sX = lds_x(mX && eX < (uint32_t)C ? L.pool + eX * (16 * T) : wX + 16);
+  if (mW && eW >= (uint32_t)C) sW = pool_ld<C, T>(L, spill, eW);
+  if (mX && eX >= (uint32_t)C) sX = pool_ld<C, T>(L, spill, eX);
   const X128 tW = lds_x(wW + 32), tX = lds_x(wX + 32);
   x_sub(L.total, X128{mW ? 0ull : tW.lo, mW ? 0ull : tW.hi});
   x_sub(L.total, X128{mX ? 0ull : tX.lo, mX ? 0ull : tX.hi});
@@ -231,7 +230,7 @@ __device__ __forceinline__ void an_merge(AnLane& L, ulonglong2* spill, bool need
   const uint32_t e = mW ? eW : (mX ? eX : fresh);
   L.pfree = (!mW && !mX) ? (L.pfree & (L.pfree - 1ull)) : L.pfree;
   L.pfree |= (mW && mX) ? (1ull << eX) : 0ull;
-  pool_st<C>(L, spill, e, sW);
+  pool_st<C, T>(L, spill, e, sW);
   sts_u8(L.lab + 4 * Wn, L_ANCHOR | L_MERGED | e);
   sts_u8(L.lab + 4 * Xn, L_PTR | Wn);
   A = Wn;
@@ -239,7 +238,7 @@ __device__ __forceinline__ void an_merge(AnLane& L, ulonglong2* spill, bool need
 
 // The label a slot held before it is handed on (or the program ends): a
 // merged anchor's region is complete -- queue it; all lanes take part.
-template <int C>
+template <int C, int T>
 __device__ __forceinline__ void an_close(AnLane& L, const ulonglong2* spill, uint32_t old, int lane,
                                          ulonglong2* qx, uint8_t* qown,
                                          int& qn, const AnArgs& a, unsigned long long* tacc, bool& inexact) {
@@ -248,7 +247,7 @@ __device__ __forceinline__ void an_close(AnLane& L, const ulonglong2* spill, uin
   if (!closing) return;
   X128 ev = {0ull, 0ull};
   if (emit) {
-    ev = pool_ld<C>(L, spill, old & 63u);
+    ev = pool_ld<C, T>(L, spill, old & 63u);
     L.pfree |= 1ull << (old & 63u);
   }
   const int cnt = __popc(closing);
@@ -268,10 +267,10 @@ __device__ __forceinline__ void an_close(AnLane& L, const ulonglong2* spill, uin
 // together, so each 32-step chunk of records is staged once per block
 // (cp.async, double-buffered) and every per-step record read is a
 // broadcast shared-memory load.
-template <int C>
-__global__ void __launch_bounds__(AN_THREADS, 6)
+template <int C, int T>
+__global__ void __launch_bounds__(T, 768 / T)
 fitness_anchor_kernel(AnArgs a, const uint64_t* __restrict__ pop, int64_t n, double* __restrict__ fit) {
-  constexpr int T = AN_THREADS, W = AN_THREADS / 32;
+  constexpr int W = T / 32;
   extern __shared__ __align__(16) unsigned char an_smem[];
   unsigned char* chunks = an_smem;                                            // [2][CH][80]
   ulonglong2* pool = reinterpret_cast<ulonglong2*>(chunks + 2 * CH * REC_BYTES);  // [C][T]
@@ -338,7 +337,7 @@ fitness_anchor_kernel(AnArgs a, const uint64_t* __restrict__ pop, int64_t n, dou
         }
         // the slot's previous owner is complete
         const uint32_t labS = L.lab + 4 * S;
-        an_close<C>(L, spill, lds_u8(labS), lane, qx, qown, qn, a, tacc, inexact);
+        an_close<C, T>(L, spill, lds_u8(labS), lane, qx, qown, qn, a, tacc, inexact);
         sts_u8(labS, on ? L_ANCHOR : 0u);
         if (on) x_add(L.total, lds_x(r + 16));
         __syncwarp();  // slot table entry visible to every lane
@@ -351,7 +350,7 @@ fitness_anchor_kernel(AnArgs a, const uint64_t* __restrict__ pop, int64_t n, dou
           const uint32_t b = lng ? (uint32_t)__ldg(a.lists + h.z + j) : (h.y >> (3 + 6 * j)) & 63u;
           const uint32_t lb = lds_u8(L.lab + 4 * b);
           const bool need = on && lb != 0u;  // b's unit is ON
-          if (__any_sync(0xffffffffu, need)) an_merge<C>(L, spill, need, b, lb, A);
+          if (__any_sync(0xffffffffu, need)) an_merge<C, T>(L, spill, need, b, lb, A);
         }
       }
       __syncthreads();  // every warp is done with buffer c & 1
@@ -360,7 +359,7 @@ fitness_anchor_kernel(AnArgs a, const uint64_t* __restrict__ pop, int64_t n, dou
     // regions open at the end of the program; labels cleared for the next genome
     for (int s = 0; s < a.F; ++s) {
       const uint32_t la = L.lab + 4 * s;
-      an_close<C>(L, spill, lds_u8(la), lane, qx, qown, qn, a, tacc, inexact);
+      an_close<C, T>(L, spill, lds_u8(la), lane, qx, qown, qn, a, tacc, inexact);
       sts_u8(la, 0u);
     }
     an_flush(qx, qown, qn, lane, a, tacc, inexact);
@@ -385,22 +384,21 @@ fitness_anchor_kernel(AnArgs a, const uint64_t* __restrict__ pop, int64_t n, dou
   if (inexact) atomicAdd(a.flags, 1ull);
 }
 
-size_t anchor_smem(int C, int F, int Fp) {
-  constexpr int T = AN_THREADS, W = AN_THREADS / 32;
+size_t anchor_smem(int C, int F, int Fp, int T) {
+  const int W = T / 32;
   return (size_t)2 * CH * REC_BYTES + (size_t)C * T * 16 +
          (size_t)W * (AN_QCAP * 16 + 64 * 8 + (size_t)F * WT_BYTES + AN_QCAP) + (size_t)(T / 4) * Fp * 4;
 }
 
-template <int C>
-int launch_anchor_t(cb_es_plan* p, const uint64_t* d_pop, int64_t n, double* d_fit, cudaStream_t stream) {
+template <int C, int T>
+int launch_anchor_tt(cb_es_plan* p, const uint64_t* d_pop, int64_t n, double* d_fit, cudaStream_t stream) {
   const int Fp = p->F | 1;  // odd row stride: a uniform slot hits 8 distinct banks
-  const size_t smem = anchor_smem(C, p->F, Fp);
-  if (cb_smem_claim((const void*)fitness_anchor_kernel<C>, smem))
-    CB_CUDA_TRY(cudaFuncSetAttribute(fitness_anchor_kernel<C>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  const size_t smem = anchor_smem(C, p->F, Fp, T);
+  if (cb_smem_claim((const void*)fitness_anchor_kernel<C, T>, smem))
+    CB_CUDA_TRY(cudaFuncSetAttribute(fitness_anchor_kernel<C, T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      (int)smem));
   int per_sm = 0;
-  CB_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fitness_anchor_kernel<C>, AN_THREADS,
-                                                            smem));
+  CB_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fitness_anchor_kernel<C, T>, T, smem));
   if (per_sm < 1) per_sm = 1;
   AnArgs a;
   a.M = p->M;
@@ -418,11 +416,22 @@ int launch_anchor_t(cb_es_plan* p, const uint64_t* d_pop, int64_t n, double* d_f
   a.infeas_mask = p->d_an_infeas_mask.p;
   a.rt = p->d_rt.p;
   a.flags = p->d_flags.p;
-  const int64_t want = (n + AN_THREADS - 1) / AN_THREADS;
+  const int64_t want = (n + T - 1) / T;
   const int64_t grid = std::min<int64_t>(want, (int64_t)per_sm * cb_sm_count());
-  fitness_anchor_kernel<C><<<(unsigned)grid, AN_THREADS, smem, stream>>>(a, d_pop, n, d_fit);
+  fitness_anchor_kernel<C, T><<<(unsigned)grid, T, smem, stream>>>(a, d_pop, n, d_fit);
   CB_CUDA_TRY(cudaGetLastError());
   return CB_OK;
+}
+
+// 128-thread blocks (four warps share each staged record chunk) when the
+// population fills the GPU; 64-thread blocks for smaller (search-sized)
+// populations, where fewer warps per block barrier wait less on the slowest
+template <int C>
+int launch_anchor_t(cb_es_plan* p, const uint64_t* d_pop, int64_t n, double* d_fit, cudaStream_t stream) {
+  const char* bt = getenv("CB_ANCHOR_BLOCK");
+  const int want = bt ? atoi(bt) : (n < (int64_t)cb_sm_count() * 6 * 128 ? 64 : 128);
+  return want == 64 ? launch_anchor_tt<C, 64>(p, d_pop, n, d_fit, stream)
+                    : launch_anchor_tt<C, 128>(p, d_pop, n, d_fit, stream);
 }
 
 }  // namespace
