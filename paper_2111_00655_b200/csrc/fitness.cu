@@ -1358,10 +1358,13 @@ extern "C" int cb_fitness_host(cb_es_plan* p, const uint64_t* h_pop, int64_t n, 
   const size_t words = (size_t)n * p->words;
   if (p->d_pop_stage.n < words) CB_CUDA_TRY(p->d_pop_stage.alloc(words));
   if (p->d_fit_stage.n < (size_t)n) CB_CUDA_TRY(p->d_fit_stage.alloc((size_t)n));
-  // Chunked pipeline over three streams: the H2D copy of chunk i+1 and the
-  // D2H copy of chunk i-1 overlap the fitness kernel of chunk i (copies are
-  // asynchronous when the host buffers are pinned).
-  const int64_t chunk = std::max<int64_t>(1 << 18, (n + 15) / 16);
+  // Chunked pipeline: the H2D copy of chunk i+1 and the D2H copy of chunk
+  // i-1 overlap the fitness kernel of chunk i (copies are asynchronous when
+  // the host buffers are pinned), and consecutive chunks' kernels alternate
+  // between two streams so one fills the SMs the other's tail leaves idle.
+  // A chunk holds at least ~1024 genomes per SM (a full wave of the walks)
+  // and at most an eighth of the batch.
+  const int64_t chunk = std::max<int64_t>((int64_t)cb_sm_count() * 1024, (n + 7) / 8);
   if (n <= chunk) {
     // one chunk (small batches, e.g. one `evolve` generation): copy in, price,
     // copy out on the plan's own stream -- no per-call stream / event setup
@@ -1380,10 +1383,12 @@ extern "C" int cb_fitness_host(cb_es_plan* p, const uint64_t* h_pop, int64_t n, 
     }
     return CB_OK;
   }
-  cudaStream_t s_in, s_run, s_out;
+  cudaStream_t s_in, s_run2[2], s_out;
   CB_CUDA_TRY(cudaStreamCreateWithFlags(&s_in, cudaStreamNonBlocking));
-  CB_CUDA_TRY(cudaStreamCreateWithFlags(&s_run, cudaStreamNonBlocking));
+  CB_CUDA_TRY(cudaStreamCreateWithFlags(&s_run2[0], cudaStreamNonBlocking));
+  CB_CUDA_TRY(cudaStreamCreateWithFlags(&s_run2[1], cudaStreamNonBlocking));
   CB_CUDA_TRY(cudaStreamCreateWithFlags(&s_out, cudaStreamNonBlocking));
+  int64_t ci = 0;
   std::vector<cudaEvent_t> copied, priced;
   int rc = CB_OK;
   for (int64_t lo = 0; lo < n && rc == CB_OK; lo += chunk) {
@@ -1401,6 +1406,9 @@ extern "C" int cb_fitness_host(cb_es_plan* p, const uint64_t* h_pop, int64_t n, 
       break;
     }
     cudaEventRecord(e_in, s_in);
+    // the global union-find kernel shares one scratch area: keep it on one stream
+    const bool shared_scratch = !(p->F > 0 && p->force_path != 0) && !p->smem_path;
+    cudaStream_t s_run = s_run2[shared_scratch ? 0 : (ci++ & 1)];
     cudaStreamWaitEvent(s_run, e_in, 0);
     rc = launch_fitness(p, dpop, cnt, dfit, s_run);
     cudaEventRecord(e_run, s_run);
@@ -1410,12 +1418,14 @@ extern "C" int cb_fitness_host(cb_es_plan* p, const uint64_t* h_pop, int64_t n, 
       rc = CB_ERR_CUDA;
   }
   cudaError_t se = cudaStreamSynchronize(s_out);
-  cudaStreamSynchronize(s_run);
+  cudaStreamSynchronize(s_run2[0]);
+  cudaStreamSynchronize(s_run2[1]);
   cudaStreamSynchronize(s_in);
   for (cudaEvent_t e : copied) cudaEventDestroy(e);
   for (cudaEvent_t e : priced) cudaEventDestroy(e);
   cudaStreamDestroy(s_in);
-  cudaStreamDestroy(s_run);
+  cudaStreamDestroy(s_run2[0]);
+  cudaStreamDestroy(s_run2[1]);
   cudaStreamDestroy(s_out);
   if (rc == CB_ERR_CUDA || se != cudaSuccess) {
     cb_set_error(std::string("cb_fitness_host: ") + cudaGetErrorString(cudaGetLastError()));

@@ -239,7 +239,7 @@ __device__ __forceinline__ void an_merge(AnLane& L, ulonglong2* spill, bool need
 // The label a slot held before it is handed on (or the program ends): a
 // merged anchor's region is complete -- queue it; all lanes take part.
 template <int C, int T>
-__device__ __forceinline__ void an_close(AnLane& L, const ulonglong2* spill, uint32_t old, int lane,
+__device__ __forceinline__ void an_close(AnLane& L, const ulonglong2* spill, uint32_t old, int lane, int owner,
                                          ulonglong2* qx, uint8_t* qown,
                                          int& qn, const AnArgs& a, unsigned long long* tacc, bool& inexact) {
   const bool emit = (old & (L_ANCHOR | L_MERGED)) == (L_ANCHOR | L_MERGED);
@@ -258,57 +258,69 @@ __device__ __forceinline__ void an_close(AnLane& L, const ulonglong2* spill, uin
   if (emit) {
     const int at = qn + __popc(closing & ((1u << lane) - 1u));
     qx[at] = make_ulonglong2(ev.lo, ev.hi);
-    qown[at] = (uint8_t)lane;
+    qown[at] = (uint8_t)owner;
   }
   qn += cnt;
 }
 
-// Block-lockstep walk: the four warps of a block step through the program
+// Block-lockstep walk: the warps of a block step through the program
 // together, so each 32-step chunk of records is staged once per block
 // (cp.async, double-buffered) and every per-step record read is a
-// broadcast shared-memory load.
-template <int C, int T>
-__global__ void __launch_bounds__(T, 768 / T)
+// broadcast shared-memory load.  Each thread walks G genomes at once
+// (independent instruction streams that hide each other's latency, one
+// record decode for both).
+template <int C, int T, int G>
+__global__ void __launch_bounds__(T, (G == 1 ? 768 : 512) / T)
 fitness_anchor_kernel(AnArgs a, const uint64_t* __restrict__ pop, int64_t n, double* __restrict__ fit) {
   constexpr int W = T / 32;
   extern __shared__ __align__(16) unsigned char an_smem[];
   unsigned char* chunks = an_smem;                                            // [2][CH][80]
-  ulonglong2* pool = reinterpret_cast<ulonglong2*>(chunks + 2 * CH * REC_BYTES);  // [C][T]
-  ulonglong2* qx_all = pool + C * T;                                          // [W][QCAP]
-  unsigned long long* tacc_all = reinterpret_cast<unsigned long long*>(qx_all + W * AN_QCAP);  // [W][32][2]
-  unsigned char* wtab_all = reinterpret_cast<unsigned char*>(tacc_all + W * 64);  // [W][F][48]
+  ulonglong2* pool = reinterpret_cast<ulonglong2*>(chunks + 2 * CH * REC_BYTES);  // [G][C][T]
+  ulonglong2* qx_all = pool + G * C * T;                                      // [W][QCAP]
+  unsigned long long* tacc_all = reinterpret_cast<unsigned long long*>(qx_all + W * AN_QCAP);  // [W][32 G][2]
+  unsigned char* wtab_all = reinterpret_cast<unsigned char*>(tacc_all + W * 64 * G);  // [W][F][48]
   uint8_t* qown_all = wtab_all + (size_t)W * a.F * WT_BYTES;                 // [W][QCAP]
-  uint8_t* LAB = qown_all + W * AN_QCAP;                                      // [T / 4][Fp][4]
+  uint8_t* LAB = qown_all + W * AN_QCAP;                                      // [G][T / 4][Fp][4]
   const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
   ulonglong2* qx = qx_all + warp * AN_QCAP;
   uint8_t* qown = qown_all + warp * AN_QCAP;
-  unsigned long long* tacc = tacc_all + warp * 64;
+  unsigned long long* tacc = tacc_all + warp * 64 * G;
   const uint32_t chunk0 = (uint32_t)__cvta_generic_to_shared(chunks);
-  AnLane L;
-  L.lab = (uint32_t)__cvta_generic_to_shared(LAB + (t >> 2) * a.Fp * 4 + (t & 3));
-  L.pool = (uint32_t)__cvta_generic_to_shared(pool + t);
-  L.wtab = (uint32_t)__cvta_generic_to_shared(wtab_all + (size_t)warp * a.F * WT_BYTES);
-  ulonglong2 spill[64 - C];
-  tacc[2 * lane] = tacc[2 * lane + 1] = 0ull;
-  for (int s = 0; s < a.F; ++s) sts_u8(L.lab + 4 * s, 0u);
+  const uint32_t wtab0 = (uint32_t)__cvta_generic_to_shared(wtab_all + (size_t)warp * a.F * WT_BYTES);
+  AnLane L[G];
+  ulonglong2 spill[G][64 - C];
+#pragma unroll
+  for (int g = 0; g < G; ++g) {
+    L[g].lab = (uint32_t)__cvta_generic_to_shared(LAB + (size_t)g * (T / 4) * a.Fp * 4 + (t >> 2) * a.Fp * 4 + (t & 3));
+    L[g].pool = (uint32_t)__cvta_generic_to_shared(pool + (size_t)g * C * T + t);
+    L[g].wtab = wtab0;
+    for (int s = 0; s < a.F; ++s) sts_u8(L[g].lab + 4 * s, 0u);
+    tacc[2 * (G * lane + g)] = tacc[2 * (G * lane + g) + 1] = 0ull;
+  }
   __syncwarp();
   bool inexact = false;
   const int32_t n_chunks = (a.M + CH - 1) / CH;
-  const int64_t stride = (int64_t)gridDim.x * T;
+  const int64_t stride = (int64_t)gridDim.x * T * G;
   // every warp of the block runs the same number of genome rounds (block syncs)
-  for (int64_t base = (int64_t)blockIdx.x * T; base < n; base += stride) {
-    const int64_t i = base + t;
-    const bool in_range = i < n;
-    const uint64_t* gen = pop + (in_range ? i : 0) * a.words;
-    bool dead = !in_range;
-    for (int32_t j = 0; j < a.n_infeas; ++j)
-      dead |= (__ldg(gen + __ldg(a.infeas_word + j)) & __ldg(a.infeas_mask + j)) != 0ull;
-    L.pfree = ~0ull;
-    L.total = {0ull, 0ull};
+  for (int64_t base = (int64_t)blockIdx.x * T * G; base < n; base += stride) {
+    int64_t gi[G];
+    const uint64_t* gen[G];
+    bool dead[G];
+    uint64_t w0[G], w1[G];
+#pragma unroll
+    for (int g = 0; g < G; ++g) {
+      gi[g] = base + (int64_t)g * T + t;
+      const bool in_range = gi[g] < n;
+      gen[g] = pop + (in_range ? gi[g] : 0) * a.words;
+      dead[g] = !in_range;
+      for (int32_t j = 0; j < a.n_infeas; ++j)
+        dead[g] |= (__ldg(gen[g] + __ldg(a.infeas_word + j)) & __ldg(a.infeas_mask + j)) != 0ull;
+      L[g].pfree = ~0ull;
+      L[g].total = {0ull, 0ull};
+      w0[g] = w1[g] = 0ull;
+    }
     int qn = 0;
-    // genome words: w0 = word cur_w, w1 = word cur_w + 1 (loaded ahead)
-    int32_t cur_w = -2;
-    uint64_t w0 = 0ull, w1 = 0ull;
+    int32_t cur_w = -2;  // genome words: w0 = word cur_w, w1 = word cur_w + 1 (loaded ahead)
     __syncthreads();  // the previous round is done with both buffers
     stage_chunk(a, 0, chunk0, t, T);
     stage_chunk(a, 1, chunk0 + CH * REC_BYTES, t, T);
@@ -322,83 +334,109 @@ fitness_anchor_kernel(AnArgs a, const uint64_t* __restrict__ pop, int64_t n, dou
         const uint4 h = lds_v4(r);
         const uint32_t bitf = h.x & 0xFFFFFFu;
         const uint32_t S = (h.x >> 24) & 63u;
-        // the unit's slot-table entry (three lanes, 16 bytes each)
-        if (lane < 3) sts_v4(L.wtab + WT_BYTES * S + 16 * lane, lds_v4(r + WT_OFF + 16 * lane));
-        bool on = !dead;
+        // the unit's slot-table entry (three lanes, 16 bytes each); the slot's
+        // previous unit may still be read by lanes finishing the last step's merges
+        __syncwarp();
+        if (lane < 3) sts_v4(wtab0 + WT_BYTES * S + 16 * lane, lds_v4(r + WT_OFF + 16 * lane));
+        bool on[G];
+#pragma unroll
+        for (int g = 0; g < G; ++g) on[g] = !dead[g];
         if (bitf != 0xFFFFFFu) {
           const int32_t wi = (int32_t)(bitf >> 6);
           if (wi != cur_w) {  // warp uniform
-            w0 = (wi == cur_w + 1) ? w1 : (dead ? 0ull : __ldg(gen + wi));
-            w1 = (!dead && wi + 1 < a.words) ? __ldg(gen + wi + 1) : 0ull;
+#pragma unroll
+            for (int g = 0; g < G; ++g) {
+              w0[g] = (wi == cur_w + 1) ? w1[g] : (dead[g] ? 0ull : __ldg(gen[g] + wi));
+              w1[g] = (!dead[g] && wi + 1 < a.words) ? __ldg(gen[g] + wi + 1) : 0ull;
+            }
             cur_w = wi;
           }
-          const uint32_t half = (bitf & 32u) ? (uint32_t)(w0 >> 32) : (uint32_t)w0;
-          on = on && ((half >> (bitf & 31u)) & 1u);
+#pragma unroll
+          for (int g = 0; g < G; ++g) {
+            const uint32_t half = (bitf & 32u) ? (uint32_t)(w0[g] >> 32) : (uint32_t)w0[g];
+            on[g] = on[g] && ((half >> (bitf & 31u)) & 1u);
+          }
         }
-        // the slot's previous owner is complete
-        const uint32_t labS = L.lab + 4 * S;
-        an_close<C, T>(L, spill, lds_u8(labS), lane, qx, qown, qn, a, tacc, inexact);
-        sts_u8(labS, on ? L_ANCHOR : 0u);
-        if (on) x_add(L.total, lds_x(r + 16));
+        const X128 tm = lds_x(r + 16);
+#pragma unroll
+        for (int g = 0; g < G; ++g) {
+          // the slot's previous owner is complete
+          const uint32_t labS = L[g].lab + 4 * S;
+          an_close<C, T>(L[g], spill[g], lds_u8(labS), lane, G * lane + g, qx, qown, qn, a, tacc, inexact);
+          sts_u8(labS, on[g] ? L_ANCHOR : 0u);
+          if (on[g]) x_add(L[g].total, tm);
+        }
         __syncwarp();  // slot table entry visible to every lane
-        uint32_t A = S;  // anchor of the new unit's component
-        // back neighbours (warp uniform); one call site keeps the loop small
+        uint32_t A[G];
+#pragma unroll
+        for (int g = 0; g < G; ++g) A[g] = S;  // anchor of the new unit's component
+        // back neighbours (warp uniform); one call site per genome keeps the loop small
         const bool lng = (h.x >> 31) != 0u;
         const int nb = lng ? (int)h.y : (int)(h.y & 7u);
 #pragma unroll 1
         for (int j = 0; j < nb; ++j) {
           const uint32_t b = lng ? (uint32_t)__ldg(a.lists + h.z + j) : (h.y >> (3 + 6 * j)) & 63u;
-          const uint32_t lb = lds_u8(L.lab + 4 * b);
-          const bool need = on && lb != 0u;  // b's unit is ON
-          if (__any_sync(0xffffffffu, need)) an_merge<C, T>(L, spill, need, b, lb, A);
+#pragma unroll
+          for (int g = 0; g < G; ++g) {
+            const uint32_t lb = lds_u8(L[g].lab + 4 * b);
+            const bool need = on[g] && lb != 0u;  // b's unit is ON
+            if (__any_sync(0xffffffffu, need)) an_merge<C, T>(L[g], spill[g], need, b, lb, A[g]);
+          }
         }
       }
       __syncthreads();  // every warp is done with buffer c & 1
       stage_chunk(a, c + 2, buf, t, T);
     }
-    // regions open at the end of the program; labels cleared for the next genome
-    for (int s = 0; s < a.F; ++s) {
-      const uint32_t la = L.lab + 4 * s;
-      an_close<C, T>(L, spill, lds_u8(la), lane, qx, qown, qn, a, tacc, inexact);
-      sts_u8(la, 0u);
-    }
-    an_flush(qx, qown, qn, lane, a, tacc, inexact);
-    X128 total = L.total;
-    x_add(total, X128{tacc[2 * lane], tacc[2 * lane + 1]});
-    tacc[2 * lane] = tacc[2 * lane + 1] = 0ull;
-    __syncwarp();
-    if (in_range) {
-      if (dead) {
-        fit[i] = __longlong_as_double(0x7ff0000000000000ll);
-      } else {
-        // sign-extend the 128-bit dynamic part, scale back, add the constant
-        const uint64_t sx = (uint64_t)((int64_t)total.hi >> 63);
-        fx192 v = fx_shl(fx192{{total.lo, total.hi, sx}}, a.shift);
-        fx_add(v, a.base_const);
-        fit[i] = fx_to_double(v);
+#pragma unroll
+    for (int g = 0; g < G; ++g) {
+      // regions open at the end of the program; labels cleared for the next genome
+      for (int s = 0; s < a.F; ++s) {
+        const uint32_t la = L[g].lab + 4 * s;
+        an_close<C, T>(L[g], spill[g], lds_u8(la), lane, G * lane + g, qx, qown, qn, a, tacc, inexact);
+        sts_u8(la, 0u);
       }
     }
+    an_flush(qx, qown, qn, lane, a, tacc, inexact);
+#pragma unroll
+    for (int g = 0; g < G; ++g) {
+      const int o = G * lane + g;
+      X128 total = L[g].total;
+      x_add(total, X128{tacc[2 * o], tacc[2 * o + 1]});
+      tacc[2 * o] = tacc[2 * o + 1] = 0ull;
+      if (gi[g] < n) {
+        if (dead[g]) {
+          fit[gi[g]] = __longlong_as_double(0x7ff0000000000000ll);
+        } else {
+          // sign-extend the 128-bit dynamic part, scale back, add the constant
+          const uint64_t sx = (uint64_t)((int64_t)total.hi >> 63);
+          fx192 v = fx_shl(fx192{{total.lo, total.hi, sx}}, a.shift);
+          fx_add(v, a.base_const);
+          fit[gi[g]] = fx_to_double(v);
+        }
+      }
+    }
+    __syncwarp();
   }
-  cp_async_wait1();
   asm volatile("cp.async.wait_all;" ::: "memory");
   if (inexact) atomicAdd(a.flags, 1ull);
 }
 
-size_t anchor_smem(int C, int F, int Fp, int T) {
+size_t anchor_smem(int C, int F, int Fp, int T, int G) {
   const int W = T / 32;
-  return (size_t)2 * CH * REC_BYTES + (size_t)C * T * 16 +
-         (size_t)W * (AN_QCAP * 16 + 64 * 8 + (size_t)F * WT_BYTES + AN_QCAP) + (size_t)(T / 4) * Fp * 4;
+  return (size_t)2 * CH * REC_BYTES + (size_t)G * C * T * 16 +
+         (size_t)W * (AN_QCAP * 16 + 64 * 8 * G + (size_t)F * WT_BYTES + AN_QCAP) +
+         (size_t)G * (T / 4) * Fp * 4;
 }
 
-template <int C, int T>
+template <int C, int T, int G>
 int launch_anchor_tt(cb_es_plan* p, const uint64_t* d_pop, int64_t n, double* d_fit, cudaStream_t stream) {
   const int Fp = p->F | 1;  // odd row stride: a uniform slot hits 8 distinct banks
-  const size_t smem = anchor_smem(C, p->F, Fp, T);
-  if (cb_smem_claim((const void*)fitness_anchor_kernel<C, T>, smem))
-    CB_CUDA_TRY(cudaFuncSetAttribute(fitness_anchor_kernel<C, T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  const size_t smem = anchor_smem(C, p->F, Fp, T, G);
+  if (cb_smem_claim((const void*)fitness_anchor_kernel<C, T, G>, smem))
+    CB_CUDA_TRY(cudaFuncSetAttribute(fitness_anchor_kernel<C, T, G>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      (int)smem));
   int per_sm = 0;
-  CB_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fitness_anchor_kernel<C, T>, T, smem));
+  CB_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fitness_anchor_kernel<C, T, G>, T, smem));
   if (per_sm < 1) per_sm = 1;
   AnArgs a;
   a.M = p->M;
@@ -416,9 +454,9 @@ int launch_anchor_tt(cb_es_plan* p, const uint64_t* d_pop, int64_t n, double* d_
   a.infeas_mask = p->d_an_infeas_mask.p;
   a.rt = p->d_rt.p;
   a.flags = p->d_flags.p;
-  const int64_t want = (n + T - 1) / T;
+  const int64_t want = (n + (int64_t)T * G - 1) / ((int64_t)T * G);
   const int64_t grid = std::min<int64_t>(want, (int64_t)per_sm * cb_sm_count());
-  fitness_anchor_kernel<C, T><<<(unsigned)grid, T, smem, stream>>>(a, d_pop, n, d_fit);
+  fitness_anchor_kernel<C, T, G><<<(unsigned)grid, T, smem, stream>>>(a, d_pop, n, d_fit);
   CB_CUDA_TRY(cudaGetLastError());
   return CB_OK;
 }
@@ -429,9 +467,14 @@ int launch_anchor_tt(cb_es_plan* p, const uint64_t* d_pop, int64_t n, double* d_
 template <int C>
 int launch_anchor_t(cb_es_plan* p, const uint64_t* d_pop, int64_t n, double* d_fit, cudaStream_t stream) {
   const char* bt = getenv("CB_ANCHOR_BLOCK");
+  const char* gt = getenv("CB_ANCHOR_GENOMES");
   const int want = bt ? atoi(bt) : (n < (int64_t)cb_sm_count() * 6 * 128 ? 64 : 128);
-  return want == 64 ? launch_anchor_tt<C, 64>(p, d_pop, n, d_fit, stream)
-                    : launch_anchor_tt<C, 128>(p, d_pop, n, d_fit, stream);
+  const int g = gt ? atoi(gt) : 1;
+  if (g == 2)
+    return want == 64 ? launch_anchor_tt<C, 64, 2>(p, d_pop, n, d_fit, stream)
+                      : launch_anchor_tt<C, 128, 2>(p, d_pop, n, d_fit, stream);
+  return want == 64 ? launch_anchor_tt<C, 64, 1>(p, d_pop, n, d_fit, stream)
+                    : launch_anchor_tt<C, 128, 1>(p, d_pop, n, d_fit, stream);
 }
 
 }  // namespace
