@@ -466,13 +466,10 @@ int launch_anchor_tt(cb_es_plan* p, const uint64_t* d_pop, int64_t n, double* d_
 // populations, where fewer warps per block barrier wait less on the slowest
 template <int C>
 int launch_anchor_t(cb_es_plan* p, const uint64_t* d_pop, int64_t n, double* d_fit, cudaStream_t stream) {
+  // (G = 2 genomes per thread measured 25-55 % slower: fewer resident
+  // blocks, twice the code in the step loop; the kernel keeps G as a parameter)
   const char* bt = getenv("CB_ANCHOR_BLOCK");
-  const char* gt = getenv("CB_ANCHOR_GENOMES");
   const int want = bt ? atoi(bt) : (n < (int64_t)cb_sm_count() * 6 * 128 ? 64 : 128);
-  const int g = gt ? atoi(gt) : 1;
-  if (g == 2)
-    return want == 64 ? launch_anchor_tt<C, 64, 2>(p, d_pop, n, d_fit, stream)
-                      : launch_anchor_tt<C, 128, 2>(p, d_pop, n, d_fit, stream);
   return want == 64 ? launch_anchor_tt<C, 64, 1>(p, d_pop, n, d_fit, stream)
                     : launch_anchor_tt<C, 128, 1>(p, d_pop, n, d_fit, stream);
 }
