@@ -33,10 +33,12 @@
 // All of them return bit-identical fitness (values in the plan's 128-bit
 // window where it exists, else 192-bit fixed point, rounded once).
 #include <algorithm>
+#include <chrono>
 #include <climits>
 #include <cstdio>
 #include <cstring>
 #include <numeric>
+#include <queue>
 
 #include "cb_internal.cuh"
 #include "fitness_plan.cuh"
@@ -81,21 +83,19 @@ static void build_frontier_program(cb_es_plan* P, int32_t n_elig_units) {
     ends_at[l].push_back(p);
   }
   std::vector<int32_t> slot(M, -1);
-  std::vector<int32_t> free_slots;  // kept sorted descending; back() = smallest
+  // free slots as a min-heap: every unit takes the smallest free slot
+  std::priority_queue<int32_t, std::vector<int32_t>, std::greater<int32_t>> free_slots;
   int32_t used = 0;
   for (int32_t p = 0; p < M; ++p) {
     int32_t s;
     if (free_slots.empty()) {
       s = used++;
     } else {
-      s = free_slots.back();
-      free_slots.pop_back();
+      s = free_slots.top();
+      free_slots.pop();
     }
     slot[p] = s;
-    for (int32_t q : ends_at[p]) {
-      free_slots.push_back(slot[q]);
-    }
-    std::sort(free_slots.begin(), free_slots.end(), std::greater<int32_t>());
+    for (int32_t q : ends_at[p]) free_slots.push(slot[q]);
   }
   P->F_needed = used;
   if (used > WIDE_MAX) {
@@ -103,9 +103,9 @@ static void build_frontier_program(cb_es_plan* P, int32_t n_elig_units) {
     return;
   }
   P->F = used;
-  // 16 entries: on the random 100k DAG 14 would fit 8 CTAs per SM instead of
-  // 7 (0.53 vs 0.48 M genomes/s on its ES population) but sends a dense
-  // population (90 % of bits set) to the fallback kernel 6x more slowly
+  // merged-sum pool entries per lane in shared memory (anchor walk; the
+  // rest in local memory): 8 measured best on the random 100k DAG (4 / 12
+  // within 6 %, 16 slower: fewer resident blocks)
   P->pool_entries = std::min(used, 8);
   // sparse walk: program position of every genome bit, fixed-unit positions
   P->prog_last.assign(last.begin(), last.end());
@@ -275,6 +275,16 @@ extern "C" int cb_es_plan_create(cb_graph* g, cb_matches* m, int32_t n_kernels,
   rc = cb_matches_ensure_host(m);
   if (rc != CB_OK) return rc;
   const int32_t n = g->n;
+  // CB_PLAN_TIMING: per-phase host times on stderr
+  const bool timing = getenv("CB_PLAN_TIMING") != nullptr;
+  auto t_last = std::chrono::steady_clock::now();
+  auto tick = [&](const char* what) {
+    if (!timing) return;
+    const auto now = std::chrono::steady_clock::now();
+    fprintf(stderr, "plan %-18s %8.2f ms\n", what, std::chrono::duration<double, std::milli>(now - t_last).count());
+    t_last = now;
+  };
+  tick("host copies");
   cb_es_plan* P = new cb_es_plan();
   auto bad = [&](const std::string& msg, int code) {
     delete P;
@@ -315,6 +325,7 @@ extern "C" int cb_es_plan_create(cb_graph* g, cb_matches* m, int32_t n_kernels,
   kadj.erase(std::unique(kadj.begin(), kadj.end(), [](int2 x, int2 y) { return x.x == y.x && x.y == y.y; }),
              kadj.end());
 
+  tick("kernel adjacency");
   // eligible slots and their replacements
   auto same_set = [&](int32_t a, int32_t b) {
     int32_t na = m->mem_ptr[a + 1] - m->mem_ptr[a];
@@ -475,7 +486,9 @@ extern "C" int cb_es_plan_create(cb_graph* g, cb_matches* m, int32_t n_kernels,
   P->rt.resize((size_t)max_cnt + 2);
   for (int64_t c = 0; c < (int64_t)P->rt.size(); ++c)
     P->rt[c] = region_r(region_alpha[target_backend], region_floor[target_backend], c);
+  tick("units and edges");
   build_frontier_program(P, n_elig_units);
+  tick("frontier program");
   // seed (all-zero genome) cost
   {
     fx192 tot = P->base_const;
@@ -508,6 +521,7 @@ extern "C" int cb_es_plan_create(cb_graph* g, cb_matches* m, int32_t n_kernels,
     if ((e = P->d_pos_of_bit.upload(P->pos_of_bit)) != cudaSuccess) return fail_cuda(e);
     if ((e = P->d_fixed_pos.upload(P->fixed_pos)) != cudaSuccess) return fail_cuda(e);
   }
+  tick("uploads");
   if ((rc = build_anchor_plan(P)) != CB_OK || (rc = build_fsm_plan(P)) != CB_OK) {
     delete P;
     return rc;
@@ -516,6 +530,7 @@ extern "C" int cb_es_plan_create(cb_graph* g, cb_matches* m, int32_t n_kernels,
   cudaMemset(P->d_flags.p, 0, 2 * sizeof(unsigned long long));
   const size_t per_warp = (size_t)P->words * 8 + (size_t)P->M * (sizeof(fx192) + 8);
   P->smem_path = per_warp * 4 <= 200 * 1024;
+  tick("anchor + fsm plans");
   *out = P;
   return CB_OK;
 }
