@@ -155,6 +155,16 @@ def build_workload(name: str):
     return tp, g, bs
 
 
+def workload_config(args, world: int, nodes: int, dp_kernels: int, k: int, P: int) -> dict:
+    """The `config` both arms print (identical for the same workload and N)."""
+    words = max(1, (k + 63) // 64)
+    return {"workload": f"{args.workload}: op-level DP + evolutionary search",
+            "nodes": nodes, "dp_kernels": dp_kernels, "genome_bits": k, "genome_words": words,
+            "population_per_gpu": P, "global_population": P * world,
+            "parallelism": f"population sharded over {world} GPU(s), all-gather of elites",
+            "l2": f"population {P * words * 8 / 1e9:.1f} GB per GPU > L2 (no flush)"}
+
+
 def shard_size(words: int, requested: int | None) -> int:
     if requested:
         return requested
@@ -332,13 +342,8 @@ def run_mine(args) -> None:
         "arithmetic": "u64 bit-genomes; exact 128-bit fixed-point cost sums (plan window), "
                       "f64 region pricing; identical to the reference's fsum results",
         "data": f"synthetic ({wl['data']}; random-init ES population; simulated cost tables)",
-        "config": {"workload": f"{args.workload}: op-level DP + evolutionary search",
-                   "nodes": len(g.nodes), "dp_kernels": len(res.placement),
-                   "genome_bits": plan.k, "genome_words": plan.words,
-                   "population_per_gpu": P, "global_population": P * world,
-                   "parallelism": f"population sharded over {world} GPU(s), "
-                                  f"{'NCCL' if backend == 'nccl' else backend} all-gather of elites",
-                   "l2": f"population {P * plan.words * 8 / 1e9:.1f} GB per GPU > L2 (no flush)"},
+        "config": workload_config(args, world, len(g.nodes), len(res.placement), plan.k, P),
+        "exchange": f"{'NCCL' if backend == 'nccl' else backend} all-gather" if world > 1 else None,
         "search": {"wall_s": search_s, **{k: v for k, v in search_t.items() if k != "wall_s"},
                    "es_population_per_gpu": args.search_population,
                    "es_generations": args.search_generations, "dp_cost_ms": res.cost_ms,
@@ -582,14 +587,13 @@ def run_reference(args) -> None:
         "dtype": "f64",
         "arithmetic": "f64 with exact sums (Kulisch accumulator, fsum-equivalent rounding), CPU",
         "data": f"synthetic ({wl['data']}; random-init ES population; simulated cost tables)",
-        "config": {"workload": f"{args.workload}: op-level DP + evolutionary search",
-                   "nodes": len(case["graph"]["nodes"]), "genome_bits": k,
-                   "dp_kernels": len(kernels), "dp_cost_ms": cost,
-                   "dp": "oracle/oracle.c or_dp_subtree (the reference DP exceeds its state cap)"
-                         if args.workload in ("random100k", "nasnet_a", "nasrnn") else
-                         "oracle/oracle.c or_dp_subtree (equal to the reference DP)",
-                   "dp_s": dp_s, "population": S,
-                   "input": f"tests/golden/cases/{args.workload}.json.gz"},
+        "config": workload_config(args, world, len(case["graph"]["nodes"]), len(kernels), k,
+                                  shard_size(max(1, (k + 63) // 64), args.population or wl["population"])),
+        "reference_sample": {"population": S, "dp_cost_ms": cost, "dp_s": dp_s,
+                             "dp": "oracle/oracle.c or_dp_subtree (the reference DP exceeds its "
+                                   "state cap)" if args.workload in ("random100k", "nasnet_a", "nasrnn")
+                                   else "oracle/oracle.c or_dp_subtree (equal to the reference DP)",
+                             "input": f"tests/golden/cases/{args.workload}.json.gz"},
         "cpu_baseline": {"value": value, "unit": "genomes/s", "cores": threads, "kind": "port",
                          "sample": f"ES generations of {S} genomes (the reference's breed, numpy; "
                                    f"every child priced by oracle/oracle.c with {threads} threads)"},

@@ -21,7 +21,14 @@ def test_reference_arm_line_without_product_library():
     assert d["impl"] == "reference" and d["metric"] == "fitness_evals_per_sec"
     assert d["value"] > 0 and d["e2e"]["value"] == d["value"]
     assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["cpu_baseline"]["kind"] == "port"
-    assert d["config"]["genome_bits"] == 99446 and d["config"]["dp_cost_ms"] == 22776.0808208
+    assert d["config"]["genome_bits"] == 99446 and d["reference_sample"]["dp_cost_ms"] == 22776.0808208
+    # the same config dict as the GPU arm prints for this workload and N
+    sys.path.insert(0, ROOT)
+    import argparse
+    import bench
+    args = argparse.Namespace(workload="random100k", population=None)
+    assert d["config"] == bench.workload_config(args, 1, 100000, 99446, 99446,
+                                                bench.shard_size(1554, 1 << 20))
     assert d["product_library_loaded"] is False
 
 
