@@ -40,7 +40,7 @@ def _genomes(plan, rng, rows_per_density=300):
 
 @pytest.mark.parametrize("seed,n,window", [(0, 2000, 64), (1, 3000, 64), (2, 1500, 128),
                                            (3, 800, 24)])
-def test_wide_plan_matches_oracle(gpu, seed, n, window):
+def test_wide_plan_matches_oracle(gpu, seed, n, window, monkeypatch):
     g = workloads.random_dag(n, seed=seed, ops=workloads.RANDOM_OPS, window=window)
     bs = workloads.random_backends(g, n_backends=8, n_graph=1, seed=seed)
     res = tp.optimize(g, bs.registry, bs.measurer, 0.01)
@@ -59,7 +59,16 @@ def test_wide_plan_matches_oracle(gpu, seed, n, window):
     for path in ("wide", "anchor"):
         plan.set_path(path)
         assert np.array_equal(plan.evaluate(genomes), want), path
-    # tiny pools: most genomes overflow to the warp-per-genome kernel
+    # the anchor walk's launch forms: 64- / 128-thread blocks, merges with
+    # selects or branches (chosen by population size; forced here)
+    for block in ("64", "128"):
+        for merge in ("0", "1"):
+            monkeypatch.setenv("CB_ANCHOR_BLOCK", block)
+            monkeypatch.setenv("CB_ANCHOR_MERGE", merge)
+            assert np.array_equal(plan.evaluate(genomes), want), (block, merge)
+    monkeypatch.delenv("CB_ANCHOR_BLOCK")
+    monkeypatch.delenv("CB_ANCHOR_MERGE")
+    # tiny shared pools: merged sums spill to the thread's local memory
     for entries in (1, 2, 5):
         plan.set_pool(entries)
         assert np.array_equal(plan.evaluate(genomes), want), entries

@@ -24,7 +24,10 @@ times = {}
 for rep in range(3):
     for combo in itertools.product(*[v for _, v in axes]):
         for (k, _), v in zip(axes, combo):
-            os.environ[k] = v
+            if k == 'POOL':  # plan-level knob: merged-sum pool entries in shared memory
+                plan.set_pool(int(v))
+            else:
+                os.environ[k] = v
         plan.evaluate_device(pop.data_ptr(), P, fit.data_ptr())  # warm
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
