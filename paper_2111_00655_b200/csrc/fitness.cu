@@ -1379,7 +1379,9 @@ extern "C" int cb_fitness_host(cb_es_plan* p, const uint64_t* h_pop, int64_t n, 
   // between two streams so one fills the SMs the other's tail leaves idle.
   // A chunk holds at least ~1024 genomes per SM (a full wave of the walks)
   // and at most an eighth of the batch.
-  const int64_t chunk = std::max<int64_t>((int64_t)cb_sm_count() * 1024, (n + 7) / 8);
+  int64_t per_sm = 1024;
+  if (const char* e = getenv("CB_HOST_CHUNK_PER_SM")) per_sm = std::max(1, atoi(e));
+  const int64_t chunk = std::max<int64_t>((int64_t)cb_sm_count() * per_sm, (n + 7) / 8);
   if (n <= chunk) {
     // one chunk (small batches, e.g. one `evolve` generation): copy in, price,
     // copy out on the plan's own stream -- no per-call stream / event setup

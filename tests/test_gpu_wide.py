@@ -232,3 +232,30 @@ def test_fsm_long_narrow_programs_match_oracle(gpu, seed, n, window):
     assert np.array_equal(plan.evaluate(genomes), want), (plan.words, plan.info.fsm_entry_bytes)
     plan.set_path("auto")
     assert np.array_equal(plan.evaluate(genomes), want)
+
+
+@pytest.mark.parametrize("n_nodes,window", [(12, 4), (40, 8), (300, 24)])
+def test_anchor_walk_small_programs_and_batches(gpu, n_nodes, window, monkeypatch):
+    """Programs shorter than one staged record chunk (32 steps), batches of
+    1..33 genomes (partial warps and blocks), every launch form."""
+    g = workloads.random_dag(n_nodes, seed=n_nodes, ops=workloads.RANDOM_OPS, window=window)
+    bs = workloads.random_backends(g, n_backends=5, n_graph=1, seed=n_nodes)
+    res = tp.optimize(g, bs.registry, bs.measurer, 0.01)
+    plan = tp.FitnessPlan(g, bs.registry, bs.measurer, res.placement, 0.01, bs.graph_backend,
+                          res.kernel_matches)
+    if plan.info.window_shift < 0 or plan.info.frontier_slots == 0:
+        pytest.skip("no anchor program for this plan")
+    oc = OracleCase(_case(g, bs, 0.01))
+    oc.price()
+    kernels = [[a.backend_pattern.order, a.root, sorted(a.nodes)]
+               for a in res.placement.assignments]
+    rng = np.random.default_rng(n_nodes)
+    feasible = np.array([k != 0 for k in plan.rep_kind], dtype=np.uint8)
+    plan.set_path("anchor")
+    for n in (1, 2, 31, 33):
+        genomes = (rng.random((n, plan.k)) < 0.5).astype(np.uint8) & feasible
+        want = oc.fitness(kernels, bs.graph_backend, genomes, threads=4)
+        for block in ("64", "128"):
+            monkeypatch.setenv("CB_ANCHOR_BLOCK", block)
+            assert np.array_equal(plan.evaluate(genomes), want), (n, block)
+    plan.set_path("auto")
