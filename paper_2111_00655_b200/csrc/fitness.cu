@@ -1377,9 +1377,9 @@ extern "C" int cb_fitness_host(cb_es_plan* p, const uint64_t* h_pop, int64_t n, 
   // i-1 overlap the fitness kernel of chunk i (copies are asynchronous when
   // the host buffers are pinned), and consecutive chunks' kernels alternate
   // between two streams so one fills the SMs the other's tail leaves idle.
-  // A chunk holds at least ~1024 genomes per SM (a full wave of the walks)
+  // A chunk holds at least 512 genomes per SM (half a wave of the walks)
   // and at most an eighth of the batch.
-  int64_t per_sm = 1024;
+  int64_t per_sm = 512;  // A/B (tools/e2e_ab.py): 512 > 256, 1024, 2048 on the 100k DAG
   if (const char* e = getenv("CB_HOST_CHUNK_PER_SM")) per_sm = std::max(1, atoi(e));
   const int64_t chunk = std::max<int64_t>((int64_t)cb_sm_count() * per_sm, (n + 7) / 8);
   if (n <= chunk) {
