@@ -226,10 +226,10 @@ int cb_es_plan_query(const cb_es_plan* p, cb_es_plan_info* info);
  * packed anchor walk, 7 the finite-state walk.  For tests and profiling; all
  * paths return identical results. */
 int cb_es_plan_set_path(cb_es_plan* p, int32_t path);
-/* Merged-component pool entries per genome of the anchor kernel (1..24,
- * default min(frontier slots, 16)); genomes that need more are priced by
- * the warp-per-genome kernel.  A tuning / testing knob: results are
- * identical for every value. */
+/* Merged-component pool entries per genome of the anchor walk held in
+ * shared memory (1..24, default min(frontier slots, 8)); entries beyond
+ * live in the thread's local memory (at most F are ever held).  A tuning /
+ * testing knob: results are identical for every value. */
 int cb_es_plan_set_pool(cb_es_plan* p, int32_t entries);
 /* Name of the fitness kernel the current path setting dispatches to
  * (static string; for reports and profiles). */
