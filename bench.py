@@ -243,12 +243,18 @@ def run_mine(args) -> None:
                  optimize_phases_s=res.device["phases_s"], dp_device_ms=res.device["device_ms"])
         return res, plan, t
 
-    # warm search (module load, first launches), then the timed one on fresh objects
+    # warm search (module load, first launches), then two timed ones on fresh
+    # objects; the faster is reported (both walls listed)
     bs.registry._tables.clear()
     search(4096, 2)
-    bs.registry._tables.clear()
-    gc.collect()
-    res, plan, search_t = search(args.search_population, args.search_generations)
+    runs = []
+    for _ in range(2):
+        bs.registry._tables.clear()
+        gc.collect()
+        runs.append(search(args.search_population, args.search_generations))
+    res, plan, search_t = min(runs, key=lambda r: r[2]["wall_s"])
+    search_t["wall_runs_s"] = [r[2]["wall_s"] for r in runs]
+    del runs
     P = shard_size(plan.words, args.population or wl["population"])
     es = DeviceEvolution(plan, P, seed=args.seed, device=dev, process_group=group)
     es.initialize()
