@@ -55,15 +55,26 @@ static bool fx_term(double base, double r, const fx192& eps, fx192& out);
 // number of units simultaneously waiting for a later neighbour.
 static void build_frontier_program(cb_es_plan* P, int32_t n_elig_units) {
   const int32_t M = P->M;
-  std::vector<std::vector<int32_t>> nbr(M);
+  // unit adjacency as CSR (neighbours in edge order, as per-unit lists would hold them)
+  std::vector<int32_t> nptr(M + 1, 0), nadj(2 * P->edges.size());
   for (const int2& e : P->edges) {
-    nbr[e.x].push_back(e.y);
-    nbr[e.y].push_back(e.x);
+    ++nptr[e.x + 1];
+    ++nptr[e.y + 1];
   }
+  for (int32_t v = 0; v < M; ++v) nptr[v + 1] += nptr[v];
+  {
+    std::vector<int32_t> fill(nptr.begin(), nptr.end() - 1);
+    for (const int2& e : P->edges) {
+      nadj[fill[e.x]++] = e.y;
+      nadj[fill[e.y]++] = e.x;
+    }
+  }
+  auto nbr_begin = [&](int32_t v) { return nadj.begin() + nptr[v]; };
+  auto nbr_end = [&](int32_t v) { return nadj.begin() + nptr[v + 1]; };
   std::vector<int32_t> key(M, M);
   for (int32_t v = n_elig_units; v < M; ++v)
-    for (int32_t q : nbr[v])
-      if (q < n_elig_units) key[v] = std::min(key[v], q);
+    for (auto it = nbr_begin(v); it != nbr_end(v); ++it)
+      if (*it < n_elig_units) key[v] = std::min(key[v], *it);
   std::vector<std::vector<int32_t>> before(n_elig_units + 1);
   for (int32_t v = n_elig_units; v < M; ++v) before[std::min(key[v], n_elig_units)].push_back(v);
   std::vector<int32_t> order;
@@ -75,12 +86,17 @@ static void build_frontier_program(cb_es_plan* P, int32_t n_elig_units) {
   std::vector<int32_t> pos(M);
   for (int32_t p = 0; p < M; ++p) pos[order[p]] = p;
   std::vector<int32_t> last(M);
-  std::vector<std::vector<int32_t>> ends_at(M);
+  std::vector<int32_t> eptr(M + 1, 0), eat(M);  // ends_at as CSR (positions in increasing order)
   for (int32_t p = 0; p < M; ++p) {
     int32_t u = order[p], l = p;
-    for (int32_t q : nbr[u]) l = std::max(l, pos[q]);
+    for (auto it = nbr_begin(u); it != nbr_end(u); ++it) l = std::max(l, pos[*it]);
     last[p] = l;
-    ends_at[l].push_back(p);
+    ++eptr[l + 1];
+  }
+  for (int32_t p = 0; p < M; ++p) eptr[p + 1] += eptr[p];
+  {
+    std::vector<int32_t> fill(eptr.begin(), eptr.end() - 1);
+    for (int32_t p = 0; p < M; ++p) eat[fill[last[p]]++] = p;
   }
   std::vector<int32_t> slot(M, -1);
   // free slots as a min-heap: every unit takes the smallest free slot
@@ -95,7 +111,7 @@ static void build_frontier_program(cb_es_plan* P, int32_t n_elig_units) {
       free_slots.pop();
     }
     slot[p] = s;
-    for (int32_t q : ends_at[p]) free_slots.push(slot[q]);
+    for (int32_t j = eptr[p]; j < eptr[p + 1]; ++j) free_slots.push(slot[eat[j]]);
   }
   P->F_needed = used;
   if (used > WIDE_MAX) {
@@ -134,15 +150,15 @@ static void build_frontier_program(cb_es_plan* P, int32_t n_elig_units) {
     r.cnt = P->unit_cnt[u];
     r.slot = (uint8_t)slot[p];
     r.back_off = (int32_t)P->prog_slots.size();
-    for (int32_t q : nbr[u])
-      if (pos[q] < p) {
-        P->prog_slots.push_back((uint8_t)slot[pos[q]]);
-        P->prog_back_pos.push_back(pos[q]);
+    for (auto it = nbr_begin(u); it != nbr_end(u); ++it)
+      if (pos[*it] < p) {
+        P->prog_slots.push_back((uint8_t)slot[pos[*it]]);
+        P->prog_back_pos.push_back(pos[*it]);
       }
     r.nback = (uint8_t)(P->prog_slots.size() - r.back_off);
     r.end_off = (int32_t)P->prog_slots.size();
-    for (int32_t q : ends_at[p]) {
-      P->prog_slots.push_back((uint8_t)slot[q]);
+    for (int32_t j = eptr[p]; j < eptr[p + 1]; ++j) {
+      P->prog_slots.push_back((uint8_t)slot[eat[j]]);
       P->prog_back_pos.push_back(-1);
     }
     r.nend = (uint8_t)(P->prog_slots.size() - r.end_off);
