@@ -128,3 +128,34 @@ def test_elite_pick_kernel_follows_the_host_rule(gpu):
         best, want = pick_elite_host(recs)
         assert val.item() == want == hist.item()
         assert np.array_equal(elite.cpu().numpy(), recs[best, 1:])
+
+
+@pytest.mark.parametrize("name", ["resnet50", "bert_base"])
+def test_host_pipeline_chunks_match_one_launch(gpu, name):
+    """cb_fitness_host over many chunks (two alternating compute streams,
+    overlapped copies) returns exactly what one device launch returns, and
+    the oracle agrees on a sample."""
+    case, res, plan = _setup(name)
+    n = 148 * 512 * 3 + 777  # > 3 chunks and a ragged tail
+    rng = np.random.default_rng(3)
+    feasible = np.array([k != 0 for k in plan.rep_kind], dtype=np.uint8)
+    bits = (rng.random((n, plan.k)) < 0.5).astype(np.uint8)
+    bits[: n // 2] &= feasible
+    packed = np.packbits(bits, axis=1, bitorder="little")
+    rows = np.zeros((n, plan.words * 8), np.uint8)
+    rows[:, :packed.shape[1]] = packed
+    rows = rows.view(np.uint64)
+    host_rows = torch.empty((n, plan.words), dtype=torch.int64, pin_memory=True)
+    host_rows.numpy().view(np.uint64)[:] = rows
+    out = torch.empty(n, dtype=torch.float64, pin_memory=True).numpy()
+    plan.evaluate_packed(host_rows.numpy().view(np.uint64), out)
+    dev_rows = host_rows.cuda()
+    dev_fit = torch.empty(n, dtype=torch.float64, device="cuda")
+    plan.evaluate_device(dev_rows.data_ptr(), n, dev_fit.data_ptr())
+    torch.cuda.synchronize()
+    assert np.array_equal(out, dev_fit.cpu().numpy())
+    oc = OracleCase(case)
+    oc.price()
+    sample = rng.choice(n, 256, replace=False)
+    want = oc.fitness(kernels_of(res.placement), case["es"]["graph_backend"], bits[sample])
+    assert np.array_equal(out[sample], want)
