@@ -24,6 +24,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <string>
+#include <numeric>
 #include <unordered_map>
 
 #include "fitness_plan.cuh"
@@ -603,6 +604,57 @@ int build_fsm_plan(cb_es_plan* P) {
     }
     hdr[p].w = max_merge | (max_emit << 8);
     cur.swap(nxt);
+  }
+  // Renumber every step's states by visit frequency (most visited first),
+  // estimated by walking 2 048 uniformly random genomes through the table:
+  // the transitions a warp gathers then crowd into fewer cache lines.
+  // CB_FSM_ORDER=0 keeps discovery order (A/B).
+  if (!getenv("CB_FSM_ORDER") || atoi(getenv("CB_FSM_ORDER")) != 0) {
+    const size_t n_ent = table.size() / 2;
+    std::vector<uint32_t> base(M + 1);
+    for (int32_t q = 0; q < M; ++q) base[q] = hdr[q].x / 2;
+    base[M] = (uint32_t)(n_ent / 2);
+    std::vector<uint32_t> visits(n_ent / 2, 0u);
+    uint64_t x = 0x9E3779B97F4A7C15ull;
+    for (int smp = 0; smp < 2048; ++smp) {
+      uint32_t st = 0;
+      for (int32_t q = 0; q < M; ++q) {
+        ++visits[base[q] + st];
+        x ^= x << 13;
+        x ^= x >> 7;
+        x ^= x << 17;
+        const uint32_t bit = P->prog[q].bit >= 0 ? (uint32_t)(x >> 63) : 1u;
+        st = table[2 * (hdr[q].x + 2 * st + bit)].x & 0xFFFFu;
+      }
+    }
+    std::vector<uint32_t> newid(n_ent / 2), old_of(n_ent / 2);
+    for (int32_t q = 0; q < M; ++q) {
+      const uint32_t b0 = base[q], ns = base[q + 1] - b0;
+      std::vector<uint32_t> ord(ns);
+      std::iota(ord.begin(), ord.end(), 0u);
+      // the walk starts in state 0 of step 0: keep it there
+      std::stable_sort(ord.begin() + (q == 0 ? 1 : 0), ord.end(),
+                       [&](uint32_t a2, uint32_t b2) { return visits[b0 + a2] > visits[b0 + b2]; });
+      for (uint32_t j = 0; j < ns; ++j) {
+        old_of[b0 + j] = ord[j];
+        newid[b0 + ord[j]] = j;
+      }
+    }
+    std::vector<uint4> t2(table.size());
+    for (int32_t q = 0; q < M; ++q) {
+      const uint32_t b0 = base[q], ns = base[q + 1] - b0;
+      for (uint32_t j = 0; j < ns; ++j)
+        for (uint32_t bit = 0; bit < 2; ++bit) {
+          const size_t src = hdr[q].x + 2 * old_of[b0 + j] + bit, dst = hdr[q].x + 2 * j + bit;
+          t2[2 * dst] = table[2 * src];
+          t2[2 * dst + 1] = table[2 * src + 1];
+          if (q + 1 < M) {
+            const uint32_t nx = t2[2 * dst].x & 0xFFFFu;
+            t2[2 * dst].x = (t2[2 * dst].x & ~0xFFFFu) | newid[base[q + 1] + nx];
+          }
+        }
+    }
+    table.swap(t2);
   }
   if (getenv("CB_FSM_STATS")) {
     int smax = 0, mm = 0, me = 0, dbits = 0, zero = 0;
