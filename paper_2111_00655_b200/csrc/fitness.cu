@@ -565,7 +565,7 @@ extern "C" int cb_es_plan_query(const cb_es_plan* p, cb_es_plan_info* info) {
   info->window_shift = p->anchor_ok ? p->anchor_shift : -1;
   info->packed_labels = p->F > 0 && p->packed_ok ? (p->pa_ok && p->anchor_ok ? 2 : 1) : 0;
   info->fsm_transitions = p->fsm_ok ? (int32_t)std::min<int64_t>(p->fsm_entries, INT32_MAX) : 0;
-  info->fsm_entry_bytes = p->fsm_ok ? (p->fsm_layout == 1 ? 8 : p->fsm_layout == 2 ? 16 : 32) : 0;
+  info->fsm_entry_bytes = p->fsm_ok ? (p->fsm_layout == 1 || p->fsm_layout == 3 ? 8 : p->fsm_layout == 2 ? 16 : 32) : 0;
   return CB_OK;
 }
 

@@ -44,6 +44,7 @@ struct FsmArgs {
   const uint4* __restrict__ table;     // transitions (32-byte layout)
   const uint2* __restrict__ ctable;    // transitions (8-byte layout)
   const uint4* __restrict__ mtable;    // transitions (16-byte layout)
+  const uint32_t* __restrict__ xtable;  // mixed layout: 8-byte steps and 16-byte steps, word offsets
   const uint4* __restrict__ dtab;      // distinct deltas of the 8- / 16-byte layouts
   int32_t n_delta;
   const uint64_t* __restrict__ infeas;
@@ -57,6 +58,7 @@ struct FsmArgs {
 #define FSM_LANE_SHIFT 40
 #define FSM_CNT_SHIFT 48
 #define FSM_BIT_FORCED 0x80u  // bit info: the unit has no genome bit (always on)
+#define FSM_WIDE_STEP 0x10000u  // header .w: the step's transitions use the 16-byte form (mixed layout)
 
 template <typename U>
 __device__ __forceinline__ void fadd2(U& lo, U& hi, uint64_t blo, uint64_t bhi) {
@@ -160,7 +162,7 @@ fitness_fsm_kernel(FsmArgs a, const uint64_t* __restrict__ pop, int64_t n, doubl
     uint4 hn = __ldg(a.hdr);  // step headers are warp uniform: prefetched one step ahead
     // the 16-byte layout (an L2-resident table) also prefetches the unit's
     // packed sum (NasNet-A +3 %; the L1-resident walks lose ~0.5 % to it)
-    constexpr bool PRE_REP = L == 2;
+    constexpr bool PRE_REP = L >= 2;
     uint4 rn = PRE_REP ? __ldg(a.hdr + 1) : make_uint4(0u, 0u, 0u, 0u);
     auto bit_of = [&](uint32_t hy) {  // W > 0: the step's genome bit from shared memory
       const uint64_t wd = swd[(hy >> 8) * T];
@@ -192,7 +194,31 @@ fitness_fsm_kernel(FsmArgs a, const uint64_t* __restrict__ pop, int64_t n, doubl
       const uint32_t idx = h.x + 2u * state + (on ? 1u : 0u);  // 32-bit index math
       uint32_t open, nmerge, nemit, merges, emits;
       uint4 dv;  // exact delta: closed one-unit regions' terms - removed term
-      if (L == 1) {
+      if (L == 3) {
+        // mixed: the step's header says whether its transitions take 8 or
+        // 16 bytes (warp-uniform); h.x is a word offset
+        if (h.w & FSM_WIDE_STEP) {
+          const uint4 e = __ldg(reinterpret_cast<const uint4*>(a.xtable + h.x + 4u * (2u * state + (on ? 1u : 0u))));
+          state = e.x & 0xFFFFu;
+          open = (e.x >> 16) & 1u;
+          nmerge = (e.x >> 17) & 7u;
+          nemit = (e.x >> 20) & 7u;
+          const uint32_t da = sdelta_base + ((e.x >> 20) & 0xFF0u);
+          asm("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(dv.x), "=r"(dv.y), "=r"(dv.z), "=r"(dv.w) : "r"(da));
+          merges = e.y;
+          emits = e.z;
+        } else {
+          const uint2 e = __ldg(reinterpret_cast<const uint2*>(a.xtable + h.x + 2u * (2u * state + (on ? 1u : 0u))));
+          state = e.x & 0xFFFu;
+          open = (e.x >> 12) & 1u;
+          nmerge = (e.x >> 13) & 3u;
+          nemit = (e.x >> 15) & 3u;
+          const uint32_t da = sdelta_base + ((e.x >> 13) & 0xFF0u);
+          asm("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(dv.x), "=r"(dv.y), "=r"(dv.z), "=r"(dv.w) : "r"(da));
+          merges = e.y & 0x3FFFFu;
+          emits = e.y >> 18;
+        }
+      } else if (L == 1) {
         const uint2 e = __ldg(a.ctable + idx);
         state = e.x & 0xFFFu;
         open = (e.x >> 12) & 1u;
@@ -326,6 +352,7 @@ int launch_fsm_t(cb_es_plan* p, const uint64_t* d_pop, int64_t n, double* d_fit,
   a.table = reinterpret_cast<const uint4*>(p->d_fsm_table.p);
   a.ctable = reinterpret_cast<const uint2*>(p->d_fsm_ctable.p);
   a.mtable = reinterpret_cast<const uint4*>(p->d_fsm_ctable.p);
+  a.xtable = p->d_fsm_ctable.p;
   a.dtab = reinterpret_cast<const uint4*>(p->d_fsm_dtab.p);
   a.n_delta = p->fsm_deltas;
   a.infeas = p->d_infeas.p;
@@ -351,6 +378,11 @@ int launch_fsm_w(cb_es_plan* p, const uint64_t* d_pop, int64_t n, double* d_fit,
     case 16 + 3: return launch_fsm_t<F, 3, 2>(p, d_pop, n, d_fit, stream);
     case 16 + 4: return launch_fsm_t<F, 4, 2>(p, d_pop, n, d_fit, stream);
     case 16 + 0: return launch_fsm_t<F, 0, 2>(p, d_pop, n, d_fit, stream);
+    case 24 + 1: return launch_fsm_t<F, 1, 3>(p, d_pop, n, d_fit, stream);
+    case 24 + 2: return launch_fsm_t<F, 2, 3>(p, d_pop, n, d_fit, stream);
+    case 24 + 3: return launch_fsm_t<F, 3, 3>(p, d_pop, n, d_fit, stream);
+    case 24 + 4: return launch_fsm_t<F, 4, 3>(p, d_pop, n, d_fit, stream);
+    case 24 + 0: return launch_fsm_t<F, 0, 3>(p, d_pop, n, d_fit, stream);
     case 1: return launch_fsm_t<F, 1, 0>(p, d_pop, n, d_fit, stream);
     case 2: return launch_fsm_t<F, 2, 0>(p, d_pop, n, d_fit, stream);
     case 3: return launch_fsm_t<F, 3, 0>(p, d_pop, n, d_fit, stream);
@@ -396,7 +428,9 @@ struct FsmTrans {  // one computed transition before its next-state id is assign
 
 }  // namespace
 
-static int fsm_entry_bytes(const cb_es_plan* P) { return P->fsm_layout == 1 ? 8 : P->fsm_layout == 2 ? 16 : 32; }
+static int fsm_entry_bytes(const cb_es_plan* P) {
+  return P->fsm_layout == 1 || P->fsm_layout == 3 ? 8 : P->fsm_layout == 2 ? 16 : 32;
+}
 
 // Enumerate the reachable frontier states step by step and tabulate every
 // (state, bit) transition.  Leaves fsm_ok false when the program is wider
@@ -658,6 +692,20 @@ int build_fsm_plan(cb_es_plan* P) {
   }
   if (getenv("CB_FSM_STATS")) {
     int smax = 0, mm = 0, me = 0, dbits = 0, zero = 0;
+    size_t wide_entries = 0, wide_steps = 0;  // entries / steps beyond the 8-byte layout
+    for (int32_t q = 0; q < M; ++q) {
+      const size_t b = hdr[q].x * 2, e = q + 1 < M ? hdr[q + 1].x * 2 : table.size();
+      bool any = false;
+      for (size_t k2 = b; k2 < e; k2 += 2) {
+        const uint32_t xx = table[k2].x;
+        const bool w = (xx & 0xFFFFu) > 0xFFFu || ((xx >> 17) & 7u) > 3 || ((xx >> 20) & 7u) > 3;
+        wide_entries += w;
+        any |= w;
+      }
+      wide_steps += any;
+    }
+    fprintf(stderr, "fsm stats: %zu of %zu entries and %zu of %d steps need more than 8 bytes\n", wide_entries,
+            table.size() / 2, wide_steps, M);
     std::unordered_map<uint64_t, int> dd;
     for (int32_t q = 0; q < M; ++q) {
       const size_t b = hdr[q].x * 2, e = q + 1 < M ? hdr[q + 1].x * 2 : table.size();
@@ -717,7 +765,55 @@ int build_fsm_plan(cb_es_plan* P) {
       const uint32_t x = table[2 * k].x;
       if ((x & 0xFFFFu) > 0xFFFu || ((x >> 17) & 7u) > 3 || ((x >> 20) & 7u) > 3) fits8 = false;
     }
-    if (fits8) {
+    // mixed layout: 8-byte transitions for every step whose entries fit,
+    // 16-byte ones for the rest (NasNet-A: 16 of 620 steps)
+    std::vector<uint8_t> step_wide(M, 0);
+    bool mixed = !fits8 && fits16 && min_bytes <= 8 &&
+                 !(getenv("CB_FSM_MIXED") && atoi(getenv("CB_FSM_MIXED")) == 0);
+    size_t narrow_steps = 0;
+    for (int32_t q = 0; mixed && q < M; ++q) {
+      const size_t b = hdr[q].x, e = q + 1 < M ? hdr[q + 1].x : n_entries;
+      bool w = e - b > 2 * 4096;
+      for (size_t k = b; k < e && !w; ++k) {
+        const uint32_t x = table[2 * k].x;
+        w = (x & 0xFFFFu) > 0xFFFu || ((x >> 17) & 7u) > 3 || ((x >> 20) & 7u) > 3;
+      }
+      step_wide[q] = w;
+      narrow_steps += !w;
+    }
+    if (mixed && narrow_steps == 0) mixed = false;
+    if (mixed) {
+      P->fsm_layout = 3;
+      std::vector<uint32_t> offs(M);
+      size_t words = 0;
+      for (int32_t q = 0; q < M; ++q) {
+        const size_t b = hdr[q].x, e = q + 1 < M ? hdr[q + 1].x : n_entries;
+        if (step_wide[q]) words = (words + 3) & ~(size_t)3;  // 16-byte aligned
+        offs[q] = (uint32_t)words;
+        words += (e - b) * (step_wide[q] ? 4 : 2);
+      }
+      stab.assign(words, 0u);
+      for (int32_t q = 0; q < M; ++q) {
+        const size_t b = hdr[q].x, e = q + 1 < M ? hdr[q + 1].x : n_entries;
+        for (size_t k = b; k < e; ++k) {
+          const uint4 t0 = table[2 * k];
+          uint32_t* dst = stab.data() + offs[q] + (k - b) * (step_wide[q] ? 4 : 2);
+          if (step_wide[q]) {
+            dst[0] = (t0.x & 0xFFFFFFu) | (dref[k] << 24);
+            dst[1] = t0.y;
+            dst[2] = t0.z;
+            dst[3] = 0u;
+          } else {
+            const uint32_t nxt = t0.x & 0xFFFFu, open = (t0.x >> 16) & 1u, nm = (t0.x >> 17) & 7u,
+                           ne = (t0.x >> 20) & 7u;
+            dst[0] = nxt | (open << 12) | (nm << 13) | (ne << 15) | (dref[k] << 17);
+            dst[1] = (t0.y & 0x3FFFFu) | ((t0.z & 0x1FFu) << 18);
+          }
+        }
+        hdr[q].x = offs[q];
+        if (step_wide[q]) hdr[q].w |= FSM_WIDE_STEP;
+      }
+    } else if (fits8) {
       P->fsm_layout = 1;
       stab.resize(2 * n_entries);
       for (size_t k = 0; k < n_entries; ++k) {
@@ -770,7 +866,9 @@ int build_fsm_plan(cb_es_plan* P) {
   // automatic selection while the table stays cache-resident: in L1 for
   // BERT-base (46 KB), in L2 for NasNet-A (13.8 MB at 16 bytes, still faster
   // than the packed-label walk); `set_path("fsm")` forces it beyond
-  P->fsm_auto = n_entries * (size_t)fsm_entry_bytes(P) <= ((size_t)32 << 20);
+  const size_t table_bytes = P->fsm_layout == 3 ? P->d_fsm_ctable.n * sizeof(uint32_t)
+                                                 : n_entries * (size_t)fsm_entry_bytes(P);
+  P->fsm_auto = table_bytes <= ((size_t)32 << 20);
   return CB_OK;
 }
 
