@@ -215,7 +215,7 @@ typedef struct {
   int32_t packed_labels; /* 1: frontier fits the packed-label kernels (<= 16 slots),
                             2: also the packed anchor kernel (<= 8 slots) */
   int32_t fsm_transitions; /* transitions of the finite-state program (0 = none) */
-  int32_t fsm_entry_bytes; /* transition layout: 8 or 16 (+ shared delta table), or 32 */
+  int32_t fsm_entry_bytes; /* transition layout: 8 (also the mixed 8 / 16 layout) or 16 (+ shared delta table), or 32 */
 } cb_es_plan_info;
 int cb_es_plan_query(const cb_es_plan* p, cb_es_plan_info* info);
 /* Evaluation path: -1 automatic (the finite-state walk when its table is
