@@ -14,8 +14,9 @@ from paper_2111_00655_b200.es_device import DeviceEvolution
 for name, g, bs in (
         ("bert", workloads.bert_base(layers=1), None),
         ("rand", workloads.random_dag(400, seed=2, ops=workloads.RANDOM_OPS, window=48), None),
-        ("narrow", workloads.random_dag(700, seed=9, ops=workloads.RANDOM_OPS, window=6), None)):
-    bs = workloads.paper_backends(g, verify=False) if name == "bert" else \
+        ("narrow", workloads.random_dag(700, seed=9, ops=workloads.RANDOM_OPS, window=6), None),
+        ("nasnet", workloads.nasnet_a(), None)):  # the mixed 8 / 16-byte FSM layout
+    bs = workloads.paper_backends(g, verify=False) if name in ("bert", "nasnet") else \
         workloads.random_backends(g, n_backends=6, n_graph=1, seed=2 if name == "rand" else 9)
     res = tp.optimize(g, bs.registry, bs.measurer, 0.01)
     plan = tp.FitnessPlan(g, bs.registry, bs.measurer, res.placement, 0.01, bs.graph_backend,
