@@ -65,6 +65,9 @@ class DPStats:
         self.measure_calls  # settle
         return {k: v for k, v in self.__dict__.items() if not k.startswith("_")}
 
+    def __getstate__(self) -> dict:  # pickling settles the lazy counters first
+        return self.to_json()
+
 
 _LAZY_COUNTERS = frozenset(("measure_calls", "cache_hits", "computations"))
 
