@@ -89,6 +89,48 @@ __device__ __forceinline__ uint64_t seg_mask(int64_t lo, int64_t hi, int64_t w) 
 // read the doubles.  32 MB for 16.7 M parents (vs 64 MB of 32-bit keys).
 typedef uint16_t cb_key_t;
 
+// Row of W words (8-byte aligned) in as few requests as its alignment
+// allows: 16-byte streaming loads for every aligned word pair, so a 24-byte
+// row is two requests instead of three (each request to a sector that is
+// still in flight counts as another L2 miss).
+template <int W>
+__device__ __forceinline__ void load_row_cs(const uint64_t* __restrict__ row, uint64_t (&v)[W]) {
+  const bool odd = (reinterpret_cast<uintptr_t>(row) & 8u) != 0u;
+  if (W == 1) {
+    v[0] = __ldcs(row);
+    return;
+  }
+  if (odd) {
+    v[0] = __ldcs(row);
+#pragma unroll
+    for (int w = 1; w + 1 < W; w += 2) {
+      const ulonglong2 x = __ldcs(reinterpret_cast<const ulonglong2*>(row + w));
+      v[w] = x.x;
+      v[w + 1] = x.y;
+    }
+    if (W % 2 == 0) v[W - 1] = __ldcs(row + W - 1);
+  } else {
+#pragma unroll
+    for (int w = 0; w + 1 < W; w += 2) {
+      const ulonglong2 x = __ldcs(reinterpret_cast<const ulonglong2*>(row + w));
+      v[w] = x.x;
+      v[w + 1] = x.y;
+    }
+    if (W % 2 == 1) v[W - 1] = __ldcs(row + W - 1);
+  }
+}
+
+// Tournament key gather with an L2 evict-last hint: the parent rows and
+// child rows stream past with evict-first, the keys are re-read ~128 times
+// per 32-byte sector within one generation.
+__device__ __forceinline__ uint32_t ld_key(const cb_key_t* p) {
+  uint64_t pol;
+  asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+  unsigned short v;
+  asm("ld.global.nc.L2::cache_hint.u16 %0, [%1], %2;" : "=h"(v) : "l"(p), "l"(pol));
+  return v;
+}
+
 // Parameters of one generation's breeding (device pointers).
 struct BreedArgs {
   int32_t k;
@@ -113,7 +155,7 @@ __device__ __forceinline__ void tournament_pair(Philox& rng, int64_t n_parents, 
 #pragma unroll
   for (int q = 0; q < 2 * TOUR; ++q) idx[q] = rng.below((uint32_t)n_parents);
 #pragma unroll
-  for (int q = 0; q < 2 * TOUR; ++q) kv[q] = __ldg(keys + idx[q]);
+  for (int q = 0; q < 2 * TOUR; ++q) kv[q] = ld_key(keys + idx[q]);
 #pragma unroll
   for (int t = 0; t < 2; ++t) {
     uint32_t best = idx[t * TOUR], bk = kv[t * TOUR];
@@ -154,10 +196,10 @@ __device__ __forceinline__ void make_child(uint64_t (&v)[W], int32_t k, const ui
     } else {
       for (int t = 0; t < 2; ++t) {
         int64_t best = rng.below((uint32_t)n_parents);
-        uint32_t bk = __ldg(keys + best);
+        uint32_t bk = ld_key(keys + best);
         for (int j = 1; j < tournament; ++j) {
           const int64_t i = rng.below((uint32_t)n_parents);
-          const uint32_t ki = __ldg(keys + i);
+          const uint32_t ki = ld_key(keys + i);
           if (ki < bk || (ki == bk && __ldg(fit + i) < __ldg(fit + best))) {
             best = i;
             bk = ki;
@@ -173,12 +215,15 @@ __device__ __forceinline__ void make_child(uint64_t (&v)[W], int32_t k, const ui
       ci = x < y ? x : y;
       cj = x < y ? y : x;
     }
+    // parent rows and child rows stream through L2 with evict-first
+    // priority so the tournament keys stay resident
+    uint64_t ra[W], rb[W];
+    load_row_cs<W>(parents + pa * W, ra);
+    load_row_cs<W>(parents + pb * W, rb);
 #pragma unroll
     for (int w = 0; w < W; ++w) {
       const uint64_t mb = seg_mask(ci, cj, w);
-      // parent rows and child rows stream through L2 with evict-first
-      // priority so the tournament keys stay resident
-      v[w] = (__ldcs(parents + pa * W + w) & ~mb) | (__ldcs(parents + pb * W + w) & mb);
+      v[w] = (ra[w] & ~mb) | (rb[w] & mb);
     }
     if (rate >= 1.0 || rate * (double)k > 8.0) {
       for (int64_t bit = 0; bit < k; ++bit) {
