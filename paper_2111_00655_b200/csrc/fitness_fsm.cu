@@ -60,6 +60,18 @@ struct FsmArgs {
 #define FSM_BIT_FORCED 0x80u  // bit info: the unit has no genome bit (always on)
 #define FSM_WIDE_STEP 0x10000u  // header .w: the step's transitions use the 16-byte form (mixed layout)
 
+__device__ __forceinline__ ulonglong2 lds_u2(uint32_t a) {
+  ulonglong2 v;
+  asm volatile("ld.shared.v2.u64 {%0, %1}, [%2];" : "=l"(v.x), "=l"(v.y) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ void sts_u2(uint32_t a, const ulonglong2& v) {
+  asm volatile("st.shared.v2.u64 [%0], {%1, %2};" ::"r"(a), "l"(v.x), "l"(v.y));
+}
+__device__ __forceinline__ void sts_u4(uint32_t a, const uint4& v) {
+  asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(a), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w));
+}
+
 template <typename U>
 __device__ __forceinline__ void fadd2(U& lo, U& hi, uint64_t blo, uint64_t bhi) {
   static_assert(sizeof(U) == 8, "64-bit words");
@@ -114,6 +126,10 @@ fitness_fsm_kernel(FsmArgs a, const uint64_t* __restrict__ pop, int64_t n, doubl
   const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
   ulonglong2* sv = reinterpret_cast<ulonglong2*>(fsm_smem);  // [F][T] packed anchor sums
   ulonglong2* mine = sv + t;                                  // slot s at mine[s * T]
+  // 32-bit shared addresses of this thread's slot sums (slot s at + s * 16 T)
+  // and genome words (word w at + 8 w T): no generic-to-shared conversion
+  // inside the step loop
+  const uint32_t mine_a = (uint32_t)__cvta_generic_to_shared(mine);
   ulonglong2* q = sv + F * T + warp * FSM_QCAP;               // pricing queue of this warp
   uint64_t* tlo = reinterpret_cast<uint64_t*>(sv + F * T + (T / 32) * FSM_QCAP) + warp * 64;
   uint64_t* thi = tlo + 32;
@@ -123,6 +139,7 @@ fitness_fsm_kernel(FsmArgs a, const uint64_t* __restrict__ pop, int64_t n, doubl
   // bit is one shared load + shift (no per-step word select)
   uint64_t* swd = reinterpret_cast<uint64_t*>(fsm_smem + FsmSmemBase<F, W>::words_off) + t;
   if (W > 0) swd[W * T] = ~0ull;
+  const uint32_t swd_a = (uint32_t)__cvta_generic_to_shared(swd);
   __syncwarp();
   int qn = 0;
   bool inexact = false;
@@ -151,7 +168,8 @@ fitness_fsm_kernel(FsmArgs a, const uint64_t* __restrict__ pop, int64_t n, doubl
       for (int w = 0; w < WR; ++w) pre[w] = inext < n ? __ldcs(pop + inext * W + w) : 0ull;
       // an infeasible genome walks all-zero bits (its result is discarded)
 #pragma unroll
-      for (int w = 0; w < WR; ++w) swd[w * T] = dead ? 0ull : cur[w];
+      for (int w = 0; w < WR; ++w)  // asm like the step loop's loads (volatile asm keeps their order)
+        asm volatile("st.shared.u64 [%0], %1;" ::"r"(swd_a + w * (8u * T)), "l"(dead ? 0ull : cur[w]));
     } else if (in_range) {
       for (int32_t w = 0; w < a.words; ++w) dead |= (__ldg(gen + w) & __ldg(a.infeas + w)) != 0ull;
     }
@@ -159,22 +177,25 @@ fitness_fsm_kernel(FsmArgs a, const uint64_t* __restrict__ pop, int64_t n, doubl
     uint64_t tot_lo = 0ull, tot_hi = 0ull;
     int32_t cached_word = -1;
     uint64_t word = 0ull, next_word = W == 0 && a.words > 0 ? __ldg(gen) : 0ull;
-    uint4 hn = __ldg(a.hdr);  // step headers are warp uniform: prefetched one step ahead
+    // step headers are warp uniform: prefetched one step ahead (the plan
+    // pads the header array with a dummy step M, so no bound check)
+    const uint4* hp = a.hdr;
+    uint4 hn = __ldg(hp);
     // the 16-byte layout (an L2-resident table) also prefetches the unit's
     // packed sum (NasNet-A +3 %; the L1-resident walks lose ~0.5 % to it)
     constexpr bool PRE_REP = L >= 2;
-    uint4 rn = PRE_REP ? __ldg(a.hdr + 1) : make_uint4(0u, 0u, 0u, 0u);
+    uint4 rn = PRE_REP ? __ldg(hp + 1) : make_uint4(0u, 0u, 0u, 0u);
     auto bit_of = [&](uint32_t hy) {  // W > 0: the step's genome bit from shared memory
-      const uint64_t wd = swd[(hy >> 8) * T];
+      uint64_t wd;
+      asm volatile("ld.shared.u64 %0, [%1];" : "=l"(wd) : "r"(swd_a + (hy >> 8) * (8u * T)));
       return (uint32_t)(wd >> (hy & 63u)) & 1u;
     };
     uint32_t on_next = W > 0 ? bit_of(hn.y) : 0u;
     for (int32_t p = 0; p < a.M; ++p) {
       const uint4 h = hn, rp = rn;
-      if (p + 1 < a.M) {
-        hn = __ldg(a.hdr + 2 * (p + 1));
-        if (PRE_REP) rn = __ldg(a.hdr + 2 * (p + 1) + 1);
-      }
+      hp += 2;
+      hn = __ldg(hp);
+      if (PRE_REP) rn = __ldg(hp + 1);
       bool on;
       if (W > 0) {
         on = on_next != 0u;
@@ -251,8 +272,8 @@ fitness_fsm_kernel(FsmArgs a, const uint64_t* __restrict__ pop, int64_t n, doubl
       }
       fadd2(tot_lo, tot_hi, ((uint64_t)dv.y << 32) | dv.x, ((uint64_t)dv.w << 32) | dv.z);
       if (open) {  // the unit opens its slot with its packed sum
-        const uint4 r = PRE_REP ? rp : __ldg(a.hdr + 2 * p + 1);
-        mine[(h.z & 0xFFu) * T] = make_ulonglong2(((uint64_t)r.y << 32) | r.x, ((uint64_t)r.w << 32) | r.z);
+        const uint4 r = PRE_REP ? rp : __ldg(hp - 1);
+        sts_u4(mine_a + (h.z & 0xFFu) * (16u * T), r);
       }
       if (h.w & 0xFF) {
         constexpr int MAXM = L == 1 ? 3 : 5;
@@ -260,10 +281,11 @@ fitness_fsm_kernel(FsmArgs a, const uint64_t* __restrict__ pop, int64_t n, doubl
         for (int k = 0; k < MAXM; ++k) {  // component sums into the surviving anchor
           if (k >= (int)nmerge) break;
           const uint32_t src = (merges >> (6 * k)) & 7u, dst = (merges >> (6 * k + 3)) & 7u;
-          ulonglong2 d = mine[dst * T];
-          const ulonglong2 v = mine[src * T];
+          const uint32_t da = mine_a + dst * (16u * T);
+          ulonglong2 d = lds_u2(da);
+          const ulonglong2 v = lds_u2(mine_a + src * (16u * T));
           fadd2(d.x, d.y, v.x, v.y);
-          mine[dst * T] = d;
+          sts_u2(da, d);
         }
       }
       const int ne = (int)nemit;
@@ -278,7 +300,7 @@ fitness_fsm_kernel(FsmArgs a, const uint64_t* __restrict__ pop, int64_t n, doubl
         const unsigned closing = __ballot_sync(0xffffffffu, emit);
         if (closing) {
           if (emit) {
-            ulonglong2 v = mine[((emits >> (3 * k)) & 7u) * T];
+            ulonglong2 v = lds_u2(mine_a + ((emits >> (3 * k)) & 7u) * (16u * T));
             v.y |= (uint64_t)lane << FSM_LANE_SHIFT;
             q[qn + __popc(closing & ((1u << lane) - 1u))] = v;
           }
@@ -839,7 +861,8 @@ int build_fsm_plan(cb_es_plan* P) {
     }
   }
   // step headers interleaved with the units' packed sums
-  std::vector<uint4> hdr2((size_t)2 * M);
+  // (+ one dummy step: the kernel prefetches step p + 1's header unguarded)
+  std::vector<uint4> hdr2((size_t)2 * M + 2, make_uint4(0u, 0u, 0u, 0u));
   for (int32_t q = 0; q < M; ++q) {
     const fx192 x = fx_shr(P->prog[q].rep, P->anchor_shift);
     const uint64_t hi = x.w[1] | ((uint64_t)P->prog[q].cnt << FSM_CNT_SHIFT);
