@@ -590,9 +590,11 @@ extern "C" const char* cb_es_plan_kernel(const cb_es_plan* p) {
   if (frontier && p->force_path == 3) return "fitness_wide_kernel";
   if (frontier && p->fsm_ok && (p->force_path == 7 || (p->force_path == -1 && p->fsm_auto))) {
     static thread_local char fbuf[48];
-    // fitness_fsm_kernel<F, W, L>: L = transition layout (1: 8 bytes, 2: 16, 0: 32)
+    // fitness_fsm_kernel<F, W, L>: L = transition layout (1: 8 bytes, 2: 16, 3: mixed, 0: 32),
+    // + 4 with the 8-byte shared delta table
     std::snprintf(fbuf, sizeof(fbuf), "fitness_fsm_kernel<%d, %d, %d>", p->F <= 4 ? 4 : p->F <= 6 ? 6 : 8,
-                  p->words <= 4 ? p->words : 0, p->fsm_layout);
+                  p->words <= 4 ? p->words : 0,
+                  p->fsm_layout + (p->fsm_d64 && p->fsm_layout != 0 ? 4 : 0));
     return fbuf;
   }
   if (frontier && p->pa_ok && p->anchor_ok && (p->force_path == 6 || p->force_path == -1)) {

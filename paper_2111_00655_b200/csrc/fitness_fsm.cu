@@ -30,6 +30,9 @@
 #include "fitness_plan.cuh"
 
 #define FSM_THREADS 256
+#ifndef FSM_BITS_IN_REGS
+#define FSM_BITS_IN_REGS 1
+#endif
 #define FSM_QCAP 64
 
 namespace {
@@ -78,6 +81,23 @@ __device__ __forceinline__ void fadd2(U& lo, U& hi, uint64_t blo, uint64_t bhi) 
   asm("add.cc.u64 %0, %0, %2;\n\taddc.u64 %1, %1, %3;" : "+l"(lo), "+l"(hi) : "l"(blo), "l"(bhi));
 }
 
+// Delta `idx` of the shared delta table as a 128-bit value (x..w, low word
+// first): 16-byte entries, or 8-byte entries sign-extended (D64).
+template <bool D64>
+__device__ __forceinline__ uint4 load_delta(uint32_t base, uint32_t idx) {
+  uint4 dv;
+  if (D64) {
+    uint32_t lo, hi;
+    asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(lo), "=r"(hi) : "r"(base + idx * 8u));
+    const uint32_t sx = (uint32_t)((int32_t)hi >> 31);
+    dv = make_uint4(lo, hi, sx, sx);
+  } else {
+    asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(dv.x), "=r"(dv.y), "=r"(dv.z), "=r"(dv.w)
+                 : "r"(base + idx * 16u));
+  }
+  return dv;
+}
+
 // Price queue entry `idx` and add its term to the owner lane's accumulator.
 __device__ __forceinline__ void fsm_price(const ulonglong2* q, int idx, const FsmArgs& a, uint64_t* tlo,
                                           uint64_t* thi, bool& inexact) {
@@ -97,7 +117,10 @@ template <int F, int W>
 struct FsmSmemBase {  // packed sums [F][T], per-warp queues and lane totals, genome words [W + 1][T]
   static constexpr size_t words_off =
       (size_t)F * FSM_THREADS * 16 + (size_t)(FSM_THREADS / 32) * (FSM_QCAP * 16 + 64 * 8);
-  static constexpr size_t bytes = words_off + (W > 0 ? (size_t)(W + 1) * FSM_THREADS * 8 : 0);
+  // (the words only when the walk reads its bits from shared memory: with
+  // FSM_BITS_IN_REGS the freed 8 (W + 1) KB per block go to L1, where the
+  // transition table lives)
+  static constexpr size_t bytes = words_off + (W > 0 && !FSM_BITS_IN_REGS ? (size_t)(W + 1) * FSM_THREADS * 8 : 0);
 };
 
 // Transition entry (32 bytes, C = false): x = next | open << 16 | n_merge << 17 |
@@ -115,12 +138,23 @@ template <int F, int W, int L>
 __global__ void __launch_bounds__(FSM_THREADS)
 fitness_fsm_kernel(FsmArgs a, const uint64_t* __restrict__ pop, int64_t n, double* __restrict__ fit) {
   constexpr int T = FSM_THREADS;
+  // L = layout (0: 32-byte entries, 1: 8, 2: 16, 3: mixed) + 4 when every
+  // distinct delta fits a signed 64-bit word: the shared delta table then
+  // holds 8-byte entries (half the shared wavefronts of the per-step read)
+  constexpr int LL = L & 3;
+  constexpr bool D64 = L >= 4;
   extern __shared__ __align__(16) unsigned char fsm_smem[];
   // deltas after the per-thread arrays (dynamic size: n_delta entries)
   uint4* sdelta = reinterpret_cast<uint4*>(fsm_smem + FsmSmemBase<F, W>::bytes);
   const uint32_t sdelta_base = (uint32_t)__cvta_generic_to_shared(sdelta);
-  if (L != 0) {
-    for (int k = threadIdx.x; k < a.n_delta; k += T) sdelta[k] = __ldg(a.dtab + k);
+  if (LL != 0) {
+    for (int k = threadIdx.x; k < a.n_delta; k += T) {
+      const uint4 d = __ldg(a.dtab + k);
+      if (D64)
+        reinterpret_cast<uint64_t*>(sdelta)[k] = ((uint64_t)d.y << 32) | d.x;
+      else
+        sdelta[k] = d;
+    }
     __syncthreads();
   }
   const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
@@ -138,7 +172,7 @@ fitness_fsm_kernel(FsmArgs a, const uint64_t* __restrict__ pop, int64_t n, doubl
   // genome bit; a step's header holds its word's byte offset and bit, so the
   // bit is one shared load + shift (no per-step word select)
   uint64_t* swd = reinterpret_cast<uint64_t*>(fsm_smem + FsmSmemBase<F, W>::words_off) + t;
-  if (W > 0) swd[W * T] = ~0ull;
+  if (W > 0 && !FSM_BITS_IN_REGS) swd[W * T] = ~0ull;
   const uint32_t swd_a = (uint32_t)__cvta_generic_to_shared(swd);
   __syncwarp();
   int qn = 0;
@@ -169,7 +203,8 @@ fitness_fsm_kernel(FsmArgs a, const uint64_t* __restrict__ pop, int64_t n, doubl
       // an infeasible genome walks all-zero bits (its result is discarded)
 #pragma unroll
       for (int w = 0; w < WR; ++w)  // asm like the step loop's loads (volatile asm keeps their order)
-        asm volatile("st.shared.u64 [%0], %1;" ::"r"(swd_a + w * (8u * T)), "l"(dead ? 0ull : cur[w]));
+        if (!FSM_BITS_IN_REGS)
+          asm volatile("st.shared.u64 [%0], %1;" ::"r"(swd_a + w * (8u * T)), "l"(dead ? 0ull : cur[w]));
     } else if (in_range) {
       for (int32_t w = 0; w < a.words; ++w) dead |= (__ldg(gen + w) & __ldg(a.infeas + w)) != 0ull;
     }
@@ -183,13 +218,26 @@ fitness_fsm_kernel(FsmArgs a, const uint64_t* __restrict__ pop, int64_t n, doubl
     uint4 hn = __ldg(hp);
     // the 16-byte layout (an L2-resident table) also prefetches the unit's
     // packed sum (NasNet-A +3 %; the L1-resident walks lose ~0.5 % to it)
-    constexpr bool PRE_REP = L >= 2;
+    constexpr bool PRE_REP = LL >= 2;
     uint4 rn = PRE_REP ? __ldg(hp + 1) : make_uint4(0u, 0u, 0u, 0u);
+#if FSM_BITS_IN_REGS
+    uint64_t gw[WR];
+#pragma unroll
+    for (int w = 0; w < WR; ++w) gw[w] = dead ? 0ull : cur[w];
+    auto bit_of = [&](uint32_t hy) {  // W > 0: the step's genome bit, word selected from registers
+      const uint32_t wi = hy >> 8;
+      uint64_t wd = ~0ull;  // word W: units without a genome bit
+#pragma unroll
+      for (int w = 0; w < WR; ++w) wd = wi == (uint32_t)w ? gw[w] : wd;
+      return (uint32_t)(wd >> (hy & 63u)) & 1u;
+    };
+#else
     auto bit_of = [&](uint32_t hy) {  // W > 0: the step's genome bit from shared memory
       uint64_t wd;
       asm volatile("ld.shared.u64 %0, [%1];" : "=l"(wd) : "r"(swd_a + (hy >> 8) * (8u * T)));
       return (uint32_t)(wd >> (hy & 63u)) & 1u;
     };
+#endif
     uint32_t on_next = W > 0 ? bit_of(hn.y) : 0u;
     for (int32_t p = 0; p < a.M; ++p) {
       const uint4 h = hn, rp = rn;
@@ -215,7 +263,7 @@ fitness_fsm_kernel(FsmArgs a, const uint64_t* __restrict__ pop, int64_t n, doubl
       const uint32_t idx = h.x + 2u * state + (on ? 1u : 0u);  // 32-bit index math
       uint32_t open, nmerge, nemit, merges, emits;
       uint4 dv;  // exact delta: closed one-unit regions' terms - removed term
-      if (L == 3) {
+      if (LL == 3) {
         // mixed: the step's header says whether its transitions take 8 or
         // 16 bytes (warp-uniform); h.x is a word offset
         if (h.w & FSM_WIDE_STEP) {
@@ -224,8 +272,7 @@ fitness_fsm_kernel(FsmArgs a, const uint64_t* __restrict__ pop, int64_t n, doubl
           open = (e.x >> 16) & 1u;
           nmerge = (e.x >> 17) & 7u;
           nemit = (e.x >> 20) & 7u;
-          const uint32_t da = sdelta_base + ((e.x >> 20) & 0xFF0u);
-          asm("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(dv.x), "=r"(dv.y), "=r"(dv.z), "=r"(dv.w) : "r"(da));
+          dv = load_delta<D64>(sdelta_base, (e.x >> 24) & 0xFFu);
           merges = e.y;
           emits = e.z;
         } else {
@@ -234,30 +281,27 @@ fitness_fsm_kernel(FsmArgs a, const uint64_t* __restrict__ pop, int64_t n, doubl
           open = (e.x >> 12) & 1u;
           nmerge = (e.x >> 13) & 3u;
           nemit = (e.x >> 15) & 3u;
-          const uint32_t da = sdelta_base + ((e.x >> 13) & 0xFF0u);
-          asm("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(dv.x), "=r"(dv.y), "=r"(dv.z), "=r"(dv.w) : "r"(da));
+          dv = load_delta<D64>(sdelta_base, (e.x >> 17) & 0xFFu);
           merges = e.y & 0x3FFFFu;
           emits = e.y >> 18;
         }
-      } else if (L == 1) {
+      } else if (LL == 1) {
         const uint2 e = __ldg(a.ctable + idx);
         state = e.x & 0xFFFu;
         open = (e.x >> 12) & 1u;
         nmerge = (e.x >> 13) & 3u;
         nemit = (e.x >> 15) & 3u;
         // one 16-byte shared load (the compiler splits a uint4 read in two)
-        const uint32_t da = sdelta_base + ((e.x >> 13) & 0xFF0u);
-        asm("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(dv.x), "=r"(dv.y), "=r"(dv.z), "=r"(dv.w) : "r"(da));
+        dv = load_delta<D64>(sdelta_base, (e.x >> 17) & 0xFFu);
         merges = e.y;
         emits = e.y >> 18;
-      } else if (L == 2) {
+      } else if (LL == 2) {
         const uint4 e = __ldg(a.mtable + idx);
         state = e.x & 0xFFFFu;
         open = (e.x >> 16) & 1u;
         nmerge = (e.x >> 17) & 7u;
         nemit = (e.x >> 20) & 7u;
-        const uint32_t da = sdelta_base + ((e.x >> 20) & 0xFF0u);
-        asm("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(dv.x), "=r"(dv.y), "=r"(dv.z), "=r"(dv.w) : "r"(da));
+        dv = load_delta<D64>(sdelta_base, (e.x >> 24) & 0xFFu);
         merges = e.y;
         emits = e.z;
       } else {
@@ -276,7 +320,7 @@ fitness_fsm_kernel(FsmArgs a, const uint64_t* __restrict__ pop, int64_t n, doubl
         sts_u4(mine_a + (h.z & 0xFFu) * (16u * T), r);
       }
       if (h.w & 0xFF) {
-        constexpr int MAXM = L == 1 ? 3 : 5;
+        constexpr int MAXM = LL == 1 ? 3 : 5;
 #pragma unroll
         for (int k = 0; k < MAXM; ++k) {  // component sums into the surviving anchor
           if (k >= (int)nmerge) break;
@@ -292,7 +336,7 @@ fitness_fsm_kernel(FsmArgs a, const uint64_t* __restrict__ pop, int64_t n, doubl
       // the step's largest emit count (uniform, from its header): later
       // iterations of lanes with fewer emits see an empty ballot
       const int nemax = (int)((h.w >> 8) & 0xFFu);
-      constexpr int MAXE = L == 1 ? 3 : 5;
+      constexpr int MAXE = LL == 1 ? 3 : 5;
 #pragma unroll
       for (int k = 0; k < MAXE; ++k) {  // multi-unit regions close: queued for pricing
         if (k >= nemax) break;
@@ -340,7 +384,7 @@ fitness_fsm_kernel(FsmArgs a, const uint64_t* __restrict__ pop, int64_t n, doubl
 
 template <int F, int W, int L>
 int launch_fsm_t(cb_es_plan* p, const uint64_t* d_pop, int64_t n, double* d_fit, cudaStream_t stream) {
-  const size_t smem = FsmSmemBase<F, W>::bytes + (L != 0 ? (size_t)p->fsm_deltas * sizeof(uint4) : 0);
+  const size_t smem = FsmSmemBase<F, W>::bytes + ((L & 3) != 0 ? (size_t)p->fsm_deltas * (L >= 4 ? 8 : 16) : 0);
   if (cb_smem_claim((const void*)fitness_fsm_kernel<F, W, L>, smem)) {
     CB_CUDA_TRY(cudaFuncSetAttribute(fitness_fsm_kernel<F, W, L>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      (int)smem));
@@ -389,6 +433,26 @@ int launch_fsm_t(cb_es_plan* p, const uint64_t* d_pop, int64_t n, double* d_fit,
 
 template <int F>
 int launch_fsm_w(cb_es_plan* p, const uint64_t* d_pop, int64_t n, double* d_fit, cudaStream_t stream) {
+  // 64-bit deltas (L + 4) when the plan found every delta within a signed 64-bit word
+  if (p->fsm_d64 && p->fsm_layout != 0) {
+    switch (p->fsm_layout * 8 + (p->words <= 4 ? p->words : 0)) {
+      case 8 + 1: return launch_fsm_t<F, 1, 5>(p, d_pop, n, d_fit, stream);
+      case 8 + 2: return launch_fsm_t<F, 2, 5>(p, d_pop, n, d_fit, stream);
+      case 8 + 3: return launch_fsm_t<F, 3, 5>(p, d_pop, n, d_fit, stream);
+      case 8 + 4: return launch_fsm_t<F, 4, 5>(p, d_pop, n, d_fit, stream);
+      case 8 + 0: return launch_fsm_t<F, 0, 5>(p, d_pop, n, d_fit, stream);
+      case 16 + 1: return launch_fsm_t<F, 1, 6>(p, d_pop, n, d_fit, stream);
+      case 16 + 2: return launch_fsm_t<F, 2, 6>(p, d_pop, n, d_fit, stream);
+      case 16 + 3: return launch_fsm_t<F, 3, 6>(p, d_pop, n, d_fit, stream);
+      case 16 + 4: return launch_fsm_t<F, 4, 6>(p, d_pop, n, d_fit, stream);
+      case 16 + 0: return launch_fsm_t<F, 0, 6>(p, d_pop, n, d_fit, stream);
+      case 24 + 1: return launch_fsm_t<F, 1, 7>(p, d_pop, n, d_fit, stream);
+      case 24 + 2: return launch_fsm_t<F, 2, 7>(p, d_pop, n, d_fit, stream);
+      case 24 + 3: return launch_fsm_t<F, 3, 7>(p, d_pop, n, d_fit, stream);
+      case 24 + 4: return launch_fsm_t<F, 4, 7>(p, d_pop, n, d_fit, stream);
+      default: return launch_fsm_t<F, 0, 7>(p, d_pop, n, d_fit, stream);
+    }
+  }
   switch (p->fsm_layout * 8 + (p->words <= 4 ? p->words : 0)) {
     case 8 + 1: return launch_fsm_t<F, 1, 1>(p, d_pop, n, d_fit, stream);
     case 8 + 2: return launch_fsm_t<F, 2, 1>(p, d_pop, n, d_fit, stream);
@@ -877,6 +941,14 @@ int build_fsm_plan(cb_es_plan* P) {
       return CB_ERR_CUDA;
     }
     P->fsm_deltas = (int32_t)dtab.size();
+    // 8-byte shared deltas when every distinct delta is a sign-extended
+    // 64-bit value (all five BASELINE models: <= 57 bits); CB_FSM_D64=0 keeps
+    // the 16-byte table (A/B, tests)
+    P->fsm_d64 = !(getenv("CB_FSM_D64") && atoi(getenv("CB_FSM_D64")) == 0);
+    for (const uint4& d : dtab) {
+      const uint64_t lo = ((uint64_t)d.y << 32) | d.x, hi = ((uint64_t)d.w << 32) | d.z;
+      P->fsm_d64 = P->fsm_d64 && hi == ((lo >> 63) ? ~0ull : 0ull);
+    }
     table.resize(2);  // only the short copy is kept on the device
   }
   if ((e = P->d_fsm_hdr.upload(reinterpret_cast<const uint32_t*>(hdr2.data()), hdr2.size() * 4)) != cudaSuccess ||

@@ -98,6 +98,7 @@ struct cb_es_plan {
   int32_t fsm_layout = 0;  // transitions: 1 = 8 bytes, 2 = 16 bytes (+ shared delta table), 0 = 32 bytes
   DBuf<uint32_t> d_fsm_ctable, d_fsm_dtab;
   int32_t fsm_deltas = 0;
+  bool fsm_d64 = false;  // shared delta table as sign-extended 8-byte entries (fitness_fsm.cu)
   int32_t fsm_states_max = 0;
   int64_t fsm_entries = 0;
   // tournament order keys of the parent population (es.cu)

@@ -196,10 +196,15 @@ def test_fsm_entry_layouts_agree(gpu, name, monkeypatch):
         plans[nbytes] = tp.FitnessPlan(*args)
     monkeypatch.delenv("CB_FSM_ENTRY_BYTES")
     default = tp.FitnessPlan(*args)
+    monkeypatch.setenv("CB_FSM_D64", "0")
+    plans["d128"] = tp.FitnessPlan(*args)  # the 16-byte shared delta table
+    monkeypatch.delenv("CB_FSM_D64")
+    assert plans["d128"].kernel_name().endswith(", 3>" if name == "nasnet_a" else ", 1>")
     assert all(p.has_fsm() for p in plans.values())
     want_small = 8
     assert default.info.fsm_entry_bytes == want_small
-    assert default.kernel_name().endswith(", 3>" if name == "nasnet_a" else ", 1>")
+    # layout 3 (mixed) for NasNet-A, 1 (8 bytes) otherwise; + 4: 8-byte deltas
+    assert default.kernel_name().endswith(", 7>" if name == "nasnet_a" else ", 5>")
     assert plans[8].info.fsm_entry_bytes == want_small
     assert plans[16].info.fsm_entry_bytes == 16 and plans[32].info.fsm_entry_bytes == 32
     assert len({p.info.fsm_transitions for p in plans.values()}) == 1
