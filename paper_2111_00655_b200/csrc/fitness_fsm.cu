@@ -130,7 +130,7 @@ struct FsmSmemBase {  // packed sums [F][T], per-warp queues and lane totals, ge
 // offloaded unit.
 //
 // Compact layout (8 bytes, C = true): x = next (12 bits) | open << 12 |
-// n_merge (2 bits) << 13 | n_emit (2 bits) << 15 | delta index (8 bits) << 17,
+// n_merge (2 bits) << 13 | n_emit (2 bits) << 15 | delta index (8 bits) << 24,
 // y = merges (6 bits) x 3 | emit slots (3 bits) x 3 << 18; the deltas (at
 // most 256 distinct values; BERT-base has 22) sit in shared memory.  Used
 // when every transition fits: a quarter of the table's cache footprint.
@@ -224,12 +224,20 @@ fitness_fsm_kernel(FsmArgs a, const uint64_t* __restrict__ pop, int64_t n, doubl
     uint64_t gw[WR];
 #pragma unroll
     for (int w = 0; w < WR; ++w) gw[w] = dead ? 0ull : cur[w];
-    auto bit_of = [&](uint32_t hy) {  // W > 0: the step's genome bit, word selected from registers
+    // W > 0: the step's genome bit from the current word, reselected from
+    // the registers only when the word changes (warp uniform: consecutive
+    // steps mostly read one word; the integer pipe is what binds)
+    uint32_t cw = ~0u;
+    uint64_t cwd = 0ull;
+    auto bit_of = [&](uint32_t hy) {
       const uint32_t wi = hy >> 8;
-      uint64_t wd = ~0ull;  // word W: units without a genome bit
+      if (wi != cw) {
+        cw = wi;
+        cwd = ~0ull;  // word W: units without a genome bit
 #pragma unroll
-      for (int w = 0; w < WR; ++w) wd = wi == (uint32_t)w ? gw[w] : wd;
-      return (uint32_t)(wd >> (hy & 63u)) & 1u;
+        for (int w = 0; w < WR; ++w) cwd = wi == (uint32_t)w ? gw[w] : cwd;
+      }
+      return (uint32_t)(cwd >> (hy & 63u)) & 1u;
     };
 #else
     auto bit_of = [&](uint32_t hy) {  // W > 0: the step's genome bit from shared memory
@@ -239,7 +247,15 @@ fitness_fsm_kernel(FsmArgs a, const uint64_t* __restrict__ pop, int64_t n, doubl
     };
 #endif
     uint32_t on_next = W > 0 ? bit_of(hn.y) : 0u;
-    for (int32_t p = 0; p < a.M; ++p) {
+    // ACC64: the deltas (|d| < 2^57, plan-checked) add into a 64-bit
+    // accumulator folded into the 128-bit total every 64 steps (NasNet-A's
+    // W = 0 walk, F = 8, lost 4 % to it: sign-extended 128-bit adds there)
+    constexpr bool ACC64 = D64 && W > 0;
+    constexpr int32_t CHUNK = ACC64 ? 64 : 0x40000000;
+    for (int32_t p0 = 0; p0 < a.M; p0 += CHUNK) {
+    const int32_t pe = min(a.M, p0 + CHUNK);
+    int64_t dacc = 0;
+    for (int32_t p = p0; p < pe; ++p) {
       const uint4 h = hn, rp = rn;
       hp += 2;
       hn = __ldg(hp);
@@ -262,7 +278,8 @@ fitness_fsm_kernel(FsmArgs a, const uint64_t* __restrict__ pop, int64_t n, doubl
       if (W == 0) on = on && !dead;
       const uint32_t idx = h.x + 2u * state + (on ? 1u : 0u);  // 32-bit index math
       uint32_t open, nmerge, nemit, merges, emits;
-      uint4 dv;  // exact delta: closed one-unit regions' terms - removed term
+      uint32_t didx = 0u;  // shared delta table index (layouts 1-3: the entry's top byte)
+      uint4 dv = make_uint4(0u, 0u, 0u, 0u);  // exact delta: closed one-unit regions' terms - removed term
       if (LL == 3) {
         // mixed: the step's header says whether its transitions take 8 or
         // 16 bytes (warp-uniform); h.x is a word offset
@@ -272,7 +289,8 @@ fitness_fsm_kernel(FsmArgs a, const uint64_t* __restrict__ pop, int64_t n, doubl
           open = (e.x >> 16) & 1u;
           nmerge = (e.x >> 17) & 7u;
           nemit = (e.x >> 20) & 7u;
-          dv = load_delta<D64>(sdelta_base, (e.x >> 24) & 0xFFu);
+          didx = e.x >> 24;
+          if (!ACC64) dv = load_delta<D64>(sdelta_base, didx);  // in the branch (NasNet-A: 4 % faster)
           merges = e.y;
           emits = e.z;
         } else {
@@ -281,7 +299,8 @@ fitness_fsm_kernel(FsmArgs a, const uint64_t* __restrict__ pop, int64_t n, doubl
           open = (e.x >> 12) & 1u;
           nmerge = (e.x >> 13) & 3u;
           nemit = (e.x >> 15) & 3u;
-          dv = load_delta<D64>(sdelta_base, (e.x >> 17) & 0xFFu);
+          didx = e.x >> 24;
+          if (!ACC64) dv = load_delta<D64>(sdelta_base, didx);  // in the branch (NasNet-A: 4 % faster)
           merges = e.y & 0x3FFFFu;
           emits = e.y >> 18;
         }
@@ -292,7 +311,7 @@ fitness_fsm_kernel(FsmArgs a, const uint64_t* __restrict__ pop, int64_t n, doubl
         nmerge = (e.x >> 13) & 3u;
         nemit = (e.x >> 15) & 3u;
         // one 16-byte shared load (the compiler splits a uint4 read in two)
-        dv = load_delta<D64>(sdelta_base, (e.x >> 17) & 0xFFu);
+        didx = e.x >> 24;
         merges = e.y;
         emits = e.y >> 18;
       } else if (LL == 2) {
@@ -301,7 +320,7 @@ fitness_fsm_kernel(FsmArgs a, const uint64_t* __restrict__ pop, int64_t n, doubl
         open = (e.x >> 16) & 1u;
         nmerge = (e.x >> 17) & 7u;
         nemit = (e.x >> 20) & 7u;
-        dv = load_delta<D64>(sdelta_base, (e.x >> 24) & 0xFFu);
+        didx = e.x >> 24;
         merges = e.y;
         emits = e.z;
       } else {
@@ -314,7 +333,14 @@ fitness_fsm_kernel(FsmArgs a, const uint64_t* __restrict__ pop, int64_t n, doubl
         merges = e.y;
         emits = e.z;
       }
-      fadd2(tot_lo, tot_hi, ((uint64_t)dv.y << 32) | dv.x, ((uint64_t)dv.w << 32) | dv.z);
+      if (ACC64) {
+        int64_t d;
+        asm volatile("ld.shared.s64 %0, [%1];" : "=l"(d) : "r"(sdelta_base + didx * 8u));
+        dacc += d;
+      } else {
+        if (LL != 0 && LL != 3) dv = load_delta<D64>(sdelta_base, didx);
+        fadd2(tot_lo, tot_hi, ((uint64_t)dv.y << 32) | dv.x, ((uint64_t)dv.w << 32) | dv.z);
+      }
       if (open) {  // the unit opens its slot with its packed sum
         const uint4 r = PRE_REP ? rp : __ldg(hp - 1);
         sts_u4(mine_a + (h.z & 0xFFu) * (16u * T), r);
@@ -360,6 +386,8 @@ fitness_fsm_kernel(FsmArgs a, const uint64_t* __restrict__ pop, int64_t n, doubl
         }
       }
       if (W > 0) on_next = bit_of(hn.y);  // next step's bit, off the state chain
+    }
+    if (ACC64) fadd2(tot_lo, tot_hi, (uint64_t)dacc, (uint64_t)(dacc >> 63));
     }
     __syncwarp();
     if (lane < qn) fsm_price(q, lane, a, tlo, thi, inexact);
@@ -894,7 +922,7 @@ int build_fsm_plan(cb_es_plan* P) {
           } else {
             const uint32_t nxt = t0.x & 0xFFFFu, open = (t0.x >> 16) & 1u, nm = (t0.x >> 17) & 7u,
                            ne = (t0.x >> 20) & 7u;
-            dst[0] = nxt | (open << 12) | (nm << 13) | (ne << 15) | (dref[k] << 17);
+            dst[0] = nxt | (open << 12) | (nm << 13) | (ne << 15) | (dref[k] << 24);
             dst[1] = (t0.y & 0x3FFFFu) | ((t0.z & 0x1FFu) << 18);
           }
         }
@@ -907,7 +935,7 @@ int build_fsm_plan(cb_es_plan* P) {
       for (size_t k = 0; k < n_entries; ++k) {
         const uint4 t0 = table[2 * k];
         const uint32_t nxt = t0.x & 0xFFFFu, open = (t0.x >> 16) & 1u, nm = (t0.x >> 17) & 7u, ne = (t0.x >> 20) & 7u;
-        stab[2 * k] = nxt | (open << 12) | (nm << 13) | (ne << 15) | (dref[k] << 17);
+        stab[2 * k] = nxt | (open << 12) | (nm << 13) | (ne << 15) | (dref[k] << 24);
         stab[2 * k + 1] = (t0.y & 0x3FFFFu) | ((t0.z & 0x1FFu) << 18);
       }
     } else if (fits16) {
@@ -942,12 +970,15 @@ int build_fsm_plan(cb_es_plan* P) {
     }
     P->fsm_deltas = (int32_t)dtab.size();
     // 8-byte shared deltas when every distinct delta is a sign-extended
-    // 64-bit value (all five BASELINE models: <= 57 bits); CB_FSM_D64=0 keeps
+    // 64-bit value below 2^57 in magnitude (all BASELINE models: <= 57 bits); CB_FSM_D64=0 keeps
     // the 16-byte table (A/B, tests)
     P->fsm_d64 = !(getenv("CB_FSM_D64") && atoi(getenv("CB_FSM_D64")) == 0);
     for (const uint4& d : dtab) {
       const uint64_t lo = ((uint64_t)d.y << 32) | d.x, hi = ((uint64_t)d.w << 32) | d.z;
-      P->fsm_d64 = P->fsm_d64 && hi == ((lo >> 63) ? ~0ull : 0ull);
+      // |d| < 2^57: 64 steps' deltas sum within the kernel's 64-bit accumulator
+      const int64_t top = (int64_t)lo >> 57;
+      P->fsm_d64 = P->fsm_d64 && hi == ((lo >> 63) ? ~0ull : 0ull) && (top == 0 || top == -1) &&
+                   (int64_t)lo != -(int64_t)(1ull << 57);
     }
     table.resize(2);  // only the short copy is kept on the device
   }
