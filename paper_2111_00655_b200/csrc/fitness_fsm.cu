@@ -62,6 +62,12 @@ struct FsmArgs {
 #define FSM_CNT_SHIFT 48
 #define FSM_BIT_FORCED 0x80u  // bit info: the unit has no genome bit (always on)
 #define FSM_WIDE_STEP 0x10000u  // header .w: the step's transitions use the 16-byte form (mixed layout)
+#define FSM_BIT_NEWWORD 0x40u   // bit info: the step's genome word differs from the previous step's
+
+// merge / emit counts as thermometer bits: merge k at bit 13 + k, emit k at bit 18 + k
+static inline uint32_t fsm_therm(int n_merge, int n_emit) {
+  return (((1u << n_merge) - 1u) << 13) | (((1u << n_emit) - 1u) << 18);
+}
 
 __device__ __forceinline__ ulonglong2 lds_u2(uint32_t a) {
   ulonglong2 v;
@@ -227,12 +233,10 @@ fitness_fsm_kernel(FsmArgs a, const uint64_t* __restrict__ pop, int64_t n, doubl
     // W > 0: the step's genome bit from the current word, reselected from
     // the registers only when the word changes (warp uniform: consecutive
     // steps mostly read one word; the integer pipe is what binds)
-    uint32_t cw = ~0u;
     uint64_t cwd = 0ull;
     auto bit_of = [&](uint32_t hy) {
-      const uint32_t wi = hy >> 8;
-      if (wi != cw) {
-        cw = wi;
+      if (hy & FSM_BIT_NEWWORD) {
+        const uint32_t wi = hy >> 8;
         cwd = ~0ull;  // word W: units without a genome bit
 #pragma unroll
         for (int w = 0; w < WR; ++w) cwd = wi == (uint32_t)w ? gw[w] : cwd;
@@ -277,7 +281,9 @@ fitness_fsm_kernel(FsmArgs a, const uint64_t* __restrict__ pop, int64_t n, doubl
       }
       if (W == 0) on = on && !dead;
       const uint32_t idx = h.x + 2u * state + (on ? 1u : 0u);  // 32-bit index math
-      uint32_t open, nmerge, nemit, merges, emits;
+      // th: merge / emit counts as thermometers (bit 13 + k: the transition
+      // has merge k, bit 18 + k: emit k), tested in place -- no field extraction
+      uint32_t open, th, merges, emits;
       uint32_t didx = 0u;  // shared delta table index (layouts 1-3: the entry's top byte)
       uint4 dv = make_uint4(0u, 0u, 0u, 0u);  // exact delta: closed one-unit regions' terms - removed term
       if (LL == 3) {
@@ -285,10 +291,9 @@ fitness_fsm_kernel(FsmArgs a, const uint64_t* __restrict__ pop, int64_t n, doubl
         // 16 bytes (warp-uniform); h.x is a word offset
         if (h.w & FSM_WIDE_STEP) {
           const uint4 e = __ldg(reinterpret_cast<const uint4*>(a.xtable + h.x + 4u * (2u * state + (on ? 1u : 0u))));
-          state = e.x & 0xFFFFu;
-          open = (e.x >> 16) & 1u;
-          nmerge = (e.x >> 17) & 7u;
-          nemit = (e.x >> 20) & 7u;
+          state = e.x & 0xFFFu;  // (mixed layouts keep <= 4096 states per step)
+          open = (e.x >> 12) & 1u;
+          th = e.x;
           didx = e.x >> 24;
           if (!ACC64) dv = load_delta<D64>(sdelta_base, didx);  // in the branch (NasNet-A: 4 % faster)
           merges = e.y;
@@ -297,8 +302,7 @@ fitness_fsm_kernel(FsmArgs a, const uint64_t* __restrict__ pop, int64_t n, doubl
           const uint2 e = __ldg(reinterpret_cast<const uint2*>(a.xtable + h.x + 2u * (2u * state + (on ? 1u : 0u))));
           state = e.x & 0xFFFu;
           open = (e.x >> 12) & 1u;
-          nmerge = (e.x >> 13) & 3u;
-          nemit = (e.x >> 15) & 3u;
+          th = e.x;
           didx = e.x >> 24;
           if (!ACC64) dv = load_delta<D64>(sdelta_base, didx);  // in the branch (NasNet-A: 4 % faster)
           merges = e.y & 0x3FFFFu;
@@ -308,9 +312,7 @@ fitness_fsm_kernel(FsmArgs a, const uint64_t* __restrict__ pop, int64_t n, doubl
         const uint2 e = __ldg(a.ctable + idx);
         state = e.x & 0xFFFu;
         open = (e.x >> 12) & 1u;
-        nmerge = (e.x >> 13) & 3u;
-        nemit = (e.x >> 15) & 3u;
-        // one 16-byte shared load (the compiler splits a uint4 read in two)
+        th = e.x;
         didx = e.x >> 24;
         merges = e.y;
         emits = e.y >> 18;
@@ -318,8 +320,7 @@ fitness_fsm_kernel(FsmArgs a, const uint64_t* __restrict__ pop, int64_t n, doubl
         const uint4 e = __ldg(a.mtable + idx);
         state = e.x & 0xFFFFu;
         open = (e.x >> 16) & 1u;
-        nmerge = (e.x >> 17) & 7u;
-        nemit = (e.x >> 20) & 7u;
+        th = e.w;
         didx = e.x >> 24;
         merges = e.y;
         emits = e.z;
@@ -328,8 +329,7 @@ fitness_fsm_kernel(FsmArgs a, const uint64_t* __restrict__ pop, int64_t n, doubl
         dv = __ldg(a.table + 2u * idx + 1u);
         state = e.x & 0xFFFFu;
         open = (e.x >> 16) & 1u;
-        nmerge = (e.x >> 17) & 7u;
-        nemit = (e.x >> 20) & 7u;
+        th = e.w;
         merges = e.y;
         emits = e.z;
       }
@@ -343,13 +343,13 @@ fitness_fsm_kernel(FsmArgs a, const uint64_t* __restrict__ pop, int64_t n, doubl
       }
       if (open) {  // the unit opens its slot with its packed sum
         const uint4 r = PRE_REP ? rp : __ldg(hp - 1);
-        sts_u4(mine_a + (h.z & 0xFFu) * (16u * T), r);
+        sts_u4(mine_a + h.z, r);  // h.z: the slot's byte offset
       }
-      if (h.w & 0xFF) {
+      if (h.w & 0x1Fu) {  // some transition of the step merges (thermometer of the step's maximum)
         constexpr int MAXM = LL == 1 ? 3 : 5;
 #pragma unroll
         for (int k = 0; k < MAXM; ++k) {  // component sums into the surviving anchor
-          if (k >= (int)nmerge) break;
+          if (!(th & (1u << (13 + k)))) break;
           const uint32_t src = (merges >> (6 * k)) & 7u, dst = (merges >> (6 * k + 3)) & 7u;
           const uint32_t da = mine_a + dst * (16u * T);
           ulonglong2 d = lds_u2(da);
@@ -358,15 +358,13 @@ fitness_fsm_kernel(FsmArgs a, const uint64_t* __restrict__ pop, int64_t n, doubl
           sts_u2(da, d);
         }
       }
-      const int ne = (int)nemit;
-      // the step's largest emit count (uniform, from its header): later
-      // iterations of lanes with fewer emits see an empty ballot
-      const int nemax = (int)((h.w >> 8) & 0xFFu);
+      // the step's largest emit count (uniform, a thermometer at header bit
+      // 8): later iterations of lanes with fewer emits see an empty ballot
       constexpr int MAXE = LL == 1 ? 3 : 5;
 #pragma unroll
       for (int k = 0; k < MAXE; ++k) {  // multi-unit regions close: queued for pricing
-        if (k >= nemax) break;
-        const bool emit = k < ne;
+        if (!(h.w & (0x100u << k))) break;
+        const bool emit = (th >> (18 + k)) & 1u;
         const unsigned closing = __ballot_sync(0xffffffffu, emit);
         if (closing) {
           if (emit) {
@@ -569,6 +567,12 @@ int build_fsm_plan(cb_es_plan* P) {
   std::vector<uint4> table;
   std::vector<uint4> hdr(M);
   std::vector<int32_t> occ_end(F, -1);
+  // genome word a step's bit lies in (W > 0 kernels reselect the word only
+  // when it changes: FSM_BIT_NEWWORD); units without a bit read word `words`
+  auto word_of = [&](int32_t q) -> int32_t {
+    if (q < 0) return -1;
+    return P->prog[q].bit >= 0 ? (int32_t)(P->prog[q].bit >> 6) : P->words;
+  };
   std::vector<FsmState> cur(1);  // the empty frontier
   std::vector<uint64_t> hkey;
   std::vector<int32_t> hval;
@@ -584,7 +588,9 @@ int build_fsm_plan(cb_es_plan* P) {
     // `words` (the kernel's all-ones word when W > 0) and is flagged for W = 0
     const uint32_t bitinfo = r.bit >= 0 ? ((uint32_t)r.bit & 63u) | ((uint32_t)(r.bit >> 6) << 8)
                                         : FSM_BIT_FORCED | ((uint32_t)P->words << 8);
-    hdr[p] = make_uint4((uint32_t)(table.size() / 2), bitinfo, (uint32_t)S | ((uint32_t)r.nend << 8), 0u);
+    // z: the slot's byte offset in the kernel's per-thread slot sums
+    hdr[p] = make_uint4((uint32_t)(table.size() / 2), bitinfo | (word_of(p) != word_of(p - 1) ? FSM_BIT_NEWWORD : 0u),
+                        (uint32_t)S * 16u * FSM_THREADS, 0u);
     if ((table.size() + 4 * cur.size()) * sizeof(uint4) > cap) return CB_OK;
     // next-state ids: open addressing on key + 1 (0 = empty), sized for
     // every transition of the step
@@ -739,7 +745,7 @@ int build_fsm_plan(cb_es_plan* P) {
       }
       table.push_back(make_uint4((uint32_t)nid | (open << 16) | ((uint32_t)n_merge << 17) |
                                      ((uint32_t)n_emit << 20),
-                                 merges, emits, 0u));
+                                 merges, emits, fsm_therm(n_merge, n_emit)));
       table.push_back(make_uint4((uint32_t)dx.w[0], (uint32_t)(dx.w[0] >> 32), (uint32_t)dx.w[1],
                                  (uint32_t)(dx.w[1] >> 32)));
     }
@@ -750,7 +756,7 @@ int build_fsm_plan(cb_es_plan* P) {
       max_merge = std::max(max_merge, (table[k].x >> 17) & 7u);
       max_emit = std::max(max_emit, (table[k].x >> 20) & 7u);
     }
-    hdr[p].w = max_merge | (max_emit << 8);
+    hdr[p].w = ((1u << max_merge) - 1u) | (((1u << max_emit) - 1u) << 8);  // thermometers
     cur.swap(nxt);
   }
   // Renumber every step's states by visit frequency (most visited first),
@@ -898,6 +904,12 @@ int build_fsm_plan(cb_es_plan* P) {
       narrow_steps += !w;
     }
     if (mixed && narrow_steps == 0) mixed = false;
+    // wide steps of the mixed layout share the 8-byte field positions (12-bit next state)
+    for (int32_t q = 0; mixed && q < M; ++q) {
+      const size_t b = hdr[q].x, e = q + 1 < M ? hdr[q + 1].x : n_entries;
+      for (size_t k = b; step_wide[q] && k < e; ++k)
+        if ((table[2 * k].x & 0xFFFFu) > 0xFFFu) mixed = false;
+    }
     if (mixed) {
       P->fsm_layout = 3;
       std::vector<uint32_t> offs(M);
@@ -915,14 +927,14 @@ int build_fsm_plan(cb_es_plan* P) {
           const uint4 t0 = table[2 * k];
           uint32_t* dst = stab.data() + offs[q] + (k - b) * (step_wide[q] ? 4 : 2);
           if (step_wide[q]) {
-            dst[0] = (t0.x & 0xFFFFFFu) | (dref[k] << 24);
+            dst[0] = (t0.x & 0xFFFu) | (((t0.x >> 16) & 1u) << 12) | t0.w | (dref[k] << 24);
             dst[1] = t0.y;
             dst[2] = t0.z;
             dst[3] = 0u;
           } else {
             const uint32_t nxt = t0.x & 0xFFFFu, open = (t0.x >> 16) & 1u, nm = (t0.x >> 17) & 7u,
                            ne = (t0.x >> 20) & 7u;
-            dst[0] = nxt | (open << 12) | (nm << 13) | (ne << 15) | (dref[k] << 24);
+            dst[0] = nxt | (open << 12) | fsm_therm(nm, ne) | (dref[k] << 24);
             dst[1] = (t0.y & 0x3FFFFu) | ((t0.z & 0x1FFu) << 18);
           }
         }
@@ -935,7 +947,7 @@ int build_fsm_plan(cb_es_plan* P) {
       for (size_t k = 0; k < n_entries; ++k) {
         const uint4 t0 = table[2 * k];
         const uint32_t nxt = t0.x & 0xFFFFu, open = (t0.x >> 16) & 1u, nm = (t0.x >> 17) & 7u, ne = (t0.x >> 20) & 7u;
-        stab[2 * k] = nxt | (open << 12) | (nm << 13) | (ne << 15) | (dref[k] << 24);
+        stab[2 * k] = nxt | (open << 12) | fsm_therm(nm, ne) | (dref[k] << 24);
         stab[2 * k + 1] = (t0.y & 0x3FFFFu) | ((t0.z & 0x1FFu) << 18);
       }
     } else if (fits16) {
@@ -946,7 +958,7 @@ int build_fsm_plan(cb_es_plan* P) {
         stab[4 * k] = (t0.x & 0xFFFFFFu) | (dref[k] << 24);
         stab[4 * k + 1] = t0.y;
         stab[4 * k + 2] = t0.z;
-        stab[4 * k + 3] = 0u;
+        stab[4 * k + 3] = t0.w;  // thermometers
       }
     } else {
       dtab.clear();
