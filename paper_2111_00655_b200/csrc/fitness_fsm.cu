@@ -280,17 +280,18 @@ fitness_fsm_kernel(FsmArgs a, const uint64_t* __restrict__ pop, int64_t n, doubl
         }
       }
       if (W == 0) on = on && !dead;
-      const uint32_t idx = h.x + 2u * state + (on ? 1u : 0u);  // 32-bit index math
+      const uint32_t onb = W > 0 ? on_next : (on ? 1u : 0u);  // (W > 0: the bit as is, no select)
+      const uint32_t idx = h.x + 2u * state + onb;  // 32-bit index math
       // th: merge / emit counts as thermometers (bit 13 + k: the transition
       // has merge k, bit 18 + k: emit k), tested in place -- no field extraction
       uint32_t open, th, merges, emits;
-      uint32_t didx = 0u;  // shared delta table index (layouts 1-3: the entry's top byte)
+      uint32_t didx = 0u, dbyte = 0u;  // shared delta table index (layouts 1-3: the entry's top byte)
       uint4 dv = make_uint4(0u, 0u, 0u, 0u);  // exact delta: closed one-unit regions' terms - removed term
       if (LL == 3) {
         // mixed: the step's header says whether its transitions take 8 or
         // 16 bytes (warp-uniform); h.x is a word offset
         if (h.w & FSM_WIDE_STEP) {
-          const uint4 e = __ldg(reinterpret_cast<const uint4*>(a.xtable + h.x + 4u * (2u * state + (on ? 1u : 0u))));
+          const uint4 e = __ldg(reinterpret_cast<const uint4*>(a.xtable + h.x + 4u * (2u * state + onb)));
           state = e.x & 0xFFFu;  // (mixed layouts keep <= 4096 states per step)
           open = (e.x >> 12) & 1u;
           th = e.x;
@@ -299,7 +300,7 @@ fitness_fsm_kernel(FsmArgs a, const uint64_t* __restrict__ pop, int64_t n, doubl
           merges = e.y;
           emits = e.z;
         } else {
-          const uint2 e = __ldg(reinterpret_cast<const uint2*>(a.xtable + h.x + 2u * (2u * state + (on ? 1u : 0u))));
+          const uint2 e = __ldg(reinterpret_cast<const uint2*>(a.xtable + h.x + 2u * (2u * state + onb)));
           state = e.x & 0xFFFu;
           open = (e.x >> 12) & 1u;
           th = e.x;
@@ -314,6 +315,7 @@ fitness_fsm_kernel(FsmArgs a, const uint64_t* __restrict__ pop, int64_t n, doubl
         open = (e.x >> 12) & 1u;
         th = e.x;
         didx = e.x >> 24;
+        dbyte = e.x >> 21;
         merges = e.y;
         emits = e.y >> 18;
       } else if (LL == 2) {
@@ -335,7 +337,10 @@ fitness_fsm_kernel(FsmArgs a, const uint64_t* __restrict__ pop, int64_t n, doubl
       }
       if (ACC64) {
         int64_t d;
-        asm volatile("ld.shared.s64 %0, [%1];" : "=l"(d) : "r"(sdelta_base + didx * 8u));
+        // layout 1: bits 21-23 of the entry are zero (emit thermometer <= 3
+        // bits), so the byte offset is one shift
+        const uint32_t doff = LL == 1 ? dbyte : didx * 8u;
+        asm volatile("ld.shared.s64 %0, [%1];" : "=l"(d) : "r"(sdelta_base + doff));
         dacc += d;
       } else {
         if (LL != 0 && LL != 3) dv = load_delta<D64>(sdelta_base, didx);
