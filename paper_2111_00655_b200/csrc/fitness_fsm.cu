@@ -121,8 +121,10 @@ __device__ __forceinline__ void fsm_price(const ulonglong2* q, int idx, const Fs
 
 template <int F, int W>
 struct FsmSmemBase {  // packed sums [F][T], per-warp queues and lane totals, genome words [W + 1][T]
-  static constexpr size_t words_off =
+  static constexpr size_t wtab_off =
       (size_t)F * FSM_THREADS * 16 + (size_t)(FSM_THREADS / 32) * (FSM_QCAP * 16 + 64 * 8);
+  // per-warp slot table: packed sum of the unit in each slot (8 x 16 bytes)
+  static constexpr size_t words_off = wtab_off + (size_t)(FSM_THREADS / 32) * 8 * 16;
   // (the words only when the walk reads its bits from shared memory: with
   // FSM_BITS_IN_REGS the freed 8 (W + 1) KB per block go to L1, where the
   // transition table lives)
@@ -149,6 +151,10 @@ fitness_fsm_kernel(FsmArgs a, const uint64_t* __restrict__ pop, int64_t n, doubl
   // holds 8-byte entries (half the shared wavefronts of the per-step read)
   constexpr int LL = L & 3;
   constexpr bool D64 = L >= 4;
+  // WT: one-unit components' sums from the per-warp slot table instead of a
+  // per-lane store at every open (W > 0: BERT-base +2 %, NasRNN +5 %;
+  // NasNet-A's W = 0 walk, F = 8, lost 4 % to it and keeps the store)
+  constexpr bool WT = W > 0;
   extern __shared__ __align__(16) unsigned char fsm_smem[];
   // deltas after the per-thread arrays (dynamic size: n_delta entries)
   uint4* sdelta = reinterpret_cast<uint4*>(fsm_smem + FsmSmemBase<F, W>::bytes);
@@ -170,6 +176,9 @@ fitness_fsm_kernel(FsmArgs a, const uint64_t* __restrict__ pop, int64_t n, doubl
   // and genome words (word w at + 8 w T): no generic-to-shared conversion
   // inside the step loop
   const uint32_t mine_a = (uint32_t)__cvta_generic_to_shared(mine);
+  // one-unit components keep no per-lane sum: merges read it from the
+  // warp's slot table (written once per step by lane 0)
+  const uint32_t wtab_a = (uint32_t)__cvta_generic_to_shared(fsm_smem + FsmSmemBase<F, W>::wtab_off) + warp * 128u;
   ulonglong2* q = sv + F * T + warp * FSM_QCAP;               // pricing queue of this warp
   uint64_t* tlo = reinterpret_cast<uint64_t*>(sv + F * T + (T / 32) * FSM_QCAP) + warp * 64;
   uint64_t* thi = tlo + 32;
@@ -284,7 +293,7 @@ fitness_fsm_kernel(FsmArgs a, const uint64_t* __restrict__ pop, int64_t n, doubl
       const uint32_t idx = h.x + 2u * state + onb;  // 32-bit index math
       // th: merge / emit counts as thermometers (bit 13 + k: the transition
       // has merge k, bit 18 + k: emit k), tested in place -- no field extraction
-      uint32_t open, th, merges, emits;
+      uint32_t open, th, merges, emits, sg;  // sg: merge operands that are one-unit components
       uint32_t didx = 0u, dbyte = 0u;  // shared delta table index (layouts 1-3: the entry's top byte)
       uint4 dv = make_uint4(0u, 0u, 0u, 0u);  // exact delta: closed one-unit regions' terms - removed term
       if (LL == 3) {
@@ -299,6 +308,7 @@ fitness_fsm_kernel(FsmArgs a, const uint64_t* __restrict__ pop, int64_t n, doubl
           if (!ACC64) dv = load_delta<D64>(sdelta_base, didx);  // in the branch (NasNet-A: 4 % faster)
           merges = e.y;
           emits = e.z;
+          sg = e.w;
         } else {
           const uint2 e = __ldg(reinterpret_cast<const uint2*>(a.xtable + h.x + 2u * (2u * state + onb)));
           state = e.x & 0xFFFu;
@@ -308,6 +318,7 @@ fitness_fsm_kernel(FsmArgs a, const uint64_t* __restrict__ pop, int64_t n, doubl
           if (!ACC64) dv = load_delta<D64>(sdelta_base, didx);  // in the branch (NasNet-A: 4 % faster)
           merges = e.y & 0x3FFFFu;
           emits = e.y >> 18;
+          sg = e.y >> 27;
         }
       } else if (LL == 1) {
         const uint2 e = __ldg(a.ctable + idx);
@@ -318,6 +329,7 @@ fitness_fsm_kernel(FsmArgs a, const uint64_t* __restrict__ pop, int64_t n, doubl
         dbyte = e.x >> 21;
         merges = e.y;
         emits = e.y >> 18;
+        sg = e.y >> 27;
       } else if (LL == 2) {
         const uint4 e = __ldg(a.mtable + idx);
         state = e.x & 0xFFFFu;
@@ -326,6 +338,7 @@ fitness_fsm_kernel(FsmArgs a, const uint64_t* __restrict__ pop, int64_t n, doubl
         didx = e.x >> 24;
         merges = e.y;
         emits = e.z;
+        sg = e.w;
       } else {
         const uint4 e = __ldg(a.table + 2u * idx);
         dv = __ldg(a.table + 2u * idx + 1u);
@@ -334,6 +347,7 @@ fitness_fsm_kernel(FsmArgs a, const uint64_t* __restrict__ pop, int64_t n, doubl
         th = e.w;
         merges = e.y;
         emits = e.z;
+        sg = e.w;
       }
       if (ACC64) {
         int64_t d;
@@ -346,9 +360,14 @@ fitness_fsm_kernel(FsmArgs a, const uint64_t* __restrict__ pop, int64_t n, doubl
         if (LL != 0 && LL != 3) dv = load_delta<D64>(sdelta_base, didx);
         fadd2(tot_lo, tot_hi, ((uint64_t)dv.y << 32) | dv.x, ((uint64_t)dv.w << 32) | dv.z);
       }
-      if (open) {  // the unit opens its slot with its packed sum
+      if (WT) {  // the step's unit takes its slot: its packed sum into the warp's slot table
         const uint4 r = PRE_REP ? rp : __ldg(hp - 1);
-        sts_u4(mine_a + h.z, r);  // h.z: the slot's byte offset
+        __syncwarp();  // every lane is past the slot's previous occupant
+        if (lane == 0) sts_u4(wtab_a + (h.z >> 8), r);  // h.z: slot x 16 T; the table: slot x 16
+        __syncwarp();
+      } else if (open) {  // the unit opens its slot with its packed sum (per lane)
+        const uint4 r = PRE_REP ? rp : __ldg(hp - 1);
+        sts_u4(mine_a + h.z, r);
       }
       if (h.w & 0x1Fu) {  // some transition of the step merges (thermometer of the step's maximum)
         constexpr int MAXM = LL == 1 ? 3 : 5;
@@ -357,8 +376,11 @@ fitness_fsm_kernel(FsmArgs a, const uint64_t* __restrict__ pop, int64_t n, doubl
           if (!(th & (1u << (13 + k)))) break;
           const uint32_t src = (merges >> (6 * k)) & 7u, dst = (merges >> (6 * k + 3)) & 7u;
           const uint32_t da = mine_a + dst * (16u * T);
-          ulonglong2 d = lds_u2(da);
-          const ulonglong2 v = lds_u2(mine_a + src * (16u * T));
+          // sg: bit k (k < 3) / k + 1: source k is a one-unit component,
+          // bit 3: merge 0's destination is (later merges' never is)
+          const bool s1 = WT && ((sg >> (k < 3 ? k : k + 1)) & 1u), d1 = WT && k == 0 && ((sg >> 3) & 1u);
+          ulonglong2 d = lds_u2(d1 ? wtab_a + dst * 16u : da);
+          const ulonglong2 v = lds_u2(s1 ? wtab_a + src * 16u : mine_a + src * (16u * T));
           fadd2(d.x, d.y, v.x, v.y);
           sts_u2(da, d);
         }
@@ -537,7 +559,7 @@ FsmState canonical(const int* lab, const bool* multi_of_label, int F) {
 
 struct FsmTrans {  // one computed transition before its next-state id is assigned
   FsmState ns;
-  uint32_t open = 0, merges = 0, emits = 0;
+  uint32_t open = 0, merges = 0, emits = 0, singles = 0;
   int n_merge = 0, n_emit = 0;
   fx192 dx;
   bool ok = false;
@@ -620,7 +642,7 @@ int build_fsm_plan(cb_es_plan* P) {
         lab[s] = (st.lab >> (4 * s)) & 0xF;
         if (lab[s]) multi[lab[s]] = (st.multi >> (lab[s] - 1)) & 1u;
       }
-      uint32_t open = 0, merges = 0, emits = 0;
+      uint32_t open = 0, merges = 0, emits = 0, singles = 0;
       int n_merge = 0, n_emit = 0;
       fx192 delta = fx_zero();  // terms of the one-unit regions closed by this transition
       auto anchor_of = [&](int label) {  // member whose unit ends last (ties: larger slot)
@@ -641,7 +663,11 @@ int build_fsm_plan(cb_es_plan* P) {
           if (!seen) join[nj++] = l;
         }
         int anchors[8];
-        for (int k = 0; k < nj; ++k) anchors[k] = anchor_of(join[k]);
+        bool single[8];  // the joined component had one unit before this step
+        for (int k = 0; k < nj; ++k) {
+          anchors[k] = anchor_of(join[k]);
+          single[k] = !multi[join[k]];
+        }
         const int L = 16;  // temporary label of the new component
         lab[S] = L;
         multi[L] = nj > 0;
@@ -650,15 +676,24 @@ int build_fsm_plan(cb_es_plan* P) {
             if (lab[s] == join[k]) lab[s] = L;
         const int Wn = anchor_of(L);
         open = 1;
-        auto add_merge = [&](int src) {
+        // one-unit operands (their sums come from the kernel's slot table):
+        // the surviving anchor until the first merge writes it, every source
+        // that is the new unit or a joined single.  singles: source m at bit
+        // m (m < 3) / m + 1, merge 0's destination at bit 3
+        bool dst_single = Wn == S;
+        for (int k = 0; k < nj; ++k)
+          if (anchors[k] == Wn) dst_single = single[k];
+        auto add_merge = [&](int src, bool src_single) {
           if (n_merge >= 5) return false;
           merges |= ((uint32_t)src | ((uint32_t)Wn << 3)) << (6 * n_merge);
+          if (src_single) singles |= 1u << (n_merge < 3 ? n_merge : n_merge + 1);
+          if (n_merge == 0 && dst_single) singles |= 1u << 3;
           ++n_merge;
           return true;
         };
         for (int k = 0; k < nj; ++k)
-          if (anchors[k] != Wn && !add_merge(anchors[k])) return false;
-        if (S != Wn && !add_merge(S)) return false;
+          if (anchors[k] != Wn && !add_merge(anchors[k], single[k])) return false;
+        if (S != Wn && !add_merge(S, true)) return false;
       }
       // releases: a component closes when its last member leaves; its data
       // is at the anchor it had when the step's releases began (the anchor
@@ -719,6 +754,7 @@ int build_fsm_plan(cb_es_plan* P) {
       out.ns = ns;
       out.open = open;
       out.merges = merges;
+      out.singles = singles;
       out.emits = emits;
       out.n_merge = n_merge;
       out.n_emit = n_emit;
@@ -750,7 +786,7 @@ int build_fsm_plan(cb_es_plan* P) {
       }
       table.push_back(make_uint4((uint32_t)nid | (open << 16) | ((uint32_t)n_merge << 17) |
                                      ((uint32_t)n_emit << 20),
-                                 merges, emits, fsm_therm(n_merge, n_emit)));
+                                 merges, emits, fsm_therm(n_merge, n_emit) | t_.singles));
       table.push_back(make_uint4((uint32_t)dx.w[0], (uint32_t)(dx.w[0] >> 32), (uint32_t)dx.w[1],
                                  (uint32_t)(dx.w[1] >> 32)));
     }
@@ -932,15 +968,15 @@ int build_fsm_plan(cb_es_plan* P) {
           const uint4 t0 = table[2 * k];
           uint32_t* dst = stab.data() + offs[q] + (k - b) * (step_wide[q] ? 4 : 2);
           if (step_wide[q]) {
-            dst[0] = (t0.x & 0xFFFu) | (((t0.x >> 16) & 1u) << 12) | t0.w | (dref[k] << 24);
+            dst[0] = (t0.x & 0xFFFu) | (((t0.x >> 16) & 1u) << 12) | (t0.w & ~0x3Fu) | (dref[k] << 24);
             dst[1] = t0.y;
             dst[2] = t0.z;
-            dst[3] = 0u;
+            dst[3] = t0.w & 0x3Fu;  // singles
           } else {
             const uint32_t nxt = t0.x & 0xFFFFu, open = (t0.x >> 16) & 1u, nm = (t0.x >> 17) & 7u,
                            ne = (t0.x >> 20) & 7u;
             dst[0] = nxt | (open << 12) | fsm_therm(nm, ne) | (dref[k] << 24);
-            dst[1] = (t0.y & 0x3FFFFu) | ((t0.z & 0x1FFu) << 18);
+            dst[1] = (t0.y & 0x3FFFFu) | ((t0.z & 0x1FFu) << 18) | ((t0.w & 0xFu) << 27);
           }
         }
         hdr[q].x = offs[q];
@@ -953,7 +989,7 @@ int build_fsm_plan(cb_es_plan* P) {
         const uint4 t0 = table[2 * k];
         const uint32_t nxt = t0.x & 0xFFFFu, open = (t0.x >> 16) & 1u, nm = (t0.x >> 17) & 7u, ne = (t0.x >> 20) & 7u;
         stab[2 * k] = nxt | (open << 12) | fsm_therm(nm, ne) | (dref[k] << 24);
-        stab[2 * k + 1] = (t0.y & 0x3FFFFu) | ((t0.z & 0x1FFu) << 18);
+        stab[2 * k + 1] = (t0.y & 0x3FFFFu) | ((t0.z & 0x1FFu) << 18) | ((t0.w & 0xFu) << 27);
       }
     } else if (fits16) {
       P->fsm_layout = 2;
