@@ -30,6 +30,9 @@
 #include "fitness_plan.cuh"
 
 #define FSM_THREADS 256
+#ifndef FSM_MINB
+#define FSM_MINB 4  // resident blocks per SM the registers are budgeted for (1 024 threads)
+#endif
 #ifndef FSM_BITS_IN_REGS
 #define FSM_BITS_IN_REGS 1
 #endif
@@ -143,7 +146,7 @@ struct FsmSmemBase {  // packed sums [F][T], per-warp queues and lane totals, ge
 // most 256 distinct values; BERT-base has 22) sit in shared memory.  Used
 // when every transition fits: a quarter of the table's cache footprint.
 template <int F, int W, int L>
-__global__ void __launch_bounds__(FSM_THREADS)
+__global__ void __launch_bounds__(FSM_THREADS, FSM_MINB)
 fitness_fsm_kernel(FsmArgs a, const uint64_t* __restrict__ pop, int64_t n, double* __restrict__ fit) {
   constexpr int T = FSM_THREADS;
   // L = layout (0: 32-byte entries, 1: 8, 2: 16, 3: mixed) + 4 when every
@@ -448,7 +451,7 @@ int launch_fsm_t(cb_es_plan* p, const uint64_t* d_pop, int64_t n, double* d_fit,
     const char* cv = getenv("CB_FSM_CARVEOUT");
     int pct = 100;
     for (int kb : {100, 132, 164, 196})
-      if ((size_t)kb * 1024 >= (1024 / FSM_THREADS) * (smem + 1024)) {
+      if ((size_t)kb * 1024 >= (size_t)FSM_MINB * (smem + 1024)) {
         pct = kb * 100 / 228;
         break;
       }
