@@ -13,7 +13,7 @@ timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 3000 --
 tail -1 gpurun_out/ncu_launch_run.log | cut -c1-200
 BARGS="--workload bert_base --steps 2 --warmup 3 --no-cpu-baseline --e2e-steps 1 --search-generations 2 --no-configs"
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:fitness_fsm -s 11 -c 1 \
-  -o gpurun_out/bert_fsm_final python bench.py $BARGS > gpurun_out/ncu_bert_fsm_final.log 2>&1; tail -1 gpurun_out/ncu_bert_fsm_final.log | cut -c1-200
+  -o gpurun_out/bert_fsm_final2 python bench.py $BARGS > gpurun_out/ncu_bert_fsm_final2.log 2>&1; tail -1 gpurun_out/ncu_bert_fsm_final2.log | cut -c1-200
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:breed_thread -s 7 -c 1 \
-  -o gpurun_out/bert_breed_final python bench.py $BARGS > gpurun_out/ncu_bert_breed_final.log 2>&1; tail -1 gpurun_out/ncu_bert_breed_final.log | cut -c1-200
+  -o gpurun_out/bert_breed_final2 python bench.py $BARGS > gpurun_out/ncu_bert_breed_final2.log 2>&1; tail -1 gpurun_out/ncu_bert_breed_final2.log | cut -c1-200
 ls gpurun_out
