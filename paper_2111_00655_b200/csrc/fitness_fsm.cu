@@ -134,17 +134,24 @@ struct FsmSmemBase {  // packed sums [F][T], per-warp queues and lane totals, ge
   static constexpr size_t bytes = words_off + (W > 0 && !FSM_BITS_IN_REGS ? (size_t)(W + 1) * FSM_THREADS * 8 : 0);
 };
 
-// Transition entry (32 bytes, C = false): x = next | open << 16 | n_merge << 17 |
+// Transition entry (32 bytes, layout 0): x = next | open << 16 | n_merge << 17 |
 // n_emit << 20, y = merges (src 3 bits | dst 3 bits) x 5, z = emit anchor
-// slots (3 bits) x 5; then the transition's exact 128-bit delta: the terms of
-// the one-unit regions it closes minus the removed op-kernel term of an
-// offloaded unit.
+// slots (3 bits) x 5, w = merge / emit thermometers (bits 13 + k / 18 + k)
+// | one-unit operand bits (source m at bit m < 3 / m + 1, merge 0's
+// destination at bit 3); then the transition's exact 128-bit delta: the
+// terms of the one-unit regions it closes minus the removed op-kernel term of
+// an offloaded unit.
 //
-// Compact layout (8 bytes, C = true): x = next (12 bits) | open << 12 |
-// n_merge (2 bits) << 13 | n_emit (2 bits) << 15 | delta index (8 bits) << 24,
-// y = merges (6 bits) x 3 | emit slots (3 bits) x 3 << 18; the deltas (at
-// most 256 distinct values; BERT-base has 22) sit in shared memory.  Used
-// when every transition fits: a quarter of the table's cache footprint.
+// 16-byte layout (2; the wide steps of the mixed layout 3 use the 8-byte x):
+// x = next (16 bits) | open | counts | delta index << 24, y = merges, z =
+// emit slots, w as above.
+//
+// Compact layout (8 bytes, 1): x = next (12 bits) | open << 12 | merge
+// thermometer (3 bits) << 13 | emit thermometer (3 bits) << 18 | delta index
+// (8 bits) << 24, y = merges (6 bits) x 3 | emit slots (3 bits) x 3 << 18 |
+// one-unit operand bits (4) << 27; the deltas (at most 256 distinct values;
+// BERT-base has 22) sit in shared memory.  Used when every transition fits:
+// a quarter of the table's cache footprint.
 template <int F, int W, int L>
 __global__ void __launch_bounds__(FSM_THREADS, FSM_MINB)
 fitness_fsm_kernel(FsmArgs a, const uint64_t* __restrict__ pop, int64_t n, double* __restrict__ fit) {
