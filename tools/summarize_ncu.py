@@ -34,7 +34,7 @@ for n, ns in rows:
 tot = sum(a[1] for a in agg.values())
 with open(os.path.join(out, f"{tag}_launches.md"), "w") as fh:
     fh.write(f"# {tag}: ncu launch list (gpu__time_duration.sum, --clock-control none)\n\n")
-    fh.write("Command: `ncu --metrics gpu__time_duration.sum --clock-control none -c 2000 "
+    fh.write("Command: `ncu --metrics gpu__time_duration.sum --clock-control none -c 3000 "
              "python bench.py --steps 3 --warmup 3 --no-cpu-baseline --e2e-steps 1 "
              "--search-generations 3` (cold-cache, serialised: compare shares).\n\n")
     fh.write("| kernel | launches | total ms | share |\n|---|---:|---:|---:|\n")
